@@ -1,0 +1,25 @@
+"""CPU ORACLE for the Θ(c) hot path — TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` / `--impl reference` legs
+may import this package. The product path (`paper_2301_12814_b200`) never imports it, and it never
+imports the product path: the two share no code, tables or helpers. The shared seeded input
+generator lives in `synth/` and holds none of the method's arithmetic.
+
+Every function is a plain, slow, obviously-correct transcription of PAPER.md (Supplementary §1.1–1.2):
+  * `sort_bonds`       — PAPER.md:92-94 (sort bonds by charge, ascending), stable tie-break
+  * `bs_unitary_block` — Eq. S4 with the convention of DESIGN.md reading R5,
+                         evaluated at 50 decimal digits with mpmath, rounded once to complex128
+  * `theta_sectors`    — Eq. S5 by the literal triple charge loop of PAPER.md:72
+  * `theta_element`    — the same sum for one output element (sampled parity at full size)
+  * `flop_counts`      — the useful-work definitions of SURVEY.md §8(d)
+
+Pins (tests/test_oracle_pins.py, `-m "not gpu"`): dense δ-tensor brute force (tiny inputs), scipy
+expm of the block generator, HOM dip, θ=0 identity, θ=π/2 swap closed form, Wigner-d (sympy),
+block unitarity, norm invariance Σ_c‖Θ(c)‖² with d=N+1, identity gate == two-site product,
+SPEC.md sort examples. No function here is "parity unpinned".
+"""
+from .theta import (sort_bonds, bs_unitary_block, packed_u, packed_u_offsets, theta_sectors,
+                    theta_element, sector_ranges, flop_counts)
+
+__all__ = ["sort_bonds", "bs_unitary_block", "packed_u", "packed_u_offsets", "theta_sectors",
+           "theta_element", "sector_ranges", "flop_counts"]
