@@ -1,0 +1,182 @@
+/*
+ * tn_theta.h — C ABI of the B200 (sm_100a) charge-sectored two-site Θ(c) builder.
+ *
+ * What it computes (Supplementary Eq. S5 "\label{theta}"):
+ *
+ *   Θ(c)[α,β] = λl[α] λr[β] Σ_{α_k} Σ_{j_k,j_{k+1}} U^{i_k,i_{k+1}}_{j_k,j_{k+1}} Γk[α,α_k] λk[α_k] Γk1[α_k,β]
+ *               × δ(c_l−c_c−j_k) δ(c_c−c_r−j_{k+1}) δ(c_l−c−i_k) δ(c−c_r−i_{k+1}),      0 ≤ c ≤ N
+ *
+ * with c_l, c_c, c_r the bond charges ("photons to the right") of α = α_{k−1},
+ * α_k and β = α_{k+1}, 0 ≤ i, j ≤ d−1, and U the two-mode gate of Eq. S4
+ * (PAPER.md:56-58). The δ's are enforced by charge-block indexing, never stored.
+ *
+ * Conventions shared by every call (DESIGN.md §2 "Readings"):
+ *   - Complex numbers are interleaved (re, im) pairs of IEEE double (cuDoubleComplex layout);
+ *     a "complex pointer" below is a `double*` to 2·count doubles.
+ *   - Bonds are sorted by charge, ascending and stable. perm_x[p] is
+ *     the caller's bond index at sorted position p; off_x[q] = #bonds of charge < q (q = 0..N+1).
+ *   - Θ(c) is a compact row-major R_c×C_c matrix (ld = C_c). Its rows are the sorted left
+ *     positions [off_l[c], off_l[min(N,c+d−1)+1]) and its columns the sorted right positions
+ *     [off_r[max(0,c−d+1)], off_r[c+1]) (R2). With world_size > 1 a rank holds the
+ *     "local slab": the rows of Θ(c) that fall in its shard [r0, r1) of sorted left positions.
+ *   - U is "packed": blocks n = 0..min(N, 2d−2) of fixed total photon number n, block n at
+ *     offset Σ_{m<n} s_m², s_n = min(n,d−1) − max(0,n−d+1) + 1, entry [i][j] at
+ *     (i − lo_n)·s_n + (j − lo_n), lo_n = max(0, n−d+1), value ⟨i, n−i|U|j, n−j⟩ (R5/R6).
+ *   - Device pointers are CUDA device (or managed) memory on the current device; "host" pointers
+ *     are ordinary CPU memory. The library never frees caller memory.
+ *   - No call aborts the process. Every call returns a tn_status; tn_last_error() gives a
+ *     thread-local human-readable detail for the most recent failure.
+ *   - There is no CPU fallback: every computing step runs in this library's sm_100a kernels.
+ */
+#ifndef TN_THETA_H
+#define TN_THETA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TN_API __attribute__((visibility("default")))
+#else
+#define TN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TN_OK = 0,
+  TN_ERR_DOMAIN = 1,       /* argument outside its domain: d<2, N<0, N>TN_MAX_N, χ<1, charge ∉ [0,N], non-finite θ/φ, c ∉ [0,N] */
+  TN_ERR_DIMENSION = 2,    /* NULL pointer for a non-empty buffer, bad bond id */
+  TN_ERR_CONSISTENCY = 3,  /* plan / communicator mismatch (world size, rank), plan not sharded */
+  TN_ERR_CUDA = 4,         /* a CUDA runtime error (launch / copy / sticky fault) */
+  TN_ERR_OOM = 5,          /* device or host allocation failed */
+  TN_ERR_NCCL = 6,         /* NCCL missing or an NCCL call failed */
+  TN_ERR_UNSUPPORTED = 7   /* a size limit of this build was exceeded (e.g. min(N+1,d) > TN_MAX_MIX) */
+} tn_status;
+
+#define TN_MAX_N 100        /* largest photon number N (charges 0..N) this build accepts */
+#define TN_MAX_MIX 64       /* largest U-mix vector length min(N+1, d) */
+
+typedef struct tn_plan tn_plan;   /* opaque; owns device tables + staging workspace */
+typedef struct tn_comm tn_comm;   /* opaque; wraps an NCCL communicator */
+typedef void* tn_stream;          /* a cudaStream_t (0 = legacy default stream) */
+
+enum { TN_BOND_LEFT = 0, TN_BOND_CENTER = 1, TN_BOND_RIGHT = 2 };
+enum { TN_GATHER_NONE = 0, TN_GATHER_ROOT = 1 };
+
+/* ------------------------------------------------------------------------------------------ */
+/* Plan: bond re-indexing (K1) + work decomposition. Not on the hot path; synchronises once.   */
+/* ------------------------------------------------------------------------------------------ */
+/* tn_theta_plan — PAPER.md:90-94 ("sort the bonds according to their charges").
+ *   d        local Fock dimension (occupations 0..d−1), d ≥ 2.
+ *   N        total photon number; charges lie in [0, N]; 0 ≤ N ≤ TN_MAX_N.
+ *   chi_*    bond dimensions of α_{k−1} (l), α_k (c), α_{k+1} (r); each ≥ 1.
+ *   q_*      int32 charge per bond index, in the caller's bond order; host OR device pointers
+ *            (told apart with cudaPointerGetAttributes). Read during the call only.
+ *   world_size, rank   row sharding of Θ over ranks (1, 0 for a single GPU). The plan computes
+ *            flop-balanced shards of the sorted left positions and keeps the work for `rank`.
+ *   out      receives the new plan; free with tn_plan_destroy.
+ * Runs the K1 counting-sort kernel on an internal stream, copies the offset tables back, builds the
+ * c_c-group tile list and sector tables, allocates the staging workspace.
+ * Errors: TN_ERR_DOMAIN (d<2, N<0 or > TN_MAX_N, χ<1, a charge ∉ [0,N], world_size<1,
+ * rank ∉ [0,world_size)), TN_ERR_UNSUPPORTED (min(N+1,d) > TN_MAX_MIX), TN_ERR_DIMENSION (NULL q),
+ * TN_ERR_OOM, TN_ERR_CUDA. On error *out is NULL. */
+TN_API tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r,
+                        const int32_t* q_l, const int32_t* q_c, const int32_t* q_r,
+                        int world_size, int rank, tn_plan** out);
+
+TN_API tn_status tn_plan_destroy(tn_plan* plan);  /* NULL is accepted. */
+
+/* Full Θ(c) shape R_c × C_c (all ranks). TN_ERR_DOMAIN for c ∉ [0,N]. */
+TN_API tn_status tn_plan_sector_shape(const tn_plan* plan, int c, int64_t* R, int64_t* C);
+/* This rank's slab of Θ(c): *R local rows × *C, its first row being row *row_begin of Θ(c). */
+TN_API tn_status tn_plan_local_sector_shape(const tn_plan* plan, int c, int64_t* R, int64_t* C,
+                                     int64_t* row_begin);
+/* Copy perm_x (χ_x int32) / off_x (N+2 int32) of bond x into caller HOST memory. */
+TN_API tn_status tn_plan_perm(const tn_plan* plan, int bond, int32_t* host_out);
+TN_API tn_status tn_plan_offsets(const tn_plan* plan, int bond, int32_t* host_out);
+/* Sorted-left-position shard [r0, r1) of rank r (any r in [0, world_size)). */
+TN_API tn_status tn_plan_shard_rows(const tn_plan* plan, int r, int64_t* r0, int64_t* r1);
+/* Useful work of the WHOLE problem: 8 flops per complex MAC.
+ *   f_contract = 8 Σ_{allowed (c_l,c_c,c_r)} n_l n_c n_r,  f_mix = 8 Σ n_l n_r #c #c_c,
+ *   f_exec     = complex DMMA flops this rank's kernels execute incl. tile padding (8/CMAC). */
+TN_API tn_status tn_plan_flops(const tn_plan* plan, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec);
+/* Number of complex entries of the packed U for this (d, N). */
+TN_API tn_status tn_plan_u_size(const tn_plan* plan, int64_t* n_entries);
+/* Device bytes the plan owns (tables + staging workspace). */
+TN_API tn_status tn_plan_workspace_bytes(const tn_plan* plan, int64_t* bytes);
+
+/* ------------------------------------------------------------------------------------------ */
+/* U builder (K2) — Eq. S4, "O(d^4) for initializing U".        */
+/* ------------------------------------------------------------------------------------------ */
+/* Writes the packed beam-splitter blocks exp[θ(e^{iφ} a†b − e^{−iφ} a b†)] (a = mode k,
+ * DESIGN.md R5) into U_out: a DEVICE complex pointer of tn_plan_u_size entries, caller-owned.
+ * Each element is the closed-form binomial sum evaluated in double-double, rounded once.
+ * Stream-ordered, no host sync. Errors: TN_ERR_DOMAIN (θ or φ not finite),
+ * TN_ERR_DIMENSION (U_out NULL), TN_ERR_CUDA. */
+TN_API tn_status tn_build_bs_unitary(const tn_plan* plan, double theta, double phi, tn_stream stream,
+                              double* U_out);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Exec: K3 staging → K4 grouped complex DMMA contraction → K5 U-mix + outer-λ epilogue.       */
+/* ------------------------------------------------------------------------------------------ */
+/* tn_theta_exec — Eq. S5 for every sector c = 0..N.
+ *   gamma_k   DEVICE complex [χ_l × χ_c] row-major, caller bond order (Γ^{[k]}).
+ *   lambda_k  DEVICE double [χ_c] (λ^{[k]}).
+ *   gamma_k1  DEVICE complex [χ_c × χ_r] row-major (Γ^{[k+1]}).
+ *   lambda_l  DEVICE double [χ_l] (λ^{[k−1]}),  lambda_r DEVICE double [χ_r] (λ^{[k+1]}).
+ *   U         DEVICE packed complex U (from tn_build_bs_unitary or any caller-built U of the
+ *             same layout — the library cannot check which gate it is).
+ *   theta_out HOST array of N+1 DEVICE complex pointers; theta_out[c] receives this rank's
+ *             slab of Θ(c) (R×C from tn_plan_local_sector_shape), row-major, ld = C. Entries
+ *             with R·C = 0 may be NULL. Buffers must not alias the inputs or each other.
+ * Γ entries outside δ-allowed charge blocks are never read. Stream-ordered, no host sync.
+ * The plan's workspace is reused: one exec per plan in flight at a time.
+ * Errors: TN_ERR_DIMENSION (a NULL input, or NULL theta_out[c] for a non-empty slab),
+ * TN_ERR_CUDA (launch failure, or a sticky error from earlier work). */
+TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
+                        const double* gamma_k, const double* lambda_k, const double* gamma_k1,
+                        const double* lambda_l, const double* lambda_r, const double* U,
+                        double* const* theta_out);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Multi-GPU (one process per GPU): row-sharded exec + NCCL.                 */
+/* ------------------------------------------------------------------------------------------ */
+/* 128-byte NCCL unique id for rank 0 to create and distribute (e.g. via torch.distributed). */
+TN_API tn_status tn_comm_unique_id(void* id128);
+/* Bootstrap a communicator; NCCL is loaded at run time (dlopen "libnccl.so.2", or $TN_NCCL_LIB). */
+TN_API tn_status tn_comm_init(const void* id128, int rank, int world_size, tn_comm** out);
+TN_API tn_status tn_comm_destroy(tn_comm* comm);
+
+/* tn_theta_exec_sharded — this rank's rows of every Θ(c), plus optional exchange.
+ *   plan          built with the communicator's world_size and rank (else TN_ERR_CONSISTENCY).
+ *   bcast_operands if non-zero, first ncclBroadcast Γk, λk, Γk1, λl, λr and U from rank 0 into
+ *                 the same (full-size, every rank) device buffers.
+ *   gather_mode   TN_GATHER_NONE: theta_out holds the local slabs (tn_plan_local_sector_shape).
+ *                 TN_GATHER_ROOT: on rank 0 theta_out holds the FULL Θ(c) (R_c×C_c) and every
+ *                 rank's slab is sent to it with grouped ncclSend/ncclRecv; on other ranks
+ *                 theta_out holds the local slabs.
+ * Other arguments as tn_theta_exec. Errors: as tn_theta_exec, plus TN_ERR_NCCL,
+ * TN_ERR_CONSISTENCY. */
+TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn_comm* comm,
+                                double* gamma_k, double* lambda_k, double* gamma_k1,
+                                double* lambda_l, double* lambda_r, double* U,
+                                double* const* theta_out, int bcast_operands, int gather_mode);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Host-only helpers (no GPU needed) and diagnostics.                                          */
+/* ------------------------------------------------------------------------------------------ */
+/* Flop-balanced row shards from per-charge bond counts n_x[0..N] (the plan's own rule):
+ * bounds[0..world_size] (world_size+1 int64) of sorted left positions, bounds[0]=0,
+ * bounds[world_size]=χ_l. Errors: TN_ERR_DOMAIN. */
+TN_API tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_c,
+                             const int64_t* n_r, int world_size, int64_t* bounds);
+
+TN_API const char* tn_status_string(tn_status s);
+TN_API const char* tn_last_error(void);       /* thread-local detail of the last failure ("" if none) */
+TN_API int tn_version(void);                  /* (major << 16) | minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TN_THETA_H */

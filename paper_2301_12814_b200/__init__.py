@@ -1,0 +1,230 @@
+"""B200-native charge-sectored two-site Θ(c) builder (arXiv 2301.12814, Supplementary Eq. S5).
+
+Python face of the C ABI in include/tn_theta.h, with the same names. PyTorch is used for device memory
+and streams only; every computing step runs in libtn_theta.so's sm_100a kernels:
+  K1 bond sort (plan) → K2 U builder → K3 staging → K4 grouped complex DMMA contraction → K5 U-mix.
+
+    plan = Plan(d, N, q_l, q_c, q_r)                 # tn_theta_plan
+    U = build_bs_unitary(plan, theta, phi)           # tn_build_bs_unitary
+    theta = theta_exec(plan, gk, lk, gk1, ll, lr, U) # tn_theta_exec → list of N+1 complex128 tensors
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT, TN_GATHER_NONE,
+                   TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, LIB_PATH)
+
+__all__ = ["Plan", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
+           "shard_rows_host", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(int(stream.cuda_stream))
+
+
+def _ptr(t) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(0)
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(t.data_ptr())
+    if isinstance(t, np.ndarray):
+        if not t.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return C.c_void_p(t.ctypes.data)
+    raise TypeError(type(t))
+
+
+def _charges(q):
+    if isinstance(q, torch.Tensor):
+        if q.dtype != torch.int32:
+            q = q.to(torch.int32)
+        return q.contiguous()
+    return np.ascontiguousarray(np.asarray(q, dtype=np.int32))
+
+
+class Plan:
+    """tn_theta_plan: bond re-indexing (K1) and work decomposition for one gate's bond charges."""
+
+    def __init__(self, d: int, N: int, q_l, q_c, q_r, world_size: int = 1, rank: int = 0):
+        self._keep = [_charges(q) for q in (q_l, q_c, q_r)]
+        ql, qc, qr = self._keep
+        self.d, self.N = int(d), int(N)
+        self.chi = (int(ql.shape[0]), int(qc.shape[0]), int(qr.shape[0]))
+        self.world_size, self.rank = int(world_size), int(rank)
+        h = C.c_void_p()
+        check(lib.tn_theta_plan(self.d, self.N, *self.chi, _ptr(ql), _ptr(qc), _ptr(qr), self.world_size,
+                                self.rank, C.byref(h)), "tn_theta_plan")
+        self._h = h
+        del self._keep
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise ValueError("plan destroyed")
+        return self._h
+
+    def destroy(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            lib.tn_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def sector_shape(self, c: int):
+        R, Cc = C.c_int64(), C.c_int64()
+        check(lib.tn_plan_sector_shape(self.handle, int(c), C.byref(R), C.byref(Cc)), "tn_plan_sector_shape")
+        return R.value, Cc.value
+
+    def local_sector_shape(self, c: int):
+        R, Cc, r0 = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.tn_plan_local_sector_shape(self.handle, int(c), C.byref(R), C.byref(Cc), C.byref(r0)),
+              "tn_plan_local_sector_shape")
+        return R.value, Cc.value, r0.value
+
+    def perm(self, bond: int) -> np.ndarray:
+        out = np.empty(self.chi[bond], dtype=np.int32)
+        check(lib.tn_plan_perm(self.handle, int(bond), _ptr(out)), "tn_plan_perm")
+        return out
+
+    def offsets(self, bond: int) -> np.ndarray:
+        out = np.empty(self.N + 2, dtype=np.int32)
+        check(lib.tn_plan_offsets(self.handle, int(bond), _ptr(out)), "tn_plan_offsets")
+        return out
+
+    def shard_rows(self, r: int):
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.tn_plan_shard_rows(self.handle, int(r), C.byref(a), C.byref(b)), "tn_plan_shard_rows")
+        return a.value, b.value
+
+    def flops(self):
+        fc, fm, fe = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.tn_plan_flops(self.handle, C.byref(fc), C.byref(fm), C.byref(fe)), "tn_plan_flops")
+        return {"f_contract": fc.value, "f_mix": fm.value, "f_exec": fe.value}
+
+    def u_size(self) -> int:
+        n = C.c_int64()
+        check(lib.tn_plan_u_size(self.handle, C.byref(n)), "tn_plan_u_size")
+        return n.value
+
+    def workspace_bytes(self) -> int:
+        n = C.c_int64()
+        check(lib.tn_plan_workspace_bytes(self.handle, C.byref(n)), "tn_plan_workspace_bytes")
+        return n.value
+
+
+def build_bs_unitary(plan: Plan, theta: float, phi: float, out: torch.Tensor | None = None, stream=None):
+    """tn_build_bs_unitary → packed complex128 U on the current device (layout in include/tn_theta.h)."""
+    if out is None:
+        out = torch.empty(plan.u_size(), dtype=torch.complex128, device="cuda")
+    if out.dtype != torch.complex128 or out.numel() < plan.u_size() or not out.is_cuda:
+        raise ValueError("U must be a CUDA complex128 tensor of tn_plan_u_size entries")
+    check(lib.tn_build_bs_unitary(plan.handle, float(theta), float(phi), _stream_ptr(stream), _ptr(out)),
+          "tn_build_bs_unitary")
+    return out
+
+
+def alloc_theta(plan: Plan, device="cuda", full: bool = False):
+    """Device buffers for every sector: this rank's slabs (or the full Θ(c) if `full`)."""
+    outs = []
+    for c in range(plan.N + 1):
+        R, Cc = plan.sector_shape(c) if full else plan.local_sector_shape(c)[:2]
+        outs.append(torch.empty((R, Cc), dtype=torch.complex128, device=device))
+    return outs
+
+
+def _theta_ptrs(outs):
+    arr = (C.c_void_p * len(outs))()
+    for i, t in enumerate(outs):
+        if t is not None and t.numel() > 0:
+            if t.dtype != torch.complex128 or not t.is_cuda:
+                raise ValueError("Θ buffers must be CUDA complex128 tensors")
+            arr[i] = _ptr(t).value
+        else:
+            arr[i] = None
+    return arr
+
+
+def _check_inputs(plan, gk, lk, gk1, ll, lr, U):
+    chi_l, chi_c, chi_r = plan.chi
+    for t, shp, dt in ((gk, (chi_l, chi_c), torch.complex128), (gk1, (chi_c, chi_r), torch.complex128),
+                       (lk, (chi_c,), torch.float64), (ll, (chi_l,), torch.float64),
+                       (lr, (chi_r,), torch.float64)):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dt or tuple(t.shape) != shp:
+            raise ValueError(f"expected CUDA {dt} tensor of shape {shp}")
+    if not isinstance(U, torch.Tensor) or not U.is_cuda or U.dtype != torch.complex128 or U.numel() < plan.u_size():
+        raise ValueError("U must be a CUDA complex128 tensor of tn_plan_u_size entries")
+
+
+def theta_exec(plan: Plan, gk, lk, gk1, ll, lr, U, out=None, stream=None):
+    """tn_theta_exec: every sector Θ(c), c = 0..N (this rank's slabs). Returns the list `out`."""
+    _check_inputs(plan, gk, lk, gk1, ll, lr, U)
+    if out is None:
+        out = alloc_theta(plan)
+    ptrs = _theta_ptrs(out)
+    check(lib.tn_theta_exec(plan.handle, _stream_ptr(stream), _ptr(gk), _ptr(lk), _ptr(gk1), _ptr(ll), _ptr(lr),
+                            _ptr(U), ptrs), "tn_theta_exec")
+    return out
+
+
+class Comm:
+    """tn_comm over NCCL; the 128-byte unique id is distributed with a torch.distributed group."""
+
+    def __init__(self, rank: int, world_size: int, group=None):
+        import torch.distributed as dist
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            check(lib.tn_comm_unique_id(uid), "tn_comm_unique_id")
+        obj = [bytes(uid)]
+        if world_size > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        check(lib.tn_comm_init(uid, int(rank), int(world_size), C.byref(h)), "tn_comm_init")
+        self._h, self.rank, self.world_size = h, rank, world_size
+
+    @property
+    def handle(self):
+        return self._h
+
+    def destroy(self):
+        if self._h is not None:
+            lib.tn_comm_destroy(self._h)
+            self._h = None
+
+
+def theta_exec_sharded(plan: Plan, comm: Comm, gk, lk, gk1, ll, lr, U, out=None, bcast_operands=False,
+                       gather_mode=TN_GATHER_NONE, stream=None):
+    """tn_theta_exec_sharded: this rank's rows (+ optional NCCL operand broadcast / gather to rank 0)."""
+    _check_inputs(plan, gk, lk, gk1, ll, lr, U)
+    if out is None:
+        out = alloc_theta(plan, full=(gather_mode == TN_GATHER_ROOT and plan.rank == 0))
+    ptrs = _theta_ptrs(out)
+    check(lib.tn_theta_exec_sharded(plan.handle, _stream_ptr(stream), comm.handle, _ptr(gk), _ptr(lk), _ptr(gk1),
+                                    _ptr(ll), _ptr(lr), _ptr(U), ptrs, int(bool(bcast_operands)), int(gather_mode)),
+          "tn_theta_exec_sharded")
+    return out
+
+
+def shard_rows_host(d: int, N: int, n_l, n_c, n_r, world_size: int) -> np.ndarray:
+    """tn_shard_rows_host: flop-balanced row-shard bounds from per-charge bond counts (no GPU)."""
+    a = [np.ascontiguousarray(np.asarray(x, dtype=np.int64)) for x in (n_l, n_c, n_r)]
+    for x in a:
+        if x.shape != (N + 1,):
+            raise ValueError("counts must have N+1 entries")
+    out = np.empty(world_size + 1, dtype=np.int64)
+    i64p = C.POINTER(C.c_int64)
+    check(lib.tn_shard_rows_host(int(d), int(N), *(x.ctypes.data_as(i64p) for x in a), int(world_size),
+                                 out.ctypes.data_as(i64p)), "tn_shard_rows_host")
+    return out

@@ -1,0 +1,85 @@
+// K1 — bond re-indexing: stable ascending counting sort of one bond by charge.
+//
+// PAPER.md:92 "we propose to sort the bonds according to their charges before GPU computation";
+// PAPER.md:94 "bond indices are sorted such that c_{α_k} only increases as the bond index
+// increases". Tie-break is stable (R1). One CTA per bond: histogram →
+// exclusive scan → chunked stable scatter (warp match_any ranks within a chunk). Latency-bound
+// (µs); it runs once per plan, off the hot path.
+#include "tn_internal.cuh"
+
+namespace tn {
+
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+
+__global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const int32_t* __restrict__ q, int64_t chi,
+                                                              int N, int32_t* __restrict__ perm,
+                                                              int32_t* __restrict__ qs,
+                                                              int32_t* __restrict__ off,
+                                                              int32_t* __restrict__ err) {
+  __shared__ int32_t hist[MAXC + 1];
+  __shared__ int32_t base[MAXC + 1];
+  __shared__ int32_t wcnt[SORT_WARPS][MAXC];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nq = N + 1;
+  for (int i = tid; i <= nq; i += SORT_THREADS) hist[i] = 0;
+  __syncthreads();
+  int bad = 0;
+  for (int64_t i = tid; i < chi; i += SORT_THREADS) {
+    int v = q[i];
+    if (v < 0 || v > N) {
+      bad = 1;
+      continue;
+    }
+    atomicAdd(&hist[v], 1);
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) *err = 1;
+    return;
+  }
+  if (tid == 0) {
+    int acc = 0;
+    for (int v = 0; v < nq; ++v) {
+      base[v] = acc;
+      off[v] = acc;
+      acc += hist[v];
+    }
+    off[nq] = acc;
+  }
+  __syncthreads();
+  // Chunked stable scatter: a chunk of SORT_THREADS consecutive bonds at a time, in order.
+  for (int64_t c0 = 0; c0 < chi; c0 += SORT_THREADS) {
+    for (int i = tid; i < SORT_WARPS * nq; i += SORT_THREADS) (&wcnt[0][0])[(i / nq) * MAXC + i % nq] = 0;
+    __syncthreads();
+    const int64_t i = c0 + tid;
+    const bool valid = i < chi;
+    const int v = valid ? q[i] : -1;
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    unsigned peers = __match_any_sync(0xffffffffu, v);
+    peers &= active;
+    const int rank_in_warp = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank_in_warp == 0) wcnt[warp][v] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      int pos = base[v] + rank_in_warp;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w][v];
+      perm[pos] = (int32_t)i;
+      qs[pos] = v;
+    }
+    __syncthreads();
+    for (int v2 = tid; v2 < nq; v2 += SORT_THREADS) {
+      int s = 0;
+      for (int w = 0; w < SORT_WARPS; ++w) s += wcnt[w][v2];
+      base[v2] += s;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_sort_bonds(const int32_t* q, int64_t chi, int N, int32_t* perm, int32_t* qs, int32_t* off,
+                              int32_t* err, cudaStream_t s) {
+  k1_sort_bonds<<<1, SORT_THREADS, 0, s>>>(q, chi, N, perm, qs, off, err);
+  return cudaGetLastError();
+}
+
+}  // namespace tn

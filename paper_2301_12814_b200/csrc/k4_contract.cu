@@ -1,0 +1,188 @@
+// K4 — grouped block-sparse complex contraction on the FP64 tensor pipe (DMMA.8x8x4).
+//
+// For every center charge c_c with a non-empty segment ("without the U and λ value
+// lookup, this is exactly the same as matrix multiplication"):
+//   P_{c_c} = A_{c_c} · B_{c_c}       (R_{c_c} × K_{c_c}) · (K_{c_c} × C_{c_c}), complex128
+// P_{c_c} has exactly the shape and index set of Θ(c_c), so it is written straight
+// into the caller's Θ(c_c) buffer; K5 then applies U along the charge axis in place.
+//
+// B200 design (DESIGN.md §4 "K4"): sm_100a has no tcgen05 FP64 MMA (`kind::f64` does not exist),
+// so the FP64 tensor path is the warp-level DMMA.8x8x4 (mma.sync.m8n8k4.f64), measured at 37.2
+// TFLOP/s. A persistent grid walks a heavy-first tile list; one producer warp streams each 64×16
+// operand chunk with a single cp.async.bulk (TMA 1-D) copy into a 3-stage mbarrier ring; four
+// consumer warps (2×2, 32×32 complex each) read fragments with conflict-free 128-bit LDS (K3 wrote
+// the panels in fragment order) and issue 4 real DMMAs per complex 8×8×4 step.
+#include "tn_internal.cuh"
+
+namespace tn {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double neg_bits(double x) {  // −x on the integer pipe (sign flip)
+  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(K4_THREADS, 2)
+    k4_contract(const GroupDesc* __restrict__ groups, const TileDesc* __restrict__ tiles, int ntiles,
+                const double2* __restrict__ ap, const double2* __restrict__ bp, const SectorParams sp) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  double2* sA = reinterpret_cast<double2*>(smem);
+  double2* sB = sA + STAGES * CHUNK;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * CHUNK);
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], K4_CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == K4_CONSUMER_WARPS) {
+    // ---------------- producer: one elected lane streams A/B chunks ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileDesc td = tiles[t];
+        const GroupDesc g = groups[td.g];
+        const double2* a = ap + g.a_off + (int64_t)td.mt * BM * g.K4;
+        const double2* b = bp + g.b_off + (int64_t)td.nt * BN * g.K4;
+        for (int kc = 0; kc * BK < g.K4; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t kcnt = (uint32_t)min(BK, g.K4 - kc * BK);
+          const uint32_t bytes = kcnt * BM * (uint32_t)sizeof(double2);
+          mbar_expect_tx(&full[stage], 2 * bytes);
+          bulk_g2s(sA + stage * CHUNK, a + (int64_t)kc * CHUNK, bytes, &full[stage]);
+          bulk_g2s(sB + stage * CHUNK, b + (int64_t)kc * CHUNK, bytes, &full[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: 2×2 warps, 32×32 complex outputs each ----------------
+  const int wm = warp >> 1, wn = warp & 1;
+  const int gq = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const TileDesc td = tiles[t];
+    const GroupDesc g = groups[td.g];
+    double acc[4][4][4];  // [mi][ni][re0, re1, im0, im1]
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
+
+    for (int kc = 0; kc * BK < g.K4; ++kc) {
+      mbar_wait(&full[stage], phase);
+      const int nks = min(BK, g.K4 - kc * BK) >> 2;
+      const double2* As = sA + stage * CHUNK + wm * 128 + lane;
+      const double2* Bs = sB + stage * CHUNK + wn * 128 + lane;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        if (ks < nks) {
+          double2 a[4], b[4];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks * 256 + mi * 32];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            const double nai = neg_bits(a[mi].y);
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+              double* c = acc[mi][ni];
+              dmma(c[0], c[1], a[mi].x, b[ni].x);  // Re += Ar·Br
+              dmma(c[2], c[3], a[mi].x, b[ni].y);  // Im += Ar·Bi
+              dmma(c[0], c[1], nai, b[ni].y);      // Re −= Ai·Bi
+              dmma(c[2], c[3], a[mi].y, b[ni].x);  // Im += Ai·Br
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // epilogue: P tile → Θ(c_c) slab (row-major, ld = C_{c_c}); lane owns rows gq, cols 2tq, 2tq+1
+    double2* out = sp.out[g.cc];
+    const int ld = sp.ld[g.cc];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int row = td.mt * BM + wm * 32 + mi * 8 + gq;
+      if (row >= g.R) continue;
+      double2* orow = out + (int64_t)row * ld;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int col = td.nt * BN + wn * 32 + ni * 8 + 2 * tq;
+        if (col < g.C) orow[col] = make_double2(acc[mi][ni][0], acc[mi][ni][2]);
+        if (col + 1 < g.C) orow[col + 1] = make_double2(acc[mi][ni][1], acc[mi][ni][3]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
+  if (p->ntiles == 0) return cudaSuccess;
+  constexpr int STAGES = K4_STAGES;
+  const size_t smem = (size_t)STAGES * CHUNK * sizeof(double2) * 2 + 2 * STAGES * sizeof(uint64_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k4_contract<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t grid = std::min<int64_t>(p->ntiles, (int64_t)p->sm_count * 2);
+  k4_contract<STAGES><<<(unsigned)grid, K4_THREADS, smem, s>>>(p->d_groups, p->d_tiles, (int)p->ntiles,
+                                                                p->d_apanel, p->d_bpanel, sp);
+  return cudaGetLastError();
+}
+
+}  // namespace tn

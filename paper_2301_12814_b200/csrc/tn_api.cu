@@ -1,0 +1,451 @@
+// C-ABI glue of libtn_theta.so: plan construction (K1 + host work decomposition), queries, the U
+// builder entry point, exec (K3 → K4 → K5) and the row-sharded exec over NCCL. See
+// include/tn_theta.h for the contract of every entry point and DESIGN.md for the design.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+
+#include "tn_internal.cuh"
+
+namespace tn {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& s) { g_last_error = s; }
+
+tn_status fail(tn_status st, const std::string& s) {
+  g_last_error = s;
+  return st;
+}
+
+tn_status cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return TN_OK;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(TN_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  return fail(TN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Work model shared by the shard split and the flop counters.
+// ---------------------------------------------------------------------------------------------
+struct Counts {
+  int d, N;
+  std::vector<int64_t> nl, nc, nr;
+};
+
+// Useful flops of one left row of charge c_l (contraction + mix), 8 per complex MAC.
+static double row_cost(const Counts& k, int c_l) {
+  const int d = k.d, N = k.N;
+  double f = 0.0;
+  for (int cc = std::max(0, c_l - d + 1); cc <= c_l; ++cc) {      // j_k = c_l − c_c ∈ [0, d−1]
+    if (k.nc[cc] == 0) continue;
+    int64_t cols = 0;                                             // columns of group c_c
+    for (int cr = std::max(0, cc - d + 1); cr <= cc; ++cr) cols += k.nr[cr];
+    f += 8.0 * (double)k.nc[cc] * (double)cols;
+  }
+  for (int cr = std::max(0, c_l - 2 * d + 2); cr <= std::min(N, c_l); ++cr) {
+    int nvc = 0, nvcc = 0;
+    for (int c = cr; c <= c_l; ++c)
+      if (c_l - c <= d - 1 && c - cr <= d - 1) {
+        ++nvc;
+        if (k.nc[c] > 0) ++nvcc;
+      }
+    f += 8.0 * (double)k.nr[cr] * nvc * nvcc;
+  }
+  return f;
+}
+
+static void shard_bounds(const Counts& k, int world, std::vector<int64_t>& bounds) {
+  std::vector<double> cost(k.N + 1);
+  double total = 0.0;
+  int64_t chi_l = 0;
+  for (int q = 0; q <= k.N; ++q) {
+    cost[q] = row_cost(k, q);
+    total += cost[q] * (double)k.nl[q];
+    chi_l += k.nl[q];
+  }
+  bounds.assign(world + 1, 0);
+  bounds[world] = chi_l;
+  // bounds[r] = first sorted row whose prefix cost reaches r/world of the total (row granularity)
+  double prefix = 0.0;
+  int64_t row = 0;
+  int r = 1;
+  for (int q = 0; q <= k.N && r < world; ++q) {
+    for (int64_t i = 0; i < k.nl[q] && r < world; ++i) {
+      while (r < world && prefix >= total * (double)r / world) bounds[r++] = row;
+      prefix += cost[q];
+      ++row;
+    }
+  }
+  while (r < world) bounds[r++] = row;
+}
+
+static void free_plan(tn_plan* p) {
+  if (!p) return;
+  for (int b = 0; b < 3; ++b) {
+    cudaFree(p->d_perm[b]);
+    cudaFree(p->d_qs[b]);
+    cudaFree(p->d_off[b]);
+  }
+  cudaFree(p->d_groups);
+  cudaFree(p->d_tiles);
+  cudaFree(p->d_apanel);
+  cudaFree(p->d_bpanel);
+  if (p->plan_stream) cudaStreamDestroy(p->plan_stream);
+  delete p;
+}
+
+static bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static SectorParams make_sector_params(const tn_plan* p, double* const* theta_out) {
+  SectorParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.d = p->d;
+  sp.N = p->N;
+  for (int c = 0; c <= p->N; ++c) {
+    sp.out[c] = reinterpret_cast<double2*>(theta_out[c]);
+    sp.lrow0[c] = p->lrow0[c];
+    sp.col0[c] = p->col0[c];
+    sp.ld[c] = (int32_t)p->C[c];
+  }
+  for (size_t n = 0; n < p->ustart.size(); ++n) sp.ustart[n] = p->ustart[n];
+  // The mix reads P_{c_c} iff seg_c(c_c) is non-empty: exactly then K4 ran group c_c for every
+  // local row that can need it (a row of Θ(c_c) in this shard).
+  for (int cc = 0; cc <= p->N; ++cc)
+    if (p->off[1][cc + 1] > p->off[1][cc]) sp.cc_mask[cc >> 5] |= 1u << (cc & 31);
+  return sp;
+}
+
+}  // namespace tn
+
+using namespace tn;
+
+extern "C" {
+
+const char* tn_status_string(tn_status s) {
+  switch (s) {
+    case TN_OK: return "TN_OK";
+    case TN_ERR_DOMAIN: return "TN_ERR_DOMAIN";
+    case TN_ERR_DIMENSION: return "TN_ERR_DIMENSION";
+    case TN_ERR_CONSISTENCY: return "TN_ERR_CONSISTENCY";
+    case TN_ERR_CUDA: return "TN_ERR_CUDA";
+    case TN_ERR_OOM: return "TN_ERR_OOM";
+    case TN_ERR_NCCL: return "TN_ERR_NCCL";
+    case TN_ERR_UNSUPPORTED: return "TN_ERR_UNSUPPORTED";
+  }
+  return "TN_ERR_UNKNOWN";
+}
+
+const char* tn_last_error(void) { return g_last_error.c_str(); }
+
+int tn_version(void) { return (0 << 16) | 1; }
+
+tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_c, const int64_t* n_r,
+                             int world_size, int64_t* bounds) {
+  if (d < 2 || N < 0 || N > TN_MAX_N || world_size < 1) return fail(TN_ERR_DOMAIN, "tn_shard_rows_host: bad d/N/world");
+  if (!n_l || !n_c || !n_r || !bounds) return fail(TN_ERR_DIMENSION, "tn_shard_rows_host: NULL pointer");
+  Counts k{d, N, std::vector<int64_t>(n_l, n_l + N + 1), std::vector<int64_t>(n_c, n_c + N + 1),
+           std::vector<int64_t>(n_r, n_r + N + 1)};
+  for (int q = 0; q <= N; ++q)
+    if (k.nl[q] < 0 || k.nc[q] < 0 || k.nr[q] < 0) return fail(TN_ERR_DOMAIN, "tn_shard_rows_host: negative count");
+  std::vector<int64_t> b;
+  shard_bounds(k, world_size, b);
+  std::copy(b.begin(), b.end(), bounds);
+  return TN_OK;
+}
+
+tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q_l,
+                        const int32_t* q_c, const int32_t* q_r, int world_size, int rank, tn_plan** out) {
+  if (!out) return fail(TN_ERR_DIMENSION, "tn_theta_plan: out is NULL");
+  *out = nullptr;
+  if (d < 2) return fail(TN_ERR_DOMAIN, "tn_theta_plan: d < 2");
+  if (N < 0 || N > TN_MAX_N) return fail(TN_ERR_DOMAIN, "tn_theta_plan: N outside [0, TN_MAX_N]");
+  if (chi_l < 1 || chi_c < 1 || chi_r < 1) return fail(TN_ERR_DOMAIN, "tn_theta_plan: bond dimension < 1");
+  if (chi_l > INT32_MAX || chi_c > INT32_MAX || chi_r > INT32_MAX)
+    return fail(TN_ERR_UNSUPPORTED, "tn_theta_plan: bond dimension > INT32_MAX");
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(TN_ERR_DOMAIN, "tn_theta_plan: bad world_size/rank");
+  if (!q_l || !q_c || !q_r) return fail(TN_ERR_DIMENSION, "tn_theta_plan: NULL charge array");
+  if (std::min(N + 1, d) > TN_MAX_MIX) return fail(TN_ERR_UNSUPPORTED, "tn_theta_plan: min(N+1, d) > TN_MAX_MIX");
+
+  tn_plan* p = new (std::nothrow) tn_plan();
+  if (!p) return fail(TN_ERR_OOM, "tn_theta_plan: host allocation");
+  p->d = d;
+  p->N = N;
+  p->world = world_size;
+  p->rank = rank;
+  p->chi[0] = chi_l;
+  p->chi[1] = chi_c;
+  p->chi[2] = chi_r;
+  p->max_mix = std::min(N + 1, d);
+  tn_status st = TN_OK;
+  int dev = 0;
+  int32_t* d_err = nullptr;
+  int32_t* d_q[3] = {nullptr, nullptr, nullptr};
+  const int32_t* qs_in[3] = {q_l, q_c, q_r};
+#define TN_TRY(expr, what)                      \
+  do {                                          \
+    st = cuda_check((expr), what);              \
+    if (st != TN_OK) goto done;                 \
+  } while (0)
+  TN_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+  TN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  TN_TRY(cudaStreamCreateWithFlags(&p->plan_stream, cudaStreamNonBlocking), "plan stream");
+  TN_TRY(cudaMalloc(&d_err, 3 * sizeof(int32_t)), "alloc err");
+  TN_TRY(cudaMemsetAsync(d_err, 0, 3 * sizeof(int32_t), p->plan_stream), "memset err");
+  // ---- K1: sort each bond by charge ----
+  for (int b = 0; b < 3; ++b) {
+    const int64_t chi = p->chi[b];
+    const int32_t* src = qs_in[b];
+    if (!is_device_ptr(src)) {
+      TN_TRY(cudaMalloc(&d_q[b], chi * sizeof(int32_t)), "alloc charges");
+      TN_TRY(cudaMemcpyAsync(d_q[b], src, chi * sizeof(int32_t), cudaMemcpyHostToDevice, p->plan_stream), "H2D charges");
+      src = d_q[b];
+    }
+    TN_TRY(cudaMalloc(&p->d_perm[b], chi * sizeof(int32_t)), "alloc perm");
+    TN_TRY(cudaMalloc(&p->d_qs[b], chi * sizeof(int32_t)), "alloc qs");
+    TN_TRY(cudaMalloc(&p->d_off[b], (N + 2) * sizeof(int32_t)), "alloc off");
+    TN_TRY(launch_sort_bonds(src, chi, N, p->d_perm[b], p->d_qs[b], p->d_off[b], d_err + b, p->plan_stream), "K1 launch");
+  }
+  {
+    int32_t herr[3];
+    for (int b = 0; b < 3; ++b) p->off[b].resize(N + 2);
+    TN_TRY(cudaMemcpyAsync(herr, d_err, sizeof(herr), cudaMemcpyDeviceToHost, p->plan_stream), "D2H err");
+    for (int b = 0; b < 3; ++b)
+      TN_TRY(cudaMemcpyAsync(p->off[b].data(), p->d_off[b], (N + 2) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             p->plan_stream), "D2H off");
+    TN_TRY(cudaStreamSynchronize(p->plan_stream), "K1 sync");
+    if (herr[0] || herr[1] || herr[2]) {
+      st = fail(TN_ERR_DOMAIN, "tn_theta_plan: a bond charge lies outside [0, N]");
+      goto done;
+    }
+  }
+  {
+    // ---- sectors (R2) ----
+    const auto& ol = p->off[0];
+    const auto& oc = p->off[1];
+    const auto& orr = p->off[2];
+    Counts k{d, N, std::vector<int64_t>(N + 1), std::vector<int64_t>(N + 1), std::vector<int64_t>(N + 1)};
+    for (int q = 0; q <= N; ++q) {
+      k.nl[q] = ol[q + 1] - ol[q];
+      k.nc[q] = oc[q + 1] - oc[q];
+      k.nr[q] = orr[q + 1] - orr[q];
+    }
+    shard_bounds(k, world_size, p->bounds);
+    p->r0 = p->bounds[rank];
+    p->r1 = p->bounds[rank + 1];
+    p->R.resize(N + 1);
+    p->C.resize(N + 1);
+    p->row0.resize(N + 1);
+    p->col0.resize(N + 1);
+    p->lR.resize(N + 1);
+    p->lrow0.resize(N + 1);
+    for (int c = 0; c <= N; ++c) {
+      const int64_t a0 = ol[c], a1 = ol[std::min(N, c + d - 1) + 1];
+      const int64_t b0 = orr[std::max(0, c - d + 1)], b1 = orr[c + 1];
+      p->row0[c] = a0;
+      p->R[c] = a1 - a0;
+      p->col0[c] = b0;
+      p->C[c] = b1 - b0;
+      const int64_t l0 = std::min(std::max(a0, p->r0), p->r1), l1 = std::min(std::max(a1, p->r0), p->r1);
+      p->lrow0[c] = l0;
+      p->lR[c] = l1 - l0;
+      if (p->C[c] > INT32_MAX || p->R[c] > INT32_MAX) {
+        st = fail(TN_ERR_UNSUPPORTED, "sector dimension > INT32_MAX");
+        goto done;
+      }
+    }
+    // ---- useful flops of the whole problem ----
+    for (int cl = 0; cl <= N; ++cl)
+      for (int cr = 0; cr <= N; ++cr) {
+        const int n = cl - cr;
+        if (n < 0 || n > 2 * d - 2) continue;
+        int64_t nvc = 0, nvcc = 0;
+        for (int c = cr; c <= cl; ++c)
+          if (cl - c <= d - 1 && c - cr <= d - 1) {
+            ++nvc;
+            if (k.nc[c] > 0) {
+              ++nvcc;
+              p->f_contract += 8 * k.nl[cl] * k.nc[c] * k.nr[cr];
+            }
+          }
+        p->f_mix += 8 * k.nl[cl] * k.nr[cr] * nvc * nvcc;
+      }
+    // ---- groups: one per center charge with a non-empty segment and local rows ----
+    int64_t a_off = 0, b_off = 0;
+    for (int cc = 0; cc <= N; ++cc) {
+      const int64_t K = oc[cc + 1] - oc[cc];
+      if (K == 0 || p->lR[cc] == 0 || p->C[cc] == 0) continue;
+      GroupDesc g{};
+      g.cc = cc;
+      g.row0 = p->lrow0[cc];
+      g.col0 = p->col0[cc];
+      g.k0 = oc[cc];
+      g.R = (int32_t)p->lR[cc];
+      g.C = (int32_t)p->C[cc];
+      g.K = (int32_t)K;
+      g.K4 = (int32_t)((K + 3) / 4 * 4);
+      g.nmt = (g.R + BM - 1) / BM;
+      g.nnt = (g.C + BN - 1) / BN;
+      g.a_off = a_off;
+      g.b_off = b_off;
+      a_off += (int64_t)g.nmt * BM * g.K4;
+      b_off += (int64_t)g.nnt * BN * g.K4;
+      p->f_exec += 8 * (int64_t)g.nmt * BM * (int64_t)g.nnt * BN * g.K4;
+      p->groups.push_back(g);
+    }
+    p->a_elems = a_off;
+    p->b_elems = b_off;
+    // ---- tile list, heavy-first (longest K first) ----
+    std::vector<int> order(p->groups.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p->groups[x].K4 > p->groups[y].K4; });
+    std::vector<TileDesc> tiles;
+    for (int gi : order) {
+      const auto& g = p->groups[gi];
+      for (int mt = 0; mt < g.nmt; ++mt)
+        for (int nt = 0; nt < g.nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
+    }
+    p->ntiles = (int64_t)tiles.size();
+    if (!p->groups.empty()) {
+      TN_TRY(cudaMalloc(&p->d_groups, p->groups.size() * sizeof(GroupDesc)), "alloc groups");
+      TN_TRY(cudaMemcpy(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice),
+             "H2D groups");
+      TN_TRY(cudaMalloc(&p->d_tiles, tiles.size() * sizeof(TileDesc)), "alloc tiles");
+      TN_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice), "H2D tiles");
+      TN_TRY(cudaMalloc(&p->d_apanel, p->a_elems * sizeof(double2)), "alloc A panels");
+      TN_TRY(cudaMalloc(&p->d_bpanel, p->b_elems * sizeof(double2)), "alloc B panels");
+    }
+    // ---- packed U layout ----
+    const int nmax = std::min(N, 2 * d - 2);
+    int64_t tot = 0;
+    for (int n = 0; n <= nmax; ++n) {
+      const int s = std::min(n, d - 1) - std::max(0, n - d + 1) + 1;
+      p->ustart.push_back((int32_t)tot);
+      tot += (int64_t)s * s;
+    }
+    p->u_size = tot;
+    p->ws_bytes = (p->a_elems + p->b_elems) * (int64_t)sizeof(double2) +
+                  (int64_t)(tiles.size() * sizeof(TileDesc) + p->groups.size() * sizeof(GroupDesc)) +
+                  (chi_l + chi_c + chi_r) * 8 + 3 * (N + 2) * 4;
+  }
+done:
+#undef TN_TRY
+  for (int b = 0; b < 3; ++b) cudaFree(d_q[b]);
+  cudaFree(d_err);
+  if (st != TN_OK) {
+    free_plan(p);
+    return st;
+  }
+  *out = p;
+  return TN_OK;
+}
+
+tn_status tn_plan_destroy(tn_plan* plan) {
+  free_plan(plan);
+  return TN_OK;
+}
+
+tn_status tn_plan_sector_shape(const tn_plan* p, int c, int64_t* R, int64_t* C) {
+  if (!p || !R || !C) return fail(TN_ERR_DIMENSION, "tn_plan_sector_shape: NULL");
+  if (c < 0 || c > p->N) return fail(TN_ERR_DOMAIN, "tn_plan_sector_shape: c outside [0, N]");
+  *R = p->R[c];
+  *C = p->C[c];
+  return TN_OK;
+}
+
+tn_status tn_plan_local_sector_shape(const tn_plan* p, int c, int64_t* R, int64_t* C, int64_t* row_begin) {
+  if (!p || !R || !C || !row_begin) return fail(TN_ERR_DIMENSION, "tn_plan_local_sector_shape: NULL");
+  if (c < 0 || c > p->N) return fail(TN_ERR_DOMAIN, "tn_plan_local_sector_shape: c outside [0, N]");
+  *R = p->lR[c];
+  *C = p->C[c];
+  *row_begin = p->lrow0[c] - p->row0[c];
+  return TN_OK;
+}
+
+tn_status tn_plan_perm(const tn_plan* p, int bond, int32_t* host_out) {
+  if (!p || !host_out) return fail(TN_ERR_DIMENSION, "tn_plan_perm: NULL");
+  if (bond < 0 || bond > 2) return fail(TN_ERR_DIMENSION, "tn_plan_perm: bond id");
+  return cuda_check(cudaMemcpy(host_out, p->d_perm[bond], p->chi[bond] * sizeof(int32_t), cudaMemcpyDeviceToHost),
+                    "tn_plan_perm D2H");
+}
+
+tn_status tn_plan_offsets(const tn_plan* p, int bond, int32_t* host_out) {
+  if (!p || !host_out) return fail(TN_ERR_DIMENSION, "tn_plan_offsets: NULL");
+  if (bond < 0 || bond > 2) return fail(TN_ERR_DIMENSION, "tn_plan_offsets: bond id");
+  std::copy(p->off[bond].begin(), p->off[bond].end(), host_out);
+  return TN_OK;
+}
+
+tn_status tn_plan_shard_rows(const tn_plan* p, int r, int64_t* r0, int64_t* r1) {
+  if (!p || !r0 || !r1) return fail(TN_ERR_DIMENSION, "tn_plan_shard_rows: NULL");
+  if (r < 0 || r >= p->world) return fail(TN_ERR_DOMAIN, "tn_plan_shard_rows: rank outside [0, world)");
+  *r0 = p->bounds[r];
+  *r1 = p->bounds[r + 1];
+  return TN_OK;
+}
+
+tn_status tn_plan_flops(const tn_plan* p, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec) {
+  if (!p) return fail(TN_ERR_DIMENSION, "tn_plan_flops: NULL");
+  if (f_contract) *f_contract = p->f_contract;
+  if (f_mix) *f_mix = p->f_mix;
+  if (f_exec) *f_exec = p->f_exec;
+  return TN_OK;
+}
+
+tn_status tn_plan_u_size(const tn_plan* p, int64_t* n) {
+  if (!p || !n) return fail(TN_ERR_DIMENSION, "tn_plan_u_size: NULL");
+  *n = p->u_size;
+  return TN_OK;
+}
+
+tn_status tn_plan_workspace_bytes(const tn_plan* p, int64_t* bytes) {
+  if (!p || !bytes) return fail(TN_ERR_DIMENSION, "tn_plan_workspace_bytes: NULL");
+  *bytes = p->ws_bytes;
+  return TN_OK;
+}
+
+tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_stream stream, double* U_out) {
+  if (!p || !U_out) return fail(TN_ERR_DIMENSION, "tn_build_bs_unitary: NULL");
+  if (!std::isfinite(theta) || !std::isfinite(phi)) return fail(TN_ERR_DOMAIN, "tn_build_bs_unitary: non-finite angle");
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_build_bs_unitary");
+  return cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->ustart.data(), reinterpret_cast<double2*>(U_out),
+                                      (cudaStream_t)stream),
+                    "K2 launch");
+}
+
+tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
+                        const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
+                        double* const* theta_out) {
+  if (!p) return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL plan");
+  if (!gamma_k || !lambda_k || !gamma_k1 || !lambda_l || !lambda_r || !U || !theta_out)
+    return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL input pointer");
+  for (int c = 0; c <= p->N; ++c)
+    if (p->lR[c] * p->C[c] > 0 && !theta_out[c])
+      return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL theta_out[c] for a non-empty sector");
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_theta_exec");
+  cudaStream_t s = (cudaStream_t)stream;
+  const SectorParams sp = make_sector_params(p, theta_out);
+  tn_status st = cuda_check(launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                                         reinterpret_cast<const double2*>(gamma_k1), s),
+                            "K3 launch");
+  if (st != TN_OK) return st;
+  st = cuda_check(launch_contract(p, sp, s), "K4 launch");
+  if (st != TN_OK) return st;
+  return cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, p->d_off[2]),
+                    "K5 launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,173 @@
+// Row-sharded Θ exec over NCCL ("High-level parallelization"; BASELINE.json
+// north_star: "partitioned across the 8 B200s of one box by sharding the α_{k-1} rows of Θ, with
+// Γ^{[k+1]}, λ and U replicated; NCCL is used only to gather the shards or broadcast the operands").
+//
+// The compute needs no collective: each rank runs K3→K4→K5 on its flop-balanced row shard
+// (tn_theta_plan(world_size, rank)). The only exchange steps are the optional operand broadcast from
+// rank 0 and the optional gather of every rank's Θ slabs to rank 0 (grouped ncclSend/ncclRecv,
+// NCCL has no gatherv). NCCL is resolved at run time with dlopen so the library loads (and its
+// single-GPU path runs) without it; torch's bundled libnccl.so.2 is normally already resident.
+#include <dlfcn.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "nccl.h"
+#include "tn_internal.cuh"
+
+struct tn_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+namespace tn {
+namespace {
+
+struct NcclApi {
+  bool loaded = false;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* env = std::getenv("TN_NCCL_LIB");
+  void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+#define TN_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+  TN_SYM(GetUniqueId, "ncclGetUniqueId");
+  TN_SYM(CommInitRank, "ncclCommInitRank");
+  TN_SYM(CommDestroy, "ncclCommDestroy");
+  TN_SYM(Broadcast, "ncclBroadcast");
+  TN_SYM(Send, "ncclSend");
+  TN_SYM(Recv, "ncclRecv");
+  TN_SYM(GroupStart, "ncclGroupStart");
+  TN_SYM(GroupEnd, "ncclGroupEnd");
+  TN_SYM(GetErrorString, "ncclGetErrorString");
+#undef TN_SYM
+  api.loaded = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.Send && api.Recv &&
+               api.GroupStart && api.GroupEnd && api.GetErrorString;
+  return api;
+}
+
+tn_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return TN_OK;
+  return fail(TN_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace
+}  // namespace tn
+
+using namespace tn;
+
+extern "C" {
+
+tn_status tn_comm_unique_id(void* id128) {
+  if (!id128) return fail(TN_ERR_DIMENSION, "tn_comm_unique_id: NULL");
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(TN_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+  ncclUniqueId id;
+  tn_status st = nccl_check(api.GetUniqueId(&id), "ncclGetUniqueId");
+  if (st == TN_OK) std::memcpy(id128, &id, sizeof(id));
+  return st;
+}
+
+tn_status tn_comm_init(const void* id128, int rank, int world_size, tn_comm** out) {
+  if (!id128 || !out) return fail(TN_ERR_DIMENSION, "tn_comm_init: NULL");
+  *out = nullptr;
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(TN_ERR_DOMAIN, "tn_comm_init: bad rank/world");
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(TN_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  tn_comm* c = new (std::nothrow) tn_comm();
+  if (!c) return fail(TN_ERR_OOM, "tn_comm_init: host allocation");
+  tn_status st = nccl_check(api.CommInitRank(&c->comm, world_size, id, rank), "ncclCommInitRank");
+  if (st != TN_OK) {
+    delete c;
+    return st;
+  }
+  c->rank = rank;
+  c->world = world_size;
+  *out = c;
+  return TN_OK;
+}
+
+tn_status tn_comm_destroy(tn_comm* comm) {
+  if (!comm) return TN_OK;
+  tn_status st = TN_OK;
+  if (comm->comm) st = nccl_check(nccl().CommDestroy(comm->comm), "ncclCommDestroy");
+  delete comm;
+  return st;
+}
+
+tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* comm, double* gamma_k,
+                                double* lambda_k, double* gamma_k1, double* lambda_l, double* lambda_r, double* U,
+                                double* const* theta_out, int bcast_operands, int gather_mode) {
+  if (!p || !comm) return fail(TN_ERR_DIMENSION, "tn_theta_exec_sharded: NULL plan/comm");
+  if (p->world != comm->world || p->rank != comm->rank)
+    return fail(TN_ERR_CONSISTENCY, "tn_theta_exec_sharded: plan world/rank differ from the communicator's");
+  if (gather_mode != TN_GATHER_NONE && gather_mode != TN_GATHER_ROOT)
+    return fail(TN_ERR_DOMAIN, "tn_theta_exec_sharded: unknown gather_mode");
+  if (!theta_out) return fail(TN_ERR_DIMENSION, "tn_theta_exec_sharded: NULL theta_out");
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(TN_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+  cudaStream_t s = (cudaStream_t)stream;
+  tn_status st;
+  if (bcast_operands && p->world > 1) {
+    st = nccl_check(api.GroupStart(), "ncclGroupStart");
+    if (st != TN_OK) return st;
+    const size_t n_gk = (size_t)(2 * p->chi[0] * p->chi[1]), n_gk1 = (size_t)(2 * p->chi[1] * p->chi[2]);
+    ncclResult_t r = ncclSuccess;
+    if (r == ncclSuccess) r = api.Broadcast(gamma_k, gamma_k, n_gk, ncclFloat64, 0, comm->comm, s);
+    if (r == ncclSuccess) r = api.Broadcast(gamma_k1, gamma_k1, n_gk1, ncclFloat64, 0, comm->comm, s);
+    if (r == ncclSuccess) r = api.Broadcast(lambda_k, lambda_k, (size_t)p->chi[1], ncclFloat64, 0, comm->comm, s);
+    if (r == ncclSuccess) r = api.Broadcast(lambda_l, lambda_l, (size_t)p->chi[0], ncclFloat64, 0, comm->comm, s);
+    if (r == ncclSuccess) r = api.Broadcast(lambda_r, lambda_r, (size_t)p->chi[2], ncclFloat64, 0, comm->comm, s);
+    if (r == ncclSuccess) r = api.Broadcast(U, U, (size_t)(2 * p->u_size), ncclFloat64, 0, comm->comm, s);
+    ncclResult_t r2 = api.GroupEnd();
+    st = nccl_check(r != ncclSuccess ? r : r2, "operand broadcast");
+    if (st != TN_OK) return st;
+  }
+  // Local slabs: on the gathering root the caller passed FULL sectors, so its slab starts at row
+  // (lrow0 − row0) of each sector.
+  const bool root_full = gather_mode == TN_GATHER_ROOT && p->rank == 0;
+  std::vector<double*> local(p->N + 1, nullptr);
+  for (int c = 0; c <= p->N; ++c) {
+    double* base = theta_out[c];
+    if (root_full && base) base += 2 * (p->lrow0[c] - p->row0[c]) * p->C[c];
+    local[c] = base;
+  }
+  st = tn_theta_exec(p, stream, gamma_k, lambda_k, gamma_k1, lambda_l, lambda_r, U, local.data());
+  if (st != TN_OK || gather_mode == TN_GATHER_NONE || p->world == 1) return st;
+  st = nccl_check(api.GroupStart(), "ncclGroupStart");
+  if (st != TN_OK) return st;
+  ncclResult_t r = ncclSuccess;
+  for (int c = 0; c <= p->N && r == ncclSuccess; ++c) {
+    const int64_t a0 = p->row0[c], a1 = a0 + p->R[c], C = p->C[c];
+    if (p->rank == 0) {
+      for (int src = 1; src < p->world && r == ncclSuccess; ++src) {
+        const int64_t s0 = std::min(std::max(a0, p->bounds[src]), a1);
+        const int64_t s1 = std::min(std::max(a0, p->bounds[src + 1]), a1);
+        if (s1 > s0 && C > 0)
+          r = api.Recv(theta_out[c] + 2 * (s0 - a0) * C, (size_t)(2 * (s1 - s0) * C), ncclFloat64, src, comm->comm, s);
+      }
+    } else if (p->lR[c] * C > 0) {
+      r = api.Send(theta_out[c], (size_t)(2 * p->lR[c] * C), ncclFloat64, 0, comm->comm, s);
+    }
+  }
+  ncclResult_t r2 = api.GroupEnd();
+  return nccl_check(r != ncclSuccess ? r : r2, "Θ gather to root");
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// Internal declarations shared by the kernels and the C-ABI glue of libtn_theta.so (product path).
+// Nothing here is shared with oracle/ (the two share no code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/tn_theta.h"
+
+namespace tn {
+
+// ---------------------------------------------------------------------------------------------
+// Tiling constants of the K4 contraction (DESIGN.md §4 "K4").
+//   CTA tile BM×BN complex outputs, 4 consumer warps in 2×2, each 32×32 = 4×4 DMMA.8x8x4 tiles.
+//   K is consumed in chunks of BK; the chunk is one cp.async.bulk (TMA 1-D) copy per operand.
+// ---------------------------------------------------------------------------------------------
+constexpr int BM = 64;
+constexpr int BN = 64;
+constexpr int BK = 16;
+constexpr int CHUNK = BM * BK;        // complex elements per full operand chunk (== BN * BK)
+constexpr int K4_STAGES = 3;
+constexpr int K4_CONSUMER_WARPS = 4;
+constexpr int K4_THREADS = (K4_CONSUMER_WARPS + 1) * 32;
+
+struct GroupDesc {          // one center charge c_c: P_{c_c} = A_{c_c} · B_{c_c}
+  int64_t a_off;            // complex offset of this group's A panel in the A workspace
+  int64_t b_off;            // complex offset of this group's B panel in the B workspace
+  int64_t row0;             // first sorted left position of the group's (local) rows
+  int64_t col0;             // first sorted right position of the group's columns
+  int64_t k0;               // first sorted center position of seg_c(c_c)
+  int32_t R, C, K, K4;      // local rows, cols, true K, K padded to a multiple of 4
+  int32_t cc;               // the center charge == the output sector written with P
+  int32_t nmt, nnt, pad;
+};
+
+struct TileDesc {
+  int32_t g, mt, nt, pad;
+};
+
+constexpr int MAXC = TN_MAX_N + 1;
+
+// Per-sector tables passed BY VALUE as a kernel parameter (no device copy needed).
+struct SectorParams {
+  double2* out[MAXC];       // this rank's slab of Θ(c) (row-major, ld = C_c)
+  int64_t lrow0[MAXC];      // sorted left position of slab row 0
+  int64_t col0[MAXC];       // sorted right position of column 0
+  int32_t ld[MAXC];         // C_c
+  int32_t ustart[MAXC];     // packed-U block offsets
+  int32_t d, N;
+  uint32_t cc_mask[4];      // bit c_c set iff seg_c(c_c) is non-empty (a group exists)
+};
+
+}  // namespace tn
+
+struct tn_plan {
+  int d = 0, N = 0, world = 1, rank = 0;
+  int64_t chi[3] = {0, 0, 0};
+  std::vector<int32_t> off[3];                 // host copies of the offset tables (N+2)
+  int32_t* d_perm[3] = {nullptr, nullptr, nullptr};  // device perm (sorted pos -> caller index)
+  int32_t* d_qs[3] = {nullptr, nullptr, nullptr};    // device sorted charges
+  int32_t* d_off[3] = {nullptr, nullptr, nullptr};   // device offset tables (N+2)
+  std::vector<int64_t> bounds;                 // world+1 shard bounds (sorted left positions)
+  int64_t r0 = 0, r1 = 0;                      // this rank's window
+  // sectors
+  std::vector<int64_t> R, C, row0, col0, lR, lrow0;   // global + local slab
+  // groups / tiles
+  std::vector<tn::GroupDesc> groups;
+  tn::GroupDesc* d_groups = nullptr;
+  tn::TileDesc* d_tiles = nullptr;
+  int64_t ntiles = 0;
+  double2* d_apanel = nullptr;
+  double2* d_bpanel = nullptr;
+  int64_t a_elems = 0, b_elems = 0;
+  int64_t u_size = 0;
+  std::vector<int32_t> ustart;
+  int64_t f_contract = 0, f_mix = 0, f_exec = 0;
+  int64_t ws_bytes = 0;
+  int max_mix = 0;                             // min(N+1, d): longest U-mix vector
+  int sm_count = 148;
+  cudaStream_t plan_stream = nullptr;
+};
+
+namespace tn {
+
+void set_error(const std::string& s);
+tn_status fail(tn_status st, const std::string& s);
+tn_status cuda_check(cudaError_t e, const char* what);
+
+// ---- kernel launchers (stream-ordered) ----
+cudaError_t launch_sort_bonds(const int32_t* q, int64_t chi, int N, int32_t* perm, int32_t* qs,
+                              int32_t* off, int32_t* err, cudaStream_t s);
+cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const int32_t* ustart_host,
+                              double2* U, cudaStream_t s);
+cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
+                         cudaStream_t s);
+cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
+cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
+                       const double2* U, cudaStream_t s, const int32_t* d_offr);
+
+// ---- double-double arithmetic (K2): error-free transforms, ~106-bit significand ----
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd dd_from(double a) { return {a, 0.0}; }
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = a + b;
+  double bb = s - a;
+  double e = (a - (s - bb)) + (b - bb);
+  return {s, e};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b) {
+  double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  double p = a * b;
+  return {p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd x, dd y) {
+  dd s = two_sum(x.hi, y.hi);
+  dd t = two_sum(x.lo, y.lo);
+  s.lo += t.hi;
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo += t.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_neg(dd x) { return {-x.hi, -x.lo}; }
+__device__ __forceinline__ dd dd_mul(dd x, dd y) {
+  dd p = two_prod(x.hi, y.hi);
+  p.lo = __fma_rn(x.hi, y.lo, p.lo);
+  p.lo = __fma_rn(x.lo, y.hi, p.lo);
+  return quick_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_div(dd x, dd y) {
+  double q1 = x.hi / y.hi;
+  dd r = dd_add(x, dd_neg(dd_mul(dd_from(q1), y)));
+  double q2 = r.hi / y.hi;
+  r = dd_add(r, dd_neg(dd_mul(dd_from(q2), y)));
+  double q3 = r.hi / y.hi;
+  dd q = quick_two_sum(q1, q2);
+  return dd_add(q, dd_from(q3));
+}
+__device__ __forceinline__ dd dd_sqrt(dd x) {
+  if (x.hi <= 0.0) return {0.0, 0.0};
+  double a = sqrt(x.hi);
+  dd r = dd_add(x, dd_neg(two_prod(a, a)));
+  return quick_two_sum(a, r.hi / (2.0 * a));
+}
+
+}  // namespace tn

@@ -20,7 +20,7 @@ from dataclasses import dataclass, field, replace
 
 import numpy as np
 
-__all__ = ["Case", "CONFIGS", "make_config", "make_case", "shuffle_case", "flat_lambda"]
+__all__ = ["Case", "CONFIGS", "make_config", "make_case", "make_charges", "shuffle_case", "flat_lambda"]
 
 
 @dataclass
@@ -114,6 +114,17 @@ def make_case(N: int, d: int, chi_l: int, chi_c: int, chi_r: int, seed, *, charg
         phi = float(rng.uniform(0.0, 2 * math.pi))
     return Case(name, N, d, q_l, q_c, q_r, gk, gk1, lam_l, lam_k, lam_r, float(theta), float(phi),
                 meta=dict(seed=seed if isinstance(seed, int) else list(seed), charges=charges, lam=lam))
+
+
+def make_charges(cfg: int, gate: int = 0, shuffled: bool = False):
+    """Only step 1 of make_config (identical draws): (N, d, q_l, q_c, q_r) without building Γ."""
+    c = CONFIGS[cfg]
+    rng = np.random.default_rng([4, gate] if cfg == 4 else c["seed"])
+    qs = [_charges(rng, c["charges"], c["N"], c["chi"]) for _ in range(3)]
+    if shuffled:
+        rng2 = np.random.default_rng(c["seed"] + 1000)
+        qs = [np.ascontiguousarray(q[rng2.permutation(c["chi"])]) for q in qs]
+    return c["N"], c["d"], qs[0], qs[1], qs[2]
 
 
 def make_config(cfg: int, gate: int = 0, *, shuffled: bool = False, flat: bool = False) -> Case:
