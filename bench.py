@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark of the Θ(c) hot path (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl tn|reference]
+  (N > 1: launched by torchrun, one rank per GPU; Θ rows are sharded flop-balanced across ranks)
+
+One STEP = one gate = every row of SURVEY.md §8(a): tn_theta_plan (K1 bond sort + work decomposition)
+→ tn_build_bs_unitary (K2) → tn_theta_exec (K3 staging → K4 DMMA contraction → K5 U-mix). Inputs
+(Γk, Γk1 268 MB each, Θ 1.28 GB at config 3) are resident in HBM and larger than the 126 MB L2.
+`value` = useful complex-FP64 GFLOP/s of the whole gate (F_contract + F_mix) over the
+max-over-ranks device time. `e2e` = the same metric through the same public calls with HOST buffers
+(pinned H2D of Γ/λ/charges and D2H of every Θ(c) inside the timed region). `--impl reference` times the
+CPU oracle (oracle/, the literal triple charge loop of PAPER.md:72) on host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Θ-build useful complex FP64 GFLOP/s & gates/s at d=32,χ=4096; % FP64 TC peak"
+FP64_TC_PEAK_TFLOPS = 37.2   # measured: DMMA.8x8x4 loop, 148 SMs @ 1965 MHz (profiles/r01_fp64_peaks.jsonl)
+LAUNCHES_PER_STEP = 6        # K1 (1 launch, 3 CTAs), K2, K3a, K3b, K4, K5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="tn", choices=["tn", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sectors", default="0,6,12,18,24,30")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------------------------- helpers
+def sector_useful_flops(N, d, nl, nc, nr):
+    """F_useful split by output sector c: contraction of P_c (group c_c = c) plus the
+    mix into Θ(c). Σ_c equals F_contract + F_mix exactly (bookkeeping only)."""
+    out = []
+    for c in range(N + 1):
+        f = 0
+        if nc[c]:
+            for cl in range(c, min(N, c + d - 1) + 1):
+                for cr in range(max(0, c - d + 1), c + 1):
+                    f += 8 * nl[cl] * nc[c] * nr[cr]
+        for cl in range(c, min(N, c + d - 1) + 1):
+            for cr in range(max(0, c - d + 1), c + 1):
+                ncc = sum(1 for x in range(max(cr, cl - d + 1), min(cl, cr + d - 1) + 1) if nc[x])
+                f += 8 * nl[cl] * nr[cr] * ncc
+        out.append(f)
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if r.returncode == 0 and r.stdout.strip():
+                    self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max(float(r[2]) for r in self.rows) if self.rows else None}
+
+
+def ncu_traffic(cfg):
+    """dram bytes per K4 launch from the committed `ncu --set full` capture, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_k4_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get(f"config{cfg}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+_UB_CACHE = {}
+
+
+def cpu_oracle_run(case, sectors):
+    """Time the oracle (as it stands) on the given sectors of `case`; returns (seconds, flops)."""
+    import numpy as np
+    import oracle
+    nq = case.N + 1
+    nl, nc, nr = (np.bincount(q, minlength=nq).tolist() for q in (case.q_l, case.q_c, case.q_r))
+    per = sector_useful_flops(case.N, case.d, nl, nc, nr)
+    key = (case.theta, case.phi, case.d, case.N)
+    if key not in _UB_CACHE:
+        _UB_CACHE[key] = [oracle.bs_unitary_block(n, case.theta, case.phi, case.d)
+                          for n in range(min(case.N, 2 * case.d - 2) + 1)]
+    ub = _UB_CACHE[key]
+    t0 = time.perf_counter()
+    oracle.theta_sectors(case.N, case.d, case.q_l, case.q_c, case.q_r, case.gamma_k, case.lam_k, case.gamma_k1,
+                         case.lam_l, case.lam_r, case.theta, case.phi, u_blocks=ub, sectors=sectors)
+    dt = time.perf_counter() - t0
+    return dt, sum(per[c] for c in sectors)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# --------------------------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import synth
+    case = synth.make_config(args.config)
+    nq = case.N + 1
+    order = [(7 * i + 3) % nq for i in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        cpu_oracle_run(case, [order[i]])
+    tot_t, tot_f = 0.0, 0
+    for i in range(args.steps):
+        dt, f = cpu_oracle_run(case, [order[args.warmup + i]])
+        tot_t += dt
+        tot_f += f
+    value = tot_f / tot_t / 1e9
+    ms = tot_t / args.steps * 1e3
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(case, args.config),
+            "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": host_cores(), "kind": "oracle",
+                             "sample": f"one Θ(c) sector per step (c = (7i+3) mod {nq}) of config {args.config}, "
+                                       "useful flops of that sector / oracle wall time; U prebuilt (mpmath)"},
+            "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(case, cfg):
+    return {"workload": f"BASELINE.json config {cfg}: single gate N={case.N}, d={case.d}, chi={case.chi_l} on all "
+                        f"three bonds, {case.meta.get('charges')} charges, {case.meta.get('lam')} lambda, seed "
+                        f"{case.meta.get('seed')}",
+            "N": case.N, "d": case.d, "chi": case.chi_l, "theta": case.theta, "phi": case.phi,
+            "l2": "inputs larger than L2 (Γk, Γk1 268 MB each at config 3; Θ 1.28 GB; staging 0.3 GB)"}
+
+
+# --------------------------------------------------------------------------------------------- our arm
+def run_tn(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_12814_b200 as tn
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    case = synth.make_config(args.config)
+    nq = case.N + 1
+    h = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+    gk, gk1 = h(case.gamma_k).to(dev), h(case.gamma_k1).to(dev)
+    lk, ll, lr = h(case.lam_k).to(dev), h(case.lam_l).to(dev), h(case.lam_r).to(dev)
+    ql, qc, qr = (h(q).to(dev) for q in (case.q_l, case.q_c, case.q_r))
+
+    probe = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)
+    flops = probe.flops()
+    f_useful = flops["f_contract"] + flops["f_mix"]
+    outs = tn.alloc_theta(probe, device=dev)
+    U = torch.empty(probe.u_size(), dtype=torch.complex128, device=dev)
+    del probe
+    stream = torch.cuda.current_stream(dev)
+
+    def step(keep):
+        plan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)          # K1 + decomposition
+        tn.build_bs_unitary(plan, case.theta, case.phi, out=U)            # K2
+        tn.theta_exec(plan, gk, lk, gk1, ll, lr, U, out=outs)            # K3 → K4 → K5
+        keep.append(plan)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    keep = []
+    for _ in range(args.warmup):
+        step(keep)
+    torch.cuda.synchronize()
+    keep.clear()
+
+    # timed region: K steps, per-kernel times read from plans two steps behind (already complete)
+    ktimes = {k: [] for k in ("k1_sort", "k2_unitary", "k3_stage", "k4_contract", "k5_mix")}
+
+    def harvest(plan):
+        for k, v in plan.kernel_times().items():
+            ktimes[k].append(v)
+        plan.destroy()
+
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(keep)
+            if len(keep) > 2:
+                harvest(keep.pop(0))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    for p in keep:
+        harvest(p)
+    keep.clear()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = f_useful / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers (pinned H2D + Θ D2H inside the region)
+    pin = lambda a: h(a).pin_memory()
+    host_in = dict(gk=pin(case.gamma_k), gk1=pin(case.gamma_k1), lk=pin(case.lam_k), ll=pin(case.lam_l),
+                   lr=pin(case.lam_r))
+    host_q = [np.ascontiguousarray(q) for q in (case.q_l, case.q_c, case.q_r)]
+    host_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+    d_in = {k: torch.empty_like(v, device=dev) for k, v in host_in.items()}
+    h2d = sum(v.numel() * v.element_size() for v in host_in.values()) + sum(q.nbytes for q in host_q)
+    d2h = sum(o.numel() * o.element_size() for o in host_out)
+
+    def e2e_step():
+        for k, v in host_in.items():
+            d_in[k].copy_(v, non_blocking=True)
+        plan = tn.Plan(case.d, case.N, *host_q, world, rank)              # host charges → H2D inside
+        tn.build_bs_unitary(plan, case.theta, case.phi, out=U)
+        tn.theta_exec(plan, d_in["gk"], d_in["lk"], d_in["gk1"], d_in["ll"], d_in["lr"], U, out=outs)
+        for o, ho in zip(outs, host_out):
+            ho.copy_(o, non_blocking=True)
+        return plan
+
+    p = e2e_step()
+    torch.cuda.synchronize()
+    p.destroy()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    prev = None
+    for _ in range(args.e2e_steps):
+        p = e2e_step()
+        if prev is not None:
+            prev.destroy()
+        prev = p
+    f1.record(stream)
+    torch.cuda.synchronize()
+    prev.destroy()
+    e2e_ms = f0.elapsed_time(f1)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_step_ms = float(te.item()) / args.e2e_steps
+    e2e_value = f_useful / (e2e_step_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        return
+    kmean = {k: (statistics.mean(v) if v else None) for k, v in ktimes.items()}
+    k4_ms = kmean["k4_contract"]
+    achieved = flops["f_contract_local"] / (k4_ms * 1e-3) / 1e12
+    step_kernel_ms = sum(v for v in kmean.values() if v is not None)
+    kernels = {k: {"ms": round(v, 4), "share_of_step": round(v / ms_step, 4)} for k, v in kmean.items()}
+    kernels["k5_mix"]["hbm_gbs"] = round(2 * 16 * sum(o.numel() for o in outs) / (kmean["k5_mix"] * 1e-3) / 1e9, 1)
+    kernels["k4_contract"]["useful_tflops"] = round(achieved, 3)
+    kernels["k4_contract"]["executed_tflops"] = round(flops["f_exec"] / (k4_ms * 1e-3) / 1e12, 3)
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        secs = [int(x) for x in args.cpu_sectors.split(",") if x.strip() != "" and int(x) <= case.N]
+        dt, f = cpu_oracle_run(case, secs)
+        cpu = {"value": round(f / dt / 1e9, 4), "unit": "GFLOP/s", "cores": host_cores(), "kind": "oracle",
+               "sample": f"sectors {secs} of config {args.config} (oracle triple charge loop, numpy/OpenBLAS "
+                         f"threads = host cores), useful flops of those sectors {f / 1e9:.2f} GFLOP in {dt:.1f} s; "
+                         "U prebuilt with mpmath (not timed)"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator synth/, BASELINE.json config recipe)",
+        "gates_per_s": round(1000.0 / ms_step, 3),
+        "pct_fp64_tc_peak": round(100.0 * value / (FP64_TC_PEAK_TFLOPS * 1e3 * world), 2),
+        "config": dict(workload_config(case, args.config), parallelism=f"rows{world}" if world > 1 else "single",
+                       f_contract=flops["f_contract"], f_mix=flops["f_mix"], f_exec_rank0=flops["f_exec"],
+                       step="tn_theta_plan + tn_build_bs_unitary + tn_theta_exec (all SURVEY §8(a) rows)"),
+        "roofline": {"bound": "tensor", "kernel": "k4_contract", "achieved": round(achieved, 3),
+                     "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_TC_PEAK_TFLOPS, 4),
+                     "traffic": ncu_traffic(args.config),
+                     "peak_source": "measured FP64 DMMA.8x8x4 rate (profiles/r01_fp64_peaks.jsonl; "
+                                    "MEASURED_PEAKS.json has no FP64 entry)",
+                     "achieved_def": "F_contract of this rank (useful complex FP64 flops, 8/CMAC) / mean K4 "
+                                     "launch time (CUDA events on the exec stream, timed region)"},
+        "kernels": kernels,
+        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step_ms, 3)},
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_tn(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

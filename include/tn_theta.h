@@ -97,14 +97,23 @@ TN_API tn_status tn_plan_perm(const tn_plan* plan, int bond, int32_t* host_out);
 TN_API tn_status tn_plan_offsets(const tn_plan* plan, int bond, int32_t* host_out);
 /* Sorted-left-position shard [r0, r1) of rank r (any r in [0, world_size)). */
 TN_API tn_status tn_plan_shard_rows(const tn_plan* plan, int r, int64_t* r0, int64_t* r1);
-/* Useful work of the WHOLE problem: 8 flops per complex MAC.
- *   f_contract = 8 Σ_{allowed (c_l,c_c,c_r)} n_l n_c n_r,  f_mix = 8 Σ n_l n_r #c #c_c,
- *   f_exec     = complex DMMA flops this rank's kernels execute incl. tile padding (8/CMAC). */
-TN_API tn_status tn_plan_flops(const tn_plan* plan, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec);
+/* Useful work, 8 flops per complex MAC; any output pointer may be NULL.
+ *   f_contract = 8 Σ_{allowed (c_l,c_c,c_r)} n_l n_c n_r  (whole problem),
+ *   f_mix      = 8 Σ_{(c_l,c_r)} n_l n_r #c #c_c           (whole problem),
+ *   f_exec     = complex DMMA flops this rank's K4 executes incl. tile padding (8 per CMAC),
+ *   f_contract_local, f_mix_local = this rank's share (its rows [r0, r1)). */
+TN_API tn_status tn_plan_flops(const tn_plan* plan, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec,
+                               int64_t* f_contract_local, int64_t* f_mix_local);
 /* Number of complex entries of the packed U for this (d, N). */
 TN_API tn_status tn_plan_u_size(const tn_plan* plan, int64_t* n_entries);
 /* Device bytes the plan owns (tables + staging workspace). */
 TN_API tn_status tn_plan_workspace_bytes(const tn_plan* plan, int64_t* bytes);
+
+/* Per-kernel device times (CUDA events recorded on the launching streams) of the most recent
+ * calls made with this plan: ms[0] K1 bond sort (inside tn_theta_plan), ms[1] K2 U build,
+ * ms[2] K3 staging, ms[3] K4 contraction, ms[4] K5 U-mix. Waits for those events. Entries for
+ * calls not yet made are −1. */
+TN_API tn_status tn_plan_kernel_times(const tn_plan* plan, float* ms5);
 
 /* ------------------------------------------------------------------------------------------ */
 /* U builder (K2) — Eq. S4, "O(d^4) for initializing U".        */
@@ -171,6 +180,13 @@ TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn
  * bounds[world_size]=χ_l. Errors: TN_ERR_DOMAIN. */
 TN_API tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_c,
                              const int64_t* n_r, int world_size, int64_t* bounds);
+
+TN_API /* Device memory: plan tables and staging workspace come from a library-owned pool. A destroyed
+ * plan's blocks are reused by later plans once the work last enqueued with them has completed
+ * (an event recorded on the last exec stream), so per-gate planning does not call cudaMalloc.
+ * tn_release_cached_memory frees every idle block (waiting for its event) and reports the bytes
+ * freed; *cached (may be NULL) receives the bytes still held by live plans. */
+TN_API tn_status tn_release_cached_memory(int64_t* freed, int64_t* cached);
 
 TN_API const char* tn_status_string(tn_status s);
 TN_API const char* tn_last_error(void);       /* thread-local detail of the last failure ("" if none) */

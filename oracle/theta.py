@@ -111,13 +111,14 @@ def _u_lookup(blocks, d, n, i, j):
 
 
 def theta_sectors(N, d, q_l, q_c, q_r, gamma_k, lam_k, gamma_k1, lam_l, lam_r, theta, phi,
-                  u_blocks=None):
+                  u_blocks=None, sectors=None):
     """Θ(c) for c = 0..N, literally as PAPER.md:72 describes.
 
     'looping through all possible left, center and right charges c_l, c_c, c_r … choose the correct
     entry of U, which takes care of the sum over the j indices, and the rest of the contraction is
     only over α_k.' Rows/cols of Θ(c) are in sorted bond order (R2); returns
-    (sectors, perms, offs, u_blocks) with sectors[c] a complex128[R_c, C_c] array.
+    (sectors, perms, offs, u_blocks) with sectors[c] a complex128[R_c, C_c] array. If `sectors` (an
+    iterable of c) is given only those are computed (others are None) — a bounded sample for timing.
     """
     perm_l, off_l = sort_bonds(q_l, N)
     perm_c, off_c = sort_bonds(q_c, N)
@@ -133,8 +134,12 @@ def theta_sectors(N, d, q_l, q_c, q_r, gamma_k, lam_k, gamma_k1, lam_l, lam_r, t
     def seg(off, q):
         return slice(int(off[q]), int(off[q + 1]))
 
+    wanted = set(range(N + 1)) if sectors is None else set(int(c) for c in sectors)
     sectors = []
     for c in range(N + 1):
+        if c not in wanted:
+            sectors.append(None)
+            continue
         (r0, r1), (k0, k1) = sector_ranges(off_l, off_r, N, d, c)
         th = np.zeros((r1 - r0, k1 - k0), dtype=np.complex128)
         for c_l in range(c, min(N, c + d - 1) + 1):              # i_k = c_l − c

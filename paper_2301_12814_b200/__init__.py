@@ -19,7 +19,7 @@ from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN
                    TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, LIB_PATH)
 
 __all__ = ["Plan", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
-           "shard_rows_host", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
+           "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
 
 
 def _stream_ptr(stream) -> C.c_void_p:
@@ -109,14 +109,20 @@ class Plan:
         return a.value, b.value
 
     def flops(self):
-        fc, fm, fe = C.c_int64(), C.c_int64(), C.c_int64()
-        check(lib.tn_plan_flops(self.handle, C.byref(fc), C.byref(fm), C.byref(fe)), "tn_plan_flops")
-        return {"f_contract": fc.value, "f_mix": fm.value, "f_exec": fe.value}
+        v = [C.c_int64() for _ in range(5)]
+        check(lib.tn_plan_flops(self.handle, *(C.byref(x) for x in v)), "tn_plan_flops")
+        return dict(zip(("f_contract", "f_mix", "f_exec", "f_contract_local", "f_mix_local"), (x.value for x in v)))
 
     def u_size(self) -> int:
         n = C.c_int64()
         check(lib.tn_plan_u_size(self.handle, C.byref(n)), "tn_plan_u_size")
         return n.value
+
+    def kernel_times(self):
+        """Device ms of the most recent K1 (plan), K2, K3, K4, K5 launched with this plan (−1: not run)."""
+        ms = np.empty(5, dtype=np.float32)
+        check(lib.tn_plan_kernel_times(self.handle, _ptr(ms)), "tn_plan_kernel_times")
+        return dict(zip(("k1_sort", "k2_unitary", "k3_stage", "k4_contract", "k5_mix"), ms.tolist()))
 
     def workspace_bytes(self) -> int:
         n = C.c_int64()
@@ -215,6 +221,13 @@ def theta_exec_sharded(plan: Plan, comm: Comm, gk, lk, gk1, ll, lr, U, out=None,
                                     _ptr(ll), _ptr(lr), _ptr(U), ptrs, int(bool(bcast_operands)), int(gather_mode)),
           "tn_theta_exec_sharded")
     return out
+
+
+def release_cached_memory():
+    """tn_release_cached_memory → (bytes freed, bytes still held by live plans)."""
+    f, c = C.c_int64(), C.c_int64()
+    check(lib.tn_release_cached_memory(C.byref(f), C.byref(c)), "tn_release_cached_memory")
+    return f.value, c.value
 
 
 def shard_rows_host(d: int, N: int, n_l, n_c, n_r, world_size: int) -> np.ndarray:

@@ -34,9 +34,11 @@ SIGNATURES = {
     "tn_plan_perm": [_p, C.c_int, _p],
     "tn_plan_offsets": [_p, C.c_int, _p],
     "tn_plan_shard_rows": [_p, C.c_int, _i64p, _i64p],
-    "tn_plan_flops": [_p, _i64p, _i64p, _i64p],
+    "tn_plan_flops": [_p, _i64p, _i64p, _i64p, _i64p, _i64p],
     "tn_plan_u_size": [_p, _i64p],
     "tn_plan_workspace_bytes": [_p, _i64p],
+    "tn_plan_kernel_times": [_p, _p],
+    "tn_release_cached_memory": [_i64p, _i64p],
     "tn_build_bs_unitary": [_p, C.c_double, C.c_double, _p, _p],
     "tn_theta_exec": [_p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
     "tn_comm_unique_id": [_p],

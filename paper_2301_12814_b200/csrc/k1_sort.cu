@@ -12,11 +12,14 @@ namespace tn {
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
-__global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const int32_t* __restrict__ q, int64_t chi,
-                                                              int N, int32_t* __restrict__ perm,
-                                                              int32_t* __restrict__ qs,
-                                                              int32_t* __restrict__ off,
-                                                              int32_t* __restrict__ err) {
+__global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs args, int N) {
+  const int bond = blockIdx.x;
+  const int32_t* __restrict__ q = args.q[bond];
+  const int64_t chi = args.chi[bond];
+  int32_t* __restrict__ perm = args.perm[bond];
+  int32_t* __restrict__ qs = args.qs[bond];
+  int32_t* __restrict__ off = args.off[bond];
+  int32_t* __restrict__ err = args.err + bond;
   __shared__ int32_t hist[MAXC + 1];
   __shared__ int32_t base[MAXC + 1];
   __shared__ int32_t wcnt[SORT_WARPS][MAXC];
@@ -76,9 +79,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const int32_t* __r
   }
 }
 
-cudaError_t launch_sort_bonds(const int32_t* q, int64_t chi, int N, int32_t* perm, int32_t* qs, int32_t* off,
-                              int32_t* err, cudaStream_t s) {
-  k1_sort_bonds<<<1, SORT_THREADS, 0, s>>>(q, chi, N, perm, qs, off, err);
+cudaError_t launch_sort_bonds(const SortArgs& a, int N, cudaStream_t s) {
+  k1_sort_bonds<<<3, SORT_THREADS, 0, s>>>(a, N);
   return cudaGetLastError();
 }
 

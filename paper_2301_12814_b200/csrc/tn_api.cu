@@ -36,8 +36,9 @@ struct Counts {
   std::vector<int64_t> nl, nc, nr;
 };
 
-// Useful flops of one left row of charge c_l (contraction + mix), 8 per complex MAC.
-static double row_cost(const Counts& k, int c_l) {
+// Useful flops of one left row of charge c_l, 8 per complex MAC: contraction part (*fc) and
+// U-mix part (*fm); returns their sum.
+static double row_cost(const Counts& k, int c_l, double* fc = nullptr, double* fm = nullptr) {
   const int d = k.d, N = k.N;
   double f = 0.0;
   for (int cc = std::max(0, c_l - d + 1); cc <= c_l; ++cc) {      // j_k = c_l − c_c ∈ [0, d−1]
@@ -46,6 +47,8 @@ static double row_cost(const Counts& k, int c_l) {
     for (int cr = std::max(0, cc - d + 1); cr <= cc; ++cr) cols += k.nr[cr];
     f += 8.0 * (double)k.nc[cc] * (double)cols;
   }
+  if (fc) *fc = f;
+  const double f_con = f;
   for (int cr = std::max(0, c_l - 2 * d + 2); cr <= std::min(N, c_l); ++cr) {
     int nvc = 0, nvcc = 0;
     for (int c = cr; c <= c_l; ++c)
@@ -55,6 +58,7 @@ static double row_cost(const Counts& k, int c_l) {
       }
     f += 8.0 * (double)k.nr[cr] * nvc * nvcc;
   }
+  if (fm) *fm = f - f_con;
   return f;
 }
 
@@ -85,18 +89,25 @@ static void shard_bounds(const Counts& k, int world, std::vector<int64_t>& bound
 
 static void free_plan(tn_plan* p) {
   if (!p) return;
-  for (int b = 0; b < 3; ++b) {
-    cudaFree(p->d_perm[b]);
-    cudaFree(p->d_qs[b]);
-    cudaFree(p->d_off[b]);
-  }
-  cudaFree(p->d_groups);
-  cudaFree(p->d_tiles);
-  cudaFree(p->d_apanel);
-  cudaFree(p->d_bpanel);
+  const bool used = p->rec_exec;
+  pool_release(p->blk_work, p->last_stream, used);
+  pool_release(p->blk_tab, p->last_stream, used);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
   if (p->plan_stream) cudaStreamDestroy(p->plan_stream);
   delete p;
 }
+
+// Carves 256-byte aligned sub-buffers out of one pool block.
+struct Carver {
+  size_t off = 0;
+  template <class T>
+  size_t take(int64_t n) {
+    const size_t at = off;
+    off += ((size_t)n * sizeof(T) + 255) / 256 * 256;
+    return at;
+  }
+};
 
 static bool is_device_ptr(const void* ptr) {
   cudaPointerAttributes a;
@@ -190,9 +201,13 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   p->max_mix = std::min(N + 1, d);
   tn_status st = TN_OK;
   int dev = 0;
-  int32_t* d_err = nullptr;
   int32_t* d_q[3] = {nullptr, nullptr, nullptr};
   const int32_t* qs_in[3] = {q_l, q_c, q_r};
+  cudaError_t aerr = cudaSuccess;
+  Carver ct;
+  size_t o_perm[3], o_qs[3], o_off[3], o_err, o_q[3] = {0, 0, 0};
+  bool host_q[3];
+  int32_t* d_err = nullptr;
 #define TN_TRY(expr, what)                      \
   do {                                          \
     st = cuda_check((expr), what);              \
@@ -201,29 +216,55 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   TN_TRY(cudaGetDevice(&dev), "cudaGetDevice");
   TN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev), "sm count");
   TN_TRY(cudaStreamCreateWithFlags(&p->plan_stream, cudaStreamNonBlocking), "plan stream");
-  TN_TRY(cudaMalloc(&d_err, 3 * sizeof(int32_t)), "alloc err");
-  TN_TRY(cudaMemsetAsync(d_err, 0, 3 * sizeof(int32_t), p->plan_stream), "memset err");
-  // ---- K1: sort each bond by charge ----
+  for (auto& e : p->ev) TN_TRY(cudaEventCreate(&e), "event create");
+  // ---- one pool block for the bond tables (+ staging of host charges) ----
   for (int b = 0; b < 3; ++b) {
-    const int64_t chi = p->chi[b];
-    const int32_t* src = qs_in[b];
-    if (!is_device_ptr(src)) {
-      TN_TRY(cudaMalloc(&d_q[b], chi * sizeof(int32_t)), "alloc charges");
-      TN_TRY(cudaMemcpyAsync(d_q[b], src, chi * sizeof(int32_t), cudaMemcpyHostToDevice, p->plan_stream), "H2D charges");
-      src = d_q[b];
+    o_perm[b] = ct.take<int32_t>(p->chi[b]);
+    o_qs[b] = ct.take<int32_t>(p->chi[b]);
+    o_off[b] = ct.take<int32_t>(N + 2);
+    host_q[b] = !is_device_ptr(qs_in[b]);
+    if (host_q[b]) o_q[b] = ct.take<int32_t>(p->chi[b]);
+  }
+  o_err = ct.take<int32_t>(4);
+  p->blk_tab = pool_alloc(ct.off, &aerr);
+  TN_TRY(aerr, "pool alloc (bond tables)");
+  {
+    char* base = static_cast<char*>(p->blk_tab);
+    SortArgs sa{};
+    for (int b = 0; b < 3; ++b) {
+      p->d_perm[b] = reinterpret_cast<int32_t*>(base + o_perm[b]);
+      p->d_qs[b] = reinterpret_cast<int32_t*>(base + o_qs[b]);
+      p->d_off[b] = reinterpret_cast<int32_t*>(base + o_off[b]);
+      const int32_t* src = qs_in[b];
+      if (host_q[b]) {
+        d_q[b] = reinterpret_cast<int32_t*>(base + o_q[b]);
+        TN_TRY(cudaMemcpyAsync(d_q[b], src, p->chi[b] * sizeof(int32_t), cudaMemcpyHostToDevice, p->plan_stream),
+               "H2D charges");
+        src = d_q[b];
+      }
+      sa.q[b] = src;
+      sa.chi[b] = p->chi[b];
+      sa.perm[b] = p->d_perm[b];
+      sa.qs[b] = p->d_qs[b];
+      sa.off[b] = p->d_off[b];
     }
-    TN_TRY(cudaMalloc(&p->d_perm[b], chi * sizeof(int32_t)), "alloc perm");
-    TN_TRY(cudaMalloc(&p->d_qs[b], chi * sizeof(int32_t)), "alloc qs");
-    TN_TRY(cudaMalloc(&p->d_off[b], (N + 2) * sizeof(int32_t)), "alloc off");
-    TN_TRY(launch_sort_bonds(src, chi, N, p->d_perm[b], p->d_qs[b], p->d_off[b], d_err + b, p->plan_stream), "K1 launch");
+    d_err = reinterpret_cast<int32_t*>(base + o_err);
+    sa.err = d_err;
+    // ---- K1: sort each bond by charge (one launch, one CTA per bond) ----
+    TN_TRY(cudaMemsetAsync(d_err, 0, 4 * sizeof(int32_t), p->plan_stream), "memset err");
+    TN_TRY(cudaEventRecord(p->ev[0], p->plan_stream), "event");
+    TN_TRY(launch_sort_bonds(sa, N, p->plan_stream), "K1 launch");
+    TN_TRY(cudaEventRecord(p->ev[1], p->plan_stream), "event");
+    p->rec_k1 = true;
   }
   {
-    int32_t herr[3];
+    // one D2H of off[3] + err: the tables are contiguous with padding, copy each
+    int32_t herr[4] = {0, 0, 0, 0};
     for (int b = 0; b < 3; ++b) p->off[b].resize(N + 2);
-    TN_TRY(cudaMemcpyAsync(herr, d_err, sizeof(herr), cudaMemcpyDeviceToHost, p->plan_stream), "D2H err");
     for (int b = 0; b < 3; ++b)
       TN_TRY(cudaMemcpyAsync(p->off[b].data(), p->d_off[b], (N + 2) * sizeof(int32_t), cudaMemcpyDeviceToHost,
                              p->plan_stream), "D2H off");
+    TN_TRY(cudaMemcpyAsync(herr, d_err, sizeof(herr), cudaMemcpyDeviceToHost, p->plan_stream), "D2H err");
     TN_TRY(cudaStreamSynchronize(p->plan_stream), "K1 sync");
     if (herr[0] || herr[1] || herr[2]) {
       st = fail(TN_ERR_DOMAIN, "tn_theta_plan: a bond charge lies outside [0, N]");
@@ -244,6 +285,19 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
     shard_bounds(k, world_size, p->bounds);
     p->r0 = p->bounds[rank];
     p->r1 = p->bounds[rank + 1];
+    {  // this rank's share of the useful work (rows [r0, r1))
+      double lc = 0.0, lm = 0.0;
+      for (int q = 0; q <= N; ++q) {
+        const int64_t a = std::max<int64_t>(ol[q], p->r0), b = std::min<int64_t>(ol[q + 1], p->r1);
+        if (b <= a) continue;
+        double fc = 0.0, fm = 0.0;
+        row_cost(k, q, &fc, &fm);
+        lc += fc * (double)(b - a);
+        lm += fm * (double)(b - a);
+      }
+      p->f_contract_local = (int64_t)llround(lc);
+      p->f_mix_local = (int64_t)llround(lm);
+    }
     p->R.resize(N + 1);
     p->C.resize(N + 1);
     p->row0.resize(N + 1);
@@ -318,14 +372,26 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
     }
     p->ntiles = (int64_t)tiles.size();
     if (!p->groups.empty()) {
-      TN_TRY(cudaMalloc(&p->d_groups, p->groups.size() * sizeof(GroupDesc)), "alloc groups");
-      TN_TRY(cudaMemcpy(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice),
-             "H2D groups");
-      TN_TRY(cudaMalloc(&p->d_tiles, tiles.size() * sizeof(TileDesc)), "alloc tiles");
-      TN_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice), "H2D tiles");
-      TN_TRY(cudaMalloc(&p->d_apanel, p->a_elems * sizeof(double2)), "alloc A panels");
-      TN_TRY(cudaMalloc(&p->d_bpanel, p->b_elems * sizeof(double2)), "alloc B panels");
+      Carver cw;
+      const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
+      const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
+      const size_t o_a = cw.take<double2>(p->a_elems);
+      const size_t o_b = cw.take<double2>(p->b_elems);
+      p->blk_work = pool_alloc(cw.off, &aerr);
+      TN_TRY(aerr, "pool alloc (workspace)");
+      char* base = static_cast<char*>(p->blk_work);
+      p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
+      p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
+      p->d_apanel = reinterpret_cast<double2*>(base + o_a);
+      p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
+      TN_TRY(cudaMemcpyAsync(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc),
+                             cudaMemcpyHostToDevice, p->plan_stream), "H2D groups");
+      TN_TRY(cudaMemcpyAsync(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice,
+                             p->plan_stream), "H2D tiles");
+      TN_TRY(cudaStreamSynchronize(p->plan_stream), "plan tables sync");
+      p->ws_bytes = (int64_t)cw.off;
     }
+    p->ws_bytes += (int64_t)ct.off;
     // ---- packed U layout ----
     const int nmax = std::min(N, 2 * d - 2);
     int64_t tot = 0;
@@ -335,14 +401,9 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
       tot += (int64_t)s * s;
     }
     p->u_size = tot;
-    p->ws_bytes = (p->a_elems + p->b_elems) * (int64_t)sizeof(double2) +
-                  (int64_t)(tiles.size() * sizeof(TileDesc) + p->groups.size() * sizeof(GroupDesc)) +
-                  (chi_l + chi_c + chi_r) * 8 + 3 * (N + 2) * 4;
   }
 done:
 #undef TN_TRY
-  for (int b = 0; b < 3; ++b) cudaFree(d_q[b]);
-  cudaFree(d_err);
   if (st != TN_OK) {
     free_plan(p);
     return st;
@@ -395,11 +456,14 @@ tn_status tn_plan_shard_rows(const tn_plan* p, int r, int64_t* r0, int64_t* r1) 
   return TN_OK;
 }
 
-tn_status tn_plan_flops(const tn_plan* p, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec) {
+tn_status tn_plan_flops(const tn_plan* p, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec,
+                        int64_t* f_contract_local, int64_t* f_mix_local) {
   if (!p) return fail(TN_ERR_DIMENSION, "tn_plan_flops: NULL");
   if (f_contract) *f_contract = p->f_contract;
   if (f_mix) *f_mix = p->f_mix;
   if (f_exec) *f_exec = p->f_exec;
+  if (f_contract_local) *f_contract_local = p->f_contract_local;
+  if (f_mix_local) *f_mix_local = p->f_mix_local;
   return TN_OK;
 }
 
@@ -415,14 +479,39 @@ tn_status tn_plan_workspace_bytes(const tn_plan* p, int64_t* bytes) {
   return TN_OK;
 }
 
+tn_status tn_plan_kernel_times(const tn_plan* p, float* ms) {
+  if (!p || !ms) return fail(TN_ERR_DIMENSION, "tn_plan_kernel_times: NULL");
+  for (int i = 0; i < 5; ++i) ms[i] = -1.0f;
+  auto span = [&](int a, int b, float* out) -> tn_status {
+    tn_status st = cuda_check(cudaEventSynchronize(p->ev[b]), "event sync");
+    if (st != TN_OK) return st;
+    return cuda_check(cudaEventElapsedTime(out, p->ev[a], p->ev[b]), "event elapsed");
+  };
+  tn_status st = TN_OK;
+  if (p->rec_k1 && (st = span(0, 1, &ms[0])) != TN_OK) return st;
+  if (p->rec_k2 && (st = span(2, 3, &ms[1])) != TN_OK) return st;
+  if (p->rec_exec) {
+    if ((st = span(4, 5, &ms[2])) != TN_OK) return st;
+    if ((st = span(5, 6, &ms[3])) != TN_OK) return st;
+    if ((st = span(6, 7, &ms[4])) != TN_OK) return st;
+  }
+  return TN_OK;
+}
+
 tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_stream stream, double* U_out) {
   if (!p || !U_out) return fail(TN_ERR_DIMENSION, "tn_build_bs_unitary: NULL");
   if (!std::isfinite(theta) || !std::isfinite(phi)) return fail(TN_ERR_DOMAIN, "tn_build_bs_unitary: non-finite angle");
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_build_bs_unitary");
-  return cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->ustart.data(), reinterpret_cast<double2*>(U_out),
-                                      (cudaStream_t)stream),
-                    "K2 launch");
+  cudaStream_t s = (cudaStream_t)stream;
+  tn_status st = cuda_check(cudaEventRecord(p->ev[2], s), "event");
+  if (st != TN_OK) return st;
+  st = cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->ustart.data(), reinterpret_cast<double2*>(U_out), s),
+                  "K2 launch");
+  if (st != TN_OK) return st;
+  st = cuda_check(cudaEventRecord(p->ev[3], s), "event");
+  p->rec_k2 = st == TN_OK;
+  return st;
 }
 
 tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
@@ -438,14 +527,22 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_theta_exec");
   cudaStream_t s = (cudaStream_t)stream;
   const SectorParams sp = make_sector_params(p, theta_out);
-  tn_status st = cuda_check(launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
-                                         reinterpret_cast<const double2*>(gamma_k1), s),
-                            "K3 launch");
+  p->last_stream = s;
+  p->rec_exec = true;  // the workspace is in use from here on (pool release fence)
+  tn_status st = cuda_check(cudaEventRecord(p->ev[4], s), "event");
   if (st != TN_OK) return st;
+  st = cuda_check(launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                               reinterpret_cast<const double2*>(gamma_k1), s),
+                  "K3 launch");
+  if (st != TN_OK) return st;
+  if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;
   st = cuda_check(launch_contract(p, sp, s), "K4 launch");
   if (st != TN_OK) return st;
-  return cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, p->d_off[2]),
-                    "K5 launch");
+  if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
+  st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, p->d_off[2]),
+                  "K5 launch");
+  if (st != TN_OK) return st;
+  return cuda_check(cudaEventRecord(p->ev[7], s), "event");
 }
 
 }  // extern "C"

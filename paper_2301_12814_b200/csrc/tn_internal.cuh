@@ -77,11 +77,17 @@ struct tn_plan {
   int64_t a_elems = 0, b_elems = 0;
   int64_t u_size = 0;
   std::vector<int32_t> ustart;
-  int64_t f_contract = 0, f_mix = 0, f_exec = 0;
+  int64_t f_contract = 0, f_mix = 0, f_exec = 0, f_contract_local = 0, f_mix_local = 0;
   int64_t ws_bytes = 0;
   int max_mix = 0;                             // min(N+1, d): longest U-mix vector
   int sm_count = 148;
   cudaStream_t plan_stream = nullptr;
+  void* blk_tab = nullptr;                     // pool block: perm / qs / off tables
+  void* blk_work = nullptr;                    // pool block: group + tile tables, A/B panels
+  // per-kernel timing events: [0,1] K1, [2,3] K2, [4] K3 start, [5] K4 start, [6] K5 start, [7] end
+  cudaEvent_t ev[8] = {};
+  mutable bool rec_k1 = false, rec_k2 = false, rec_exec = false;
+  mutable cudaStream_t last_stream = nullptr;  // stream of the last exec (pool release fence)
 };
 
 namespace tn {
@@ -91,8 +97,17 @@ tn_status fail(tn_status st, const std::string& s);
 tn_status cuda_check(cudaError_t e, const char* what);
 
 // ---- kernel launchers (stream-ordered) ----
-cudaError_t launch_sort_bonds(const int32_t* q, int64_t chi, int N, int32_t* perm, int32_t* qs,
-                              int32_t* off, int32_t* err, cudaStream_t s);
+struct SortArgs {           // K1: one CTA per bond (0 = left, 1 = center, 2 = right)
+  const int32_t* q[3];
+  int64_t chi[3];
+  int32_t* perm[3];
+  int32_t* qs[3];
+  int32_t* off[3];
+  int32_t* err;             // err[b] = 1 if a charge of bond b lies outside [0, N]
+};
+cudaError_t launch_sort_bonds(const SortArgs& a, int N, cudaStream_t s);
+void* pool_alloc(size_t bytes, cudaError_t* err);
+void pool_release(void* ptr, cudaStream_t last_stream, bool used);
 cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const int32_t* ustart_host,
                               double2* U, cudaStream_t s);
 cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
