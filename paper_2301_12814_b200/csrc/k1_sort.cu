@@ -9,7 +9,7 @@
 
 namespace tn {
 
-constexpr int SORT_THREADS = 256;
+constexpr int SORT_THREADS = 1024;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
 __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs args, int N) {

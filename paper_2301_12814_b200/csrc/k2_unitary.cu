@@ -12,19 +12,10 @@
 
 namespace tn {
 
-__device__ __forceinline__ dd binom_dd(int n, int k) {
-  if (k < 0 || k > n) return {0.0, 0.0};
-  if (k > n - k) k = n - k;
-  unsigned __int128 c = 1;
-  for (int t = 1; t <= k; ++t) c = c * (unsigned __int128)(n - k + t) / (unsigned __int128)t;  // exact
-  double hi = (double)c;
-  unsigned __int128 hi_i = (unsigned __int128)hi;
-  double lo = (c >= hi_i) ? (double)(c - hi_i) : -(double)(hi_i - c);
-  return quick_two_sum(hi, lo);
-}
-
-__global__ void __launch_bounds__(256) k2_bs_unitary(int d, double theta, double phi,
-                                                     double2* __restrict__ U) {
+// binom: (nmax+1)×(nmax+1) table of C(n,k) as double-double pairs (exact below 2^106), built by the
+// plan from exact 128-bit integers (host), row-major.
+__global__ void __launch_bounds__(256) k2_bs_unitary(int d, int nmax, double theta, double phi,
+                                                     const double2* __restrict__ binom, double2* __restrict__ U) {
   const int n = blockIdx.x;
   __shared__ dd cpow[2 * TN_MAX_N + 2];
   __shared__ dd spow[2 * TN_MAX_N + 2];
@@ -51,15 +42,19 @@ __global__ void __launch_bounds__(256) k2_bs_unitary(int d, double theta, double
   for (int e = threadIdx.x; e < sn * sn; e += blockDim.x) {
     const int i = lo + e / sn, j = lo + e % sn;
     dd acc = dd_from(0.0);
-    for (int k = 0; k <= j; ++k) {
+    const int ld = nmax + 1;
+    auto B = [&](int nn, int kk) {
+      const double2 v = binom[nn * ld + kk];
+      return dd{v.x, v.y};
+    };
+    for (int k = max(0, i - (n - j)); k <= min(j, i); ++k) {
       const int l = i - k;
-      if (l < 0 || l > n - j) continue;
-      dd t = dd_mul(binom_dd(j, k), binom_dd(n - j, l));
+      dd t = dd_mul(B(j, k), B(n - j, l));
       t = dd_mul(t, cpow[n - j - i + 2 * k]);
       t = dd_mul(t, spow[i + j - 2 * k]);
       acc = ((j - k) & 1) ? dd_add(acc, dd_neg(t)) : dd_add(acc, t);
     }
-    const dd pref = dd_sqrt(dd_div(binom_dd(n, j), binom_dd(n, i)));
+    const dd pref = dd_sqrt(dd_div(B(n, j), B(n, i)));
     const dd v = dd_mul(pref, acc);
     const double mag = v.hi + v.lo;
     // e^{iφ(i−j)}: argument formed exactly in double-double, then one correction step.
@@ -71,11 +66,10 @@ __global__ void __launch_bounds__(256) k2_bs_unitary(int d, double theta, double
   }
 }
 
-cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const int32_t* ustart_host, double2* U,
+cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const double2* binom, double2* U,
                               cudaStream_t s) {
-  (void)ustart_host;
   const int nmax = min(N, 2 * d - 2);
-  k2_bs_unitary<<<nmax + 1, 256, 0, s>>>(d, theta, phi, U);
+  k2_bs_unitary<<<nmax + 1, 256, 0, s>>>(d, nmax, theta, phi, binom, U);
   return cudaGetLastError();
 }
 

@@ -8,10 +8,13 @@
 //
 // B200 design (DESIGN.md §4 "K4"): sm_100a has no tcgen05 FP64 MMA (`kind::f64` does not exist),
 // so the FP64 tensor path is the warp-level DMMA.8x8x4 (mma.sync.m8n8k4.f64), measured at 37.2
-// TFLOP/s. A persistent grid walks a heavy-first tile list; one producer warp streams each 64×16
-// operand chunk with a single cp.async.bulk (TMA 1-D) copy into a 3-stage mbarrier ring; four
-// consumer warps (2×2, 32×32 complex each) read fragments with conflict-free 128-bit LDS (K3 wrote
-// the panels in fragment order) and issue 4 real DMMAs per complex 8×8×4 step.
+// TFLOP/s. A persistent grid (one CTA per SM) walks a heavy-first tile list; one producer warp
+// streams each 64×16 operand chunk with a single cp.async.bulk (TMA 1-D) copy into a K4_STAGES-deep
+// mbarrier ring; eight consumer warps (2×4, 32×16 complex outputs each) read fragments with
+// conflict-free 128-bit LDS (K3 wrote the panels in fragment order). The complex product uses the
+// 3-multiplication (Gauss) form, 3 real DMMAs per complex 8×8×4 step instead of 4:
+//   T1 = Ar·Br, T2 = Ai·Bi, T3 = (Ar+Ai)·(Br+Bi);  Re = T1 − T2,  Im = T3 − T1 − T2
+// (error bound ~ eps·|Ar+Ai||Br+Bi| per term, same order as the 4-product form).
 #include "tn_internal.cuh"
 
 namespace tn {
@@ -49,12 +52,9 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
-__device__ __forceinline__ double neg_bits(double x) {  // −x on the integer pipe (sign flip)
-  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
-}
 
 template <int STAGES>
-__global__ void __launch_bounds__(K4_THREADS, 2)
+__global__ void __launch_bounds__(K4_THREADS, 1)
     k4_contract(const GroupDesc* __restrict__ groups, const TileDesc* __restrict__ tiles, int ntiles,
                 const double2* __restrict__ ap, const double2* __restrict__ bp, const SectorParams sp) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -100,45 +100,47 @@ __global__ void __launch_bounds__(K4_THREADS, 2)
     return;
   }
 
-  // ---------------- consumers: 2×2 warps, 32×32 complex outputs each ----------------
-  const int wm = warp >> 1, wn = warp & 1;
+  // ---------------- consumers: 2×4 warps, 32×16 complex outputs each ----------------
+  const int wm = warp >> 2, wn = warp & 3;
   const int gq = lane >> 2, tq = lane & 3;
   int stage = 0;
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const TileDesc td = tiles[t];
     const GroupDesc g = groups[td.g];
-    double acc[4][4][4];  // [mi][ni][re0, re1, im0, im1]
+    double acc[4][2][6];  // [mi][ni][T1 0,1 | T2 0,1 | T3 0,1]
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
+        for (int q = 0; q < 6; ++q) acc[mi][ni][q] = 0.0;
 
     for (int kc = 0; kc * BK < g.K4; ++kc) {
       mbar_wait(&full[stage], phase);
       const int nks = min(BK, g.K4 - kc * BK) >> 2;
       const double2* As = sA + stage * CHUNK + wm * 128 + lane;
-      const double2* Bs = sB + stage * CHUNK + wn * 128 + lane;
+      const double2* Bs = sB + stage * CHUNK + wn * 64 + lane;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         if (ks < nks) {
-          double2 a[4], b[4];
+          double2 a[4], b[2];
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks * 256 + mi * 32];
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
+          for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
+          double bsum[2];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) bsum[ni] = b[ni].x + b[ni].y;
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi) {
-            const double nai = neg_bits(a[mi].y);
+            const double asum = a[mi].x + a[mi].y;
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
+            for (int ni = 0; ni < 2; ++ni) {
               double* c = acc[mi][ni];
-              dmma(c[0], c[1], a[mi].x, b[ni].x);  // Re += Ar·Br
-              dmma(c[2], c[3], a[mi].x, b[ni].y);  // Im += Ar·Bi
-              dmma(c[0], c[1], nai, b[ni].y);      // Re −= Ai·Bi
-              dmma(c[2], c[3], a[mi].y, b[ni].x);  // Im += Ai·Br
+              dmma(c[0], c[1], a[mi].x, b[ni].x);  // T1 += Ar·Br
+              dmma(c[2], c[3], a[mi].y, b[ni].y);  // T2 += Ai·Bi
+              dmma(c[4], c[5], asum, bsum[ni]);    // T3 += (Ar+Ai)·(Br+Bi)
             }
           }
         }
@@ -160,10 +162,13 @@ __global__ void __launch_bounds__(K4_THREADS, 2)
       if (row >= g.R) continue;
       double2* orow = out + (int64_t)row * ld;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int col = td.nt * BN + wn * 32 + ni * 8 + 2 * tq;
-        if (col < g.C) orow[col] = make_double2(acc[mi][ni][0], acc[mi][ni][2]);
-        if (col + 1 < g.C) orow[col + 1] = make_double2(acc[mi][ni][1], acc[mi][ni][3]);
+      for (int ni = 0; ni < 2; ++ni) {
+        const int col = td.nt * BN + wn * 16 + ni * 8 + 2 * tq;
+        const double* c = acc[mi][ni];
+        const double re0 = c[0] - c[2], re1 = c[1] - c[3];
+        const double im0 = c[4] - c[0] - c[2], im1 = c[5] - c[1] - c[3];
+        if (col < g.C) orow[col] = make_double2(re0, im0);
+        if (col + 1 < g.C) orow[col + 1] = make_double2(re1, im1);
       }
     }
   }
@@ -179,7 +184,7 @@ cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int64_t grid = std::min<int64_t>(p->ntiles, (int64_t)p->sm_count * 2);
+  const int64_t grid = std::min<int64_t>(p->ntiles, (int64_t)p->sm_count);
   k4_contract<STAGES><<<(unsigned)grid, K4_THREADS, smem, s>>>(p->d_groups, p->d_tiles, (int)p->ntiles,
                                                                 p->d_apanel, p->d_bpanel, sp);
   return cudaGetLastError();

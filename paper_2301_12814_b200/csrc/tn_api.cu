@@ -208,6 +208,9 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   size_t o_perm[3], o_qs[3], o_off[3], o_err, o_q[3] = {0, 0, 0};
   bool host_q[3];
   int32_t* d_err = nullptr;
+  const int nmax_u = std::min(N, 2 * d - 2);
+  size_t o_bin = 0;
+  std::vector<double2> hbin((size_t)(nmax_u + 1) * (nmax_u + 1), double2{0.0, 0.0});
 #define TN_TRY(expr, what)                      \
   do {                                          \
     st = cuda_check((expr), what);              \
@@ -226,6 +229,17 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
     if (host_q[b]) o_q[b] = ct.take<int32_t>(p->chi[b]);
   }
   o_err = ct.take<int32_t>(4);
+  o_bin = ct.take<double2>((int64_t)(nmax_u + 1) * (nmax_u + 1));
+  for (int n = 0; n <= nmax_u; ++n) {  // exact C(n,k) as a double-double pair (n ≤ TN_MAX_N)
+    unsigned __int128 c = 1;
+    for (int k = 0; k <= n; ++k) {
+      if (k > 0) c = c * (unsigned __int128)(n - k + 1) / (unsigned __int128)k;
+      const double hi = (double)c;
+      const unsigned __int128 hi_i = (unsigned __int128)hi;
+      const double lo = c >= hi_i ? (double)(c - hi_i) : -(double)(hi_i - c);
+      hbin[(size_t)n * (nmax_u + 1) + k] = double2{hi, lo};
+    }
+  }
   p->blk_tab = pool_alloc(ct.off, &aerr);
   TN_TRY(aerr, "pool alloc (bond tables)");
   {
@@ -250,6 +264,9 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
     }
     d_err = reinterpret_cast<int32_t*>(base + o_err);
     sa.err = d_err;
+    p->d_binom = reinterpret_cast<double2*>(base + o_bin);
+    TN_TRY(cudaMemcpyAsync(p->d_binom, hbin.data(), hbin.size() * sizeof(double2), cudaMemcpyHostToDevice,
+                           p->plan_stream), "H2D binomials");
     // ---- K1: sort each bond by charge (one launch, one CTA per bond) ----
     TN_TRY(cudaMemsetAsync(d_err, 0, 4 * sizeof(int32_t), p->plan_stream), "memset err");
     TN_TRY(cudaEventRecord(p->ev[0], p->plan_stream), "event");
@@ -371,10 +388,14 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
         for (int nt = 0; nt < g.nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
     }
     p->ntiles = (int64_t)tiles.size();
-    if (!p->groups.empty()) {
+    std::vector<MixTile> mix;
+    build_mix_tiles(p, mix);
+    p->nmix = (int64_t)mix.size();
+    if (!p->groups.empty() || !mix.empty()) {
       Carver cw;
       const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
       const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
+      const size_t o_m = cw.take<MixTile>((int64_t)mix.size());
       const size_t o_a = cw.take<double2>(p->a_elems);
       const size_t o_b = cw.take<double2>(p->b_elems);
       p->blk_work = pool_alloc(cw.off, &aerr);
@@ -382,12 +403,18 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
       char* base = static_cast<char*>(p->blk_work);
       p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
       p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
+      p->d_mix = reinterpret_cast<MixTile*>(base + o_m);
       p->d_apanel = reinterpret_cast<double2*>(base + o_a);
       p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
-      TN_TRY(cudaMemcpyAsync(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc),
-                             cudaMemcpyHostToDevice, p->plan_stream), "H2D groups");
-      TN_TRY(cudaMemcpyAsync(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice,
-                             p->plan_stream), "H2D tiles");
+      if (!p->groups.empty()) {
+        TN_TRY(cudaMemcpyAsync(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc),
+                               cudaMemcpyHostToDevice, p->plan_stream), "H2D groups");
+        TN_TRY(cudaMemcpyAsync(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice,
+                               p->plan_stream), "H2D tiles");
+      }
+      if (!mix.empty())
+        TN_TRY(cudaMemcpyAsync(p->d_mix, mix.data(), mix.size() * sizeof(MixTile), cudaMemcpyHostToDevice,
+                               p->plan_stream), "H2D mix tiles");
       TN_TRY(cudaStreamSynchronize(p->plan_stream), "plan tables sync");
       p->ws_bytes = (int64_t)cw.off;
     }
@@ -506,7 +533,7 @@ tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_str
   cudaStream_t s = (cudaStream_t)stream;
   tn_status st = cuda_check(cudaEventRecord(p->ev[2], s), "event");
   if (st != TN_OK) return st;
-  st = cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->ustart.data(), reinterpret_cast<double2*>(U_out), s),
+  st = cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->d_binom, reinterpret_cast<double2*>(U_out), s),
                   "K2 launch");
   if (st != TN_OK) return st;
   st = cuda_check(cudaEventRecord(p->ev[3], s), "event");
@@ -539,8 +566,7 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   st = cuda_check(launch_contract(p, sp, s), "K4 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
-  st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, p->d_off[2]),
-                  "K5 launch");
+  st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
   if (st != TN_OK) return st;
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");
 }

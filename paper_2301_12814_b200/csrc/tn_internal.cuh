@@ -15,15 +15,15 @@ namespace tn {
 
 // ---------------------------------------------------------------------------------------------
 // Tiling constants of the K4 contraction (DESIGN.md §4 "K4").
-//   CTA tile BM×BN complex outputs, 4 consumer warps in 2×2, each 32×32 = 4×4 DMMA.8x8x4 tiles.
+//   CTA tile BM×BN complex outputs, 8 consumer warps in 2×4, each 32×16 = 4×2 DMMA.8x8x4 tiles.
 //   K is consumed in chunks of BK; the chunk is one cp.async.bulk (TMA 1-D) copy per operand.
 // ---------------------------------------------------------------------------------------------
 constexpr int BM = 64;
 constexpr int BN = 64;
 constexpr int BK = 16;
 constexpr int CHUNK = BM * BK;        // complex elements per full operand chunk (== BN * BK)
-constexpr int K4_STAGES = 3;
-constexpr int K4_CONSUMER_WARPS = 4;
+constexpr int K4_STAGES = 6;
+constexpr int K4_CONSUMER_WARPS = 8;
 constexpr int K4_THREADS = (K4_CONSUMER_WARPS + 1) * 32;
 
 struct GroupDesc {          // one center charge c_c: P_{c_c} = A_{c_c} · B_{c_c}
@@ -39,6 +39,13 @@ struct GroupDesc {          // one center charge c_c: P_{c_c} = A_{c_c} · B_{c_
 
 struct TileDesc {
   int32_t g, mt, nt, pad;
+};
+
+struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive columns of one row) of one (c_l, c_r) block
+  int32_t cl, cr;           // left / right charge
+  int32_t e0, ne;           // first 8-group (row-major within the block) and count
+  int32_t nr, ngr;          // columns of the block (n_r(c_r)) and 8-groups per row ⌈nr/8⌉
+  int32_t pl0, pr0;         // sorted positions of the block's first (local) row / first column
 };
 
 constexpr int MAXC = TN_MAX_N + 1;
@@ -63,6 +70,7 @@ struct tn_plan {
   int32_t* d_perm[3] = {nullptr, nullptr, nullptr};  // device perm (sorted pos -> caller index)
   int32_t* d_qs[3] = {nullptr, nullptr, nullptr};    // device sorted charges
   int32_t* d_off[3] = {nullptr, nullptr, nullptr};   // device offset tables (N+2)
+  double2* d_binom = nullptr;                  // (nmax+1)² exact binomials as double-double (K2)
   std::vector<int64_t> bounds;                 // world+1 shard bounds (sorted left positions)
   int64_t r0 = 0, r1 = 0;                      // this rank's window
   // sectors
@@ -72,6 +80,8 @@ struct tn_plan {
   tn::GroupDesc* d_groups = nullptr;
   tn::TileDesc* d_tiles = nullptr;
   int64_t ntiles = 0;
+  tn::MixTile* d_mix = nullptr;
+  int64_t nmix = 0;                            // K5 tiles
   double2* d_apanel = nullptr;
   double2* d_bpanel = nullptr;
   int64_t a_elems = 0, b_elems = 0;
@@ -108,13 +118,14 @@ struct SortArgs {           // K1: one CTA per bond (0 = left, 1 = center, 2 = r
 cudaError_t launch_sort_bonds(const SortArgs& a, int N, cudaStream_t s);
 void* pool_alloc(size_t bytes, cudaError_t* err);
 void pool_release(void* ptr, cudaStream_t last_stream, bool used);
-cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const int32_t* ustart_host,
-                              double2* U, cudaStream_t s);
+cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const double2* binom, double2* U,
+                              cudaStream_t s);
 cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
                          cudaStream_t s);
 cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                       const double2* U, cudaStream_t s, const int32_t* d_offr);
+                       const double2* U, cudaStream_t s);
+void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out);
 
 // ---- double-double arithmetic (K2): error-free transforms, ~106-bit significand ----
 struct dd {
