@@ -78,9 +78,15 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      TileDesc pd_next = tiles[blockIdx.x];
+      GroupDesc pg_next = groups[pd_next.g];
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileDesc td = tiles[t];
-        const GroupDesc g = groups[td.g];
+        const TileDesc td = pd_next;
+        const GroupDesc g = pg_next;
+        if (t + (int)gridDim.x < ntiles) {
+          pd_next = tiles[t + gridDim.x];
+          pg_next = groups[pd_next.g];
+        }
         const double2* a = ap + g.a_off + (int64_t)td.mt * BM * g.K4;
         const double2* b = bp + g.b_off + (int64_t)td.nt * BN * g.K4;
         for (int kc = 0; kc * BK < g.K4; ++kc) {
@@ -105,9 +111,21 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   const int gq = lane >> 2, tq = lane & 3;
   int stage = 0;
   uint32_t phase = 0;
+  // tile / group descriptors of the NEXT tile are loaded during the current one (their global-load
+  // latency would otherwise stall all consumer warps at every tile start)
+  TileDesc td_next;
+  GroupDesc g_next;
+  if (blockIdx.x < ntiles) {
+    td_next = tiles[blockIdx.x];
+    g_next = groups[td_next.g];
+  }
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const TileDesc td = tiles[t];
-    const GroupDesc g = groups[td.g];
+    const TileDesc td = td_next;
+    const GroupDesc g = g_next;
+    if (t + (int)gridDim.x < ntiles) {
+      td_next = tiles[t + gridDim.x];
+      g_next = groups[td_next.g];
+    }
     double acc[4][2][6];  // [mi][ni][T1 0,1 | T2 0,1 | T3 0,1]
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)

@@ -57,6 +57,21 @@ __global__ void row_order(Sec s, const int* __restrict__ rowcl) {
   }
 }
 
+// (d): item order: a CTA handles (row, c_r block, W-column chunk) and streams the L sector runs of
+// W×16 B each (the TMA-item K5 design); items ordered row-major so neighbours share DRAM pages
+struct Item { int row, cl, cr, j0, w; };
+__global__ void item_order(Sec s, const Item* __restrict__ it, int n) {
+  const Item I = it[blockIdx.x];
+  const int L = I.cl - I.cr + 1;
+  for (int idx = threadIdx.x; idx < L * I.w; idx += blockDim.x) {
+    const int u = idx / I.w, col = idx - u * I.w;
+    const int c = I.cr + u;
+    double2* p = s.p[c] + (size_t)(I.row - s.off_l[c]) * s.ld[c] + (s.off_r[I.cr] + I.j0 + col);
+    double2 x = __ldcs(p);
+    __stcs(p, make_double2(x.x * 1.0000001, x.y));
+  }
+}
+
 int main() {
   FILE* f = fopen("tools/config3_counts.txt", "r");
   int nl[NQ], nc[NQ], nr[NQ];
@@ -106,6 +121,20 @@ int main() {
     cudaEventRecord(e0); for (int r = 0; r < 5; ++r) row_order<<<ol[NQ], bs>>>(s, drc); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
     printf("{\"probe\": \"row_order\", \"block\": %d, \"ms\": %.4f, \"GBps\": %.1f}\n", bs, ms, tot * 32 / ms / 1e6);
+  }
+  // (d)
+  for (int W : {64, 128, 256}) {
+    std::vector<Item> items;
+    for (int cl = 0; cl < NQ; ++cl) for (int row = ol[cl]; row < ol[cl + 1]; ++row) for (int cr = 0; cr <= cl; ++cr)
+      for (int j0 = 0; j0 < nr[cr]; j0 += W) items.push_back(Item{row, cl, cr, j0, nr[cr] - j0 < W ? nr[cr] - j0 : W});
+    Item* di; CK(cudaMalloc(&di, items.size() * sizeof(Item)));
+    CK(cudaMemcpy(di, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+    const int n = (int)items.size();
+    for (int r = 0; r < 3; ++r) item_order<<<n, 256>>>(s, di, n);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) item_order<<<n, 256>>>(s, di, n); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
+    printf("{\"probe\": \"item_order\", \"W\": %d, \"items\": %d, \"ms\": %.4f, \"GBps\": %.1f}\n", W, n, ms, tot * 32 / ms / 1e6);
+    cudaFree(di);
   }
   return 0;
 }
