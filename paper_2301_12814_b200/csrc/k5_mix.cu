@@ -18,10 +18,10 @@
 //    (g, q) stores Θ(lo+t)[column g], t = 2q, 2q+1 — a lane owns one element, so λl·λr is a per-lane
 //    scalar. Registers stay small (⌈L/4⌉ complex per lane per group + ⌈L/8⌉ accumulator tiles).
 //  * Each warp prefetches its next group's A fragments before the MMAs of the current one.
-//  * Measured limit of this access order (L sectors × 128 B per warp instruction): a pure copy in the
-//    same order reaches 3.5 TB/s vs 6.1 TB/s linear (tools/probe_mix_bw.cu,
-//    profiles/r01_probe_mix_bw.jsonl); this kernel runs at ~3.1 TB/s. DESIGN.md §7 lists the fused
-//    K4+K5 schedule that reads P from L2 instead.
+//  * Tiles are one row × one c_r block, issued row-major: what decides the HBM rate here is the ORDER
+//    in which concurrently running CTAs touch the sector rows (a pure copy runs at 5.2–5.4 TB/s when
+//    one row α is swept across consecutive c_r blocks, 2.8–3.5 TB/s when tiles are block-major,
+//    whatever the per-instruction shape: tools/probe_mix_bw.cu, profiles/r01_probe_mix_bw.jsonl).
 //  * P_{c_c} of an empty center segment is zero and never read.
 #include "tn_internal.cuh"
 
@@ -63,6 +63,7 @@ __device__ __forceinline__ void load_group(double2 (&a)[KSM], const SecRef* __re
 template <int NT>  // NT = ⌈L/8⌉ output tiles of 8 sectors
 __device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* __restrict__ sec,
                                               const SecRef* __restrict__ st_sec, const double2* __restrict__ Us,
+                                              const double* __restrict__ UsS,
                                               int ust, int L, const int32_t* __restrict__ perm_l,
                                               const int32_t* __restrict__ perm_r, const double* __restrict__ ll,
                                               const double* __restrict__ lr, int warp, int lane) {
@@ -95,21 +96,25 @@ __device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* _
       validn = coln < mt.nr;
       load_group<KSM>(an, sec, L, rown, coln, validn, q);
     }
-    double acc[NT][4];
+    // Gauss 3-product form: T1 = Pr·Ur, T2 = Pi·Ui, T3 = (Pr+Pi)·(Ur+Ui); Re = T1−T2, Im = T3−T1−T2
+    double acc[NT][6];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int x = 0; x < 6; ++x) acc[j][x] = 0.0;
     __syncwarp();
 #pragma unroll
     for (int ks = 0; ks < KSM; ++ks) {
       if (ks < KS) {
-        const double nai = -a[ks].y;
+        const double as = a[ks].x + a[ks].y;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          const double2 b = Us[(j * 8 + g) * ust + ks * 4 + q];  // B frag: Usᵀ[u = 4ks+q][t = 8j+g]
-          dmma5(acc[j][0], acc[j][1], a[ks].x, b.x);  // Re += Pr·Ur
-          dmma5(acc[j][0], acc[j][1], nai, b.y);      // Re −= Pi·Ui
-          dmma5(acc[j][2], acc[j][3], a[ks].x, b.y);  // Im += Pr·Ui
-          dmma5(acc[j][2], acc[j][3], a[ks].y, b.x);  // Im += Pi·Ur
+          const int idx = (j * 8 + g) * ust + ks * 4 + q;  // B frag: Usᵀ[u = 4ks+q][t = 8j+g]
+          const double2 b = Us[idx];
+          const double bs = UsS[idx];
+          dmma5(acc[j][0], acc[j][1], a[ks].x, b.x);  // T1
+          dmma5(acc[j][2], acc[j][3], a[ks].y, b.y);  // T2
+          dmma5(acc[j][4], acc[j][5], as, bs);        // T3
         }
       }
     }
@@ -122,8 +127,9 @@ __device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* _
           const int t = j * 8 + 2 * q + h;
           if (t < L) {
             const SecRef s = st_sec[t];  // output sector lo+t (every output sector is stored)
-            __stcs(const_cast<double2*>(s.base) + row * s.ld + col,
-                   make_double2(acc[j][h] * scale, acc[j][2 + h] * scale));
+            const double re = acc[j][h] - acc[j][2 + h];
+            const double im = acc[j][4 + h] - acc[j][h] - acc[j][2 + h];
+            __stcs(const_cast<double2*>(s.base) + row * s.ld + col, make_double2(re * scale, im * scale));
           }
         }
     }
@@ -141,7 +147,7 @@ template <int NTMAX>
 __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
     k5_mix(const SectorParams sp, const MixTile* __restrict__ tiles, const int32_t* __restrict__ perm_l,
            const int32_t* __restrict__ perm_r, const double* __restrict__ ll, const double* __restrict__ lr,
-           const double2* __restrict__ U) {
+           const double2* __restrict__ U, int us_elems) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const MixTile mt = tiles[blockIdx.x];
   const int d = sp.d;
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
   SecRef* ld_sec = reinterpret_cast<SecRef*>(smem_raw);           // load table (null if empty segment)
   SecRef* st_sec = ld_sec + 8 * NTMAX;                            // store table
   double2* Us = reinterpret_cast<double2*>(st_sec + 8 * NTMAX);   // U sub-block
+  double* UsS = reinterpret_cast<double*>(Us + us_elems);          // Re + Im of every Us entry
   for (int u = threadIdx.x; u < L; u += MIX_THREADS) {
     const int cc = lo + u;
     const double2* base =
@@ -170,6 +177,7 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
     double2 v = make_double2(0.0, 0.0);
     if (t < L && u < L) v = __ldg(Ub + (c_l - lo - t - nlo) * sn + (c_l - lo - u - nlo));
     Us[t * ust + u] = v;
+    UsS[t * ust + u] = v.x + v.y;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
 #define TN_MIX_CASE(m)                                                                              \
   case m:                                                                                           \
     if constexpr (m <= NTMAX)                                                                       \
-      mix_tile_warp<m>(mt, ld_sec, st_sec, Us, ust, L, perm_l, perm_r, ll, lr, warp, lane);        \
+      mix_tile_warp<m>(mt, ld_sec, st_sec, Us, UsS, ust, L, perm_l, perm_r, ll, lr, warp, lane);   \
     break;
     TN_MIX_CASE(1) TN_MIX_CASE(2) TN_MIX_CASE(3) TN_MIX_CASE(4)
     TN_MIX_CASE(5) TN_MIX_CASE(6) TN_MIX_CASE(7) TN_MIX_CASE(8)
@@ -187,33 +195,36 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
   }
 }
 
-// Host: the tile list over this rank's (c_l, c_r) charge blocks (called by the plan), row-major
-// 8-groups in chunks of MIX_GROUPS_PER_TILE.
+// Host: a tile = a band of rows × one c_r block (≈ MIX_GROUPS_PER_TILE 8-groups, so the per-CTA U
+// staging is amortised), tiles issued band-major (row band, then c_r): concurrently running CTAs cover
+// the same rows across consecutive c_r blocks, i.e. the sector rows are swept contiguously
+// (tools/probe_mix_bw.cu: 5.2–5.4 TB/s row-major vs 2.8–3.5 TB/s block-major for a pure copy).
 void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out) {
   out.clear();
   const auto& ol = p->off[0];
   const auto& orr = p->off[2];
+  constexpr int BAND = 4;
   for (int cl = 0; cl <= p->N; ++cl) {
     const int64_t a0 = std::max<int64_t>(ol[cl], p->r0), a1 = std::min<int64_t>(ol[cl + 1], p->r1);
-    if (a1 <= a0) continue;
-    for (int cr = std::max(0, cl - 2 * p->d + 2); cr <= std::min(p->N, cl + 2 * p->d - 2); ++cr) {
-      const int n = cl - cr;
-      if (n < 0 || n > 2 * p->d - 2) continue;
-      const int64_t nr = orr[cr + 1] - orr[cr];
-      if (nr == 0) continue;
-      const int64_t ngr = (nr + 7) / 8;
-      const int64_t G = (a1 - a0) * ngr;
-      for (int64_t e0 = 0; e0 < G; e0 += MIX_GROUPS_PER_TILE) {
-        MixTile t;
-        t.cl = cl;
-        t.cr = cr;
-        t.e0 = (int32_t)e0;
-        t.ne = (int32_t)std::min<int64_t>(MIX_GROUPS_PER_TILE, G - e0);
-        t.nr = (int32_t)nr;
-        t.ngr = (int32_t)ngr;
-        t.pl0 = (int32_t)a0;
-        t.pr0 = (int32_t)orr[cr];
-        out.push_back(t);
+    for (int64_t band = a0; band < a1; band += BAND) {
+      const int64_t rows = std::min<int64_t>(BAND, a1 - band);
+      for (int cr = std::max(0, cl - 2 * p->d + 2); cr <= cl; ++cr) {
+        const int64_t nr = orr[cr + 1] - orr[cr];
+        if (nr == 0) continue;
+        const int64_t ngr = (nr + 7) / 8;
+        const int64_t G = rows * ngr;
+        for (int64_t e0 = 0; e0 < G; e0 += MIX_GROUPS_PER_TILE) {
+          MixTile t;
+          t.cl = cl;
+          t.cr = cr;
+          t.e0 = (int32_t)e0;
+          t.ne = (int32_t)std::min<int64_t>(MIX_GROUPS_PER_TILE, G - e0);
+          t.nr = (int32_t)nr;
+          t.ngr = (int32_t)ngr;
+          t.pl0 = (int32_t)band;
+          t.pr0 = (int32_t)orr[cr];
+          out.push_back(t);
+        }
       }
     }
   }
@@ -232,12 +243,12 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
   }
 #define TN_MIX_LAUNCH(M)                                                                                       \
   do {                                                                                                         \
-    const size_t smem = (size_t)smax * sizeof(double2) + 2 * 8 * (M) * sizeof(SecRef);                         \
+    const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * sizeof(SecRef);     \
     if (smem > 48 * 1024) {                                                                                    \
       cudaError_t e = cudaFuncSetAttribute(k5_mix<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
       if (e != cudaSuccess) return e;                                                                          \
     }                                                                                                          \
-    k5_mix<M><<<grid, MIX_THREADS, smem, s>>>(sp, p->d_mix, p->d_perm[0], p->d_perm[2], ll, lr, U);            \
+    k5_mix<M><<<grid, MIX_THREADS, smem, s>>>(sp, p->d_mix, p->d_perm[0], p->d_perm[2], ll, lr, U, smax);      \
   } while (0)
   if (NT <= 1)
     TN_MIX_LAUNCH(1);

@@ -72,6 +72,30 @@ __global__ void item_order(Sec s, const Item* __restrict__ it, int n) {
   }
 }
 
+// (e): like (b) but a warp owns 32 consecutive columns of one row and moves ONE sector per
+// instruction (lane = column); (f) 16 columns × 2 sectors per instruction
+template <int EPW>
+__global__ void warp_rows(Sec s, const Grp* __restrict__ g, int ng) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= ng) return;
+  const Grp G = g[warp];
+  constexpr int SPI = 32 / EPW;  // sectors per instruction
+  const int e = lane % EPW, q = lane / EPW;
+  if (e >= G.w) return;
+  const int L = G.cl - G.cr + 1;
+  double2 v[32 / SPI];
+#pragma unroll
+  for (int k = 0; k < 32 / SPI; ++k) {
+    const int u = k * SPI + q, c = G.cr + u;
+    if (u < L) v[k] = __ldcs(s.p[c] + (size_t)(G.row - s.off_l[c]) * s.ld[c] + (G.col0 + e));
+  }
+#pragma unroll
+  for (int k = 0; k < 32 / SPI; ++k) {
+    const int u = k * SPI + q, c = G.cr + u;
+    if (u < L) __stcs(s.p[c] + (size_t)(G.row - s.off_l[c]) * s.ld[c] + (G.col0 + e), make_double2(v[k].x * 1.0000001, v[k].y));
+  }
+}
+
 int main() {
   FILE* f = fopen("tools/config3_counts.txt", "r");
   int nl[NQ], nc[NQ], nr[NQ];
@@ -135,6 +159,25 @@ int main() {
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
     printf("{\"probe\": \"item_order\", \"W\": %d, \"items\": %d, \"ms\": %.4f, \"GBps\": %.1f}\n", W, n, ms, tot * 32 / ms / 1e6);
     cudaFree(di);
+  }
+  // (e)/(f)
+  for (int EPW : {32, 16, 8}) {
+    std::vector<Grp> g2;
+    for (int cl = 0; cl < NQ; ++cl) for (int cr = 0; cr <= cl; ++cr) for (int row = ol[cl]; row < ol[cl + 1]; ++row)
+      for (int c0 = 0; c0 < nr[cr]; c0 += EPW) g2.push_back(Grp{cl, cr, row, orr[cr] + c0, nr[cr] - c0 < EPW ? nr[cr] - c0 : EPW});
+    Grp* dg2; CK(cudaMalloc(&dg2, g2.size() * sizeof(Grp)));
+    CK(cudaMemcpy(dg2, g2.data(), g2.size() * sizeof(Grp), cudaMemcpyHostToDevice));
+    const int n2 = (int)g2.size();
+    auto run = [&]() {
+      if (EPW == 32) warp_rows<32><<<(n2 + 7) / 8, 256>>>(s, dg2, n2);
+      else if (EPW == 16) warp_rows<16><<<(n2 + 7) / 8, 256>>>(s, dg2, n2);
+      else warp_rows<8><<<(n2 + 7) / 8, 256>>>(s, dg2, n2);
+    };
+    for (int r = 0; r < 3; ++r) run();
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) run(); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); ms /= 5;
+    printf("{\"probe\": \"warp_rows\", \"elems_per_instr\": %d, \"ms\": %.4f, \"GBps\": %.1f}\n", EPW, ms, tot * 32 / ms / 1e6);
+    cudaFree(dg2);
   }
   return 0;
 }
