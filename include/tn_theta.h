@@ -115,6 +115,20 @@ TN_API tn_status tn_plan_workspace_bytes(const tn_plan* plan, int64_t* bytes);
  * calls not yet made are −1. */
 TN_API tn_status tn_plan_kernel_times(const tn_plan* plan, float* ms5);
 
+/* Contraction engine of tn_theta_exec (default TN_CONTRACT_F64_DMMA):
+ *   TN_CONTRACT_F64_DMMA   — FP64 tensor cores (DMMA.8x8x4), complex products in the 3-multiplication
+ *                            form; rounding error ~1e-16 relative.
+ *   TN_CONTRACT_INT8_OZAKI — FP64-accurate emulation on the tcgen05 INT8 tensor cores: each real
+ *                            operand is split into `slices` signed 7-bit slices with per-row (A) /
+ *                            per-column (B) power-of-two scales; slice products accumulate exactly in
+ *                            int32 TMEM per diagonal p+q ≤ slices+1 and are recombined in FP64.
+ *                            Truncation error ≈ √K·2^(−7·slices) relative (slices = 7: ~1e-13).
+ * slices ∈ [4, 8] (ignored for DMMA). Builds the slice layout (pooled workspace) and syncs once.
+ * Errors: TN_ERR_DOMAIN (unknown mode / slices out of range), TN_ERR_OOM, TN_ERR_CUDA. */
+enum { TN_CONTRACT_F64_DMMA = 0, TN_CONTRACT_INT8_OZAKI = 1 };
+TN_API tn_status tn_plan_set_contraction(tn_plan* plan, int mode, int slices);
+TN_API tn_status tn_plan_get_contraction(const tn_plan* plan, int* mode, int* slices);
+
 /* ------------------------------------------------------------------------------------------ */
 /* U builder (K2) — Eq. S4, "O(d^4) for initializing U".        */
 /* ------------------------------------------------------------------------------------------ */

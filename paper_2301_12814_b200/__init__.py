@@ -16,9 +16,9 @@ import numpy as np
 import torch
 
 from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT, TN_GATHER_NONE,
-                   TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, LIB_PATH)
+                   TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH)
 
-__all__ = ["Plan", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
+__all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
            "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
 
 
@@ -117,6 +117,17 @@ class Plan:
         n = C.c_int64()
         check(lib.tn_plan_u_size(self.handle, C.byref(n)), "tn_plan_u_size")
         return n.value
+
+    def set_contraction(self, mode, slices: int = 7):
+        """tn_plan_set_contraction: "dmma" (FP64 tensor cores) or "int8" (tcgen05 INT8 emulation)."""
+        m = {"dmma": TN_CONTRACT_F64_DMMA, "int8": TN_CONTRACT_INT8_OZAKI}.get(mode, mode)
+        check(lib.tn_plan_set_contraction(self.handle, int(m), int(slices)), "tn_plan_set_contraction")
+        return self
+
+    def contraction(self):
+        m, s = C.c_int(), C.c_int()
+        check(lib.tn_plan_get_contraction(self.handle, C.byref(m), C.byref(s)), "tn_plan_get_contraction")
+        return ("dmma" if m.value == TN_CONTRACT_F64_DMMA else "int8"), s.value
 
     def kernel_times(self):
         """Device ms of the most recent K1 (plan), K2, K3, K4, K5 launched with this plan (−1: not run)."""

@@ -18,6 +18,7 @@ STATUS = {0: "TN_OK", 1: "TN_ERR_DOMAIN", 2: "TN_ERR_DIMENSION", 3: "TN_ERR_CONS
           5: "TN_ERR_OOM", 6: "TN_ERR_NCCL", 7: "TN_ERR_UNSUPPORTED"}
 TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT = 0, 1, 2
 TN_GATHER_NONE, TN_GATHER_ROOT = 0, 1
+TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI = 0, 1
 TN_MAX_N, TN_MAX_MIX = 100, 64
 
 _p = C.c_void_p
@@ -38,6 +39,8 @@ SIGNATURES = {
     "tn_plan_u_size": [_p, _i64p],
     "tn_plan_workspace_bytes": [_p, _i64p],
     "tn_plan_kernel_times": [_p, _p],
+    "tn_plan_set_contraction": [_p, C.c_int, C.c_int],
+    "tn_plan_get_contraction": [_p, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "tn_release_cached_memory": [_i64p, _i64p],
     "tn_build_bs_unitary": [_p, C.c_double, C.c_double, _p, _p],
     "tn_theta_exec": [_p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],

@@ -1,6 +1,7 @@
 """Build libtn_theta.so in-tree with nvcc for sm_100a (no torch JIT cache; the .so travels with gpurun).
 
-Usage: python -m paper_2301_12814_b200.build [--force] [-v]
+Usage: python paper_2301_12814_b200/build.py [--force] [-v]
+(run it by path: importing the package requires the library this script builds)
 """
 from __future__ import annotations
 

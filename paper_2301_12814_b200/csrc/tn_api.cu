@@ -90,6 +90,7 @@ static void shard_bounds(const Counts& k, int world, std::vector<int64_t>& bound
 static void free_plan(tn_plan* p) {
   if (!p) return;
   const bool used = p->rec_exec;
+  pool_release(p->blk_oz, p->last_stream, used);
   pool_release(p->blk_work, p->last_stream, used);
   pool_release(p->blk_tab, p->last_stream, used);
   for (auto& e : p->ev)
@@ -506,6 +507,102 @@ tn_status tn_plan_workspace_bytes(const tn_plan* p, int64_t* bytes) {
   return TN_OK;
 }
 
+tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
+  if (!p) return fail(TN_ERR_DIMENSION, "tn_plan_set_contraction: NULL plan");
+  if (mode == TN_CONTRACT_F64_DMMA) {
+    p->contraction = mode;
+    return TN_OK;
+  }
+  if (mode != TN_CONTRACT_INT8_OZAKI) return fail(TN_ERR_DOMAIN, "tn_plan_set_contraction: unknown mode");
+  if (slices < OZ_SMIN || slices > OZ_SMAX) return fail(TN_ERR_DOMAIN, "tn_plan_set_contraction: slices outside [4, 8]");
+  if (p->blk_oz && p->oz_slices == slices) {
+    p->contraction = mode;
+    return TN_OK;
+  }
+  // (re)build the slice layout: same groups (center charges) as the DMMA path
+  if (p->blk_oz) {
+    cudaStreamSynchronize(p->last_stream);
+    pool_release(p->blk_oz, nullptr, false);
+    p->blk_oz = nullptr;
+  }
+  p->oz_groups.clear();
+  int64_t a_off = 0, b_off = 0, ea = 0, eb = 0;
+  p->oz_macs = 0;
+  for (const auto& gd : p->groups) {
+    OzGroup g{};
+    g.cc = gd.cc;
+    g.row0 = gd.row0;
+    g.col0 = gd.col0;
+    g.k0 = gd.k0;
+    g.R = gd.R;
+    g.C = gd.C;
+    g.K = gd.K;
+    g.Kp = (gd.K + OZ_BK - 1) / OZ_BK * OZ_BK;
+    g.nmt = (g.R + OZ_BM - 1) / OZ_BM;
+    g.nnt = (g.C + OZ_BN - 1) / OZ_BN;
+    g.nkc = g.Kp / OZ_BK;
+    g.a_off = a_off;
+    g.b_off = b_off;
+    g.ea_off = ea;
+    g.eb_off = eb;
+    a_off += (int64_t)g.nmt * g.nkc * 2 * slices * OZ_A_TILE;
+    b_off += (int64_t)g.nnt * g.nkc * 4 * slices * OZ_B_TILE;
+    ea += g.R;
+    eb += g.C;
+    p->oz_macs += (int64_t)g.nmt * g.nnt * 2 * g.nkc * (slices * (slices + 1) / 2) * 2 * OZ_BM * OZ_BN * OZ_BK;
+    p->oz_groups.push_back(g);
+  }
+  std::vector<int> order(p->oz_groups.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p->oz_groups[x].Kp > p->oz_groups[y].Kp; });
+  std::vector<OzTile> tiles;
+  for (int gi : order)
+    for (int mt = 0; mt < p->oz_groups[gi].nmt; ++mt)
+      for (int nt = 0; nt < p->oz_groups[gi].nnt; ++nt) tiles.push_back(OzTile{gi, mt, nt, 0});
+  p->oz_ntiles = (int64_t)tiles.size();
+  if (p->oz_groups.empty()) {
+    p->oz_slices = slices;
+    p->contraction = mode;
+    return TN_OK;
+  }
+  Carver cw;
+  const size_t o_g = cw.take<OzGroup>((int64_t)p->oz_groups.size());
+  const size_t o_t = cw.take<OzTile>((int64_t)tiles.size());
+  const size_t o_ea = cw.take<int32_t>(ea);
+  const size_t o_eb = cw.take<int32_t>(eb);
+  const size_t o_a = cw.take<int8_t>(a_off);
+  const size_t o_b = cw.take<int8_t>(b_off);
+  cudaError_t aerr = cudaSuccess;
+  p->blk_oz = pool_alloc(cw.off, &aerr);
+  if (aerr != cudaSuccess) return cuda_check(aerr, "pool alloc (INT8 emulation workspace)");
+  char* base = static_cast<char*>(p->blk_oz);
+  p->d_oz_groups = reinterpret_cast<OzGroup*>(base + o_g);
+  p->d_oz_tiles = reinterpret_cast<OzTile*>(base + o_t);
+  p->d_oea = reinterpret_cast<int32_t*>(base + o_ea);
+  p->d_oeb = reinterpret_cast<int32_t*>(base + o_eb);
+  p->d_oa = reinterpret_cast<int8_t*>(base + o_a);
+  p->d_ob = reinterpret_cast<int8_t*>(base + o_b);
+  tn_status st = cuda_check(cudaMemcpyAsync(p->d_oz_groups, p->oz_groups.data(), p->oz_groups.size() * sizeof(OzGroup),
+                                            cudaMemcpyHostToDevice, p->plan_stream), "H2D oz groups");
+  if (st != TN_OK) return st;
+  st = cuda_check(cudaMemcpyAsync(p->d_oz_tiles, tiles.data(), tiles.size() * sizeof(OzTile), cudaMemcpyHostToDevice,
+                                  p->plan_stream), "H2D oz tiles");
+  if (st != TN_OK) return st;
+  st = cuda_check(cudaStreamSynchronize(p->plan_stream), "oz tables sync");
+  if (st != TN_OK) return st;
+  p->ws_bytes += (int64_t)cw.off;
+  p->oz_slices = slices;
+  p->contraction = mode;
+  return TN_OK;
+}
+
+tn_status tn_plan_get_contraction(const tn_plan* p, int* mode, int* slices) {
+  if (!p || !mode || !slices) return fail(TN_ERR_DIMENSION, "tn_plan_get_contraction: NULL");
+  *mode = p->contraction;
+  *slices = p->contraction == TN_CONTRACT_INT8_OZAKI ? p->oz_slices : 0;
+  return TN_OK;
+}
+
 tn_status tn_plan_kernel_times(const tn_plan* p, float* ms) {
   if (!p || !ms) return fail(TN_ERR_DIMENSION, "tn_plan_kernel_times: NULL");
   for (int i = 0; i < 5; ++i) ms[i] = -1.0f;
@@ -558,12 +655,15 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   p->rec_exec = true;  // the workspace is in use from here on (pool release fence)
   tn_status st = cuda_check(cudaEventRecord(p->ev[4], s), "event");
   if (st != TN_OK) return st;
-  st = cuda_check(launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
-                               reinterpret_cast<const double2*>(gamma_k1), s),
+  const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
+  st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                                        reinterpret_cast<const double2*>(gamma_k1), s)
+                      : launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                                     reinterpret_cast<const double2*>(gamma_k1), s),
                   "K3 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;
-  st = cuda_check(launch_contract(p, sp, s), "K4 launch");
+  st = cuda_check(emu ? launch_oz_contract(p, sp, s) : launch_contract(p, sp, s), "K4 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
   st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");

@@ -50,6 +50,30 @@ struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive c
 
 constexpr int MAXC = TN_MAX_N + 1;
 
+// ---------------------------------------------------------------------------------------------
+// INT8 tensor-core emulation of the FP64 contraction (Ozaki splitting; DESIGN.md §4 "K3O/K4O").
+//   Tile: OZ_BM rows × OZ_BN columns of one group, K consumed in OZ_BK-byte steps (one UMMA K).
+//   A (R×K) and B (K×C) are split into S signed 7-bit slices with per-row / per-column power-of-two
+//   scales; slice products accumulate exactly in int32 TMEM, one accumulator per diagonal p+q.
+// ---------------------------------------------------------------------------------------------
+constexpr int OZ_BM = 128;
+constexpr int OZ_BN = 64;
+constexpr int OZ_BK = 32;
+constexpr int OZ_SMIN = 4, OZ_SMAX = 8;
+constexpr int OZ_A_TILE = OZ_BM * OZ_BK;  // bytes of one A slice tile (canonical K-major layout)
+constexpr int OZ_B_TILE = OZ_BN * OZ_BK;  // bytes of one B slice tile
+
+struct OzGroup {
+  int64_t a_off, b_off;     // byte offsets of this group's A / B slice tiles
+  int64_t ea_off, eb_off;   // offsets of its row / column exponents (int32)
+  int64_t row0, col0, k0;   // sorted positions of the first row / column / center bond
+  int32_t R, C, K, Kp;      // local rows, cols, K, K padded to OZ_BK
+  int32_t nmt, nnt, nkc, cc;
+};
+struct OzTile {
+  int32_t g, mt, nt, pad;
+};
+
 // Per-sector tables passed BY VALUE as a kernel parameter (no device copy needed).
 struct SectorParams {
   double2* out[MAXC];       // this rank's slab of Θ(c) (row-major, ld = C_c)
@@ -98,6 +122,19 @@ struct tn_plan {
   cudaEvent_t ev[8] = {};
   mutable bool rec_k1 = false, rec_k2 = false, rec_exec = false;
   mutable cudaStream_t last_stream = nullptr;  // stream of the last exec (pool release fence)
+  // contraction mode (TN_CONTRACT_*) and the INT8-emulation layout (built by tn_plan_set_contraction)
+  int contraction = TN_CONTRACT_F64_DMMA;
+  int oz_slices = 0;
+  std::vector<tn::OzGroup> oz_groups;
+  tn::OzGroup* d_oz_groups = nullptr;
+  tn::OzTile* d_oz_tiles = nullptr;
+  int64_t oz_ntiles = 0;
+  int8_t* d_oa = nullptr;
+  int8_t* d_ob = nullptr;
+  int32_t* d_oea = nullptr;
+  int32_t* d_oeb = nullptr;
+  void* blk_oz = nullptr;
+  int64_t oz_macs = 0;                         // int8 MACs one exec issues
 };
 
 namespace tn {
@@ -123,6 +160,9 @@ cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const doub
 cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
                          cudaStream_t s);
 cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
+cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
+                            cudaStream_t s);
+cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s);
 void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out);

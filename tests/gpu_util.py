@@ -14,11 +14,14 @@ def to_dev(case):
                 lr=torch.from_numpy(np.ascontiguousarray(case.lam_r)).to(dv))
 
 
-def gpu_theta(case, world_size=1, rank=0, U=None, plan=None):
-    """(plan, U, list of numpy sector slabs) computed entirely by libtn_theta.so."""
+def gpu_theta(case, world_size=1, rank=0, U=None, plan=None, contraction=None):
+    """(plan, U, list of numpy sector slabs) computed entirely by libtn_theta.so.
+    `contraction` = None (plan default, FP64 DMMA) or ("int8", slices) for the tcgen05 INT8 emulation."""
     import paper_2301_12814_b200 as tn
     if plan is None:
         plan = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r, world_size, rank)
+    if contraction is not None:
+        plan.set_contraction(*contraction)
     if U is None:
         U = tn.build_bs_unitary(plan, case.theta, case.phi)
     t = to_dev(case)

@@ -17,6 +17,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--gate", type=int, default=0)
+ap.add_argument("--contraction", default="dmma")
+ap.add_argument("--slices", type=int, default=7)
 a = ap.parse_args()
 
 case = synth.make_config(a.config, gate=a.gate)
@@ -30,6 +32,7 @@ for r in range(a.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     plan = tn.Plan(case.d, case.N, ql, qc, qr)
+    plan.set_contraction(a.contraction, a.slices)
     t_plan = (time.perf_counter() - t0) * 1e3
     if outs is None:
         outs = tn.alloc_theta(plan)
