@@ -187,9 +187,8 @@ constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(O
                               ((uint32_t)(OZ_BM >> 4) << 24);  // s8×s8→s32, K-major, M=128, N=64
 
 constexpr int OZ_THREADS = 10 * 32;
-constexpr int OZ_STAGES = 2;
 
-template <int S>
+template <int S, int OZ_STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k4o_contract(const OzGroup* __restrict__ groups, const OzTile* __restrict__ tiles, int ntiles,
                  const int8_t* __restrict__ oa, const int8_t* __restrict__ ob, const int32_t* __restrict__ oea,
@@ -201,8 +200,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + OZ_STAGES * B_STAGE);
   uint64_t* empty = full + OZ_STAGES;
   uint64_t* acc_full = empty + OZ_STAGES;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* acc_empty = acc_full + 1;  // one per diagonal m = 2..S+1 (index m − 2)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + S);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -211,7 +210,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       ob_init(&empty[s], 1);
     }
     ob_init(acc_full, 1);
-    ob_init(acc_empty, 8);  // the 8 epilogue warps
+    for (int m = 0; m < S; ++m) ob_init(&acc_empty[m], 8);  // the 8 epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -256,26 +255,39 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const OzTile td = tiles[t];
         const OzGroup g = groups[td.g];
         for (int pass = 0; pass < 2; ++pass) {
-          ob_wait(acc_empty, acc_phase ^ 1);  // the epilogue has drained the accumulators
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           for (int kc = 0; kc < g.nkc; ++kc) {
             ob_wait(&full[stage], phase);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a0 = s32(sA + stage * A_STAGE), b0 = s32(sB + stage * B_STAGE);
-#pragma unroll
-            for (int p = 1; p <= S; ++p)
-#pragma unroll
-              for (int q = 1; q <= S + 1 - p; ++q)
-#pragma unroll
-                for (int prod = 0; prod < 2; ++prod) {
-                  const uint64_t da = oz_desc(a0 + (prod * S + p - 1) * OZ_A_TILE);
-                  const uint64_t db = oz_desc(b0 + (prod * S + q - 1) * OZ_B_TILE);
-                  const uint32_t d = tmem + (uint32_t)(p + q - 2) * OZ_BN;
-                  const uint32_t acc = (kc == 0 && p == 1 && prod == 0) ? 0u : 1u;
-                  asm volatile("{\n .reg .pred pp;\n setp.ne.b32 pp, %4, 0;\n"
-                               " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp;\n}\n" ::"r"(d),
-                               "l"(da), "l"(db), "r"(OZ_IDESC), "r"(acc));
+            auto mma = [&](int p, int q, int prod, uint32_t acc) {
+              const uint64_t da = oz_desc(a0 + (prod * S + p - 1) * OZ_A_TILE);
+              const uint64_t db = oz_desc(b0 + (prod * S + q - 1) * OZ_B_TILE);
+              const uint32_t d = tmem + (uint32_t)(p + q - 2) * OZ_BN;
+              asm volatile("{\n .reg .pred pp;\n setp.ne.b32 pp, %4, 0;\n"
+                           " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp;\n}\n" ::"r"(d),
+                           "l"(da), "l"(db), "r"(OZ_IDESC), "r"(acc));
+            };
+            if (kc == 0) {
+              // first K step of a pass: diagonal by diagonal, each only once the epilogue has drained it
+              // (per-diagonal release overlaps the previous pass's epilogue with these MMAs)
+#pragma unroll 1
+              for (int m = 2; m <= S + 1; ++m) {
+                ob_wait(&acc_empty[m - 2], acc_phase ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int p = (m - S > 1 ? m - S : 1); p <= (m - 1 < S ? m - 1 : S); ++p) {
+                  mma(p, m - p, 0, p == (m - S > 1 ? m - S : 1) ? 0u : 1u);
+                  mma(p, m - p, 1, 1u);
                 }
+              }
+            } else {
+#pragma unroll 1
+              for (int p = 1; p <= S; ++p)
+#pragma unroll 1
+                for (int q = 1; q <= S + 1 - p; ++q) {
+                  mma(p, q, 0, 1u);
+                  mma(p, q, 1, 1u);
+                }
+            }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              s32(&empty[stage]))
                          : "memory");
@@ -301,6 +313,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const OzGroup g = groups[td.g];
       const int row = td.mt * OZ_BM + quad * 32 + lane;
       const int col0 = td.nt * OZ_BN + half * 32;
+      // exponents first (global loads off the accumulator critical path)
+      const int er = row < g.R ? oea[g.ea_off + row] : 0;
+      // lane j holds the exponent of column col0 + j (broadcast with shuffles below)
+      const int ec_lane = (col0 + lane < g.C) ? oeb[g.eb_off + col0 + lane] : 0;
       double re[32];
       for (int pass = 0; pass < 2; ++pass) {
         ob_wait(acc_full, acc_phase);
@@ -308,12 +324,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         double v[32];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {  // two 16-column halves keep the live registers low
-          double w16[16];
+        for (int j = 0; j < 32; ++j) v[j] = 0.0;
+#pragma unroll 1
+        for (int m = 2; m <= S + 1; ++m) {
+          const double w = ldexp(1.0, -7 * m);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) w16[j] = 0.0;
-#pragma unroll
-          for (int m = 2; m <= S + 1; ++m) {
+          for (int hh = 0; hh < 2; ++hh) {
             uint32_t r[16];
             const uint32_t ta =
                 tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(m - 2) * OZ_BN + half * 32 + hh * 16;
@@ -325,31 +341,24 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                   "=r"(r[15])
                 : "r"(ta));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const double w = ldexp(1.0, -7 * m);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) w16[j] = fma((double)(int32_t)r[j], w, w16[j]);
+            for (int j = 0; j < 16; ++j) v[hh * 16 + j] = fma((double)(int32_t)r[j], w, v[hh * 16 + j]);
           }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[hh * 16 + j] = w16[j];
+          // diagonal m drained: the MMA warp may overwrite it for the next pass
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) ob_arrive(&acc_empty[m - 2]);
         }
-        // accumulators drained: let the MMA warp start the next pass
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) ob_arrive(acc_empty);
-        const int er = row < g.R ? oea[g.ea_off + row] : 0;
         if (pass == 0) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + j;
-            const int ec = col < g.C ? oeb[g.eb_off + col] : 0;
-            re[j] = ldexp(v[j], er + ec);
-          }
-        } else if (row < g.R) {
+          for (int j = 0; j < 32; ++j) re[j] = ldexp(v[j], er + __shfl_sync(0xffffffffu, ec_lane, j));
+        } else {
           double2* orow = sp.out[g.cc] + (int64_t)row * sp.ld[g.cc];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = col0 + j;
-            if (col < g.C) orow[col] = make_double2(re[j], ldexp(v[j], er + oeb[g.eb_off + col]));
+            const int ecj = __shfl_sync(0xffffffffu, ec_lane, j);  // whole warp participates
+            if (row < g.R && col < g.C) orow[col] = make_double2(re[j], ldexp(v[j], er + ecj));
           }
         }
       }
@@ -390,23 +399,31 @@ cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* l
   return cudaErrorInvalidValue;
 }
 
-template <int S>
-static cudaError_t contract_s(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
-  const size_t smem = (size_t)OZ_STAGES * 2 * S * (OZ_A_TILE + OZ_B_TILE) + 8 * (2 * OZ_STAGES + 2) + 16;
-  cudaError_t e = cudaFuncSetAttribute(k4o_contract<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int S, int STG>
+static cudaError_t contract_st(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
+  const size_t smem = (size_t)STG * 2 * S * (OZ_A_TILE + OZ_B_TILE) + 8 * (2 * STG + 1 + S) + 16;
+  cudaError_t e = cudaFuncSetAttribute(k4o_contract<S, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p->oz_ntiles, p->sm_count);
-  k4o_contract<S><<<grid, OZ_THREADS, smem, s>>>(p->d_oz_groups, p->d_oz_tiles, (int)p->oz_ntiles, p->d_oa, p->d_ob,
-                                                 p->d_oea, p->d_oeb, sp);
+  k4o_contract<S, STG><<<grid, OZ_THREADS, smem, s>>>(p->d_oz_groups, p->d_oz_tiles, (int)p->oz_ntiles, p->d_oa,
+                                                      p->d_ob, p->d_oea, p->d_oeb, sp);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k4o_contract<S>);
+    cudaFuncGetAttributes(&fa, k4o_contract<S, STG>);
     fprintf(stderr, "k4o launch failed: %s regs=%d maxthreads=%d static_smem=%zu dyn_smem=%zu max_dyn=%d local=%zu\n",
             cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem,
             fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
   }
   return e;
+}
+
+// deepest TMA ring that fits in ~220 KB of shared memory
+template <int S>
+static cudaError_t contract_s(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
+  constexpr int stage = 2 * S * (OZ_A_TILE + OZ_B_TILE);
+  if constexpr (3 * stage <= 220 * 1024) return contract_st<S, 3>(p, sp, s);
+  else return contract_st<S, 2>(p, sp, s);
 }
 
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {

@@ -128,6 +128,78 @@ int run() {
   return bad != 0;
 }
 
+// Throughput: every SM issues ITER × 56 back-to-back M=128×N×K=32 int8 MMAs on resident smem operands
+template <int N>
+__global__ void umma_rate(int iters, int32_t* sink) {
+  constexpr int K = 32;
+  __shared__ __align__(1024) int8_t As[4][M * K];
+  __shared__ __align__(1024) int8_t Bs[2][N * K];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 4 * M * K; i += blockDim.x) (&As[0][0])[i] = (int8_t)(i * 7);
+  for (int i = tid; i < 2 * N * K; i += blockDim.x) (&Bs[0][0])[i] = (int8_t)(i * 3);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = make_idesc_i8(M, N);
+    uint32_t phase = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int j = 0; j < 56; ++j) {
+        const uint64_t da = make_desc(su32(As[j & 3]), 128, 256);
+        const uint64_t db = make_desc(su32(Bs[(j >> 2) & 1]), 128, 256);
+        const uint32_t d = tmem + (uint32_t)((j % (512 / N)) * N);
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                     " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                     "l"(da), "l"(db), "r"(idesc), "r"(1u));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
+                   : "memory");
+      if (it >= 2) {  // keep ≤ 2 commit groups in flight
+        uint32_t done = 0;
+        while (!done)
+          asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                       : "=r"(done) : "r"(su32(&mbar)), "r"(phase) : "memory");
+        phase ^= 1;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) sink[blockIdx.x] = 1;
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int N>
+void rate() {
+  int32_t* sink; cudaMalloc(&sink, 1024 * 4);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  umma_rate<N><<<sms, 128>>>(10, sink);
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int iters = 2000;
+  cudaEventRecord(e0);
+  umma_rate<N><<<sms, 128>>>(iters, sink);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  const double macs = (double)sms * iters * 56 * M * N * 32;
+  printf("{\"test\": \"umma_i8_rate\", \"N\": %d, \"ms\": %.3f, \"TOPS\": %.1f, \"err\": \"%s\"}\n", N, ms,
+         2 * macs / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(sink);
+}
+
 int main() {
   int fails = 0;
   fails += run<64, 64>();
@@ -135,5 +207,8 @@ int main() {
   fails += run<128, 96>();
   fails += run<16, 32>();
   printf("{\"umma_i8_all_ok\": %s}\n", fails ? "false" : "true");
+  rate<64>();
+  rate<128>();
+  rate<256>();
   return fails;
 }
