@@ -188,16 +188,26 @@ constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(O
 
 constexpr int OZ_THREADS = 10 * 32;
 
+// One ring stage = one "half step": A plane h (S slices, 128×32 each) and B plane 2·pass + h (S slices,
+// 64×32 each) of one K step of one tile; the Re pass pairs (Ar, Br), (Ai, −Bi), the Im pass (Ar, Bi),
+// (Ai, Br). Small stages let the ring run 5–6 deep (the v1 ring of whole K steps was only 2 deep).
+template <int S>
+__device__ __forceinline__ void oz_mma(uint32_t d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile("{\n .reg .pred pp;\n setp.ne.b32 pp, %4, 0;\n"
+               " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp;\n}\n" ::"r"(d),
+               "l"(da), "l"(db), "r"(OZ_IDESC), "r"(acc));
+}
+
 template <int S, int OZ_STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k4o_contract(const OzGroup* __restrict__ groups, const OzTile* __restrict__ tiles, int ntiles,
                  const int8_t* __restrict__ oa, const int8_t* __restrict__ ob, const int32_t* __restrict__ oea,
                  const int32_t* __restrict__ oeb, const SectorParams sp) {
-  constexpr int A_STAGE = 2 * S * OZ_A_TILE, B_STAGE = 2 * S * OZ_B_TILE;
+  constexpr int A_HS = S * OZ_A_TILE, B_HS = S * OZ_B_TILE;   // one plane of one K step
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
-  uint8_t* sB = smem + OZ_STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + OZ_STAGES * B_STAGE);
+  uint8_t* sB = smem + OZ_STAGES * A_HS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + OZ_STAGES * B_HS);
   uint64_t* empty = full + OZ_STAGES;
   uint64_t* acc_full = empty + OZ_STAGES;
   uint64_t* acc_empty = acc_full + 1;  // one per diagonal m = 2..S+1 (index m − 2)
@@ -230,20 +240,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const OzTile td = tiles[t];
         const OzGroup g = groups[td.g];
+        const int8_t* a_t = oa + g.a_off + (int64_t)td.mt * g.nkc * 2 * A_HS;
+        const int8_t* b_t = ob + g.b_off + (int64_t)td.nt * g.nkc * 4 * B_HS;
         for (int pass = 0; pass < 2; ++pass)
-          for (int kc = 0; kc < g.nkc; ++kc) {
-            ob_wait(&empty[stage], phase ^ 1);
-            ob_expect_tx(&full[stage], A_STAGE + B_STAGE);
-            ob_bulk(sA + stage * A_STAGE, oa + g.a_off + (int64_t)(td.mt * g.nkc + kc) * A_STAGE, A_STAGE,
-                    &full[stage]);
-            ob_bulk(sB + stage * B_STAGE,
-                    ob + g.b_off + (int64_t)(td.nt * g.nkc + kc) * (2 * B_STAGE) + pass * B_STAGE, B_STAGE,
-                    &full[stage]);
-            if (++stage == OZ_STAGES) {
-              stage = 0;
-              phase ^= 1;
+          for (int kc = 0; kc < g.nkc; ++kc)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              ob_wait(&empty[stage], phase ^ 1);
+              ob_expect_tx(&full[stage], A_HS + B_HS);
+              ob_bulk(sA + stage * A_HS, a_t + (int64_t)(kc * 2 + h) * A_HS, A_HS, &full[stage]);
+              ob_bulk(sB + stage * B_HS, b_t + (int64_t)(kc * 4 + pass * 2 + h) * B_HS, B_HS, &full[stage]);
+              if (++stage == OZ_STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
             }
-          }
       }
     }
   } else if (warp == 1) {
@@ -252,48 +263,44 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const OzTile td = tiles[t];
-        const OzGroup g = groups[td.g];
+        const int nkc = groups[tiles[t].g].nkc;
         for (int pass = 0; pass < 2; ++pass) {
-          for (int kc = 0; kc < g.nkc; ++kc) {
-            ob_wait(&full[stage], phase);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a0 = s32(sA + stage * A_STAGE), b0 = s32(sB + stage * B_STAGE);
-            auto mma = [&](int p, int q, int prod, uint32_t acc) {
-              const uint64_t da = oz_desc(a0 + (prod * S + p - 1) * OZ_A_TILE);
-              const uint64_t db = oz_desc(b0 + (prod * S + q - 1) * OZ_B_TILE);
-              const uint32_t d = tmem + (uint32_t)(p + q - 2) * OZ_BN;
-              asm volatile("{\n .reg .pred pp;\n setp.ne.b32 pp, %4, 0;\n"
-                           " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pp;\n}\n" ::"r"(d),
-                           "l"(da), "l"(db), "r"(OZ_IDESC), "r"(acc));
-            };
-            if (kc == 0) {
-              // first K step of a pass: diagonal by diagonal, each only once the epilogue has drained it
-              // (per-diagonal release overlaps the previous pass's epilogue with these MMAs)
-#pragma unroll 1
-              for (int m = 2; m <= S + 1; ++m) {
-                ob_wait(&acc_empty[m - 2], acc_phase ^ 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (int p = (m - S > 1 ? m - S : 1); p <= (m - 1 < S ? m - 1 : S); ++p) {
-                  mma(p, m - p, 0, p == (m - S > 1 ? m - S : 1) ? 0u : 1u);
-                  mma(p, m - p, 1, 1u);
+          for (int kc = 0; kc < nkc; ++kc) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              ob_wait(&full[stage], phase);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              // descriptor of slice p = base + p·tile bytes (16-byte units; no carry out of the 14-bit field)
+              const uint64_t da = oz_desc(s32(sA + stage * A_HS)), db = oz_desc(s32(sB + stage * B_HS));
+              if (kc == 0 && h == 0) {
+                // first half step of a pass: diagonal by diagonal, each once the epilogue has drained it
+#pragma unroll
+                for (int m = 2; m <= S + 1; ++m) {
+                  ob_wait(&acc_empty[m - 2], acc_phase ^ 1);
+                  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                  for (int p = 1; p <= S; ++p) {
+                    const int q = m - p;
+                    if (q < 1 || q > S) continue;
+                    oz_mma<S>(tmem + (uint32_t)(m - 2) * OZ_BN, da + (uint64_t)((p - 1) * OZ_A_TILE >> 4),
+                              db + (uint64_t)((q - 1) * OZ_B_TILE >> 4), p == (m - S > 1 ? m - S : 1) ? 0u : 1u);
+                  }
                 }
+              } else {
+#pragma unroll
+                for (int p = 1; p <= S; ++p)
+#pragma unroll
+                  for (int q = 1; q <= S + 1 - p; ++q)
+                    oz_mma<S>(tmem + (uint32_t)(p + q - 2) * OZ_BN, da + (uint64_t)((p - 1) * OZ_A_TILE >> 4),
+                              db + (uint64_t)((q - 1) * OZ_B_TILE >> 4), 1u);
               }
-            } else {
-#pragma unroll 1
-              for (int p = 1; p <= S; ++p)
-#pragma unroll 1
-                for (int q = 1; q <= S + 1 - p; ++q) {
-                  mma(p, q, 0, 1u);
-                  mma(p, q, 1, 1u);
-                }
-            }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             s32(&empty[stage]))
-                         : "memory");
-            if (++stage == OZ_STAGES) {
-              stage = 0;
-              phase ^= 1;
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               s32(&empty[stage]))
+                           : "memory");
+              if (++stage == OZ_STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
             }
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -401,7 +408,7 @@ cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* l
 
 template <int S, int STG>
 static cudaError_t contract_st(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
-  const size_t smem = (size_t)STG * 2 * S * (OZ_A_TILE + OZ_B_TILE) + 8 * (2 * STG + 1 + S) + 16;
+  const size_t smem = (size_t)STG * S * (OZ_A_TILE + OZ_B_TILE) + 8 * (2 * STG + 1 + S) + 16;
   cudaError_t e = cudaFuncSetAttribute(k4o_contract<S, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p->oz_ntiles, p->sm_count);
@@ -418,12 +425,14 @@ static cudaError_t contract_st(const tn_plan* p, const SectorParams& sp, cudaStr
   return e;
 }
 
-// deepest TMA ring that fits in ~220 KB of shared memory
+// deepest TMA ring of half steps that fits in the 227 KB opt-in shared memory (S=6: 6, S=7: 5, S=8: 4)
 template <int S>
 static cudaError_t contract_s(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
-  constexpr int stage = 2 * S * (OZ_A_TILE + OZ_B_TILE);
-  if constexpr (3 * stage <= 220 * 1024) return contract_st<S, 3>(p, sp, s);
-  else return contract_st<S, 2>(p, sp, s);
+  constexpr int stage = S * (OZ_A_TILE + OZ_B_TILE);
+  constexpr int limit = 227 * 1024 - 512;
+  if constexpr (6 * stage <= limit) return contract_st<S, 6>(p, sp, s);
+  else if constexpr (5 * stage <= limit) return contract_st<S, 5>(p, sp, s);
+  else return contract_st<S, 4>(p, sp, s);
 }
 
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {

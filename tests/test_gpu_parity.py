@@ -320,3 +320,56 @@ def test_error_codes(tn):
     outs[1] = None                                         # NULL for a non-empty sector
     with pytest.raises(tn.TnError, match="DIMENSION"):
         tn.theta_exec(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U, out=outs)
+
+
+# ------------------------------------------------------------------ T10: φ shift; T11: padding invariance
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_metamorphic_phi_shift(tn, cfg):
+    # U_n[i][j] = e^{iφ(i−j)} U_n(θ,0)[i][j] with i − j = c_c − c, so
+    # Θ(c; θ, φ) = e^{−iφc} Θ'(c; θ, 0) where Γk1' has row α_k multiplied by e^{iφ q_c[α_k]}.
+    case = _case(cfg)
+    plan = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r)
+    _, _, got = gpu_theta(case, plan=plan)
+    shifted = synth.make_config(cfg)
+    shifted.gamma_k1 = shifted.gamma_k1 * np.exp(1j * case.phi * case.q_c)[:, None]
+    _, _, got0 = gpu_theta(shifted, plan=plan, U=tn.build_bs_unitary(plan, case.theta, 0.0))
+    for c in range(case.N + 1):
+        assert rel_err(got[c], np.exp(-1j * case.phi * c) * got0[c]) < 1e-11, c
+
+
+@pytest.mark.parametrize("cfg,extra", [(1, (37, 61, 45)), (2, (129, 3, 200))])
+def test_padding_invariance(tn, cfg, extra):
+    # T11: extra bonds move every tile and segment boundary but must not change Θ on the
+    # original (α, β). Extra left/right bonds carry random Γ (their rows/cols are new rows/cols of Θ);
+    # extra centre bonds carry random Γ but λk = 0, so they add exact zeros to every contraction.
+    case = _case(cfg)
+    rng = np.random.default_rng(77)
+    el, ec, er = extra
+    N, d = case.N, case.d
+    q = [np.concatenate([qq, rng.integers(0, N + 1, e).astype(np.int32)]) for qq, e in
+         zip((case.q_l, case.q_c, case.q_r), extra)]
+    allowed = lambda a, b: ((a[:, None] - b[None, :] >= 0) & (a[:, None] - b[None, :] <= d - 1))
+    cn = lambda *s: (rng.standard_normal(s) + 1j * rng.standard_normal(s)) / math.sqrt(2)
+    gk = cn(case.chi_l + el, case.chi_c + ec)
+    gk[:case.chi_l, :case.chi_c] = case.gamma_k
+    gk1 = cn(case.chi_c + ec, case.chi_r + er)
+    gk1[:case.chi_c, :case.chi_r] = case.gamma_k1
+    big = synth.Case("padded", N, d, q[0], q[1], q[2], gk * allowed(q[0], q[1]), gk1 * allowed(q[1], q[2]),
+                     np.concatenate([case.lam_l, rng.random(el)]), np.concatenate([case.lam_k, np.zeros(ec)]),
+                     np.concatenate([case.lam_r, rng.random(er)]), case.theta, case.phi)
+    pa = tn.Plan(d, N, case.q_l, case.q_c, case.q_r)
+    pb = tn.Plan(d, N, big.q_l, big.q_c, big.q_r)
+    _, _, a = gpu_theta(case, plan=pa)
+    _, _, b = gpu_theta(big, plan=pb)
+    inv_l, inv_r = np.argsort(pa.perm(0)), np.argsort(pa.perm(2))
+    for c in range(N + 1):
+        (r0, r1), (k0, k1) = oracle.sector_ranges(pa.offsets(0), pa.offsets(2), N, d, c)
+        (s0, s1), (m0, m1) = oracle.sector_ranges(pb.offsets(0), pb.offsets(2), N, d, c)
+        bl, br = pb.perm(0)[s0:s1], pb.perm(2)[m0:m1]
+        rows = np.nonzero(bl < case.chi_l)[0]
+        cols = np.nonzero(br < case.chi_r)[0]
+        sub = b[c][np.ix_(rows, cols)]
+        ra = inv_l[bl[rows]] - r0
+        ca = inv_r[br[cols]] - k0
+        assert sub.shape == a[c].shape
+        assert rel_err(sub, a[c][np.ix_(ra, ca)]) < 1e-13, c
