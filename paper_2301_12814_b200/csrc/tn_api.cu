@@ -519,6 +519,10 @@ tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
     p->contraction = mode;
     return TN_OK;
   }
+  // exactness of the int32 diagonal accumulators (and of the S ≤ 6 int64 recombination) needs K ≤ 2048
+  for (const auto& gd : p->groups)
+    if (gd.K > OZ_KMAX)
+      return fail(TN_ERR_UNSUPPORTED, "tn_plan_set_contraction: a centre charge segment exceeds 2048 bonds (INT8 emulation)");
   // (re)build the slice layout: same groups (center charges) as the DMMA path
   if (p->blk_oz) {
     cudaStreamSynchronize(p->last_stream);
@@ -546,7 +550,7 @@ tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
     g.ea_off = ea;
     g.eb_off = eb;
     a_off += (int64_t)g.nmt * g.nkc * 2 * slices * OZ_A_TILE;
-    b_off += (int64_t)g.nnt * g.nkc * 4 * slices * OZ_B_TILE;
+    b_off += (int64_t)g.nnt * g.nkc * 3 * slices * OZ_B_TILE;
     ea += g.R;
     eb += g.C;
     p->oz_macs += (int64_t)g.nmt * g.nnt * 2 * g.nkc * (slices * (slices + 1) / 2) * 2 * OZ_BM * OZ_BN * OZ_BK;

@@ -60,6 +60,7 @@ constexpr int OZ_BM = 128;
 constexpr int OZ_BN = 64;
 constexpr int OZ_BK = 32;
 constexpr int OZ_SMIN = 4, OZ_SMAX = 8;
+constexpr int OZ_KMAX = 2048;             // largest centre segment the INT8 emulation accepts
 constexpr int OZ_A_TILE = OZ_BM * OZ_BK;  // bytes of one A slice tile (canonical K-major layout)
 constexpr int OZ_B_TILE = OZ_BN * OZ_BK;  // bytes of one B slice tile
 
