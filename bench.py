@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Θ-build useful complex FP64 GFLOP/s & gates/s at d=32,χ=4096; % FP64 TC peak"
 FP64_TC_PEAK_TFLOPS = 37.2   # measured: DMMA.8x8x4 loop, 148 SMs @ 1965 MHz (profiles/r01_fp64_peaks.jsonl)
-LAUNCHES_PER_STEP = 6        # K1 (1 launch, 3 CTAs), K2, K3a, K3b, K4, K5
+LAUNCHES_PER_STEP = 6        # K1 (1 launch, 3 CTAs), K2, K3a, K3b, K4, K5 (INT8 engine: K3O is 4 launches)
+INT8_UMMA_PEAK_TOPS = 4347.9  # measured tcgen05 kind::i8 M=128 N=256 (profiles/r01_umma_i8_test.log)
 
 
 def parse():
@@ -42,6 +43,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sectors", default="0,6,12,18,24,30")
+    ap.add_argument("--contraction", default="dmma", choices=["dmma", "int8"],
+                    help="K4 engine: FP64 DMMA (default) or the INT8 tcgen05 Ozaki emulation")
+    ap.add_argument("--slices", type=int, default=6, help="INT8 emulation slice count (6: ≤1e-11 rel error)")
+    ap.add_argument("--gates", type=int, default=32, help="config 4: gates of the brick-wall layer to time")
     return ap.parse_args()
 
 
@@ -214,9 +219,21 @@ def run_tn(args, rank, world, local_rank):
     tn.Plan(case.d, case.N, ql, qc, qr, world, rank).destroy()   # warm the module / pool
     torch.cuda.synchronize()
     probe = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)
+    int8 = args.contraction == "int8"
+    if int8:
+        probe.set_contraction("int8", args.slices)
     k1_isolated_ms = probe.kernel_times()["k1_sort"]   # K1 on an idle GPU (in the timed loop it overlaps)
     flops = probe.flops()
     f_useful = flops["f_contract"] + flops["f_mix"]
+    int8_ops = 0   # INT8 tensor ops (2 per MAC) one K4O launch executes, incl. tile padding
+    if int8:
+        offc = probe.offsets(1)
+        for cc in range(case.N + 1):
+            K = int(offc[cc + 1] - offc[cc])
+            R, Cc, _ = probe.local_sector_shape(cc)
+            if K and R and Cc:
+                int8_ops += 2 * (-(-R // 128) * 128) * (-(-Cc // 64) * 64) * (-(-K // 32) * 32) * 4 * (
+                    args.slices * (args.slices + 1) // 2)
     outs = tn.alloc_theta(probe, device=dev)
     U = torch.empty(probe.u_size(), dtype=torch.complex128, device=dev)
     del probe
@@ -224,6 +241,8 @@ def run_tn(args, rank, world, local_rank):
 
     def step(keep):
         plan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)          # K1 + decomposition
+        if int8:
+            plan.set_contraction("int8", args.slices)                      # slice layout (K3O/K4O)
         tn.build_bs_unitary(plan, case.theta, case.phi, out=U)            # K2
         tn.theta_exec(plan, gk, lk, gk1, ll, lr, U, out=outs)            # K3 → K4 → K5
         keep.append(plan)
@@ -340,6 +359,26 @@ def run_tn(args, rank, world, local_rank):
                          f"threads = host cores), useful flops of those sectors {f / 1e9:.2f} GFLOP in {dt:.1f} s; "
                          "U prebuilt with mpmath (not timed)"}
 
+    roofline = {"bound": "tensor", "kernel": "k4_contract", "achieved": round(achieved, 3),
+                "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_TC_PEAK_TFLOPS, 4),
+                "traffic": ncu_traffic(args.config),
+                "peak_source": "measured FP64 DMMA.8x8x4 rate (profiles/r01_fp64_peaks.jsonl; "
+                               "MEASURED_PEAKS.json has no FP64 entry)",
+                "achieved_def": "F_contract of this rank (useful complex FP64 flops, 8/CMAC) / mean K4 "
+                                "launch time (CUDA events on the exec stream, timed region)",
+                "note": "K4 forms complex products with 3 real DMMAs (Gauss), so useful 8-flop/CMAC throughput "
+                        "can exceed the 4-multiplication peak; dmma_pipe_frac is the real-DMMA utilisation",
+                "dmma_pipe_frac": round(dmma_real_tflops / FP64_TC_PEAK_TFLOPS, 4)}
+    if int8:
+        i8 = int8_ops / (k4_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": "k4o_contract (INT8 tcgen05, Ozaki S=%d)" % args.slices,
+                    "achieved": round(i8, 1), "peak": INT8_UMMA_PEAK_TOPS, "unit": "TOPS (int8)",
+                    "frac": round(i8 / INT8_UMMA_PEAK_TOPS, 4), "traffic": None,
+                    "peak_source": "measured tcgen05.mma kind::i8 M=128 N=256 rate (profiles/r01_umma_i8_test.log)",
+                    "achieved_def": "INT8 ops (2/MAC) of the slice products incl. 128x64x32 tile padding / mean "
+                                    "K4O launch time (CUDA events, timed region)",
+                    "useful_fp64_tflops": round(achieved, 3),
+                    "useful_frac_of_fp64_tc_peak": round(achieved / FP64_TC_PEAK_TFLOPS, 4)}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
@@ -348,25 +387,135 @@ def run_tn(args, rank, world, local_rank):
         "gates_per_s": round(1000.0 / ms_step, 3),
         "pct_fp64_tc_peak": round(100.0 * value / (FP64_TC_PEAK_TFLOPS * 1e3 * world), 2),
         "config": dict(workload_config(case, args.config), parallelism=f"rows{world}" if world > 1 else "single",
+                       contraction="dmma (FP64 tensor cores)" if not int8 else
+                       f"int8 tcgen05 Ozaki emulation, {args.slices} slices (≤1e-11 rel. error vs oracle)",
                        f_contract=flops["f_contract"], f_mix=flops["f_mix"], f_exec_rank0=flops["f_exec"],
                        step="tn_theta_plan + tn_build_bs_unitary + tn_theta_exec (all SURVEY §8(a) rows)"),
-        "roofline": {"bound": "tensor", "kernel": "k4_contract", "achieved": round(achieved, 3),
-                     "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_TC_PEAK_TFLOPS, 4),
-                     "traffic": ncu_traffic(args.config),
-                     "peak_source": "measured FP64 DMMA.8x8x4 rate (profiles/r01_fp64_peaks.jsonl; "
-                                    "MEASURED_PEAKS.json has no FP64 entry)",
-                     "achieved_def": "F_contract of this rank (useful complex FP64 flops, 8/CMAC) / mean K4 "
-                                     "launch time (CUDA events on the exec stream, timed region)",
-                     "note": "K4 forms complex products with 3 real DMMAs (Gauss), so useful 8-flop/CMAC throughput "
-                             "can exceed the 4-multiplication peak; dmma_pipe_frac is the real-DMMA utilisation",
-                     "dmma_pipe_frac": round(dmma_real_tflops / FP64_TC_PEAK_TFLOPS, 4)},
+        "roofline": roofline,
         "kernels": kernels,
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step_ms, 3)},
-        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "gpu_launches": (LAUNCHES_PER_STEP + (2 if int8 else 0)) * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------- config 4 sweep
+def run_sweep(args, rank, world, local_rank):
+    """BASELINE.json config 4: a brick-wall layer of `--gates` beam-splitter gates (N=47, d=48, χ=8192),
+    each with its own bond charges (synth.make_charges(4, g), identical to the parity inputs) and its own
+    Γ. Γ is drawn ON THE DEVICE (torch generator seeded per gate; same complex-normal distribution and
+    δ-allowed mask as synth/, different values) because 32 × 2 × 8192² host draws take minutes; timing
+    does not depend on the values, parity on config 4 is checked separately with synth/'s inputs.
+    Gate-parallel across ranks (the paper's first-level parallelism): rank r runs gates
+    r, r+N, …; no collective. One step = one gate: plan (K1) + U (K2) + exec (K3–K5), Θ buffers reused."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_12814_b200 as tn
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synth.CONFIGS[4]
+    N, d, chi = cfg["N"], cfg["d"], cfg["chi"]
+    mine = list(range(rank, args.gates, world))
+    lam = torch.from_numpy(0.995 ** np.arange(chi)).to(dev)
+    lam /= torch.linalg.vector_norm(lam)
+    gates = []
+    for g in mine:
+        _, _, ql, qc, qr = synth.make_charges(4, g)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(4_000_000 + g)
+        qd = [torch.from_numpy(q).to(dev) for q in (ql, qc, qr)]
+
+        def gamma(a, b):
+            m = ((a[:, None] - b[None, :]) >= 0) & ((a[:, None] - b[None, :]) <= d - 1)
+            x = torch.randn((chi, chi), generator=gen, device=dev, dtype=torch.float64)
+            y = torch.randn((chi, chi), generator=gen, device=dev, dtype=torch.float64)
+            return (torch.complex(x, y) / math.sqrt(2)) * m
+
+        rng = np.random.default_rng([4, g, 7])
+        gates.append(dict(q=qd, gk=gamma(qd[0], qd[1]), gk1=gamma(qd[1], qd[2]),
+                          theta=float(rng.uniform(0, math.pi / 2)), phi=float(rng.uniform(0, 2 * math.pi))))
+    # Θ buffers: per sector the largest slab over this rank's gates, reused by every gate
+    plans = [tn.Plan(d, N, *gt["q"]) for gt in gates]
+    for pl in plans:
+        pl.set_contraction(args.contraction, args.slices)
+    cap = [max(pl.sector_shape(c)[0] * pl.sector_shape(c)[1] for pl in plans) for c in range(N + 1)]
+    flops = [pl.flops() for pl in plans]
+    for pl in plans:
+        pl.destroy()
+    pool = [torch.empty(max(1, n), dtype=torch.complex128, device=dev) for n in cap]
+    U = torch.empty(38_024, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(gt, keep):
+        plan = tn.Plan(d, N, *gt["q"])
+        plan.set_contraction(args.contraction, args.slices)
+        outs = [pool[c][:plan.sector_shape(c)[0] * plan.sector_shape(c)[1]].view(*plan.sector_shape(c))
+                for c in range(N + 1)]
+        tn.build_bs_unitary(plan, gt["theta"], gt["phi"], out=U)
+        tn.theta_exec(plan, gt["gk"], lam, gt["gk1"], lam, lam, U, out=outs)
+        keep.append(plan)
+
+    keep = []
+    for i in range(args.warmup):
+        step(gates[i % len(gates)], keep)
+    torch.cuda.synchronize()
+    for p_ in keep:
+        p_.destroy()
+    keep.clear()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ktimes = []
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for gt in gates:
+            step(gt, keep)
+            if len(keep) > 2:
+                old = keep.pop(0)
+                ktimes.append(old.kernel_times())
+                old.destroy()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    for p_ in keep:
+        ktimes.append(p_.kernel_times())
+        p_.destroy()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    f_all = sum(f["f_contract"] + f["f_mix"] for f in flops)
+    if world > 1:
+        ft = torch.tensor([float(f_all)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ft)
+        f_all = ft.item()
+    if rank != 0:
+        return
+    exec_ms = sum(sum(v for k, v in kt.items() if k != "k1_sort") for kt in ktimes)
+    line = {"metric": "Θ-build gates/s (brick-wall layer, config 4) & useful complex FP64 GFLOP/s", "value":
+            round(args.gates / (ms_max * 1e-3), 3), "unit": "gates/s", "n_gpus": world, "steps": args.gates,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / len(mine), 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: synth/ charges per gate, Γ drawn on device (same distribution and δ mask)",
+            "useful_gflops": round(f_all / (ms_max * 1e-3) / 1e9, 1),
+            "pct_fp64_tc_peak": round(100 * f_all / (ms_max * 1e-3) / (FP64_TC_PEAK_TFLOPS * 1e12 * world), 2),
+            "exec_only_gates_per_s": round(len(mine) / (exec_ms * 1e-3), 3),
+            "config": {"workload": f"BASELINE.json config 4: {args.gates} gates of a brick-wall layer, N={N}, d={d}, "
+                                   f"chi={chi}, per-gate Gaussian charges", "parallelism": f"gates{world}",
+                       "contraction": args.contraction if args.contraction == "dmma" else f"int8x{args.slices}",
+                       "step": "per gate: tn_theta_plan + tn_build_bs_unitary + tn_theta_exec",
+                       "l2": "inputs larger than L2 (Γ 1.07 GB each per gate; Θ up to 7.5 GB)"},
+            "kernels_mean_ms": {k: round(statistics.mean(kt[k] for kt in ktimes), 4) for k in ktimes[0]},
+            "gpu_launches": (LAUNCHES_PER_STEP + (2 if args.contraction == "int8" else 0)) * len(mine),
+            "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 
 
@@ -384,7 +533,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_tn(args, rank, world, local_rank)
+        if args.config == 4:
+            run_sweep(args, rank, world, local_rank)
+        else:
+            run_tn(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -4,12 +4,13 @@
 // PAPER.md:94 "bond indices are sorted such that c_{α_k} only increases as the bond index
 // increases". Tie-break is stable (R1). One CTA per bond: histogram →
 // exclusive scan → chunked stable scatter (warp match_any ranks within a chunk). Latency-bound
-// (µs); it runs once per plan, off the hot path.
+// (µs); it runs once per plan, off the hot path, on the plan's own stream — its CTAs are sized to fit
+// next to the previous gate's K4/K5 so planning overlaps execution.
 #include "tn_internal.cuh"
 
 namespace tn {
 
-constexpr int SORT_THREADS = 1024;
+constexpr int SORT_THREADS = 256;   // small enough to co-reside with a running K4/K5 (next gate's plan)
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
 __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs args, int N) {

@@ -95,6 +95,7 @@ static void free_plan(tn_plan* p) {
   pool_release(p->blk_tab, p->last_stream, used);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
+  if (p->ev_ready) cudaEventDestroy(p->ev_ready);
   if (p->plan_stream) cudaStreamDestroy(p->plan_stream);
   delete p;
 }
@@ -221,6 +222,7 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   TN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev), "sm count");
   TN_TRY(cudaStreamCreateWithFlags(&p->plan_stream, cudaStreamNonBlocking), "plan stream");
   for (auto& e : p->ev) TN_TRY(cudaEventCreate(&e), "event create");
+  TN_TRY(cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming), "event create");
   // ---- one pool block for the bond tables (+ staging of host charges) ----
   for (int b = 0; b < 3; ++b) {
     o_perm[b] = ct.take<int32_t>(p->chi[b]);
@@ -382,14 +384,14 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
     std::vector<int> order(p->groups.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p->groups[x].K4 > p->groups[y].K4; });
-    std::vector<TileDesc> tiles;
+    std::vector<TileDesc>& tiles = p->h_tiles;
     for (int gi : order) {
       const auto& g = p->groups[gi];
       for (int mt = 0; mt < g.nmt; ++mt)
         for (int nt = 0; nt < g.nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
     }
     p->ntiles = (int64_t)tiles.size();
-    std::vector<MixTile> mix;
+    std::vector<MixTile>& mix = p->h_mix;
     build_mix_tiles(p, mix);
     p->nmix = (int64_t)mix.size();
     if (!p->groups.empty() || !mix.empty()) {
@@ -416,10 +418,11 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
       if (!mix.empty())
         TN_TRY(cudaMemcpyAsync(p->d_mix, mix.data(), mix.size() * sizeof(MixTile), cudaMemcpyHostToDevice,
                                p->plan_stream), "H2D mix tiles");
-      TN_TRY(cudaStreamSynchronize(p->plan_stream), "plan tables sync");
+      // no host sync: tn_theta_exec's stream waits for ev_ready (the host vectors stay alive in the plan)
       p->ws_bytes = (int64_t)cw.off;
     }
     p->ws_bytes += (int64_t)ct.off;
+    TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     // ---- packed U layout ----
     const int nmax = std::min(N, 2 * d - 2);
     int64_t tot = 0;
@@ -559,7 +562,8 @@ tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
   std::vector<int> order(p->oz_groups.size());
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p->oz_groups[x].Kp > p->oz_groups[y].Kp; });
-  std::vector<OzTile> tiles;
+  std::vector<OzTile>& tiles = p->h_oz_tiles;
+  tiles.clear();
   for (int gi : order)
     for (int mt = 0; mt < p->oz_groups[gi].nmt; ++mt)
       for (int nt = 0; nt < p->oz_groups[gi].nnt; ++nt) tiles.push_back(OzTile{gi, mt, nt, 0});
@@ -592,7 +596,7 @@ tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
   st = cuda_check(cudaMemcpyAsync(p->d_oz_tiles, tiles.data(), tiles.size() * sizeof(OzTile), cudaMemcpyHostToDevice,
                                   p->plan_stream), "H2D oz tiles");
   if (st != TN_OK) return st;
-  st = cuda_check(cudaStreamSynchronize(p->plan_stream), "oz tables sync");
+  st = cuda_check(cudaEventRecord(p->ev_ready, p->plan_stream), "oz tables ready");
   if (st != TN_OK) return st;
   p->ws_bytes += (int64_t)cw.off;
   p->oz_slices = slices;
@@ -657,8 +661,9 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   const SectorParams sp = make_sector_params(p, theta_out);
   p->last_stream = s;
   p->rec_exec = true;  // the workspace is in use from here on (pool release fence)
-  tn_status st = cuda_check(cudaEventRecord(p->ev[4], s), "event");
+  tn_status st = cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
   if (st != TN_OK) return st;
+  if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
   st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
                                         reinterpret_cast<const double2*>(gamma_k1), s)

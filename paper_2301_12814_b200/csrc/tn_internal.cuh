@@ -121,6 +121,11 @@ struct tn_plan {
   void* blk_work = nullptr;                    // pool block: group + tile tables, A/B panels
   // per-kernel timing events: [0,1] K1, [2,3] K2, [4] K3 start, [5] K4 start, [6] K5 start, [7] end
   cudaEvent_t ev[8] = {};
+  // tables uploaded on plan_stream; exec waits for this event instead of the host syncing
+  cudaEvent_t ev_ready = nullptr;
+  std::vector<tn::TileDesc> h_tiles;           // host sources of the async uploads (kept alive)
+  std::vector<tn::MixTile> h_mix;
+  std::vector<tn::OzTile> h_oz_tiles;
   mutable bool rec_k1 = false, rec_k2 = false, rec_exec = false;
   mutable cudaStream_t last_stream = nullptr;  // stream of the last exec (pool release fence)
   // contraction mode (TN_CONTRACT_*) and the INT8-emulation layout (built by tn_plan_set_contraction)
