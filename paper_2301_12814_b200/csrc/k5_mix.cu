@@ -23,125 +23,12 @@
 //    one row α is swept across consecutive c_r blocks, 2.8–3.5 TB/s when tiles are block-major,
 //    whatever the per-instruction shape: tools/probe_mix_bw.cu, profiles/r01_probe_mix_bw.jsonl).
 //  * P_{c_c} of an empty center segment is zero and never read.
-#include "tn_internal.cuh"
+#include "k5_mix.cuh"
 
 namespace tn {
 
 constexpr int MIX_THREADS = 128;
 constexpr int MIX_WARPS = MIX_THREADS / 32;
-constexpr int MIX_GROUPS_PER_TILE = 128;  // 8-groups per CTA tile (32 per warp)
-
-__device__ __forceinline__ void dmma5(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
-
-// Row stride (complex entries) of the staged Us: a quarter warp's B-fragment LDS.128 (two rows × 4
-// consecutive u) then covers all 32 banks once.
-__host__ __device__ __forceinline__ int us_stride(int UP) { return ((UP * 16) % 128 == 64) ? UP : UP + 4; }
-
-struct SecRef {             // sector lo+u at the tile block's origin (row pl0, column pr0)
-  const double2* base;      // (load table: nullptr for an empty center segment → P = 0)
-  int64_t ld;
-};
-
-template <int KSM>
-__device__ __forceinline__ void load_group(double2 (&a)[KSM], const SecRef* __restrict__ sec, int L, int64_t row,
-                                           int col, bool valid, int q) {
-#pragma unroll
-  for (int ks = 0; ks < KSM; ++ks) {
-    const int u = ks * 4 + q;
-    a[ks] = make_double2(0.0, 0.0);
-    if (valid && u < L) {
-      const SecRef s = sec[u];
-      if (s.base) a[ks] = __ldcs(s.base + row * s.ld + col);
-    }
-  }
-}
-
-template <int NT>  // NT = ⌈L/8⌉ output tiles of 8 sectors
-__device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* __restrict__ sec,
-                                              const SecRef* __restrict__ st_sec, const double2* __restrict__ Us,
-                                              const double* __restrict__ UsS,
-                                              int ust, int L, const int32_t* __restrict__ perm_l,
-                                              const int32_t* __restrict__ perm_r, const double* __restrict__ ll,
-                                              const double* __restrict__ lr, int warp, int lane) {
-  constexpr int KSM = 2 * NT;
-  const int g = lane >> 2, q = lane & 3;
-  const int KS = (L + 3) >> 2;
-  int k = warp;
-  if (k >= mt.ne) return;
-  auto coords = [&](int kk, int64_t& row, int& col) {
-    const int grp = mt.e0 + kk;
-    row = grp / mt.ngr;
-    col = (int)(grp - row * mt.ngr) * 8 + g;
-  };
-  int64_t row;
-  int col;
-  coords(k, row, col);
-  bool valid = col < mt.nr;
-  double2 a[KSM];
-  load_group<KSM>(a, sec, L, row, col, valid, q);
-  while (true) {
-    // prefetch the next group of this warp before computing the current one
-    const int kn = k + MIX_WARPS;
-    const bool has_next = kn < mt.ne;
-    int64_t rown = 0;
-    int coln = 0;
-    bool validn = false;
-    double2 an[KSM];
-    if (has_next) {
-      coords(kn, rown, coln);
-      validn = coln < mt.nr;
-      load_group<KSM>(an, sec, L, rown, coln, validn, q);
-    }
-    // Gauss 3-product form: T1 = Pr·Ur, T2 = Pi·Ui, T3 = (Pr+Pi)·(Ur+Ui); Re = T1−T2, Im = T3−T1−T2
-    double acc[NT][6];
-#pragma unroll
-    for (int j = 0; j < NT; ++j)
-#pragma unroll
-      for (int x = 0; x < 6; ++x) acc[j][x] = 0.0;
-    __syncwarp();
-#pragma unroll
-    for (int ks = 0; ks < KSM; ++ks) {
-      if (ks < KS) {
-        const double as = a[ks].x + a[ks].y;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const int idx = (j * 8 + g) * ust + ks * 4 + q;  // B frag: Usᵀ[u = 4ks+q][t = 8j+g]
-          const double2 b = Us[idx];
-          const double bs = UsS[idx];
-          dmma5(acc[j][0], acc[j][1], a[ks].x, b.x);  // T1
-          dmma5(acc[j][2], acc[j][3], a[ks].y, b.y);  // T2
-          dmma5(acc[j][4], acc[j][5], as, bs);        // T3
-        }
-      }
-    }
-    if (valid) {
-      const double scale = ll[perm_l[mt.pl0 + row]] * lr[perm_r[mt.pr0 + col]];
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int t = j * 8 + 2 * q + h;
-          if (t < L) {
-            const SecRef s = st_sec[t];  // output sector lo+t (every output sector is stored)
-            const double re = acc[j][h] - acc[j][2 + h];
-            const double im = acc[j][4 + h] - acc[j][h] - acc[j][2 + h];
-            __stcs(const_cast<double2*>(s.base) + row * s.ld + col, make_double2(re * scale, im * scale));
-          }
-        }
-    }
-    if (!has_next) break;
-    k = kn;
-    row = rown;
-    col = coln;
-    valid = validn;
-#pragma unroll
-    for (int ks = 0; ks < KSM; ++ks) a[ks] = an[ks];
-  }
-}
 
 template <int NTMAX>
 __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
@@ -150,42 +37,20 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
            const double2* __restrict__ U, int us_elems) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const MixTile mt = tiles[blockIdx.x];
-  const int d = sp.d;
-  const int c_l = mt.cl, c_r = mt.cr, n = c_l - c_r;
-  const int lo = max(c_r, c_l - d + 1), hi = min(c_l, c_r + d - 1);
-  const int L = hi - lo + 1;
-  const int nlo = max(0, n - d + 1);
-  const int sn = min(n, d - 1) - nlo + 1;
-  const int TP = (L + 7) & ~7, UP = (L + 3) & ~3;
-  const int ust = us_stride(UP);
   SecRef* ld_sec = reinterpret_cast<SecRef*>(smem_raw);           // load table (null if empty segment)
   SecRef* st_sec = ld_sec + 8 * NTMAX;                            // store table
   double2* Us = reinterpret_cast<double2*>(st_sec + 8 * NTMAX);   // U sub-block
   double* UsS = reinterpret_cast<double*>(Us + us_elems);          // Re + Im of every Us entry
-  for (int u = threadIdx.x; u < L; u += MIX_THREADS) {
-    const int cc = lo + u;
-    const double2* base =
-        sp.out[cc] + ((int64_t)mt.pl0 - sp.lrow0[cc]) * sp.ld[cc] + ((int64_t)mt.pr0 - sp.col0[cc]);
-    const bool ne = (sp.cc_mask[cc >> 5] >> (cc & 31)) & 1u;
-    ld_sec[u] = SecRef{ne ? base : nullptr, (int64_t)sp.ld[cc]};
-    st_sec[u] = SecRef{base, (int64_t)sp.ld[cc]};
-  }
-  // Us[t][u] = U_n[i = c_l − (lo+t)][j = c_l − (lo+u)], zero-padded to TP × UP
-  const double2* Ub = U + sp.ustart[n];
-  for (int x = threadIdx.x; x < TP * UP; x += MIX_THREADS) {
-    const int t = x / UP, u = x - t * UP;
-    double2 v = make_double2(0.0, 0.0);
-    if (t < L && u < L) v = __ldg(Ub + (c_l - lo - t - nlo) * sn + (c_l - lo - u - nlo));
-    Us[t * ust + u] = v;
-    UsS[t * ust + u] = v.x + v.y;
-  }
+  int L, ust;
+  mix_stage(mt, sp, U, ld_sec, st_sec, Us, UsS, threadIdx.x, MIX_THREADS, L, ust);
+  const int TP = (L + 7) & ~7;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   switch (TP >> 3) {
 #define TN_MIX_CASE(m)                                                                              \
   case m:                                                                                           \
     if constexpr (m <= NTMAX)                                                                       \
-      mix_tile_warp<m>(mt, ld_sec, st_sec, Us, UsS, ust, L, perm_l, perm_r, ll, lr, warp, lane);   \
+      mix_tile_warp<m, MIX_WARPS>(mt, ld_sec, st_sec, Us, UsS, ust, L, perm_l, perm_r, ll, lr, warp, lane);   \
     break;
     TN_MIX_CASE(1) TN_MIX_CASE(2) TN_MIX_CASE(3) TN_MIX_CASE(4)
     TN_MIX_CASE(5) TN_MIX_CASE(6) TN_MIX_CASE(7) TN_MIX_CASE(8)
@@ -206,8 +71,10 @@ void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out) {
   constexpr int BAND = 4;
   for (int cl = 0; cl <= p->N; ++cl) {
     const int64_t a0 = std::max<int64_t>(ol[cl], p->r0), a1 = std::min<int64_t>(ol[cl + 1], p->r1);
-    for (int64_t band = a0; band < a1; band += BAND) {
-      const int64_t rows = std::min<int64_t>(BAND, a1 - band);
+    for (int64_t band = a0, rows = 0; band < a1; band += rows) {
+      // ≤ BAND rows, never crossing a K45_BAND boundary (the fused kernel waits per band)
+      const int64_t next = p->r0 + ((band - p->r0) / K45_BAND + 1) * K45_BAND;
+      rows = std::min<int64_t>(std::min<int64_t>(BAND, a1 - band), next - band);
       for (int cr = std::max(0, cl - 2 * p->d + 2); cr <= cl; ++cr) {
         const int64_t nr = orr[cr + 1] - orr[cr];
         if (nr == 0) continue;
@@ -236,11 +103,7 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
   const unsigned grid = (unsigned)p->nmix;
   const int L = p->max_mix;
   const int NT = (L + 7) >> 3;
-  int smax = 0;  // largest staged Us over every L ≤ max_mix
-  for (int l = 1; l <= L; ++l) {
-    const int tp = (l + 7) & ~7, up = (l + 3) & ~3;
-    smax = std::max(smax, tp * us_stride(up));
-  }
+  const int smax = mix_us_elems(L);
 #define TN_MIX_LAUNCH(M)                                                                                       \
   do {                                                                                                         \
     const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * sizeof(SecRef);     \

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <cstdlib>
+
 #include "tn_internal.cuh"
 
 namespace tn {
@@ -391,6 +393,40 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
         for (int nt = 0; nt < g.nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
     }
     p->ntiles = (int64_t)tiles.size();
+    // ---- fused K4+K5 (k45_fused.cu): band-major tile order + per-band tile counts ----
+    {
+      const char* env = getenv("TN_FUSED");
+      // opt-in (TN_FUSED=1): measured slower than K4 + K5 (4.79 vs 3.35 ms at config 3)
+      p->fused = (env && env[0] == '1') && k45_smem_bytes(5, p->max_mix) <= 227 * 1024 && p->r1 > p->r0;
+      p->nbands = (p->r1 - p->r0 + K45_BAND - 1) / K45_BAND;
+      p->h_band_need.assign((size_t)p->nbands, 0);
+      auto band_span = [&](const TileDesc& t, int64_t* b0, int64_t* b1) {
+        const auto& g = p->groups[t.g];
+        const int64_t a0 = g.row0 + (int64_t)t.mt * BM - p->r0;
+        const int64_t a1 = std::min<int64_t>(g.row0 + g.R, g.row0 + (int64_t)t.mt * BM + BM) - p->r0;
+        *b0 = a0 / K45_BAND;
+        *b1 = (a1 - 1) / K45_BAND;
+      };
+      for (const auto& t : tiles) {
+        int64_t b0, b1;
+        band_span(t, &b0, &b1);
+        for (int64_t b = b0; b <= b1; ++b) ++p->h_band_need[(size_t)b];
+      }
+      if (p->fused) {  // band of the first row, then the heavy-first order above
+        std::vector<int64_t> key(tiles.size());
+        for (size_t i = 0; i < tiles.size(); ++i) {
+          int64_t b0, b1;
+          band_span(tiles[i], &b0, &b1);
+          key[i] = b0;
+        }
+        std::vector<size_t> idx(tiles.size());
+        std::iota(idx.begin(), idx.end(), 0);
+        std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return key[x] < key[y]; });
+        std::vector<TileDesc> sorted(tiles.size());
+        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = tiles[idx[i]];
+        tiles.swap(sorted);
+      }
+    }
     std::vector<MixTile>& mix = p->h_mix;
     build_mix_tiles(p, mix);
     p->nmix = (int64_t)mix.size();
@@ -399,6 +435,8 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
       const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
       const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
       const size_t o_m = cw.take<MixTile>((int64_t)mix.size());
+      const size_t o_bn = cw.take<int32_t>(p->nbands);
+      const size_t o_bd = cw.take<int32_t>(p->nbands);
       const size_t o_a = cw.take<double2>(p->a_elems);
       const size_t o_b = cw.take<double2>(p->b_elems);
       p->blk_work = pool_alloc(cw.off, &aerr);
@@ -407,6 +445,11 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
       p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
       p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
       p->d_mix = reinterpret_cast<MixTile*>(base + o_m);
+      p->d_band_need = reinterpret_cast<int32_t*>(base + o_bn);
+      p->d_band_done = reinterpret_cast<int32_t*>(base + o_bd);
+      if (p->nbands)
+        TN_TRY(cudaMemcpyAsync(p->d_band_need, p->h_band_need.data(), p->nbands * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, p->plan_stream), "H2D band counts");
       p->d_apanel = reinterpret_cast<double2*>(base + o_a);
       p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
       if (!p->groups.empty()) {
@@ -672,11 +715,17 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
                   "K3 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;
-  st = cuda_check(emu ? launch_oz_contract(p, sp, s) : launch_contract(p, sp, s), "K4 launch");
-  if (st != TN_OK) return st;
-  if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
-  st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
-  if (st != TN_OK) return st;
+  if (!emu && p->fused) {  // K4 + K5 in one kernel; its time is reported as K4's, K5's as 0
+    st = cuda_check(launch_fused(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K45 launch");
+    if (st != TN_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
+  } else {
+    st = cuda_check(emu ? launch_oz_contract(p, sp, s) : launch_contract(p, sp, s), "K4 launch");
+    if (st != TN_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
+    st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
+    if (st != TN_OK) return st;
+  }
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");
 }
 

@@ -25,6 +25,7 @@ constexpr int CHUNK = BM * BK;        // complex elements per full operand chunk
 constexpr int K4_STAGES = 6;
 constexpr int K4_CONSUMER_WARPS = 8;
 constexpr int K4_THREADS = (K4_CONSUMER_WARPS + 1) * 32;
+constexpr int K45_BAND = 256;         // rows (sorted left positions) per band of the fused K4+K5 kernel
 
 struct GroupDesc {          // one center charge c_c: P_{c_c} = A_{c_c} · B_{c_c}
   int64_t a_off;            // complex offset of this group's A panel in the A workspace
@@ -107,6 +108,11 @@ struct tn_plan {
   int64_t ntiles = 0;
   tn::MixTile* d_mix = nullptr;
   int64_t nmix = 0;                            // K5 tiles
+  bool fused = false;                          // K4 + K5 in one kernel (k45_fused.cu)
+  int64_t nbands = 0;                          // K45_BAND-row bands of this rank's rows
+  std::vector<int32_t> h_band_need;            // K4 tiles touching each band
+  int32_t* d_band_need = nullptr;
+  int32_t* d_band_done = nullptr;
   double2* d_apanel = nullptr;
   double2* d_bpanel = nullptr;
   int64_t a_elems = 0, b_elems = 0;
@@ -172,6 +178,9 @@ cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStr
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s);
 void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out);
+cudaError_t launch_fused(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
+                         const double2* U, cudaStream_t s);
+size_t k45_smem_bytes(int stages, int max_mix);
 
 // ---- double-double arithmetic (K2): error-free transforms, ~106-bit significand ----
 struct dd {

@@ -373,3 +373,15 @@ def test_padding_invariance(tn, cfg, extra):
         ca = inv_r[br[cols]] - k0
         assert sub.shape == a[c].shape
         assert rel_err(sub, a[c][np.ix_(ra, ca)]) < 1e-13, c
+
+
+# ------------------------------------------------------------------ experimental fused K4+K5 (opt-in)
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_fused_k45_parity(tn, cfg, monkeypatch):
+    # TN_FUSED=1 (read at plan time) runs K4 and K5 in one kernel (k45_fused.cu, band-ordered handoff
+    # through global counters); same arithmetic, so the same ≤ 1e-10 bar against the oracle.
+    monkeypatch.setenv("TN_FUSED", "1")
+    case = _case(cfg)
+    ref, *_ = _oracle(cfg)
+    _, _, got = gpu_theta(case)
+    assert_sectors_close(got, ref, TOL, f"fused config{cfg}")
