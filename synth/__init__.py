@@ -20,7 +20,8 @@ from dataclasses import dataclass, field, replace
 
 import numpy as np
 
-__all__ = ["Case", "CONFIGS", "make_config", "make_case", "make_charges", "shuffle_case", "flat_lambda"]
+__all__ = ["Case", "CONFIGS", "make_config", "make_case", "make_charges", "shuffle_case", "flat_lambda",
+           "PairCase", "PAIR_CONFIGS", "make_pair_case", "make_pair_config", "vectorize_pure"]
 
 
 @dataclass
@@ -165,3 +166,104 @@ def flat_lambda(case: Case) -> Case:
                    lam_k=np.full(case.chi_c, 1 / math.sqrt(case.chi_c)),
                    lam_r=np.full(case.chi_r, 1 / math.sqrt(case.chi_r)),
                    meta=dict(case.meta, flat=True))
+
+
+# ---------------------------------------------------------------------------------------------
+# MPO (doubled-charge) inputs: each bond carries a charge pair (c1, c2). No
+# BASELINE.json config covers this path; PAIR_CONFIGS are shaped like the paper's MPO GPU runs
+# (N = 5 photons, d = N + 1, PAPER.md:192/:207 use χ = 4096) — DESIGN.md §3.
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class PairCase:
+    name: str
+    N: int
+    d: int
+    q1_l: np.ndarray
+    q2_l: np.ndarray
+    q1_c: np.ndarray
+    q2_c: np.ndarray
+    q1_r: np.ndarray
+    q2_r: np.ndarray
+    gamma_k: np.ndarray
+    gamma_k1: np.ndarray
+    lam_l: np.ndarray
+    lam_k: np.ndarray
+    lam_r: np.ndarray
+    theta: float
+    phi: float
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def chi_l(self) -> int:
+        return int(self.q1_l.shape[0])
+
+    @property
+    def chi_c(self) -> int:
+        return int(self.q1_c.shape[0])
+
+    @property
+    def chi_r(self) -> int:
+        return int(self.q1_r.shape[0])
+
+
+PAIR_CONFIGS = {
+    0: dict(N=2, d=3, chi=24, charges="uniform", lam="random", seed=100, theta=0.7, phi=0.3),
+    1: dict(N=4, d=5, chi=256, charges="uniform", lam="random", seed=101),
+    2: dict(N=5, d=6, chi=1024, charges="gauss", lam="geometric", seed=102),
+    3: dict(N=5, d=6, chi=4096, charges="gauss", lam="geometric", seed=103),
+}
+
+
+def _pair_charges(rng, kind, N, chi):
+    """Two charge components per bond, drawn independently, then ordered lexicographically."""
+    a = _charges(rng, kind, N, chi)
+    b = _charges(rng, kind, N, chi)
+    b = b[rng.permutation(chi)]          # decorrelate the sorted second component
+    o = np.lexsort((b, a))
+    return a[o].astype(np.int32), b[o].astype(np.int32)
+
+
+def _pair_gamma(rng, r1, r2, c1, c2, d):
+    shape = (r1.shape[0], c1.shape[0])
+    g = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / math.sqrt(2.0)
+    for a, b in ((r1, c1), (r2, c2)):
+        diff = a[:, None].astype(np.int64) - b[None, :].astype(np.int64)
+        g *= (diff >= 0) & (diff <= d - 1)
+    return g
+
+
+def make_pair_case(N, d, chi_l, chi_c, chi_r, seed, *, charges="uniform", lam="random", theta=None, phi=None,
+                   name="pair") -> PairCase:
+    rng = np.random.default_rng(seed)
+    q1_l, q2_l = _pair_charges(rng, charges, N, chi_l)
+    q1_c, q2_c = _pair_charges(rng, charges, N, chi_c)
+    q1_r, q2_r = _pair_charges(rng, charges, N, chi_r)
+    gk = _pair_gamma(rng, q1_l, q2_l, q1_c, q2_c, d)
+    gk1 = _pair_gamma(rng, q1_c, q2_c, q1_r, q2_r, d)
+    lam_l, lam_k, lam_r = _lam(rng, lam, chi_l), _lam(rng, lam, chi_c), _lam(rng, lam, chi_r)
+    if theta is None:
+        theta = float(rng.uniform(0.0, math.pi / 2))
+        phi = float(rng.uniform(0.0, 2 * math.pi))
+    return PairCase(name, N, d, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r, gk, gk1, lam_l, lam_k, lam_r, float(theta),
+                    float(phi), meta=dict(seed=seed, charges=charges, lam=lam))
+
+
+def make_pair_config(cfg: int) -> PairCase:
+    c = PAIR_CONFIGS[cfg]
+    return make_pair_case(c["N"], c["d"], c["chi"], c["chi"], c["chi"], c["seed"], charges=c["charges"],
+                          lam=c["lam"], theta=c.get("theta"), phi=c.get("phi"), name=f"pair{cfg}")
+
+
+def vectorize_pure(case: Case) -> PairCase:
+    """The vectorized pure state |ψ⟩⟨ψ| of a single-charge case: bond (α, α') with charges
+    (q[α], q[α']), Γ2[(α,α'),(β,β')] = Γ[α,β]·conj(Γ[α',β']), λ2 = λ[α]λ[α'] (row-major pair index)."""
+    def pairq(q):
+        return np.repeat(q, q.shape[0]).astype(np.int32), np.tile(q, q.shape[0]).astype(np.int32)
+    q1_l, q2_l = pairq(case.q_l)
+    q1_c, q2_c = pairq(case.q_c)
+    q1_r, q2_r = pairq(case.q_r)
+    gk = np.kron(case.gamma_k, np.conj(case.gamma_k))
+    gk1 = np.kron(case.gamma_k1, np.conj(case.gamma_k1))
+    return PairCase(case.name + "-vectorized", case.N, case.d, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r, gk, gk1,
+                    np.kron(case.lam_l, case.lam_l), np.kron(case.lam_k, case.lam_k), np.kron(case.lam_r, case.lam_r),
+                    case.theta, case.phi, meta=dict(vectorized=case.name))
