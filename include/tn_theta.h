@@ -85,6 +85,21 @@ TN_API tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64
                         const int32_t* q_l, const int32_t* q_c, const int32_t* q_r,
                         int world_size, int rank, tn_plan** out);
 
+/* tn_theta2_plan — the MPO (vectorized density operator) variant, PAPER.md:101, :107 ("MPOs are
+ * vectorized into the MPS form, U → U⊗U*, and two conserved charges are present"; SPEC.md:142-150,
+ * :348-356). Every bond carries a charge PAIR (q1, q2) ∈ [0, N]² (ket and bra photon numbers to the
+ * right); bonds are sorted by the lexicographic key q1·(N+1) + q2, stable. The plan's
+ * sectors are Θ(c1, c2), indexed s = c1·(N+1) + c2 ∈ [0, (N+1)²) in every query and in theta_out;
+ * Θ(c1,c2) is compact row-major, rows = sorted left positions with l1−c1, l2−c2 ∈ [0, d−1], columns
+ * = sorted right positions with c1−r1, c2−r2 ∈ [0, d−1] (R16–R18). tn_build_bs_unitary and
+ * tn_theta_exec are used unchanged (exec applies U to species 1 and conj(U) to species 2);
+ * tn_plan_offsets returns (N+1)²+1 entries over the keys. Single GPU only (world_size 1).
+ * Errors: as tn_theta_plan, plus TN_ERR_UNSUPPORTED when (N+1)² exceeds this build's sector limit
+ * (N ≤ 9). tn_theta_exec_sharded rejects pair plans with TN_ERR_UNSUPPORTED. */
+TN_API tn_status tn_theta2_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r,
+                                const int32_t* q1_l, const int32_t* q2_l, const int32_t* q1_c,
+                                const int32_t* q2_c, const int32_t* q1_r, const int32_t* q2_r, tn_plan** out);
+
 TN_API tn_status tn_plan_destroy(tn_plan* plan);  /* NULL is accepted. */
 
 /* Full Θ(c) shape R_c × C_c (all ranks). TN_ERR_DOMAIN for c ∉ [0,N]. */

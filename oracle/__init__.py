@@ -26,8 +26,9 @@ species, identity gate == two-site product, and Σ‖Θ2‖² invariance. No fun
 """
 from .theta import (sort_bonds, bs_unitary_block, packed_u, packed_u_offsets, theta_sectors,
                     theta_element, sector_ranges, flop_counts)
-from .theta2 import sort_pair_bonds, pair_sector_rows, pair_sector_cols, theta2_sectors, flop_counts2
+from .theta2 import (sort_pair_bonds, pair_sector_rows, pair_sector_cols, theta2_sectors, theta2_element,
+                     flop_counts2)
 
 __all__ = ["sort_bonds", "bs_unitary_block", "packed_u", "packed_u_offsets", "theta_sectors",
            "theta_element", "sector_ranges", "flop_counts", "sort_pair_bonds", "pair_sector_rows",
-           "pair_sector_cols", "theta2_sectors", "flop_counts2"]
+           "pair_sector_cols", "theta2_sectors", "theta2_element", "flop_counts2"]

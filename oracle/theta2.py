@@ -141,3 +141,34 @@ def flop_counts2(N, d, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r):
             if L1 and L2:
                 fm += 8 * nla * nrb * (L1 * L1 * L2 + L1 * L2 * L2)
     return int(fc), int(fm)
+
+
+def theta2_element(N, d, c1, c2, a, b, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r, gamma_k, lam_k, gamma_k1, lam_l, lam_r,
+                   u_blocks, perms):
+    """One element Θ(c1,c2)[a, b] (local indices in sorted order) by the same literal sum — sampled parity at
+    sizes where the full loop is too slow. `perms` = (perm_l, perm_c, perm_r) from sort_pair_bonds."""
+    perm_l, perm_c, perm_r = perms
+    l1s, l2s = np.asarray(q1_l)[perm_l], np.asarray(q2_l)[perm_l]
+    r1s, r2s = np.asarray(q1_r)[perm_r], np.asarray(q2_r)[perm_r]
+    al = int(perm_l[pair_sector_rows(l1s, l2s, d, c1, c2)[a]])
+    be = int(perm_r[pair_sector_cols(r1s, r2s, d, c1, c2)[b]])
+    l1, l2, r1, r2 = int(q1_l[al]), int(q2_l[al]), int(q1_r[be]), int(q2_r[be])
+
+    def U(n, i, j):
+        lo = max(0, n - d + 1)
+        return u_blocks[n][i - lo, j - lo]
+
+    m1s, m2s = np.asarray(q1_c), np.asarray(q2_c)
+    acc = 0j
+    for cc1 in range(r1, l1 + 1):
+        if l1 - cc1 > d - 1 or cc1 - r1 > d - 1:
+            continue
+        for cc2 in range(r2, l2 + 1):
+            if l2 - cc2 > d - 1 or cc2 - r2 > d - 1:
+                continue
+            g = np.nonzero((m1s == cc1) & (m2s == cc2))[0]
+            if len(g) == 0:
+                continue
+            w = U(l1 - r1, l1 - c1, l1 - cc1) * np.conj(U(l2 - r2, l2 - c2, l2 - cc2))
+            acc += w * np.sum(gamma_k[al, g] * lam_k[g] * gamma_k1[g, be])
+    return acc * lam_l[al] * lam_r[be]

@@ -18,7 +18,7 @@ import torch
 from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT, TN_GATHER_NONE,
                    TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH)
 
-__all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
+__all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Plan2", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
            "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
 
 
@@ -63,6 +63,7 @@ class Plan:
         check(lib.tn_theta_plan(self.d, self.N, *self.chi, _ptr(ql), _ptr(qc), _ptr(qr), self.world_size,
                                 self.rank, C.byref(h)), "tn_theta_plan")
         self._h = h
+        self.nsec = self.N + 1
         del self._keep
 
     @property
@@ -99,7 +100,7 @@ class Plan:
         return out
 
     def offsets(self, bond: int) -> np.ndarray:
-        out = np.empty(self.N + 2, dtype=np.int32)
+        out = np.empty(self.nsec + 1, dtype=np.int32)
         check(lib.tn_plan_offsets(self.handle, int(bond), _ptr(out)), "tn_plan_offsets")
         return out
 
@@ -141,6 +142,26 @@ class Plan:
         return n.value
 
 
+class Plan2(Plan):
+    """tn_theta2_plan: the MPO (doubled-charge) plan — every bond carries a charge pair (q1, q2); sectors are
+    Θ(c1, c2), indexed s = c1·(N+1) + c2 (use `sector(c1, c2)`). theta_exec returns (N+1)² tensors."""
+
+    def __init__(self, d: int, N: int, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r):
+        self._keep = [_charges(q) for q in (q1_l, q2_l, q1_c, q2_c, q1_r, q2_r)]
+        k = self._keep
+        self.d, self.N = int(d), int(N)
+        self.chi = (int(k[0].shape[0]), int(k[2].shape[0]), int(k[4].shape[0]))
+        self.world_size, self.rank = 1, 0
+        h = C.c_void_p()
+        check(lib.tn_theta2_plan(self.d, self.N, *self.chi, *(_ptr(x) for x in k), C.byref(h)), "tn_theta2_plan")
+        self._h = h
+        self.nsec = (self.N + 1) ** 2
+        del self._keep
+
+    def sector(self, c1: int, c2: int) -> int:
+        return int(c1) * (self.N + 1) + int(c2)
+
+
 def build_bs_unitary(plan: Plan, theta: float, phi: float, out: torch.Tensor | None = None, stream=None):
     """tn_build_bs_unitary → packed complex128 U on the current device (layout in include/tn_theta.h)."""
     if out is None:
@@ -155,7 +176,7 @@ def build_bs_unitary(plan: Plan, theta: float, phi: float, out: torch.Tensor | N
 def alloc_theta(plan: Plan, device="cuda", full: bool = False):
     """Device buffers for every sector: this rank's slabs (or the full Θ(c) if `full`)."""
     outs = []
-    for c in range(plan.N + 1):
+    for c in range(plan.nsec):
         R, Cc = plan.sector_shape(c) if full else plan.local_sector_shape(c)[:2]
         outs.append(torch.empty((R, Cc), dtype=torch.complex128, device=device))
     return outs

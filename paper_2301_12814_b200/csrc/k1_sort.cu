@@ -16,6 +16,7 @@ constexpr int SORT_WARPS = SORT_THREADS / 32;
 __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs args, int N) {
   const int bond = blockIdx.x;
   const int32_t* __restrict__ q = args.q[bond];
+  const int32_t* __restrict__ q2 = args.q2[bond];  // MPO pair plans: sort by the lexicographic key
   const int64_t chi = args.chi[bond];
   int32_t* __restrict__ perm = args.perm[bond];
   int32_t* __restrict__ qs = args.qs[bond];
@@ -25,13 +26,20 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs arg
   __shared__ int32_t base[MAXC + 1];
   __shared__ int32_t wcnt[SORT_WARPS][MAXC];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nq = N + 1;
+  const int nq = q2 ? (N + 1) * (N + 1) : N + 1;   // number of (pair) charge keys ≤ MAXC
   for (int i = tid; i <= nq; i += SORT_THREADS) hist[i] = 0;
   __syncthreads();
   int bad = 0;
+  auto key = [&](int64_t i) -> int {  // −1 for a charge outside [0, N]
+    const int a = q[i];
+    if (a < 0 || a > N) return -1;
+    if (!q2) return a;
+    const int b = q2[i];
+    return (b < 0 || b > N) ? -1 : a * (N + 1) + b;
+  };
   for (int64_t i = tid; i < chi; i += SORT_THREADS) {
-    int v = q[i];
-    if (v < 0 || v > N) {
+    const int v = key(i);
+    if (v < 0) {
       bad = 1;
       continue;
     }
@@ -57,7 +65,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs arg
     __syncthreads();
     const int64_t i = c0 + tid;
     const bool valid = i < chi;
-    const int v = valid ? q[i] : -1;
+    const int v = valid ? key(i) : -1;
     const unsigned active = __ballot_sync(0xffffffffu, valid);
     unsigned peers = __match_any_sync(0xffffffffu, v);
     peers &= active;

@@ -4,6 +4,7 @@
 // For each center charge c_c (one "group"):
 //   A_{c_c}[r][k] = Γk[perm_l[row0+r]][perm_c[k0+k]] · λk[perm_c[k0+k]]   (rows: Θ(c_c)'s rows)
 //   B_{c_c}[k][n] = Γk1[perm_c[k0+k]][perm_r[col0+n]]                       (cols: Θ(c_c)'s cols)
+// (pair plans pass per-group gathered row / column lists in place of perm_l / perm_r, tn_pair.cu)
 // for k in seg_c(c_c). Only δ-allowed blocks of Γ are read. Panels are written in the
 // exact DMMA fragment order the K4 consumer warps read, zero-padded to 64-row/col tiles and to a
 // multiple of 4 in K (the "empty bonds" of PAPER.md:92), so one K4 chunk is a single contiguous
@@ -83,11 +84,11 @@ cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, 
     int64_t cap = std::max<int64_t>(1, target * 4 / ng);
     return (unsigned)std::max<int64_t>(1, std::min(b, cap));
   };
-  k3_stage_a<<<dim3(blocks(amax), ng), 256, 0, s>>>(p->d_groups, p->d_perm[0], p->d_perm[1], gk, p->chi[1],
+  k3_stage_a<<<dim3(blocks(amax), ng), 256, 0, s>>>(p->d_groups, p->d_rowperm, p->d_perm[1], gk, p->chi[1],
                                                      lk, p->d_apanel);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k3_stage_b<<<dim3(blocks(bmax), ng), 256, 0, s>>>(p->d_groups, p->d_perm[1], p->d_perm[2], gk1, p->chi[2],
+  k3_stage_b<<<dim3(blocks(bmax), ng), 256, 0, s>>>(p->d_groups, p->d_perm[1], p->d_colperm, gk1, p->chi[2],
                                                      p->d_bpanel);
   return cudaGetLastError();
 }

@@ -574,13 +574,13 @@ static cudaError_t stage_s(const tn_plan* p, const double2* gk, const double* lk
     maxa = std::max(maxa, g.nmt * g.nkc);
     maxb = std::max(maxb, g.nnt * ((g.nkc + 3) / 4));
   }
-  if (maxr > 0) k3o_row_exp<<<dim3((maxr + 7) / 8, ng), 256, 0, s>>>(p->d_oz_groups, p->d_perm[0], p->d_perm[1], gk,
+  if (maxr > 0) k3o_row_exp<<<dim3((maxr + 7) / 8, ng), 256, 0, s>>>(p->d_oz_groups, p->d_rowperm, p->d_perm[1], gk,
                                                                      p->chi[1], lk, p->d_oea);
-  if (maxc > 0) k3o_col_exp<<<dim3((maxc + 63) / 64, ng), 256, 0, s>>>(p->d_oz_groups, p->d_perm[1], p->d_perm[2],
+  if (maxc > 0) k3o_col_exp<<<dim3((maxc + 63) / 64, ng), 256, 0, s>>>(p->d_oz_groups, p->d_perm[1], p->d_colperm,
                                                                          gk1, p->chi[2], p->d_oeb);
-  k3o_rows<S><<<dim3(maxa, ng), OZ_BM, 0, s>>>(p->d_oz_groups, p->d_perm[0], p->d_perm[1], gk, p->chi[1], lk, p->d_oea,
+  k3o_rows<S><<<dim3(maxa, ng), OZ_BM, 0, s>>>(p->d_oz_groups, p->d_rowperm, p->d_perm[1], gk, p->chi[1], lk, p->d_oea,
                                                p->d_oa);
-  k3o_cols<S><<<dim3(maxb, ng), 4 * OZ_BN, 0, s>>>(p->d_oz_groups, p->d_perm[1], p->d_perm[2], gk1, p->chi[2], p->d_oeb,
+  k3o_cols<S><<<dim3(maxb, ng), 4 * OZ_BN, 0, s>>>(p->d_oz_groups, p->d_perm[1], p->d_colperm, gk1, p->chi[2], p->d_oeb,
                                                p->d_ob);
   return cudaGetLastError();
 }

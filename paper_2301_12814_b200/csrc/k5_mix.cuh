@@ -110,7 +110,7 @@ __device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* _
       }
     }
     if (valid) {
-      const double scale = ll[perm_l[mt.pl0 + row]] * lr[perm_r[mt.pr0 + col]];
+      const double scale = ll ? ll[perm_l[mt.pl0 + row]] * lr[perm_r[mt.pr0 + col]] : 1.0;  // ll = nullptr: no λ
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll

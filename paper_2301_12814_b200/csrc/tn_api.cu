@@ -128,7 +128,7 @@ static SectorParams make_sector_params(const tn_plan* p, double* const* theta_ou
   std::memset(&sp, 0, sizeof(sp));
   sp.d = p->d;
   sp.N = p->N;
-  for (int c = 0; c <= p->N; ++c) {
+  for (int c = 0; c < p->nsec; ++c) {
     sp.out[c] = reinterpret_cast<double2*>(theta_out[c]);
     sp.lrow0[c] = p->lrow0[c];
     sp.col0[c] = p->col0[c];
@@ -137,8 +137,9 @@ static SectorParams make_sector_params(const tn_plan* p, double* const* theta_ou
   for (size_t n = 0; n < p->ustart.size(); ++n) sp.ustart[n] = p->ustart[n];
   // The mix reads P_{c_c} iff seg_c(c_c) is non-empty: exactly then K4 ran group c_c for every
   // local row that can need it (a row of Θ(c_c) in this shard).
-  for (int cc = 0; cc <= p->N; ++cc)
-    if (p->off[1][cc + 1] > p->off[1][cc]) sp.cc_mask[cc >> 5] |= 1u << (cc & 31);
+  if (!p->pair)
+    for (int cc = 0; cc <= p->N; ++cc)
+      if (p->off[1][cc + 1] > p->off[1][cc]) sp.cc_mask[cc >> 5] |= 1u << (cc & 31);
   return sp;
 }
 
@@ -180,8 +181,22 @@ tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_
   return TN_OK;
 }
 
-tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q_l,
-                        const int32_t* q_c, const int32_t* q_r, int world_size, int rank, tn_plan** out) {
+// packed U layout (SURVEY.md §8(c) "Packed U")
+static void u_layout(tn_plan* p) {
+  const int nmax = std::min(p->N, 2 * p->d - 2);
+  int64_t tot = 0;
+  p->ustart.clear();
+  for (int n = 0; n <= nmax; ++n) {
+    const int s = std::min(n, p->d - 1) - std::max(0, n - p->d + 1) + 1;
+    p->ustart.push_back((int32_t)tot);
+    tot += (int64_t)s * s;
+  }
+  p->u_size = tot;
+}
+
+static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q_l,
+                           const int32_t* q_c, const int32_t* q_r, const int32_t* const* q2, int world_size, int rank,
+                           tn_plan** out) {
   if (!out) return fail(TN_ERR_DIMENSION, "tn_theta_plan: out is NULL");
   *out = nullptr;
   if (d < 2) return fail(TN_ERR_DOMAIN, "tn_theta_plan: d < 2");
@@ -192,6 +207,12 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   if (world_size < 1 || rank < 0 || rank >= world_size) return fail(TN_ERR_DOMAIN, "tn_theta_plan: bad world_size/rank");
   if (!q_l || !q_c || !q_r) return fail(TN_ERR_DIMENSION, "tn_theta_plan: NULL charge array");
   if (std::min(N + 1, d) > TN_MAX_MIX) return fail(TN_ERR_UNSUPPORTED, "tn_theta_plan: min(N+1, d) > TN_MAX_MIX");
+  if (q2) {
+    if (!q2[0] || !q2[1] || !q2[2]) return fail(TN_ERR_DIMENSION, "tn_theta2_plan: NULL charge array");
+    if ((N + 1) * (N + 1) > MAXC)
+      return fail(TN_ERR_UNSUPPORTED, "tn_theta2_plan: (N+1)^2 charge pairs exceed this build's sector limit (N <= 9)");
+    if (world_size != 1) return fail(TN_ERR_UNSUPPORTED, "tn_theta2_plan: row sharding of pair plans is not built");
+  }
 
   tn_plan* p = new (std::nothrow) tn_plan();
   if (!p) return fail(TN_ERR_OOM, "tn_theta_plan: host allocation");
@@ -203,14 +224,17 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   p->chi[1] = chi_c;
   p->chi[2] = chi_r;
   p->max_mix = std::min(N + 1, d);
+  p->pair = q2 != nullptr;
+  p->nq = p->pair ? (N + 1) * (N + 1) : N + 1;
+  p->nsec = p->nq;
   tn_status st = TN_OK;
   int dev = 0;
   int32_t* d_q[3] = {nullptr, nullptr, nullptr};
   const int32_t* qs_in[3] = {q_l, q_c, q_r};
   cudaError_t aerr = cudaSuccess;
   Carver ct;
-  size_t o_perm[3], o_qs[3], o_off[3], o_err, o_q[3] = {0, 0, 0};
-  bool host_q[3];
+  size_t o_perm[3], o_qs[3], o_off[3], o_err, o_q[3] = {0, 0, 0}, o_q2[3] = {0, 0, 0};
+  bool host_q[3], host_q2[3] = {false, false, false};
   int32_t* d_err = nullptr;
   const int nmax_u = std::min(N, 2 * d - 2);
   size_t o_bin = 0;
@@ -229,9 +253,13 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   for (int b = 0; b < 3; ++b) {
     o_perm[b] = ct.take<int32_t>(p->chi[b]);
     o_qs[b] = ct.take<int32_t>(p->chi[b]);
-    o_off[b] = ct.take<int32_t>(N + 2);
+    o_off[b] = ct.take<int32_t>(p->nq + 1);
     host_q[b] = !is_device_ptr(qs_in[b]);
     if (host_q[b]) o_q[b] = ct.take<int32_t>(p->chi[b]);
+    if (q2) {
+      host_q2[b] = !is_device_ptr(q2[b]);
+      if (host_q2[b]) o_q2[b] = ct.take<int32_t>(p->chi[b]);
+    }
   }
   o_err = ct.take<int32_t>(4);
   o_bin = ct.take<double2>((int64_t)(nmax_u + 1) * (nmax_u + 1));
@@ -262,12 +290,21 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
         src = d_q[b];
       }
       sa.q[b] = src;
+      sa.q2[b] = q2 ? q2[b] : nullptr;
+      if (q2 && host_q2[b]) {
+        int32_t* dq2 = reinterpret_cast<int32_t*>(base + o_q2[b]);
+        TN_TRY(cudaMemcpyAsync(dq2, q2[b], p->chi[b] * sizeof(int32_t), cudaMemcpyHostToDevice, p->plan_stream),
+               "H2D charges (second species)");
+        sa.q2[b] = dq2;
+      }
       sa.chi[b] = p->chi[b];
       sa.perm[b] = p->d_perm[b];
       sa.qs[b] = p->d_qs[b];
       sa.off[b] = p->d_off[b];
     }
     d_err = reinterpret_cast<int32_t*>(base + o_err);
+    p->d_rowperm = p->d_perm[0];  // single-charge groups index sorted positions directly
+    p->d_colperm = p->d_perm[2];
     sa.err = d_err;
     p->d_binom = reinterpret_cast<double2*>(base + o_bin);
     TN_TRY(cudaMemcpyAsync(p->d_binom, hbin.data(), hbin.size() * sizeof(double2), cudaMemcpyHostToDevice,
@@ -282,9 +319,9 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
   {
     // one D2H of off[3] + err: the tables are contiguous with padding, copy each
     int32_t herr[4] = {0, 0, 0, 0};
-    for (int b = 0; b < 3; ++b) p->off[b].resize(N + 2);
+    for (int b = 0; b < 3; ++b) p->off[b].resize(p->nq + 1);
     for (int b = 0; b < 3; ++b)
-      TN_TRY(cudaMemcpyAsync(p->off[b].data(), p->d_off[b], (N + 2) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+      TN_TRY(cudaMemcpyAsync(p->off[b].data(), p->d_off[b], (p->nq + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost,
                              p->plan_stream), "D2H off");
     TN_TRY(cudaMemcpyAsync(herr, d_err, sizeof(herr), cudaMemcpyDeviceToHost, p->plan_stream), "D2H err");
     TN_TRY(cudaStreamSynchronize(p->plan_stream), "K1 sync");
@@ -293,7 +330,14 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
       goto done;
     }
   }
-  {
+  if (p->pair) {
+    // ---- MPO pair plan: sectors, groups, two-pass mix (tn_pair.cu) ----
+    st = build_pair_tables(p);
+    if (st != TN_OK) goto done;
+    p->ws_bytes += (int64_t)ct.off;
+    TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
+    u_layout(p);
+  } else {
     // ---- sectors (R2) ----
     const auto& ol = p->off[0];
     const auto& oc = p->off[1];
@@ -466,15 +510,7 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
     }
     p->ws_bytes += (int64_t)ct.off;
     TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
-    // ---- packed U layout ----
-    const int nmax = std::min(N, 2 * d - 2);
-    int64_t tot = 0;
-    for (int n = 0; n <= nmax; ++n) {
-      const int s = std::min(n, d - 1) - std::max(0, n - d + 1) + 1;
-      p->ustart.push_back((int32_t)tot);
-      tot += (int64_t)s * s;
-    }
-    p->u_size = tot;
+    u_layout(p);
   }
 done:
 #undef TN_TRY
@@ -486,6 +522,19 @@ done:
   return TN_OK;
 }
 
+tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q_l,
+                        const int32_t* q_c, const int32_t* q_r, int world_size, int rank, tn_plan** out) {
+  return plan_impl(d, N, chi_l, chi_c, chi_r, q_l, q_c, q_r, nullptr, world_size, rank, out);
+}
+
+tn_status tn_theta2_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q1_l,
+                         const int32_t* q2_l, const int32_t* q1_c, const int32_t* q2_c, const int32_t* q1_r,
+                         const int32_t* q2_r, tn_plan** out) {
+  if (!q1_l || !q1_c || !q1_r) return fail(TN_ERR_DIMENSION, "tn_theta2_plan: NULL charge array");
+  const int32_t* q2[3] = {q2_l, q2_c, q2_r};
+  return plan_impl(d, N, chi_l, chi_c, chi_r, q1_l, q1_c, q1_r, q2, 1, 0, out);
+}
+
 tn_status tn_plan_destroy(tn_plan* plan) {
   free_plan(plan);
   return TN_OK;
@@ -493,7 +542,7 @@ tn_status tn_plan_destroy(tn_plan* plan) {
 
 tn_status tn_plan_sector_shape(const tn_plan* p, int c, int64_t* R, int64_t* C) {
   if (!p || !R || !C) return fail(TN_ERR_DIMENSION, "tn_plan_sector_shape: NULL");
-  if (c < 0 || c > p->N) return fail(TN_ERR_DOMAIN, "tn_plan_sector_shape: c outside [0, N]");
+  if (c < 0 || c >= p->nsec) return fail(TN_ERR_DOMAIN, "tn_plan_sector_shape: sector outside [0, N] (pair plans: [0, (N+1)^2))");
   *R = p->R[c];
   *C = p->C[c];
   return TN_OK;
@@ -501,7 +550,7 @@ tn_status tn_plan_sector_shape(const tn_plan* p, int c, int64_t* R, int64_t* C) 
 
 tn_status tn_plan_local_sector_shape(const tn_plan* p, int c, int64_t* R, int64_t* C, int64_t* row_begin) {
   if (!p || !R || !C || !row_begin) return fail(TN_ERR_DIMENSION, "tn_plan_local_sector_shape: NULL");
-  if (c < 0 || c > p->N) return fail(TN_ERR_DOMAIN, "tn_plan_local_sector_shape: c outside [0, N]");
+  if (c < 0 || c >= p->nsec) return fail(TN_ERR_DOMAIN, "tn_plan_local_sector_shape: sector out of range");
   *R = p->lR[c];
   *C = p->C[c];
   *row_begin = p->lrow0[c] - p->row0[c];
@@ -695,7 +744,7 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   if (!p) return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL plan");
   if (!gamma_k || !lambda_k || !gamma_k1 || !lambda_l || !lambda_r || !U || !theta_out)
     return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL input pointer");
-  for (int c = 0; c <= p->N; ++c)
+  for (int c = 0; c < p->nsec; ++c)
     if (p->lR[c] * p->C[c] > 0 && !theta_out[c])
       return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL theta_out[c] for a non-empty sector");
   cudaError_t e = cudaPeekAtLastError();
@@ -715,7 +764,13 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
                   "K3 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;
-  if (!emu && p->fused) {  // K4 + K5 in one kernel; its time is reported as K4's, K5's as 0
+  if (p->pair) {  // MPO pair plan: K4 (or K4O), then the two-pass U⊗U* mix (tn_pair.cu)
+    st = cuda_check(emu ? launch_oz_contract(p, sp, s) : launch_contract(p, sp, s), "K4 launch");
+    if (st != TN_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
+    st = cuda_check(launch_pair_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5P launch");
+    if (st != TN_OK) return st;
+  } else if (!emu && p->fused) {  // K4 + K5 in one kernel; its time is reported as K4's, K5's as 0
     st = cuda_check(launch_fused(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K45 launch");
     if (st != TN_OK) return st;
     if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;

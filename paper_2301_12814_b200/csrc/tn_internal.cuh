@@ -42,6 +42,14 @@ struct TileDesc {
   int32_t g, mt, nt, pad;
 };
 
+struct MixTile2 {           // K5P work unit (pair plans): one species' U mix over ≤ 128 8-groups of one (l, r) block
+  int32_t cl, n, lo, L;     // that species' left charge, U block n = l_s − r_s, first index lo, vector length L
+  int32_t e0, ne, nr, ngr;  // as MixTile
+  int32_t pl0, pr0;         // sorted positions of the band's first row / the block's first column
+  int32_t sl_off;           // first of L entries {sector, local row of the band, local col of the block, src valid}
+  int32_t flags;            // bit 0: conj(U) (bra species); bit 1: apply λl·λr (last pass)
+};
+
 struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive columns of one row) of one (c_l, c_r) block
   int32_t cl, cr;           // left / right charge
   int32_t e0, ne;           // first 8-group (row-major within the block) and count
@@ -91,6 +99,9 @@ struct SectorParams {
 
 struct tn_plan {
   int d = 0, N = 0, world = 1, rank = 0;
+  bool pair = false;                           // MPO plan: two charge species, key = c1·(N+1) + c2
+  int nq = 0;                                  // charge keys: N+1, or (N+1)² for pair plans
+  int nsec = 0;                                // output sectors (= nq)
   int64_t chi[3] = {0, 0, 0};
   std::vector<int32_t> off[3];                 // host copies of the offset tables (N+2)
   int32_t* d_perm[3] = {nullptr, nullptr, nullptr};  // device perm (sorted pos -> caller index)
@@ -113,6 +124,17 @@ struct tn_plan {
   std::vector<int32_t> h_band_need;            // K4 tiles touching each band
   int32_t* d_band_need = nullptr;
   int32_t* d_band_done = nullptr;
+  // row / column index lists K3 and K3O gather through: perm_l / perm_r themselves for single-charge
+  // plans (group rows are contiguous sorted positions), per-group gathered lists for pair plans
+  const int32_t* d_rowperm = nullptr;
+  const int32_t* d_colperm = nullptr;
+  // pair plans: two-pass U⊗U* mix (tn_pair.cu)
+  tn::MixTile2* d_mix2 = nullptr;
+  int4* d_seclist = nullptr;
+  int64_t nmix2[2] = {0, 0};                   // tiles of pass 1 (species 1) and pass 2 (species 2)
+  std::vector<tn::MixTile2> h_mix2;
+  std::vector<int4> h_seclist;
+  std::vector<int32_t> h_rowperm_pos, h_colperm_pos;
   double2* d_apanel = nullptr;
   double2* d_bpanel = nullptr;
   int64_t a_elems = 0, b_elems = 0;
@@ -158,6 +180,7 @@ tn_status cuda_check(cudaError_t e, const char* what);
 // ---- kernel launchers (stream-ordered) ----
 struct SortArgs {           // K1: one CTA per bond (0 = left, 1 = center, 2 = right)
   const int32_t* q[3];
+  const int32_t* q2[3];     // second charge species (MPO pair plans; nullptr otherwise): key = q·(N+1) + q2
   int64_t chi[3];
   int32_t* perm[3];
   int32_t* qs[3];
@@ -178,6 +201,9 @@ cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStr
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s);
 void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out);
+tn_status build_pair_tables(tn_plan* p);
+cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
+                            const double2* U, cudaStream_t s);
 cudaError_t launch_fused(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                          const double2* U, cudaStream_t s);
 size_t k45_smem_bytes(int stages, int max_mix);

@@ -1,0 +1,349 @@
+// MPO (doubled-charge) plans — Θ(c1, c2) of PAPER.md:101, :107 ("MPOs are vectorized into the MPS form,
+// U → U⊗U*, and two conserved charges are present"). DESIGN.md §4 "Pair plans".
+//
+// A bond carries a charge pair (c1, c2); K1 sorts bonds by the lexicographic key c1·(N+1) + c2,
+// so every charge PAIR is one contiguous segment of sorted positions. The product-once reformulation of
+// the single-charge path carries over pair by pair:
+//   P_m = A_m · B_m for every centre pair m = (m1, m2)   (K3 staging + K4 contraction, unchanged kernels)
+//   Θ(c1,c2)[α,β] = λlλr Σ_{m1,m2} U_{n1}[l1−c1][l1−m1] · conj(U_{n2}[l2−c2][l2−m2]) · P_m[α,β]
+// and the U⊗U* weight factorises, so the mix is applied one species at a time (K5P, two launches):
+//   pass 1:  Q(c1, m2) = Σ_{m1} U_{n1}[l1−c1][l1−m1] P(m1, m2)              (in place, per m2)
+//   pass 2:  Θ(c1, c2) = λlλr Σ_{m2} conj(U_{n2}[l2−c2][l2−m2]) Q(c1, m2)     (in place, per c1)
+// L1²L2 + L1L2² complex MACs per element instead of (L1L2)². Sector (c1, c2) is compact row-major; its rows
+// are the sorted left positions with l − c ∈ [0, d−1]² — a union of whole pair segments, in sorted order —
+// and its columns likewise. P_m has exactly Θ(m)'s shape, so K4 writes it straight into Θ(m) as before;
+// the group's rows/columns are gathered through per-group position lists (d_rowperm / d_colperm).
+#include "k5_mix.cuh"
+
+namespace tn {
+
+__global__ void k_gather_idx(int32_t* __restrict__ out, const int32_t* __restrict__ perm,
+                             const int32_t* __restrict__ pos, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = perm[pos[i]];
+}
+
+namespace {
+struct Carve {  // bump allocator over one pool block (256-byte aligned pieces)
+  size_t off = 0;
+  template <class T>
+  size_t take(int64_t n) {
+    const size_t o = off;
+    off += ((size_t)std::max<int64_t>(n, 0) * sizeof(T) + 255) & ~(size_t)255;
+    return o;
+  }
+};
+}  // namespace
+
+tn_status build_pair_tables(tn_plan* p) {
+  const int N = p->N, d = p->d, nk = N + 1, nq = p->nq;
+  const auto& ol = p->off[0];
+  const auto& oc = p->off[1];
+  const auto& orr = p->off[2];
+  auto cnt = [](const std::vector<int32_t>& o, int k) { return (int64_t)o[k + 1] - o[k]; };
+  auto ok = [d](int a, int b) { return a - b >= 0 && a - b <= d - 1; };
+  // ---- sector layouts: local row / column offset of every pair segment inside every sector ----
+  std::vector<int64_t> rowoff((size_t)nq * nq, -1), coloff((size_t)nq * nq, -1);
+  p->R.assign(nq, 0);
+  p->C.assign(nq, 0);
+  p->row0.assign(nq, 0);
+  p->col0.assign(nq, 0);
+  p->lR.assign(nq, 0);
+  p->lrow0.assign(nq, 0);
+  p->bounds = {0, p->chi[0]};
+  p->r0 = 0;
+  p->r1 = p->chi[0];
+  for (int c1 = 0; c1 <= N; ++c1)
+    for (int c2 = 0; c2 <= N; ++c2) {
+      const int s = c1 * nk + c2;
+      int64_t r = 0, c = 0;
+      for (int l1 = c1; l1 <= std::min(N, c1 + d - 1); ++l1)  // keys ascend = sorted order
+        for (int l2 = c2; l2 <= std::min(N, c2 + d - 1); ++l2) {
+          rowoff[(size_t)s * nq + l1 * nk + l2] = r;
+          r += cnt(ol, l1 * nk + l2);
+        }
+      for (int r1 = std::max(0, c1 - d + 1); r1 <= c1; ++r1)
+        for (int r2 = std::max(0, c2 - d + 1); r2 <= c2; ++r2) {
+          coloff[(size_t)s * nq + r1 * nk + r2] = c;
+          c += cnt(orr, r1 * nk + r2);
+        }
+      if (r > INT32_MAX || c > INT32_MAX) return fail(TN_ERR_UNSUPPORTED, "sector dimension > INT32_MAX");
+      p->R[s] = p->lR[s] = r;
+      p->C[s] = c;
+    }
+  // ---- useful work (oracle.flop_counts2 definitions) ----
+  p->f_contract = p->f_mix = 0;
+  for (int l = 0; l < nq; ++l) {
+    const int64_t nl = cnt(ol, l);
+    if (!nl) continue;
+    for (int r = 0; r < nq; ++r) {
+      const int64_t nr = cnt(orr, r);
+      if (!nr) continue;
+      const int l1 = l / nk, l2 = l % nk, r1 = r / nk, r2 = r % nk;
+      int64_t L1 = 0, L2 = 0;
+      for (int x = 0; x <= N; ++x) L1 += ok(l1, x) && ok(x, r1);
+      for (int y = 0; y <= N; ++y) L2 += ok(l2, y) && ok(y, r2);
+      for (int m = 0; m < nq; ++m)
+        if (cnt(oc, m) && ok(l1, m / nk) && ok(m / nk, r1) && ok(l2, m % nk) && ok(m % nk, r2))
+          p->f_contract += 8 * nl * cnt(oc, m) * nr;
+      if (L1 && L2) p->f_mix += 8 * nl * nr * (L1 * L1 * L2 + L1 * L2 * L2);
+    }
+  }
+  p->f_contract_local = p->f_contract;
+  p->f_mix_local = p->f_mix;
+  // ---- groups: one per non-empty centre pair; rows / cols = those of Θ(m), gathered by position ----
+  std::vector<int32_t>& rpos = p->h_rowperm_pos;
+  std::vector<int32_t>& cpos = p->h_colperm_pos;
+  rpos.clear();
+  cpos.clear();
+  int64_t a_off = 0, b_off = 0;
+  p->groups.clear();
+  p->f_exec = 0;
+  for (int m = 0; m < nq; ++m) {
+    const int64_t K = cnt(oc, m);
+    if (K == 0 || p->R[m] == 0 || p->C[m] == 0) continue;
+    const int m1 = m / nk, m2 = m % nk;
+    GroupDesc g{};
+    g.cc = m;
+    g.row0 = (int64_t)rpos.size();
+    for (int l1 = m1; l1 <= std::min(N, m1 + d - 1); ++l1)
+      for (int l2 = m2; l2 <= std::min(N, m2 + d - 1); ++l2)
+        for (int32_t q = ol[l1 * nk + l2]; q < ol[l1 * nk + l2 + 1]; ++q) rpos.push_back(q);
+    g.col0 = (int64_t)cpos.size();
+    for (int r1 = std::max(0, m1 - d + 1); r1 <= m1; ++r1)
+      for (int r2 = std::max(0, m2 - d + 1); r2 <= m2; ++r2)
+        for (int32_t q = orr[r1 * nk + r2]; q < orr[r1 * nk + r2 + 1]; ++q) cpos.push_back(q);
+    g.k0 = oc[m];
+    g.R = (int32_t)p->R[m];
+    g.C = (int32_t)p->C[m];
+    g.K = (int32_t)K;
+    g.K4 = (int32_t)((K + 3) / 4 * 4);
+    g.nmt = (g.R + BM - 1) / BM;
+    g.nnt = (g.C + BN - 1) / BN;
+    g.a_off = a_off;
+    g.b_off = b_off;
+    a_off += (int64_t)g.nmt * BM * g.K4;
+    b_off += (int64_t)g.nnt * BN * g.K4;
+    p->f_exec += 8 * (int64_t)g.nmt * BM * (int64_t)g.nnt * BN * g.K4;
+    p->groups.push_back(g);
+  }
+  p->a_elems = a_off;
+  p->b_elems = b_off;
+  std::vector<int> order(p->groups.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p->groups[x].K4 > p->groups[y].K4; });
+  std::vector<TileDesc>& tiles = p->h_tiles;
+  tiles.clear();
+  for (int gi : order)
+    for (int mt = 0; mt < p->groups[gi].nmt; ++mt)
+      for (int nt = 0; nt < p->groups[gi].nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
+  p->ntiles = (int64_t)tiles.size();
+  // ---- two-pass mix tiles: ≤ 4 rows of one left pair segment × one right pair segment ----
+  std::vector<MixTile2>& mix = p->h_mix2;
+  std::vector<int4>& sl = p->h_seclist;
+  mix.clear();
+  sl.clear();
+  constexpr int BAND = 4;
+  int max_l = 1;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int l = 0; l < nq; ++l) {
+      const int64_t nl = cnt(ol, l);
+      if (!nl) continue;
+      const int l1 = l / nk, l2 = l % nk;
+      for (int r = 0; r < nq; ++r) {
+        const int64_t nr = cnt(orr, r);
+        if (!nr) continue;
+        const int r1 = r / nk, r2 = r % nk;
+        const int lo1 = std::max(r1, l1 - d + 1), hi1 = std::min(l1, r1 + d - 1);
+        const int lo2 = std::max(r2, l2 - d + 1), hi2 = std::min(l2, r2 + d - 1);
+        if (hi1 < lo1 || hi2 < lo2) continue;
+        const int L = pass == 0 ? hi1 - lo1 + 1 : hi2 - lo2 + 1;
+        max_l = std::max(max_l, L);
+        const int fixed_lo = pass == 0 ? lo2 : lo1, fixed_hi = pass == 0 ? hi2 : hi1;
+        for (int f = fixed_lo; f <= fixed_hi; ++f)
+          for (int64_t band = 0; band < nl; band += BAND) {
+            const int64_t rows = std::min<int64_t>(BAND, nl - band);
+            const int64_t ngr = (nr + 7) / 8, G = rows * ngr;
+            for (int64_t e0 = 0; e0 < G; e0 += MIX_GROUPS_PER_TILE) {
+              MixTile2 t{};
+              t.cl = pass == 0 ? l1 : l2;
+              t.n = pass == 0 ? l1 - r1 : l2 - r2;
+              t.lo = pass == 0 ? lo1 : lo2;
+              t.L = L;
+              t.e0 = (int32_t)e0;
+              t.ne = (int32_t)std::min<int64_t>(MIX_GROUPS_PER_TILE, G - e0);
+              t.nr = (int32_t)nr;
+              t.ngr = (int32_t)ngr;
+              t.pl0 = (int32_t)(ol[l] + band);
+              t.pr0 = orr[r];
+              t.sl_off = (int32_t)sl.size();
+              t.flags = pass == 0 ? 0 : 3;  // pass 2: conj(U) and the outer λ's
+              for (int u = 0; u < L; ++u) {
+                const int x = pass == 0 ? lo1 + u : f, y = pass == 0 ? f : lo2 + u;
+                const int s = x * nk + y;
+                const int64_t ro = rowoff[(size_t)s * nq + l], co = coloff[(size_t)s * nq + r];
+                if (ro < 0 || co < 0) return fail(TN_ERR_CONSISTENCY, "pair plan: block outside a sector (internal)");
+                // pass 1 reads P(x, y) only where the centre pair has bonds; pass 2 reads Q (always written)
+                const int valid = pass == 1 || cnt(oc, s) > 0;
+                sl.push_back(make_int4(s, (int)(ro + band), (int)co, valid));
+              }
+              mix.push_back(t);
+            }
+          }
+      }
+    }
+    p->nmix2[pass] = (int64_t)mix.size() - (pass ? p->nmix2[0] : 0);
+  }
+  p->max_mix = max_l;
+  p->nmix = 0;
+  // ---- device tables ----
+  Carve cw;
+  const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
+  const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
+  const size_t o_m = cw.take<MixTile2>((int64_t)mix.size());
+  const size_t o_s = cw.take<int4>((int64_t)sl.size());
+  const size_t o_rp = cw.take<int32_t>((int64_t)rpos.size());
+  const size_t o_cp = cw.take<int32_t>((int64_t)cpos.size());
+  const size_t o_rg = cw.take<int32_t>((int64_t)rpos.size());
+  const size_t o_cg = cw.take<int32_t>((int64_t)cpos.size());
+  const size_t o_a = cw.take<double2>(p->a_elems);
+  const size_t o_b = cw.take<double2>(p->b_elems);
+  cudaError_t aerr = cudaSuccess;
+  p->blk_work = pool_alloc(cw.off, &aerr);
+  if (aerr != cudaSuccess) return cuda_check(aerr, "pool alloc (pair workspace)");
+  char* base = static_cast<char*>(p->blk_work);
+  p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
+  p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
+  p->d_mix2 = reinterpret_cast<MixTile2*>(base + o_m);
+  p->d_seclist = reinterpret_cast<int4*>(base + o_s);
+  int32_t* d_rpos = reinterpret_cast<int32_t*>(base + o_rp);
+  int32_t* d_cpos = reinterpret_cast<int32_t*>(base + o_cp);
+  int32_t* d_rg = reinterpret_cast<int32_t*>(base + o_rg);
+  int32_t* d_cg = reinterpret_cast<int32_t*>(base + o_cg);
+  p->d_apanel = reinterpret_cast<double2*>(base + o_a);
+  p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
+  p->d_rowperm = d_rg;
+  p->d_colperm = d_cg;
+  p->ws_bytes += (int64_t)cw.off;
+  auto up = [&](void* dst, const void* src, size_t bytes, const char* what) -> tn_status {
+    if (!bytes) return TN_OK;
+    return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->plan_stream), what);
+  };
+  tn_status st;
+  if ((st = up(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc), "H2D groups")) != TN_OK) return st;
+  if ((st = up(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), "H2D tiles")) != TN_OK) return st;
+  if ((st = up(p->d_mix2, mix.data(), mix.size() * sizeof(MixTile2), "H2D mix tiles")) != TN_OK) return st;
+  if ((st = up(p->d_seclist, sl.data(), sl.size() * sizeof(int4), "H2D sector lists")) != TN_OK) return st;
+  if ((st = up(d_rpos, rpos.data(), rpos.size() * sizeof(int32_t), "H2D row positions")) != TN_OK) return st;
+  if ((st = up(d_cpos, cpos.data(), cpos.size() * sizeof(int32_t), "H2D col positions")) != TN_OK) return st;
+  // gathered index lists: original bond index of every group row / column (K1's perm already on device)
+  if (!rpos.empty())
+    k_gather_idx<<<(unsigned)std::min<int64_t>(1024, ((int64_t)rpos.size() + 255) / 256), 256, 0, p->plan_stream>>>(
+        d_rg, p->d_perm[0], d_rpos, (int64_t)rpos.size());
+  if (!cpos.empty())
+    k_gather_idx<<<(unsigned)std::min<int64_t>(1024, ((int64_t)cpos.size() + 255) / 256), 256, 0, p->plan_stream>>>(
+        d_cg, p->d_perm[2], d_cpos, (int64_t)cpos.size());
+  return cuda_check(cudaGetLastError(), "pair gather launch");
+}
+
+// ---- K5P: one species' mix of one pair tile (same warp loop as K5, sector list from the plan) ----
+constexpr int K5P_THREADS = 128;
+
+template <int NTMAX>
+__global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
+    k5p_mix(const SectorParams sp, const MixTile2* __restrict__ tiles, const int4* __restrict__ seclist,
+            const int32_t* __restrict__ perm_l, const int32_t* __restrict__ perm_r, const double* __restrict__ ll,
+            const double* __restrict__ lr, const double2* __restrict__ U, int us_elems) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const MixTile2 t = tiles[blockIdx.x];
+  SecRef* ld_sec = reinterpret_cast<SecRef*>(smem_raw);
+  SecRef* st_sec = ld_sec + 8 * NTMAX;
+  double2* Us = reinterpret_cast<double2*>(st_sec + 8 * NTMAX);
+  double* UsS = reinterpret_cast<double*>(Us + us_elems);
+  const int L = t.L, d = sp.d;
+  const bool cj = t.flags & 1;
+  for (int u = threadIdx.x; u < L; u += K5P_THREADS) {
+    const int4 e = seclist[t.sl_off + u];
+    const double2* base = sp.out[e.x] + (int64_t)e.y * sp.ld[e.x] + e.z;
+    ld_sec[u] = SecRef{e.w ? base : nullptr, (int64_t)sp.ld[e.x]};
+    st_sec[u] = SecRef{base, (int64_t)sp.ld[e.x]};
+  }
+  // Us[t][u] = U_n[i = cl − (lo+t)][j = cl − (lo+u)]  (conjugated for the bra species), padded to TP × UP
+  const int TP = (L + 7) & ~7, UP = (L + 3) & ~3;
+  const int ust = us_stride(UP);
+  const int nlo = max(0, t.n - d + 1), sn = min(t.n, d - 1) - nlo + 1;
+  const double2* Ub = U + sp.ustart[t.n];
+  for (int x = threadIdx.x; x < TP * UP; x += K5P_THREADS) {
+    const int tt = x / UP, u = x - tt * UP;
+    double2 v = make_double2(0.0, 0.0);
+    if (tt < L && u < L) {
+      v = __ldg(Ub + (t.cl - t.lo - tt - nlo) * sn + (t.cl - t.lo - u - nlo));
+      if (cj) v.y = -v.y;
+    }
+    Us[tt * ust + u] = v;
+    UsS[tt * ust + u] = v.x + v.y;
+  }
+  __syncthreads();
+  MixTile mt;
+  mt.cl = t.cl;
+  mt.cr = 0;
+  mt.e0 = t.e0;
+  mt.ne = t.ne;
+  mt.nr = t.nr;
+  mt.ngr = t.ngr;
+  mt.pl0 = t.pl0;
+  mt.pr0 = t.pr0;
+  const bool sc = t.flags & 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  switch (TP >> 3) {
+#define TN_MIX_CASE(m)                                                                                       \
+  case m:                                                                                                    \
+    if constexpr (m <= NTMAX)                                                                                \
+      mix_tile_warp<m, K5P_THREADS / 32>(mt, ld_sec, st_sec, Us, UsS, ust, L, perm_l, perm_r, sc ? ll : nullptr, \
+                                         lr, warp, lane);                                                    \
+    break;
+    TN_MIX_CASE(1) TN_MIX_CASE(2) TN_MIX_CASE(3) TN_MIX_CASE(4)
+    TN_MIX_CASE(5) TN_MIX_CASE(6) TN_MIX_CASE(7) TN_MIX_CASE(8)
+#undef TN_MIX_CASE
+    default:
+      break;
+  }
+}
+
+cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
+                            const double2* U, cudaStream_t s) {
+  const int L = p->max_mix;
+  const int NT = (L + 7) >> 3;
+  const int smax = mix_us_elems(L);
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t n = p->nmix2[pass];
+    if (n == 0) continue;
+    const MixTile2* tiles = p->d_mix2 + (pass ? p->nmix2[0] : 0);
+#define TN_P_LAUNCH(M)                                                                                        \
+  do {                                                                                                        \
+    const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * sizeof(SecRef);    \
+    if (smem > 48 * 1024) {                                                                                   \
+      cudaError_t e = cudaFuncSetAttribute(k5p_mix<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                                         \
+    }                                                                                                         \
+    k5p_mix<M><<<(unsigned)n, K5P_THREADS, smem, s>>>(sp, tiles, p->d_seclist, p->d_perm[0], p->d_perm[2], ll, lr, \
+                                                       U, smax);                                             \
+  } while (0)
+    if (NT <= 1)
+      TN_P_LAUNCH(1);
+    else if (NT <= 2)
+      TN_P_LAUNCH(2);
+    else if (NT <= 4)
+      TN_P_LAUNCH(4);
+    else if (NT <= 6)
+      TN_P_LAUNCH(6);
+    else
+      TN_P_LAUNCH(8);
+#undef TN_P_LAUNCH
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace tn

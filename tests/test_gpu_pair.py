@@ -1,0 +1,164 @@
+"""GPU parity of the MPO (doubled-charge) path Θ(c1, c2) (tn_theta2_plan + tn_theta_exec) against the
+pinned pair oracle (oracle/theta2.py): bond tables bit-exact, sector shapes identical, Θ ≤ 1e-10 relative
+Frobenius per sector (the north_star bar carried over), plus the vectorized-pure-state factorisation
+against the single-charge GPU path at sizes the literal pair loop cannot reach."""
+import functools
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def tn(cuda_ok):
+    import paper_2301_12814_b200 as tn
+    return tn
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_theta2(tn, case, contraction=None, plan=None, theta=None):
+    if plan is None:
+        plan = tn.Plan2(case.d, case.N, case.q1_l, case.q2_l, case.q1_c, case.q2_c, case.q1_r, case.q2_r)
+    if contraction is not None:
+        plan.set_contraction(*contraction)
+    U = tn.build_bs_unitary(plan, case.theta if theta is None else theta, case.phi)
+    out = tn.theta_exec(plan, _dev(case.gamma_k), _dev(case.lam_k), _dev(case.gamma_k1), _dev(case.lam_l),
+                        _dev(case.lam_r), U)
+    torch.cuda.synchronize()
+    N = case.N
+    return plan, {(c1, c2): out[c1 * (N + 1) + c2].cpu().numpy() for c1, c2 in itertools.product(range(N + 1), repeat=2)}
+
+
+@functools.lru_cache(maxsize=None)
+def _pair(cfg):
+    return synth.make_pair_config(cfg)
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle2(cfg):
+    c = _pair(cfg)
+    return oracle.theta2_sectors(c.N, c.d, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r, c.gamma_k, c.lam_k,
+                                 c.gamma_k1, c.lam_l, c.lam_r, c.theta, c.phi)
+
+
+def _check(got, ref, tol, what):
+    worst = 0.0
+    for key, r in ref.items():
+        g = got[key]
+        assert g.shape == r.shape, (what, key, g.shape, r.shape)
+        e = rel_err(g, r)
+        assert e <= tol, f"{what} sector {key}: {e:.3e}"
+        worst = max(worst, e)
+    return worst
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_pair_tables_bit_exact(tn, cfg):
+    c = _pair(cfg)
+    plan = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
+    nk = c.N + 1
+    for b, (q1, q2) in enumerate(((c.q1_l, c.q2_l), (c.q1_c, c.q2_c), (c.q1_r, c.q2_r))):
+        assert np.array_equal(plan.perm(b), oracle.sort_pair_bonds(q1, q2))
+        key = q1.astype(np.int64) * nk + q2
+        ref = np.concatenate([[0], np.cumsum(np.bincount(key, minlength=nk * nk))]).astype(np.int32)
+        assert np.array_equal(plan.offsets(b), ref)
+    perms = tuple(oracle.sort_pair_bonds(*q) for q in ((c.q1_l, c.q2_l), (c.q1_c, c.q2_c), (c.q1_r, c.q2_r)))
+    for c1, c2 in itertools.product(range(nk), repeat=2):
+        rows = oracle.pair_sector_rows(c.q1_l[perms[0]], c.q2_l[perms[0]], c.d, c1, c2)
+        cols = oracle.pair_sector_cols(c.q1_r[perms[2]], c.q2_r[perms[2]], c.d, c1, c2)
+        assert plan.sector_shape(plan.sector(c1, c2)) == (len(rows), len(cols))
+    fc, fm = oracle.flop_counts2(c.N, c.d, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
+    f = plan.flops()
+    assert (f["f_contract"], f["f_mix"]) == (fc, fm)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_pair_parity(tn, cfg):
+    ref, *_ = _oracle2(cfg)
+    _, got = gpu_theta2(tn, _pair(cfg))
+    _check(got, ref, TOL, f"pair config {cfg}")
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_pair_parity_int8(tn, cfg):
+    ref, *_ = _oracle2(cfg)
+    _, got = gpu_theta2(tn, _pair(cfg), contraction=("int8", 6))
+    _check(got, ref, TOL, f"pair config {cfg} int8")
+
+
+def test_pair_config3_sampled(tn):
+    c = _pair(3)
+    plan, got = gpu_theta2(tn, c)
+    ub = [oracle.bs_unitary_block(n, c.theta, c.phi, c.d) for n in range(min(c.N, 2 * c.d - 2) + 1)]
+    perms = tuple(oracle.sort_pair_bonds(*q) for q in ((c.q1_l, c.q2_l), (c.q1_c, c.q2_c), (c.q1_r, c.q2_r)))
+    rng = np.random.default_rng(5)
+    for key in [(0, 0), (2, 3), (3, 2), (5, 5), (1, 4)]:
+        g = got[key]
+        if g.size == 0:
+            continue
+        for _ in range(6):
+            a, b = int(rng.integers(g.shape[0])), int(rng.integers(g.shape[1]))
+            v = oracle.theta2_element(c.N, c.d, *key, a, b, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r,
+                                      c.gamma_k, c.lam_k, c.gamma_k1, c.lam_l, c.lam_r, ub, perms)
+            scale = np.linalg.norm(g) / np.sqrt(g.size)       # element error relative to the sector's rms
+            assert abs(g[a, b] - v) <= 1e-10 * max(scale, abs(v)), (key, a, b)
+
+
+def test_pair_vectorized_pure_state_matches_single_path(tn):
+    # Θ2(c1,c2)[(α,α'),(β,β')] = Θ(c1)[α,β]·conj(Θ(c2)[α',β']) — both sides on the GPU, at χ = 24 → 576 pairs
+    base = synth.make_case(4, 5, 24, 24, 24, seed=21, charges="uniform", lam="random")
+    vec = synth.vectorize_pure(base)
+    from gpu_util import gpu_theta
+    p1, _, s1 = gpu_theta(base)
+    p2, s2 = gpu_theta2(tn, vec)
+    pl1, pr1, pl2, pr2 = p1.perm(0), p1.perm(2), p2.perm(0), p2.perm(2)
+    inv_l, inv_r = np.argsort(pl1), np.argsort(pr1)
+    off_l, off_r = p1.offsets(0), p1.offsets(2)
+    N, d, chi = base.N, base.d, 24
+    for c1, c2 in itertools.product(range(N + 1), repeat=2):
+        rows = oracle.pair_sector_rows(vec.q1_l[pl2], vec.q2_l[pl2], d, c1, c2)
+        cols = oracle.pair_sector_cols(vec.q1_r[pr2], vec.q2_r[pr2], d, c1, c2)
+        g = s2[(c1, c2)]
+        assert g.shape == (len(rows), len(cols))
+        if g.size == 0:
+            continue
+        (a0, _), (b0, _) = oracle.sector_ranges(off_l, off_r, N, d, c1)
+        (e0, _), (f0, _) = oracle.sector_ranges(off_l, off_r, N, d, c2)
+        al, alp = np.divmod(pl2[rows].astype(np.int64), chi)
+        be, bep = np.divmod(pr2[cols].astype(np.int64), chi)
+        ref = s1[c1][np.ix_(inv_l[al] - a0, inv_r[be] - b0)] * np.conj(s1[c2][np.ix_(inv_l[alp] - e0, inv_r[bep] - f0)])
+        assert rel_err(g, ref) < 1e-12, (c1, c2)
+
+
+@pytest.mark.parametrize("name,N,d,chi", [("N0", 0, 2, (3, 4, 5)), ("d_lt_N1", 3, 2, (40, 33, 29)),
+                                          ("d_gt_N1", 2, 5, (30, 31, 32)), ("ragged", 3, 4, (77, 65, 90))])
+def test_pair_edge_cases(tn, name, N, d, chi):
+    case = synth.make_pair_case(N, d, *chi, seed=31, charges="uniform", lam="random")
+    ref, *_ = oracle.theta2_sectors(case.N, case.d, case.q1_l, case.q2_l, case.q1_c, case.q2_c, case.q1_r,
+                                    case.q2_r, case.gamma_k, case.lam_k, case.gamma_k1, case.lam_l, case.lam_r,
+                                    case.theta, case.phi)
+    _, got = gpu_theta2(tn, case)
+    _check(got, ref, 1e-12, name)
+
+
+def test_pair_errors(tn):
+    with pytest.raises(tn.TnError, match="UNSUPPORTED"):
+        tn.Plan2(11, 10, [0], [0], [0], [0], [0], [0])        # (N+1)^2 sectors beyond this build
+    with pytest.raises(tn.TnError, match="DOMAIN"):
+        tn.Plan2(4, 3, [0, 4], [0, 0], [0], [0], [0], [0])    # charge outside [0, N]
+    with pytest.raises(tn.TnError, match="DOMAIN"):
+        tn.Plan2(4, 3, [0], [-1], [0], [0], [0], [0])
+    plan = tn.Plan2(4, 3, [0, 1], [1, 0], [0, 1], [0, 1], [0, 1], [1, 1])
+    with pytest.raises(tn.TnError, match="DOMAIN"):
+        plan.sector_shape(16)

@@ -164,3 +164,17 @@ def test_flop_counts2_against_bruteforce_count():
     ar = ok(case.q1_c[:, None], case.q1_r[None, :]) & ok(case.q2_c[:, None], case.q2_r[None, :])
     assert fc == 8 * int(al.astype(np.int64).sum(axis=0) @ ar.astype(np.int64).sum(axis=1))
     assert fm > 0
+
+
+def test_theta2_element_matches_sectors():
+    case = synth.make_pair_config(1)
+    secs, perms, ub = _theta2(case)
+    rng = np.random.default_rng(0)
+    for key in [(0, 0), (2, 3), (4, 4), (1, 2)]:
+        R, Cc = secs[key].shape
+        for _ in range(5):
+            a, b = int(rng.integers(R)), int(rng.integers(Cc))
+            v = oracle.theta2_element(case.N, case.d, *key, a, b, case.q1_l, case.q2_l, case.q1_c, case.q2_c,
+                                      case.q1_r, case.q2_r, case.gamma_k, case.lam_k, case.gamma_k1, case.lam_l,
+                                      case.lam_r, ub, perms)
+            assert abs(v - secs[key][a, b]) <= 1e-13 * max(abs(v), 1e-300)
