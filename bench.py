@@ -47,6 +47,8 @@ def parse():
                     help="K4 engine: FP64 DMMA (default) or the INT8 tcgen05 Ozaki emulation")
     ap.add_argument("--slices", type=int, default=6, help="INT8 emulation slice count (6: ≤1e-11 rel error)")
     ap.add_argument("--gates", type=int, default=32, help="config 4: gates of the brick-wall layer to time")
+    ap.add_argument("--pair", type=int, default=None,
+                    help="time the MPO doubled-charge path on synth.PAIR_CONFIGS[k] instead (tn_theta2_plan)")
     return ap.parse_args()
 
 
@@ -402,6 +404,87 @@ def run_tn(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------------------------- MPO pair path
+def run_pair(args, rank, world, local_rank):
+    """One step = tn_theta2_plan (K1 on pair keys + tables) + tn_build_bs_unitary (K2) + tn_theta_exec
+    (K3 → K4 → two-pass K5P) on synth.PAIR_CONFIGS[k] (PAPER.md:101/:107 MPO workload; single GPU)."""
+    import numpy as np
+    import torch
+
+    import paper_2301_12814_b200 as tn
+    import synth
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = synth.make_pair_config(args.pair)
+    h = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    gk, gk1, lk, ll, lr = h(c.gamma_k), h(c.gamma_k1), h(c.lam_k), h(c.lam_l), h(c.lam_r)
+    qs = [h(q) for q in (c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)]
+    int8 = args.contraction == "int8"
+
+    def mk():
+        p = tn.Plan2(c.d, c.N, *qs)
+        if int8:
+            p.set_contraction("int8", args.slices)
+        return p
+
+    probe = mk()
+    flops = probe.flops()
+    f_useful = flops["f_contract"] + flops["f_mix"]
+    outs = tn.alloc_theta(probe, device=dev)
+    U = torch.empty(probe.u_size(), dtype=torch.complex128, device=dev)
+    probe.destroy()
+    stream = torch.cuda.current_stream(dev)
+    keep, kt = [], []
+
+    def step():
+        p = mk()
+        tn.build_bs_unitary(p, c.theta, c.phi, out=U)
+        tn.theta_exec(p, gk, lk, gk1, ll, lr, U, out=outs)
+        keep.append(p)
+        if len(keep) > 2:
+            old = keep.pop(0)
+            kt.append(old.kernel_times())
+            old.destroy()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    kt.clear()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    for p in keep:
+        kt.append(p.kernel_times())
+        p.destroy()
+    ms = e0.elapsed_time(e1) / args.steps
+    km = {k: statistics.mean(x[k] for x in kt[-args.steps:]) for k in kt[0]}
+    k4 = km["k4_contract"]
+    achieved = flops["f_contract"] / (k4 * 1e-3) / 1e12
+    line = {"metric": "Θ(c1,c2) MPO build useful complex FP64 GFLOP/s", "value": round(f_useful / (ms * 1e-3) / 1e9, 3),
+            "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth.PAIR_CONFIGS, seeded)",
+            "gates_per_s": round(1000.0 / ms, 3),
+            "config": {"workload": f"MPO pair config {args.pair}: N={c.N}, d={c.d}, chi={c.chi_l}, "
+                                   f"{c.meta['charges']} charge pairs", "f_contract": flops["f_contract"],
+                       "f_mix": flops["f_mix"], "contraction": args.contraction,
+                       "step": "tn_theta2_plan + tn_build_bs_unitary + tn_theta_exec"},
+            "roofline": {"bound": "tensor", "kernel": "k4_contract", "achieved": round(achieved, 3),
+                         "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_TC_PEAK_TFLOPS, 4),
+                         "achieved_def": "F_contract (useful, 8/CMAC) / mean K4 launch time"},
+            "kernels_ms": {k: round(v, 4) for k, v in km.items()},
+            "mix_hbm_gbs": round(2 * 2 * 16 * sum(o.numel() for o in outs) / (km["k5_mix"] * 1e-3) / 1e9, 1),
+            "gpu_launches": 7 * args.steps, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------------------------------- config 4 sweep
 def run_sweep(args, rank, world, local_rank):
     """BASELINE.json config 4: a brick-wall layer of `--gates` beam-splitter gates (N=47, d=48, χ=8192),
@@ -533,7 +616,9 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if args.config == 4:
+        if args.pair is not None:
+            run_pair(args, rank, world, local_rank)
+        elif args.config == 4:
             run_sweep(args, rank, world, local_rank)
         else:
             run_tn(args, rank, world, local_rank)

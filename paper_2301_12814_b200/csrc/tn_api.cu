@@ -137,9 +137,8 @@ static SectorParams make_sector_params(const tn_plan* p, double* const* theta_ou
   for (size_t n = 0; n < p->ustart.size(); ++n) sp.ustart[n] = p->ustart[n];
   // The mix reads P_{c_c} iff seg_c(c_c) is non-empty: exactly then K4 ran group c_c for every
   // local row that can need it (a row of Θ(c_c) in this shard).
-  if (!p->pair)
-    for (int cc = 0; cc <= p->N; ++cc)
-      if (p->off[1][cc + 1] > p->off[1][cc]) sp.cc_mask[cc >> 5] |= 1u << (cc & 31);
+  for (int cc = 0; cc < p->nq; ++cc)  // pair plans: one bit per centre KEY
+    if (p->off[1][cc + 1] > p->off[1][cc]) sp.cc_mask[cc >> 5] |= 1u << (cc & 31);
   return sp;
 }
 

@@ -42,12 +42,13 @@ struct TileDesc {
   int32_t g, mt, nt, pad;
 };
 
-struct MixTile2 {           // K5P work unit (pair plans): one species' U mix over ≤ 128 8-groups of one (l, r) block
+struct MixTile2 {           // K5P work unit (pair plans): one species' U mix over ≤ ~128 8-groups of one (l, r) block
   int32_t cl, n, lo, L;     // that species' left charge, U block n = l_s − r_s, first index lo, vector length L
-  int32_t e0, ne, nr, ngr;  // as MixTile
-  int32_t pl0, pr0;         // sorted positions of the band's first row / the block's first column
-  int32_t sl_off;           // first of L entries {sector, local row of the band, local col of the block, src valid}
-  int32_t flags;            // bit 0: conj(U) (bra species); bit 1: apply λl·λr (last pass)
+  int32_t e0, ne, nr, ngr;  // as MixTile (8-groups row-major over the tile's rows of segment l)
+  int32_t pl0, pr0;         // sorted positions of the tile's first row / the block's first column
+  int32_t lkey, rkey;       // pair keys of the left / right segment
+  int32_t fixed, band;      // the other species' output value; the tile's first row within segment l
+  int32_t flags, pad;       // bit 0: pass 2 (species 2: conj(U), sectors (fixed, lo+u), outer λ's)
 };
 
 struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive columns of one row) of one (c_l, c_r) block
@@ -130,10 +131,11 @@ struct tn_plan {
   const int32_t* d_colperm = nullptr;
   // pair plans: two-pass U⊗U* mix (tn_pair.cu)
   tn::MixTile2* d_mix2 = nullptr;
-  int4* d_seclist = nullptr;
+  int32_t* d_rowoff = nullptr;                 // [sector][left key]: local row of the segment in the sector (−1: absent)
+  int32_t* d_coloff = nullptr;                 // [sector][right key]: local column of the segment
   int64_t nmix2[2] = {0, 0};                   // tiles of pass 1 (species 1) and pass 2 (species 2)
   std::vector<tn::MixTile2> h_mix2;
-  std::vector<int4> h_seclist;
+  std::vector<int32_t> h_rowoff, h_coloff;
   std::vector<int32_t> h_rowperm_pos, h_colperm_pos;
   double2* d_apanel = nullptr;
   double2* d_bpanel = nullptr;

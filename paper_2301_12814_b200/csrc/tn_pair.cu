@@ -43,7 +43,10 @@ tn_status build_pair_tables(tn_plan* p) {
   auto cnt = [](const std::vector<int32_t>& o, int k) { return (int64_t)o[k + 1] - o[k]; };
   auto ok = [d](int a, int b) { return a - b >= 0 && a - b <= d - 1; };
   // ---- sector layouts: local row / column offset of every pair segment inside every sector ----
-  std::vector<int64_t> rowoff((size_t)nq * nq, -1), coloff((size_t)nq * nq, -1);
+  std::vector<int32_t>& rowoff = p->h_rowoff;
+  std::vector<int32_t>& coloff = p->h_coloff;
+  rowoff.assign((size_t)nq * nq, -1);
+  coloff.assign((size_t)nq * nq, -1);
   p->R.assign(nq, 0);
   p->C.assign(nq, 0);
   p->row0.assign(nq, 0);
@@ -59,12 +62,12 @@ tn_status build_pair_tables(tn_plan* p) {
       int64_t r = 0, c = 0;
       for (int l1 = c1; l1 <= std::min(N, c1 + d - 1); ++l1)  // keys ascend = sorted order
         for (int l2 = c2; l2 <= std::min(N, c2 + d - 1); ++l2) {
-          rowoff[(size_t)s * nq + l1 * nk + l2] = r;
+          rowoff[(size_t)s * nq + l1 * nk + l2] = (int32_t)r;
           r += cnt(ol, l1 * nk + l2);
         }
       for (int r1 = std::max(0, c1 - d + 1); r1 <= c1; ++r1)
         for (int r2 = std::max(0, c2 - d + 1); r2 <= c2; ++r2) {
-          coloff[(size_t)s * nq + r1 * nk + r2] = c;
+          coloff[(size_t)s * nq + r1 * nk + r2] = (int32_t)c;
           c += cnt(orr, r1 * nk + r2);
         }
       if (r > INT32_MAX || c > INT32_MAX) return fail(TN_ERR_UNSUPPORTED, "sector dimension > INT32_MAX");
@@ -138,12 +141,9 @@ tn_status build_pair_tables(tn_plan* p) {
     for (int mt = 0; mt < p->groups[gi].nmt; ++mt)
       for (int nt = 0; nt < p->groups[gi].nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
   p->ntiles = (int64_t)tiles.size();
-  // ---- two-pass mix tiles: ≤ 4 rows of one left pair segment × one right pair segment ----
+  // ---- two-pass mix tiles: rows of one left pair segment (≈ 128 8-groups) × one right pair segment ----
   std::vector<MixTile2>& mix = p->h_mix2;
-  std::vector<int4>& sl = p->h_seclist;
   mix.clear();
-  sl.clear();
-  constexpr int BAND = 4;
   int max_l = 1;
   for (int pass = 0; pass < 2; ++pass) {
     for (int l = 0; l < nq; ++l) {
@@ -159,36 +159,29 @@ tn_status build_pair_tables(tn_plan* p) {
         if (hi1 < lo1 || hi2 < lo2) continue;
         const int L = pass == 0 ? hi1 - lo1 + 1 : hi2 - lo2 + 1;
         max_l = std::max(max_l, L);
+        const int64_t ngr = (nr + 7) / 8;
+        const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
         const int fixed_lo = pass == 0 ? lo2 : lo1, fixed_hi = pass == 0 ? hi2 : hi1;
         for (int f = fixed_lo; f <= fixed_hi; ++f)
-          for (int64_t band = 0; band < nl; band += BAND) {
-            const int64_t rows = std::min<int64_t>(BAND, nl - band);
-            const int64_t ngr = (nr + 7) / 8, G = rows * ngr;
-            for (int64_t e0 = 0; e0 < G; e0 += MIX_GROUPS_PER_TILE) {
-              MixTile2 t{};
-              t.cl = pass == 0 ? l1 : l2;
-              t.n = pass == 0 ? l1 - r1 : l2 - r2;
-              t.lo = pass == 0 ? lo1 : lo2;
-              t.L = L;
-              t.e0 = (int32_t)e0;
-              t.ne = (int32_t)std::min<int64_t>(MIX_GROUPS_PER_TILE, G - e0);
-              t.nr = (int32_t)nr;
-              t.ngr = (int32_t)ngr;
-              t.pl0 = (int32_t)(ol[l] + band);
-              t.pr0 = orr[r];
-              t.sl_off = (int32_t)sl.size();
-              t.flags = pass == 0 ? 0 : 3;  // pass 2: conj(U) and the outer λ's
-              for (int u = 0; u < L; ++u) {
-                const int x = pass == 0 ? lo1 + u : f, y = pass == 0 ? f : lo2 + u;
-                const int s = x * nk + y;
-                const int64_t ro = rowoff[(size_t)s * nq + l], co = coloff[(size_t)s * nq + r];
-                if (ro < 0 || co < 0) return fail(TN_ERR_CONSISTENCY, "pair plan: block outside a sector (internal)");
-                // pass 1 reads P(x, y) only where the centre pair has bonds; pass 2 reads Q (always written)
-                const int valid = pass == 1 || cnt(oc, s) > 0;
-                sl.push_back(make_int4(s, (int)(ro + band), (int)co, valid));
-              }
-              mix.push_back(t);
-            }
+          for (int64_t band = 0; band < nl; band += rows_per) {
+            const int64_t rows = std::min<int64_t>(rows_per, nl - band);
+            MixTile2 t{};
+            t.cl = pass == 0 ? l1 : l2;
+            t.n = pass == 0 ? l1 - r1 : l2 - r2;
+            t.lo = pass == 0 ? lo1 : lo2;
+            t.L = L;
+            t.e0 = 0;
+            t.ne = (int32_t)(rows * ngr);
+            t.nr = (int32_t)nr;
+            t.ngr = (int32_t)ngr;
+            t.pl0 = (int32_t)(ol[l] + band);
+            t.pr0 = orr[r];
+            t.lkey = l;
+            t.rkey = r;
+            t.fixed = f;
+            t.band = (int32_t)band;
+            t.flags = pass;
+            mix.push_back(t);
           }
       }
     }
@@ -201,7 +194,8 @@ tn_status build_pair_tables(tn_plan* p) {
   const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
   const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
   const size_t o_m = cw.take<MixTile2>((int64_t)mix.size());
-  const size_t o_s = cw.take<int4>((int64_t)sl.size());
+  const size_t o_ro = cw.take<int32_t>((int64_t)nq * nq);
+  const size_t o_co = cw.take<int32_t>((int64_t)nq * nq);
   const size_t o_rp = cw.take<int32_t>((int64_t)rpos.size());
   const size_t o_cp = cw.take<int32_t>((int64_t)cpos.size());
   const size_t o_rg = cw.take<int32_t>((int64_t)rpos.size());
@@ -215,7 +209,8 @@ tn_status build_pair_tables(tn_plan* p) {
   p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
   p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
   p->d_mix2 = reinterpret_cast<MixTile2*>(base + o_m);
-  p->d_seclist = reinterpret_cast<int4*>(base + o_s);
+  p->d_rowoff = reinterpret_cast<int32_t*>(base + o_ro);
+  p->d_coloff = reinterpret_cast<int32_t*>(base + o_co);
   int32_t* d_rpos = reinterpret_cast<int32_t*>(base + o_rp);
   int32_t* d_cpos = reinterpret_cast<int32_t*>(base + o_cp);
   int32_t* d_rg = reinterpret_cast<int32_t*>(base + o_rg);
@@ -233,7 +228,8 @@ tn_status build_pair_tables(tn_plan* p) {
   if ((st = up(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc), "H2D groups")) != TN_OK) return st;
   if ((st = up(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), "H2D tiles")) != TN_OK) return st;
   if ((st = up(p->d_mix2, mix.data(), mix.size() * sizeof(MixTile2), "H2D mix tiles")) != TN_OK) return st;
-  if ((st = up(p->d_seclist, sl.data(), sl.size() * sizeof(int4), "H2D sector lists")) != TN_OK) return st;
+  if ((st = up(p->d_rowoff, rowoff.data(), rowoff.size() * sizeof(int32_t), "H2D row offsets")) != TN_OK) return st;
+  if ((st = up(p->d_coloff, coloff.data(), coloff.size() * sizeof(int32_t), "H2D col offsets")) != TN_OK) return st;
   if ((st = up(d_rpos, rpos.data(), rpos.size() * sizeof(int32_t), "H2D row positions")) != TN_OK) return st;
   if ((st = up(d_cpos, cpos.data(), cpos.size() * sizeof(int32_t), "H2D col positions")) != TN_OK) return st;
   // gathered index lists: original bond index of every group row / column (K1's perm already on device)
@@ -251,22 +247,25 @@ constexpr int K5P_THREADS = 128;
 
 template <int NTMAX>
 __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
-    k5p_mix(const SectorParams sp, const MixTile2* __restrict__ tiles, const int4* __restrict__ seclist,
-            const int32_t* __restrict__ perm_l, const int32_t* __restrict__ perm_r, const double* __restrict__ ll,
-            const double* __restrict__ lr, const double2* __restrict__ U, int us_elems) {
+    k5p_mix(const SectorParams sp, const MixTile2* __restrict__ tiles, const int32_t* __restrict__ rowoff,
+            const int32_t* __restrict__ coloff, int nq, const int32_t* __restrict__ perm_l,
+            const int32_t* __restrict__ perm_r, const double* __restrict__ ll, const double* __restrict__ lr,
+            const double2* __restrict__ U, int us_elems) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const MixTile2 t = tiles[blockIdx.x];
   SecRef* ld_sec = reinterpret_cast<SecRef*>(smem_raw);
   SecRef* st_sec = ld_sec + 8 * NTMAX;
   double2* Us = reinterpret_cast<double2*>(st_sec + 8 * NTMAX);
   double* UsS = reinterpret_cast<double*>(Us + us_elems);
-  const int L = t.L, d = sp.d;
-  const bool cj = t.flags & 1;
+  const int L = t.L, d = sp.d, nk = sp.N + 1;
+  const bool pass2 = t.flags & 1;
   for (int u = threadIdx.x; u < L; u += K5P_THREADS) {
-    const int4 e = seclist[t.sl_off + u];
-    const double2* base = sp.out[e.x] + (int64_t)e.y * sp.ld[e.x] + e.z;
-    ld_sec[u] = SecRef{e.w ? base : nullptr, (int64_t)sp.ld[e.x]};
-    st_sec[u] = SecRef{base, (int64_t)sp.ld[e.x]};
+    // pass 1: sectors (lo+u, fixed), sources P valid only for a non-empty centre pair; pass 2: (fixed, lo+u)
+    const int s = pass2 ? t.fixed * nk + t.lo + u : (t.lo + u) * nk + t.fixed;
+    const double2* base = sp.out[s] + (int64_t)(rowoff[s * nq + t.lkey] + t.band) * sp.ld[s] + coloff[s * nq + t.rkey];
+    const bool valid = pass2 || ((sp.cc_mask[s >> 5] >> (s & 31)) & 1u);
+    ld_sec[u] = SecRef{valid ? base : nullptr, (int64_t)sp.ld[s]};
+    st_sec[u] = SecRef{base, (int64_t)sp.ld[s]};
   }
   // Us[t][u] = U_n[i = cl − (lo+t)][j = cl − (lo+u)]  (conjugated for the bra species), padded to TP × UP
   const int TP = (L + 7) & ~7, UP = (L + 3) & ~3;
@@ -278,7 +277,7 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
     double2 v = make_double2(0.0, 0.0);
     if (tt < L && u < L) {
       v = __ldg(Ub + (t.cl - t.lo - tt - nlo) * sn + (t.cl - t.lo - u - nlo));
-      if (cj) v.y = -v.y;
+      if (pass2) v.y = -v.y;  // the bra species carries conj(U)
     }
     Us[tt * ust + u] = v;
     UsS[tt * ust + u] = v.x + v.y;
@@ -293,7 +292,7 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
   mt.ngr = t.ngr;
   mt.pl0 = t.pl0;
   mt.pr0 = t.pr0;
-  const bool sc = t.flags & 2;
+  const bool sc = pass2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   switch (TP >> 3) {
 #define TN_MIX_CASE(m)                                                                                       \
@@ -326,8 +325,8 @@ cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const doub
       cudaError_t e = cudaFuncSetAttribute(k5p_mix<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                                         \
     }                                                                                                         \
-    k5p_mix<M><<<(unsigned)n, K5P_THREADS, smem, s>>>(sp, tiles, p->d_seclist, p->d_perm[0], p->d_perm[2], ll, lr, \
-                                                       U, smax);                                             \
+    k5p_mix<M><<<(unsigned)n, K5P_THREADS, smem, s>>>(sp, tiles, p->d_rowoff, p->d_coloff, p->nq, p->d_perm[0],   \
+                                                       p->d_perm[2], ll, lr, U, smax);                       \
   } while (0)
     if (NT <= 1)
       TN_P_LAUNCH(1);
