@@ -15,6 +15,8 @@ Every function is a plain, slow, obviously-correct transcription of PAPER.md (Su
   * `theta2_sectors`   — the MPO (doubled-charge) Θ(c1, c2) of PAPER.md:101, :107 (U → U⊗U*, two
                          conserved charges) by the literal loop over three charge PAIRS (oracle/theta2.py)
   * `sort_pair_bonds`, `pair_sector_rows/cols`, `flop_counts2` — its tables and useful work
+  * `svd.truncate_update` — per-sector SVD (numpy) + global top-χ
+                         + the new canonical factors Γ^{[k]}, λ^{[k]}, Γ^{[k+1]} (oracle/svd.py)
 
 Pins (tests/test_oracle_pins.py, `-m "not gpu"`): dense δ-tensor brute force (tiny inputs), scipy
 expm of the block generator, HOM dip, θ=0 identity, θ=π/2 swap closed form, Wigner-d (sympy),
@@ -22,10 +24,14 @@ block unitarity, norm invariance Σ_c‖Θ(c)‖² with d=N+1, identity gate == 
 SPEC.md sort examples; for the MPO path (tests/test_oracle2_pins.py): the vectorized-pure-state
 factorisation Θ2(c1,c2)[(α,α'),(β,β')] = Θ(c1)[α,β]·conj(Θ(c2)[α',β']) against the pinned single-charge
 oracle, a dense brute force with the doubled gate built from scipy expm and explicit δ tensors per
-species, identity gate == two-site product, and Σ‖Θ2‖² invariance. No function here is "parity unpinned".
+species, identity gate == two-site product, and Σ‖Θ2‖² invariance; for the SVD step
+(tests/test_oracle_svd_pins.py): SPEC.md's worked example, known spectra, Eckart–Young on the
+block-diagonal Θ, exact reconstruction without truncation, orthonormal factors, the tie-break rule.
+No function here is "parity unpinned".
 """
 from .theta import (sort_bonds, bs_unitary_block, packed_u, packed_u_offsets, theta_sectors,
                     theta_element, sector_ranges, flop_counts)
+from . import svd
 from .theta2 import (sort_pair_bonds, pair_sector_rows, pair_sector_cols, theta2_sectors, theta2_element,
                      flop_counts2)
 

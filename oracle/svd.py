@@ -1,0 +1,84 @@
+"""Plain CPU oracle of the per-sector SVD + global top-χ truncation + new bond (TEST INFRASTRUCTURE ONLY).
+
+PAPER.md:67: "Singular value decompositions are then performed on Θ(c^{[k]}), and the largest χ singular
+values out of the singular values for all Θ(c^{[k]}) and their corresponding bonds are retained. The
+produced outputs are manipulated to update the MPS representation." SPEC.md:70-78 (truncated_svd_global)
+fixes the contract this follows, with its design decisions: global ranking by value
+descending, then charge ascending, then within-slice index ascending; values ≤ cutoff (1e−14) never kept.
+
+Update (Vidal's canonical form, the MPS of PAPER.md:45; R21): Θ(c) = U_c diag(s_c) V_c†;
+the kept values form the new λ^{[k]} (not renormalised: the factors reproduce the retained slices,
+SPEC.md:74), each kept value carries its sector's charge c; the new bond is ordered by charge
+ascending, then by value descending (a prefix of each sector's spectrum);
+  Γ^{[k]}_new[α, a]   = U_c[α, s] / λ^{[k−1]}[α]     (α in Θ(c)'s rows; 0 elsewhere)
+  Γ^{[k+1]}_new[a, β] = V_c†[s, β] / λ^{[k+1]}[β]    (β in Θ(c)'s columns; 0 elsewhere)
+with a ↔ (c, s), and x/0 := 0. Rows/columns are returned in the CALLER's bond order.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .theta import sector_ranges, sort_bonds
+
+
+def sector_svds(sectors):
+    """numpy SVD of every sector (library routine): list of (U, s, Vh), s descending."""
+    out = []
+    for th in sectors:
+        if th.size == 0:
+            out.append((np.zeros((th.shape[0], 0), complex), np.zeros(0), np.zeros((0, th.shape[1]), complex)))
+        else:
+            out.append(np.linalg.svd(th, full_matrices=False))
+    return out
+
+
+def global_top_chi(svals, chi_max: int, cutoff: float = 1e-14):
+    """Global ranking: value desc, then charge asc, then index asc; keep ≤ chi_max values > cutoff.
+    Returns (kept per sector k_c, discarded weight Σ dropped s²)."""
+    entries = [(-float(v), c, i) for c, s in enumerate(svals) for i, v in enumerate(s)]
+    entries.sort()
+    kept = [0] * len(svals)
+    disc = 0.0
+    n = 0
+    for negv, c, i in entries:
+        v = -negv
+        if n < chi_max and v > cutoff:
+            kept[c] += 1
+            n += 1
+        else:
+            disc += v * v
+    return kept, disc
+
+
+def truncate_update(N, d, q_l, q_r, sectors, lam_l, lam_r, chi_max, cutoff=1e-14):
+    """The whole step on host. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
+    [chi × χ_r], kept, discarded, svals)."""
+    perm_l, off_l = sort_bonds(q_l, N)
+    perm_r, off_r = sort_bonds(q_r, N)
+    svd = sector_svds(sectors)
+    kept, disc = global_top_chi([s for _, s, _ in svd], chi_max, cutoff)
+    chi = sum(kept)
+    gk = np.zeros((len(q_l), chi), dtype=np.complex128)
+    gk1 = np.zeros((chi, len(q_r)), dtype=np.complex128)
+    q_new = np.zeros(chi, dtype=np.int32)
+    lam_new = np.zeros(chi)
+    a = 0
+    for c in range(N + 1):
+        k = kept[c]
+        if k == 0:
+            continue
+        U, s, Vh = svd[c]
+        (r0, r1), (k0, k1) = sector_ranges(off_l, off_r, N, d, c)
+        rows = perm_l[r0:r1]                    # caller indices of Θ(c)'s rows
+        cols = perm_r[k0:k1]
+        ll = np.asarray(lam_l)[rows]
+        lr = np.asarray(lam_r)[cols]
+        inv_l = np.divide(1.0, ll, out=np.zeros_like(ll), where=ll != 0)
+        inv_r = np.divide(1.0, lr, out=np.zeros_like(lr), where=lr != 0)
+        gk[rows, a:a + k] = U[:, :k] * inv_l[:, None]
+        gk1[a:a + k][:, cols] = Vh[:k, :] * inv_r[None, :]
+        q_new[a:a + k] = c
+        lam_new[a:a + k] = s[:k]
+        a += k
+    return dict(chi=chi, q_new=q_new, lam_new=lam_new, gamma_k_new=gk, gamma_k1_new=gk1, kept=kept,
+                discarded=disc, svals=[s for _, s, _ in svd])
