@@ -178,6 +178,33 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
                         double* const* theta_out);
 
 /* ------------------------------------------------------------------------------------------ */
+/* SVD step after Θ: PAPER.md:67.                      */
+/* ------------------------------------------------------------------------------------------ */
+/* tn_svd_truncate — per-sector SVD Θ(c) = U_c diag(s_c) V_c† (cuSOLVER Jacobi), global ranking of
+ * every singular value (value descending, then charge ascending, then index ascending),
+ * keep the first min(chi_max, #{s > cutoff}) (SPEC.md:98 uses cutoff 1e−14), and write the new
+ * canonical factors of bond k (Vidal form, R21): the new bond is ordered by charge
+ * ascending, then value descending; for new bond a ↔ (c, s):
+ *   q_new[a] = c,  lambda_new[a] = s_c[s]  (not renormalised),
+ *   gamma_k_new [α × a] (complex, row-major, ld = chi_max, rows in the CALLER's α_{k−1} order)
+ *                  = U_c[α, s] / λ^{[k−1]}[α] for α in Θ(c)'s rows, 0 elsewhere (x/0 := 0),
+ *   gamma_k1_new[a × β] (complex, row-major, ld = χ_r, columns in the caller's α_{k+1} order)
+ *                  = V_c†[s, β] / λ^{[k+1]}[β] for β in Θ(c)'s columns, 0 elsewhere.
+ *   theta      HOST array of N+1 DEVICE sector pointers from tn_theta_exec — DESTROYED (used as the
+ *              SVD's input/workspace).
+ *   lambda_l, lambda_r  DEVICE λ^{[k−1]}, λ^{[k+1]} (the ones passed to tn_theta_exec).
+ *   q_new [chi_max] int32, lambda_new [chi_max] double, gamma_k_new [χ_l·chi_max] and
+ *   gamma_k1_new [chi_max·χ_r] complex: DEVICE, caller-owned; entries beyond *chi_out are zero /
+ *   unspecified. *chi_out (HOST) = number kept, *discarded (HOST) = Σ of dropped s².
+ * Synchronises the stream once (the kept count is returned on the host). Single-GPU single-charge
+ * plans only. Errors: TN_ERR_DIMENSION (NULL), TN_ERR_DOMAIN (chi_max < 1, cutoff < 0),
+ * TN_ERR_UNSUPPORTED (sharded or pair plan), TN_ERR_OOM, TN_ERR_CUDA (incl. SVD non-convergence). */
+TN_API tn_status tn_svd_truncate(const tn_plan* plan, tn_stream stream, double* const* theta,
+                                 const double* lambda_l, const double* lambda_r, int64_t chi_max,
+                                 double cutoff, int32_t* q_new, double* lambda_new, double* gamma_k_new,
+                                 double* gamma_k1_new, int64_t* chi_out, double* discarded);
+
+/* ------------------------------------------------------------------------------------------ */
 /* Multi-GPU (one process per GPU): row-sharded exec + NCCL.                 */
 /* ------------------------------------------------------------------------------------------ */
 /* 128-byte NCCL unique id for rank 0 to create and distribute (e.g. via torch.distributed). */

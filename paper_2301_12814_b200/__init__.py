@@ -18,7 +18,7 @@ import torch
 from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT, TN_GATHER_NONE,
                    TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH)
 
-__all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Plan2", "Comm", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
+__all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Plan2", "Comm", "svd_truncate", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
            "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
 
 
@@ -214,6 +214,25 @@ def theta_exec(plan: Plan, gk, lk, gk1, ll, lr, U, out=None, stream=None):
     check(lib.tn_theta_exec(plan.handle, _stream_ptr(stream), _ptr(gk), _ptr(lk), _ptr(gk1), _ptr(ll), _ptr(lr),
                             _ptr(U), ptrs), "tn_theta_exec")
     return out
+
+
+def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None):
+    """tn_svd_truncate: per-sector SVD + global top-χ + new canonical factors. `theta` (the list from
+    theta_exec) is DESTROYED. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
+    [chi × χ_r], discarded) as CUDA tensors (views of chi_max-capacity buffers)."""
+    chi_l, _, chi_r = plan.chi
+    dev = ll.device
+    q_new = torch.zeros(chi_max, dtype=torch.int32, device=dev)
+    lam_new = torch.zeros(chi_max, dtype=torch.float64, device=dev)
+    gk = torch.empty((chi_l, chi_max), dtype=torch.complex128, device=dev)
+    gk1 = torch.empty((chi_max, chi_r), dtype=torch.complex128, device=dev)
+    chi_out, disc = C.c_int64(), C.c_double()
+    check(lib.tn_svd_truncate(plan.handle, _stream_ptr(stream), _theta_ptrs(theta), _ptr(ll), _ptr(lr), int(chi_max),
+                              float(cutoff), _ptr(q_new), _ptr(lam_new), _ptr(gk), _ptr(gk1), C.byref(chi_out),
+                              C.byref(disc)), "tn_svd_truncate")
+    k = chi_out.value
+    return dict(chi=k, q_new=q_new[:k], lam_new=lam_new[:k], gamma_k_new=gk[:, :k], gamma_k1_new=gk1[:k],
+                discarded=disc.value)
 
 
 class Comm:

@@ -45,6 +45,8 @@ SIGNATURES = {
     "tn_release_cached_memory": [_i64p, _i64p],
     "tn_build_bs_unitary": [_p, C.c_double, C.c_double, _p, _p],
     "tn_theta_exec": [_p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
+    "tn_svd_truncate": [_p, _p, C.POINTER(_p), _p, _p, C.c_int64, C.c_double, _p, _p, _p, _p, _i64p,
+                        C.POINTER(C.c_double)],
     "tn_comm_unique_id": [_p],
     "tn_comm_init": [_p, C.c_int, C.c_int, C.POINTER(_p)],
     "tn_comm_destroy": [_p],

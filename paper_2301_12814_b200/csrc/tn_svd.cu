@@ -1,0 +1,278 @@
+// SVD step after Θ: per-sector SVD, global top-χ, new canonical factors.
+//
+// PAPER.md:67 "Singular value decompositions are then performed on Θ(c^{[k]}), and the largest χ singular
+// values out of the singular values for all Θ(c^{[k]}) and their corresponding bonds are retained";
+// PAPER.md:192 (SVD "takes up the majority" of GPU time); contract SPEC.md:70-78, tie-break SPEC.md:97.
+//
+// B200 design (DESIGN.md §4 "SVD step"):
+//  * Per-sector SVD with cuSOLVER's one-sided Jacobi (cusolverDnZgesvdj, econ): a library routine, as the
+//    paper treats SVD ("a well-researched and optimized routine"). Θ(c) is row-major, i.e.
+//    the column-major C×R matrix X = Θᵀ = U_x S V_xᴴ, so Θ = conj(V_x) S U_xᵀ.
+//  * Global ranking on the device: one stable radix sort (cub) of all singular values, descending, whose
+//    input order is (charge asc, index asc) — exactly SPEC.md:97's tie-break; the kept set is a prefix.
+//  * K_sel (one CTA): kept count per charge, discarded weight Σ dropped s², new-bond offsets (charge
+//    ascending, then value descending = a prefix of every sector's spectrum), q_new and λ_new.
+//  * K_fac: Γ^{[k]}_new[α, a] = U_c[α, s]/λl[α] and Γ^{[k+1]}_new[a, β] = V_c†[s, β]/λr[β] (x/0 := 0),
+//    written straight into the caller's bond order through perm_l / perm_r.
+#include <cub/device/device_radix_sort.cuh>
+#include <cusolverDn.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tn_internal.cuh"
+
+namespace tn {
+
+namespace {
+struct SvdCtx {  // cuSOLVER handle + a grow-only device scratch, per process
+  cusolverDnHandle_t h = nullptr;
+  gesvdjInfo_t params = nullptr;
+  void* buf = nullptr;
+  size_t cap = 0;
+  std::mutex mu;
+};
+SvdCtx& ctx() {
+  static SvdCtx c;
+  return c;
+}
+}  // namespace
+
+struct SvdSector {          // device views of one sector's SVD
+  const double2* ux;        // C × k column-major (ld C)
+  const double2* vx;        // R × k column-major (ld R)
+  const double* s;          // k values, descending
+  int64_t row0, col0;       // sorted positions of Θ(c)'s first row / column
+  int32_t R, C, k;
+};
+
+constexpr int SVD_MAXSEC = MAXC;
+struct SvdParams {
+  SvdSector sec[SVD_MAXSEC];
+  int nsec;
+};
+
+__global__ void k_svd_pack(const SvdParams sp, double* __restrict__ keys, int32_t* __restrict__ vals,
+                           const int64_t* __restrict__ base) {
+  const int c = blockIdx.y;
+  const SvdSector S = sp.sec[c];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S.k; i += gridDim.x * blockDim.x) {
+    keys[base[c] + i] = S.s[i];
+    vals[base[c] + i] = (c << 20) | i;  // k < 2^20 (χ ≤ INT32 and sectors ≤ 2^20 columns)
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_svd_select(const SvdParams sp, const double* __restrict__ skeys,
+                                                      const int32_t* __restrict__ svals, int64_t total,
+                                                      int64_t chi_max, double cutoff, int32_t* __restrict__ q_new,
+                                                      double* __restrict__ lam_new, int32_t* __restrict__ off_new,
+                                                      int64_t* __restrict__ chi_out, double* __restrict__ disc_out) {
+  __shared__ int32_t kept[SVD_MAXSEC + 1];
+  __shared__ double red[32];
+  __shared__ int64_t nkeep_s;
+  const int tid = threadIdx.x;
+  for (int c = tid; c <= SVD_MAXSEC; c += blockDim.x) kept[c] = 0;
+  if (tid == 0) {
+    // kept = the first min(chi_max, #(s > cutoff)) sorted entries (values > cutoff form a prefix)
+    int64_t lo = 0, hi = total;  // first index with s ≤ cutoff
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (skeys[mid] > cutoff) lo = mid + 1;
+      else hi = mid;
+    }
+    nkeep_s = lo < chi_max ? lo : chi_max;
+  }
+  __syncthreads();
+  const int64_t nkeep = nkeep_s;
+  double acc = 0.0;
+  for (int64_t i = tid; i < total; i += blockDim.x) {
+    if (i < nkeep) atomicAdd(&kept[svals[i] >> 20], 1);
+    else acc += skeys[i] * skeys[i];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *disc_out = t;
+    *chi_out = nkeep;
+    int32_t o = 0;
+    for (int c = 0; c < sp.nsec; ++c) {
+      off_new[c] = o;
+      o += kept[c];
+    }
+    off_new[sp.nsec] = o;
+  }
+  __syncthreads();
+  for (int c = 0; c < sp.nsec; ++c) {  // new bond a = off_new[c] + s, s < kept[c]
+    const int32_t o = off_new[c];
+    for (int s = tid; s < kept[c]; s += blockDim.x) {
+      q_new[o + s] = c;
+      lam_new[o + s] = sp.sec[c].s[s];
+    }
+  }
+}
+
+// blockIdx.y = sector; Γk_new rows (α of Θ(c)) × kept columns, then Γk1_new kept rows × columns (β)
+__global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ off_new, const int32_t* __restrict__ perm_l,
+                              const int32_t* __restrict__ perm_r, const double* __restrict__ lam_l,
+                              const double* __restrict__ lam_r, int64_t chi_max, int64_t chi_r,
+                              double2* __restrict__ gk_new, double2* __restrict__ gk1_new) {
+  const int c = blockIdx.y;
+  const SvdSector S = sp.sec[c];
+  const int32_t a0 = off_new[c], kc = off_new[c + 1] - a0;
+  if (kc == 0) return;
+  const int64_t na = (int64_t)S.R * kc, nb = (int64_t)kc * S.C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < na) {  // U_Θ[r, s] = conj(V_x[r, s]); consecutive threads → consecutive new-bond columns
+      const int r = (int)(i / kc), s = (int)(i - (int64_t)r * kc);
+      const int32_t al = perm_l[S.row0 + r];
+      const double l = lam_l[al];
+      const double2 v = S.vx[r + (int64_t)s * S.R];
+      const double inv = l != 0.0 ? 1.0 / l : 0.0;
+      gk_new[(int64_t)al * chi_max + a0 + s] = make_double2(v.x * inv, -v.y * inv);
+    } else {       // V_Θ†[s, col] = U_x[col, s]
+      const int64_t j = i - na;
+      const int s = (int)(j / S.C), col = (int)(j - (int64_t)s * S.C);
+      const int32_t be = perm_r[S.col0 + col];
+      const double l = lam_r[be];
+      const double2 u = S.ux[col + (int64_t)s * S.C];
+      const double inv = l != 0.0 ? 1.0 / l : 0.0;
+      gk1_new[(int64_t)(a0 + s) * chi_r + be] = make_double2(u.x * inv, u.y * inv);
+    }
+  }
+}
+
+}  // namespace tn
+
+using namespace tn;
+
+extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double* const* theta, const double* lambda_l,
+                                     const double* lambda_r, int64_t chi_max, double cutoff, int32_t* q_new,
+                                     double* lambda_new, double* gamma_k_new, double* gamma_k1_new, int64_t* chi_out,
+                                     double* discarded) {
+  if (chi_max < 1 || !(cutoff >= 0.0)) return fail(TN_ERR_DOMAIN, "tn_svd_truncate: chi_max < 1 or cutoff < 0");
+  if (!p || !theta || !lambda_l || !lambda_r || !q_new || !lambda_new || !gamma_k_new || !gamma_k1_new || !chi_out ||
+      !discarded)
+    return fail(TN_ERR_DIMENSION, "tn_svd_truncate: NULL argument");
+  if (p->world != 1 || p->pair)
+    return fail(TN_ERR_UNSUPPORTED, "tn_svd_truncate: needs a single-GPU, single-charge plan (full sectors)");
+  cudaStream_t s = (cudaStream_t)stream;
+  SvdCtx& X = ctx();
+  std::lock_guard<std::mutex> lock(X.mu);
+  if (!X.h) {
+    if (cusolverDnCreate(&X.h) != CUSOLVER_STATUS_SUCCESS) return fail(TN_ERR_CUDA, "cusolverDnCreate failed");
+    if (cusolverDnCreateGesvdjInfo(&X.params) != CUSOLVER_STATUS_SUCCESS)
+      return fail(TN_ERR_CUDA, "cusolverDnCreateGesvdjInfo failed");
+    cusolverDnXgesvdjSetTolerance(X.params, 0.0);      // 0 → machine accuracy
+    cusolverDnXgesvdjSetMaxSweeps(X.params, 100);
+  }
+  cusolverDnSetStream(X.h, s);
+  const int ns = p->nsec;
+  // ---- scratch layout: per sector U_x, V_x, S, workspace; then sort buffers ----
+  SvdParams sp{};
+  sp.nsec = ns;
+  std::vector<size_t> o_ux(ns), o_vx(ns), o_s(ns), o_w(ns);
+  std::vector<int> lwork(ns, 0);
+  std::vector<int64_t> base(ns + 1, 0);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  for (int c = 0; c < ns; ++c) {
+    const int R = (int)p->R[c], C = (int)p->C[c], k = std::min(R, C);
+    base[c + 1] = base[c] + k;
+    if (k == 0) continue;
+    if (cusolverDnZgesvdj_bufferSize(X.h, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, nullptr, C, nullptr, nullptr, C, nullptr,
+                                     R, &lwork[c], X.params) != CUSOLVER_STATUS_SUCCESS)
+      return fail(TN_ERR_CUDA, "cusolverDnZgesvdj_bufferSize failed");
+    o_ux[c] = take((size_t)C * k * 16);
+    o_vx[c] = take((size_t)R * k * 16);
+    o_s[c] = take((size_t)k * 8);
+    o_w[c] = take((size_t)lwork[c] * 16);
+  }
+  const int64_t total = base[ns];
+  const size_t o_info = take((size_t)ns * 4);
+  const size_t o_kin = take((size_t)std::max<int64_t>(total, 1) * 8), o_kout = take((size_t)std::max<int64_t>(total, 1) * 8);
+  const size_t o_vin = take((size_t)std::max<int64_t>(total, 1) * 4), o_vout = take((size_t)std::max<int64_t>(total, 1) * 4);
+  const size_t o_base = take((size_t)(ns + 1) * 8);
+  const size_t o_off = take((size_t)(ns + 1) * 4);
+  const size_t o_res = take(16);
+  size_t sort_bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const double*)nullptr, (double*)nullptr,
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(total, 1));
+  const size_t o_sort = take(sort_bytes);
+  if (off > X.cap) {
+    if (X.buf) cudaFree(X.buf);
+    X.buf = nullptr;
+    X.cap = 0;
+    if (cudaMalloc(&X.buf, off) != cudaSuccess) return fail(TN_ERR_OOM, "tn_svd_truncate: scratch allocation");
+    X.cap = off;
+  }
+  char* B = static_cast<char*>(X.buf);
+  int* d_info = reinterpret_cast<int*>(B + o_info);
+  for (int c = 0; c < ns; ++c) {
+    const int R = (int)p->R[c], C = (int)p->C[c], k = std::min(R, C);
+    SvdSector& S = sp.sec[c];
+    S.R = R;
+    S.C = C;
+    S.k = k;
+    S.row0 = p->row0[c];
+    S.col0 = p->col0[c];
+    if (k == 0) continue;
+    if (!theta[c]) return fail(TN_ERR_DIMENSION, "tn_svd_truncate: NULL Θ(c) for a non-empty sector");
+    S.ux = reinterpret_cast<double2*>(B + o_ux[c]);
+    S.vx = reinterpret_cast<double2*>(B + o_vx[c]);
+    S.s = reinterpret_cast<double*>(B + o_s[c]);
+    // X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
+    if (cusolverDnZgesvdj(X.h, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, reinterpret_cast<cuDoubleComplex*>(theta[c]), C,
+                          const_cast<double*>(S.s), reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)), C,
+                          reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
+                          reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c,
+                          X.params) != CUSOLVER_STATUS_SUCCESS)
+      return fail(TN_ERR_CUDA, "cusolverDnZgesvdj failed");
+  }
+  double* kin = reinterpret_cast<double*>(B + o_kin);
+  double* kout = reinterpret_cast<double*>(B + o_kout);
+  int32_t* vin = reinterpret_cast<int32_t*>(B + o_vin);
+  int32_t* vout = reinterpret_cast<int32_t*>(B + o_vout);
+  int64_t* d_base = reinterpret_cast<int64_t*>(B + o_base);
+  int32_t* d_off = reinterpret_cast<int32_t*>(B + o_off);
+  int64_t* d_chi = reinterpret_cast<int64_t*>(B + o_res);
+  double* d_disc = reinterpret_cast<double*>(B + o_res + 8);
+  tn_status st = cuda_check(cudaMemcpyAsync(d_base, base.data(), (ns + 1) * 8, cudaMemcpyHostToDevice, s), "H2D bases");
+  if (st != TN_OK) return st;
+  if (total > 0) {
+    k_svd_pack<<<dim3(8, ns), 256, 0, s>>>(sp, kin, vin, d_base);
+    size_t sb = sort_bytes;
+    if (cub::DeviceRadixSort::SortPairsDescending(B + o_sort, sb, kin, kout, vin, vout, (int)total, 0, 64, s) !=
+        cudaSuccess)
+      return fail(TN_ERR_CUDA, "radix sort of singular values failed");
+  }
+  k_svd_select<<<1, 1024, 0, s>>>(sp, kout, vout, total, chi_max, cutoff, q_new, lambda_new, d_off, d_chi, d_disc);
+  if ((st = cuda_check(cudaMemsetAsync(gamma_k_new, 0, (size_t)p->chi[0] * chi_max * 16, s), "memset Γk_new")) != TN_OK)
+    return st;
+  if ((st = cuda_check(cudaMemsetAsync(gamma_k1_new, 0, (size_t)chi_max * p->chi[2] * 16, s), "memset Γk1_new")) != TN_OK)
+    return st;
+  k_svd_factors<<<dim3(std::max(1, 2 * p->sm_count / std::max(1, ns) + 1), ns), 256, 0, s>>>(
+      sp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, lambda_r, chi_max, p->chi[2],
+      reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
+  if ((st = cuda_check(cudaGetLastError(), "SVD kernels")) != TN_OK) return st;
+  std::vector<int> info(ns, 0);
+  int64_t res[2];
+  if ((st = cuda_check(cudaMemcpyAsync(info.data(), d_info, ns * 4, cudaMemcpyDeviceToHost, s), "D2H info")) != TN_OK)
+    return st;
+  if ((st = cuda_check(cudaMemcpyAsync(res, d_chi, 16, cudaMemcpyDeviceToHost, s), "D2H results")) != TN_OK) return st;
+  if ((st = cuda_check(cudaStreamSynchronize(s), "SVD sync")) != TN_OK) return st;
+  for (int c = 0; c < ns; ++c)
+    if (info[c] != 0)
+      return fail(TN_ERR_CUDA, "tn_svd_truncate: gesvdj did not converge in sector " + std::to_string(c));
+  *chi_out = res[0];
+  std::memcpy(discarded, &res[1], 8);
+  return TN_OK;
+}

@@ -1,0 +1,91 @@
+"""GPU parity of the SVD step (tn_svd_truncate) against the pinned oracle (oracle/svd.py).
+
+Singular vectors are unique only up to a phase per value, so the comparison is on what is unique:
+kept count, charges and values of the new bond (bit-exact charges; values ≤ 1e-12 relative), the
+discarded weight, and — phase-free — every sector's truncated reconstruction
+λl Γk_new diag(λ_new) Γk1_new λr (≤ 1e-10 relative Frobenius, the Θ bar) plus orthonormality of the
+new factors (λl·Γk_new columns and Γk1_new·λr rows of each charge are orthonormal, ≤ 1e-12)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import oracle.svd as osvd
+import synth
+from gpu_util import gpu_theta, oracle_theta
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tn(cuda_ok):
+    import paper_2301_12814_b200 as tn
+    return tn
+
+
+def _run(tn, case, chi_max, cutoff=1e-14):
+    plan, U, got = gpu_theta(case)
+    t = [torch.from_numpy(np.ascontiguousarray(g)).cuda() for g in got]
+    ll = torch.from_numpy(case.lam_l).cuda()
+    lr = torch.from_numpy(case.lam_r).cuda()
+    res = tn.svd_truncate(plan, t, ll, lr, chi_max, cutoff)
+    torch.cuda.synchronize()
+    out = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
+    return got, out
+
+
+def _recon(case, res, c):
+    perm_l, off_l = oracle.sort_bonds(case.q_l, case.N)
+    perm_r, off_r = oracle.sort_bonds(case.q_r, case.N)
+    (r0, r1), (k0, k1) = oracle.sector_ranges(off_l, off_r, case.N, case.d, c)
+    rows, cols = perm_l[r0:r1], perm_r[k0:k1]
+    a = np.nonzero(res["q_new"] == c)[0]
+    A = case.lam_l[rows][:, None] * res["gamma_k_new"][np.ix_(rows, a)]
+    B = res["gamma_k1_new"][np.ix_(a, cols)] * case.lam_r[cols][None, :]
+    return (A * res["lam_new"][a][None, :]) @ B, A, B
+
+
+@pytest.mark.parametrize("cfg,chi", [(0, 5), (1, 64), (1, 100000), (2, 1024), (2, 300)])
+def test_svd_truncate_parity(tn, cfg, chi):
+    case = synth.make_config(cfg)
+    got, res = _run(tn, case, chi)
+    ref_secs, *_ = oracle_theta(case)
+    ref = osvd.truncate_update(case.N, case.d, case.q_l, case.q_r, ref_secs, case.lam_l, case.lam_r, chi)
+    assert res["chi"] == ref["chi"]
+    assert np.array_equal(res["q_new"], ref["q_new"])
+    smax = max(float(s.max()) for s in ref["svals"] if s.size)
+    assert np.max(np.abs(res["lam_new"] - ref["lam_new"]), initial=0.0) <= 1e-12 * smax
+    tot = sum(np.linalg.norm(x) ** 2 for x in ref_secs)
+    assert abs(res["discarded"] - ref["discarded"]) <= 1e-12 * tot
+    for c in range(case.N + 1):
+        if ref_secs[c].size == 0:
+            continue
+        rg, A, B = _recon(case, res, c)
+        rr, *_ = _recon(case, ref, c)
+        n = np.linalg.norm(rr)
+        assert np.linalg.norm(rg - rr) <= 1e-10 * max(n, 1e-300), c
+        if A.shape[1]:
+            assert np.allclose(A.conj().T @ A, np.eye(A.shape[1]), atol=1e-12)
+            assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
+
+
+def test_svd_no_truncation_reconstructs_theta(tn):
+    case = synth.make_config(1)
+    got, res = _run(tn, case, 10 ** 6)
+    assert res["discarded"] <= 1e-24
+    for c in range(case.N + 1):
+        if got[c].size:
+            rg, _, _ = _recon(case, res, c)
+            assert np.linalg.norm(rg - got[c]) <= 1e-12 * np.linalg.norm(got[c])
+
+
+def test_svd_errors(tn):
+    case = synth.make_config(0)
+    plan, U, got = gpu_theta(case)
+    t = [torch.from_numpy(np.ascontiguousarray(g)).cuda() for g in got]
+    ll, lr = torch.from_numpy(case.lam_l).cuda(), torch.from_numpy(case.lam_r).cuda()
+    with pytest.raises(tn.TnError, match="DOMAIN"):
+        tn.svd_truncate(plan, t, ll, lr, 0)
+    sharded = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r, 2, 0)
+    with pytest.raises(tn.TnError, match="UNSUPPORTED"):
+        tn.svd_truncate(sharded, t, ll, lr, 4)
