@@ -1,0 +1,100 @@
+"""Plain CPU oracle of a brick-wall layer of beam-splitter gates on a U(1) MPS (TEST INFRASTRUCTURE ONLY).
+
+SURVEY.md §8(f) NEXT-3, BASELINE.json config 4 ("a brick-wall layer of beam-splitter gates on an M-mode
+MPS"), PAPER.md:99 ("beam splitter updates within a layer are parallel"). The MPS is the Vidal form of
+PAPER.md:45 with the U(1) constraint of PAPER.md:49-51: sites 0..M−1 carry Γ^{[k]} [χ_k × χ_{k+1}] (the
+physical index i_k = c(α_k) − c(α_{k+1}) is implied by the bond charges), bonds 0..M carry λ and charges
+(bond 0: one bond of charge N; bond M: one bond of charge 0). A gate on sites (k, k+1) is Eq. S5's Θ
+(oracle.theta_sectors with left/centre/right bonds k, k+1, k+2) followed by the SVD update
+(oracle.svd.truncate_update); gates of one layer act on disjoint site pairs.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+from .svd import truncate_update
+from .theta import theta_sectors
+
+
+def apply_gate(state, k, theta, phi, chi_max, cutoff=1e-14):
+    """In-place TEBD update of sites (k, k+1). `state` = dict(N, d, q: [M+1 int arrays], gam: [M complex],
+    lam: [M+1 real]). Returns the discarded weight."""
+    N, d = state["N"], state["d"]
+    q, gam, lam = state["q"], state["gam"], state["lam"]
+    secs, *_ = theta_sectors(N, d, q[k], q[k + 1], q[k + 2], gam[k], lam[k + 1], gam[k + 1], lam[k], lam[k + 2],
+                             theta, phi)
+    res = truncate_update(N, d, q[k], q[k + 2], secs, lam[k], lam[k + 2], chi_max, cutoff)
+    q[k + 1] = res["q_new"]
+    lam[k + 1] = res["lam_new"]
+    gam[k] = res["gamma_k_new"]
+    gam[k + 1] = res["gamma_k1_new"]
+    return res["discarded"]
+
+
+def apply_layer(state, parity, thetas, phis, chi_max, cutoff=1e-14):
+    """Gates on (k, k+1) for k = parity, parity+2, … < M−1, in increasing k (they commute)."""
+    M = len(state["gam"])
+    disc = []
+    for g, k in enumerate(range(parity, M - 1, 2)):
+        disc.append(apply_gate(state, k, thetas[g], phis[g], chi_max, cutoff))
+    return disc
+
+
+def dense_state(state):
+    """c[i_0, …, i_{M−1}] = Σ Γ^{[0]} λ^{[1]} Γ^{[1]} … Γ^{[M−1]} with the outer λ's (bond 0 and M) and the δ's
+    (i_k = c(α_k) − c(α_{k+1}) ∈ [0, d−1]) written out — small M only."""
+    N, d = state["N"], state["d"]
+    q, gam, lam = state["q"], state["gam"], state["lam"]
+    M = len(gam)
+    # vec[α_k, i_0..i_{k−1}]
+    vec = np.asarray(lam[0], dtype=np.complex128).copy()
+    for k in range(M):
+        G = gam[k] * lam[k + 1][None, :]
+        new = np.zeros((len(q[k + 1]),) + (d,) * (k + 1), dtype=np.complex128)
+        for a in range(len(q[k])):
+            for b in range(len(q[k + 1])):
+                i = int(q[k][a]) - int(q[k + 1][b])
+                if 0 <= i <= d - 1 and G[a, b] != 0:
+                    new[(b,) + (slice(None),) * k + (i,)] += vec[a] * G[a, b]
+        vec = new
+    return vec.sum(axis=0)     # the single right boundary bond
+
+
+def dense_gate(psi, k, U4):
+    """Apply ⟨i,i'|U|j,j'⟩ (U4[i, i', j, j']) to modes (k, k+1) of a dense state."""
+    M = psi.ndim
+    perm = [k, k + 1] + [m for m in range(M) if m not in (k, k + 1)]
+    x = np.transpose(psi, perm)
+    sh = x.shape
+    x = np.einsum("abij,ij...->ab...", U4, x.reshape(sh))
+    return np.transpose(x, np.argsort(perm))
+
+
+def random_mps(M, N, d, chi, seed):
+    """A random U(1) MPS with valid charges: bond k's charges lie in the reachable window
+    [max(0, N − k(d−1)), min(N, (M−k)(d−1))] (photons to the right), sorted; Γ masked to allowed blocks."""
+    rng = np.random.default_rng(seed)
+    q = []
+    for k in range(M + 1):
+        if k == 0:
+            q.append(np.array([N], dtype=np.int32))
+        elif k == M:
+            q.append(np.array([0], dtype=np.int32))
+        else:
+            lo, hi = max(0, N - k * (d - 1)), min(N, (M - k) * (d - 1))
+            q.append(np.sort(rng.integers(lo, hi + 1, size=chi)).astype(np.int32))
+    gam = []
+    for k in range(M):
+        a, b = q[k], q[k + 1]
+        g = (rng.standard_normal((len(a), len(b))) + 1j * rng.standard_normal((len(a), len(b)))) / np.sqrt(2)
+        diff = a[:, None].astype(np.int64) - b[None, :]
+        gam.append(g * ((diff >= 0) & (diff <= d - 1)))
+    lam = [np.ones(1)] + [np.sort(rng.uniform(0.2, 1.0, size=len(q[k])))[::-1].copy() for k in range(1, M)] + [np.ones(1)]
+    return dict(N=N, d=d, q=q, gam=gam, lam=lam)
+
+
+def copy_state(s):
+    return dict(N=s["N"], d=s["d"], q=[x.copy() for x in s["q"]], gam=[x.copy() for x in s["gam"]],
+                lam=[x.copy() for x in s["lam"]])
