@@ -219,7 +219,7 @@ def theta_exec(plan: Plan, gk, lk, gk1, ll, lr, U, out=None, stream=None):
 def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None):
     """tn_svd_truncate: per-sector SVD + global top-χ + new canonical factors. `theta` (the list from
     theta_exec) is DESTROYED. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
-    [chi × χ_r], discarded) as CUDA tensors (views of chi_max-capacity buffers)."""
+    [chi × χ_r], discarded) as contiguous CUDA tensors (views of chi_max-capacity buffers)."""
     chi_l, _, chi_r = plan.chi
     dev = ll.device
     q_new = torch.zeros(chi_max, dtype=torch.int32, device=dev)
@@ -231,8 +231,8 @@ def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14,
                               float(cutoff), _ptr(q_new), _ptr(lam_new), _ptr(gk), _ptr(gk1), C.byref(chi_out),
                               C.byref(disc)), "tn_svd_truncate")
     k = chi_out.value
-    return dict(chi=k, q_new=q_new[:k], lam_new=lam_new[:k], gamma_k_new=gk[:, :k], gamma_k1_new=gk1[:k],
-                discarded=disc.value)
+    return dict(chi=k, q_new=q_new[:k], lam_new=lam_new[:k], gamma_k_new=gk.view(-1)[:chi_l * k].view(chi_l, k),
+                gamma_k1_new=gk1[:k], discarded=disc.value)
 
 
 class Comm:

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(1024) k_svd_select(const SvdParams sp, const d
 // blockIdx.y = sector; Γk_new rows (α of Θ(c)) × kept columns, then Γk1_new kept rows × columns (β)
 __global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ off_new, const int32_t* __restrict__ perm_l,
                               const int32_t* __restrict__ perm_r, const double* __restrict__ lam_l,
-                              const double* __restrict__ lam_r, int64_t chi_max, int64_t chi_r,
+                              const double* __restrict__ lam_r, int64_t ld_k, int64_t chi_r,
                               double2* __restrict__ gk_new, double2* __restrict__ gk1_new) {
   const int c = blockIdx.y;
   const SvdSector S = sp.sec[c];
@@ -152,7 +152,7 @@ __global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ of
       const double l = lam_l[al];
       const double2 v = S.vx[r + (int64_t)s * S.R];
       const double inv = l != 0.0 ? 1.0 / l : 0.0;
-      gk_new[(int64_t)al * chi_max + a0 + s] = make_double2(v.x * inv, -v.y * inv);
+      gk_new[(int64_t)al * ld_k + a0 + s] = make_double2(v.x * inv, -v.y * inv);
     } else {       // V_Θ†[s, col] = U_x[col, s]
       const int64_t j = i - na;
       const int s = (int)(j / S.C), col = (int)(j - (int64_t)s * S.C);
@@ -285,7 +285,9 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
       load[l] += (double)p->R[c] * p->C[c] * std::min(p->R[c], p->C[c]);
     }
   }
-  tn_status st = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
+  tn_status st = cuda_check(cudaMemsetAsync(d_info, 0, ns * sizeof(int), s), "memset info");  // empty sectors
+  if (st != TN_OK) return st;
+  st = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
   if (st != TN_OK) return st;
   std::vector<std::string> errs(SVD_LANES);
   auto work = [&](int l) {
@@ -347,14 +349,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
       return fail(TN_ERR_CUDA, "radix sort of singular values failed");
   }
   k_svd_select<<<1, 1024, 0, s>>>(sp, kout, vout, total, chi_max, cutoff, q_new, lambda_new, d_off, d_chi, d_disc);
-  if ((st = cuda_check(cudaMemsetAsync(gamma_k_new, 0, (size_t)p->chi[0] * chi_max * 16, s), "memset Γk_new")) != TN_OK)
-    return st;
-  if ((st = cuda_check(cudaMemsetAsync(gamma_k1_new, 0, (size_t)chi_max * p->chi[2] * 16, s), "memset Γk1_new")) != TN_OK)
-    return st;
-  k_svd_factors<<<dim3(std::max(1, 2 * p->sm_count / std::max(1, ns) + 1), ns), 256, 0, s>>>(
-      sp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, lambda_r, chi_max, p->chi[2],
-      reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
-  if ((st = cuda_check(cudaGetLastError(), "SVD kernels")) != TN_OK) return st;
+  if ((st = cuda_check(cudaGetLastError(), "SVD select")) != TN_OK) return st;
   std::vector<int> info(ns, 0);
   int64_t res[2];
   if ((st = cuda_check(cudaMemcpyAsync(info.data(), d_info, ns * 4, cudaMemcpyDeviceToHost, s), "D2H info")) != TN_OK)
@@ -363,7 +358,22 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   if ((st = cuda_check(cudaStreamSynchronize(s), "SVD sync")) != TN_OK) return st;
   for (int c = 0; c < ns; ++c)
     if (info[c] != 0)
-      return fail(TN_ERR_CUDA, "tn_svd_truncate: gesvdj did not converge in sector " + std::to_string(c));
+      return fail(TN_ERR_CUDA, "tn_svd_truncate: the SVD failed in sector " + std::to_string(c) + " (" +
+                                   std::to_string(p->R[c]) + "x" + std::to_string(p->C[c]) + ", info " +
+                                   std::to_string(info[c]) + ")");
+  // factors in their compact layout: Γk_new [χ_l × χ_new] (ld χ_new), Γk1_new [χ_new × χ_r]
+  const int64_t chi_new = res[0];
+  if (chi_new > 0) {
+    if ((st = cuda_check(cudaMemsetAsync(gamma_k_new, 0, (size_t)p->chi[0] * chi_new * 16, s), "memset Γk_new")) != TN_OK)
+      return st;
+    if ((st = cuda_check(cudaMemsetAsync(gamma_k1_new, 0, (size_t)chi_new * p->chi[2] * 16, s), "memset Γk1_new")) !=
+        TN_OK)
+      return st;
+    k_svd_factors<<<dim3(std::max(1, 2 * p->sm_count / std::max(1, ns) + 1), ns), 256, 0, s>>>(
+        sp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, lambda_r, chi_new, p->chi[2],
+        reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
+    if ((st = cuda_check(cudaGetLastError(), "SVD factors")) != TN_OK) return st;
+  }
   *chi_out = res[0];
   std::memcpy(discarded, &res[1], 8);
   return TN_OK;
