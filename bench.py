@@ -47,6 +47,9 @@ def parse():
                     help="K4 engine: FP64 DMMA (default) or the INT8 tcgen05 Ozaki emulation")
     ap.add_argument("--slices", type=int, default=6, help="INT8 emulation slice count (6: ≤1e-11 rel error)")
     ap.add_argument("--gates", type=int, default=32, help="config 4: gates of the brick-wall layer to time")
+    ap.add_argument("--layer", type=int, default=None, metavar="M",
+                    help="time brick-wall layers (Θ + SVD per gate) on an M-site MPS with config-N bonds")
+    ap.add_argument("--chi-max", type=int, default=None, help="layer mode: truncation χ (default: the config's χ)")
     ap.add_argument("--pair", type=int, default=None,
                     help="time the MPO doubled-charge path on synth.PAIR_CONFIGS[k] instead (tn_theta2_plan)")
     return ap.parse_args()
@@ -404,6 +407,67 @@ def run_tn(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------------------------- brick-wall layer
+def run_layer(args, rank, world, local_rank):
+    """Two brick-wall layers (even, then odd site pairs) of real TEBD gates on an M-site MPS whose inner bonds
+    have the shape of BASELINE.json config `--config` (N, d, χ, Gaussian charges, 0.995^i λ): each gate is
+    tn_theta_plan + U + tn_theta_exec + tn_svd_truncate, the next gate consuming the previous one's output.
+    Γ is drawn on the device (same distribution, δ-masked). Reports gates/s (host wall clock: the SVD step
+    synchronises once per gate to learn the kept bond dimension)."""
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2301_12814_b200.mps import MPS
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synth.CONFIGS[args.config]
+    N, d, chi, M = cfg["N"], cfg["d"], cfg["chi"], args.layer
+    chi_max = args.chi_max or chi
+    rng = np.random.default_rng(cfg["seed"] + 77)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(cfg["seed"] + 77)
+    q = [np.array([N], np.int32)]
+    for k in range(1, M):
+        lo, hi = max(0, N - k * (d - 1)), min(N, (M - k) * (d - 1))
+        q.append(np.sort(np.clip(np.rint(rng.normal(N / 2, N / 4, chi)), lo, hi)).astype(np.int32))
+    q.append(np.array([0], np.int32))
+    qd = [torch.from_numpy(x).to(dev) for x in q]
+    gam = []
+    for k in range(M):
+        a, b = qd[k].long(), qd[k + 1].long()
+        m = ((a[:, None] - b[None, :]) >= 0) & ((a[:, None] - b[None, :]) <= d - 1)
+        x = torch.randn(tuple(m.shape), generator=gen, device=dev, dtype=torch.float64)
+        y = torch.randn(tuple(m.shape), generator=gen, device=dev, dtype=torch.float64)
+        gam.append(torch.complex(x, y) / math.sqrt(2) * m)
+    lam = [torch.ones(1, dtype=torch.float64, device=dev)]
+    for k in range(1, M):
+        v = torch.from_numpy(0.995 ** np.arange(chi)).to(dev)
+        lam.append(v / torch.linalg.vector_norm(v))
+    lam.append(torch.ones(1, dtype=torch.float64, device=dev))
+    mps = MPS(N, d, qd, gam, lam, device=dev)
+    th = rng.uniform(0, math.pi / 2, M)
+    ph = rng.uniform(0, 2 * math.pi, M)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    disc = mps.apply_layer(0, th, ph, chi_max) + mps.apply_layer(1, th, ph, chi_max)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    ngates = len(disc)
+    line = {"metric": "brick-wall TEBD gates/s (Θ + per-sector SVD + truncation per gate)",
+            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": 1, "steps": ngates, "warmup": 0,
+            "ms_per_step": round(dt / ngates * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-drawn Γ, config-shaped bonds)",
+            "config": {"workload": f"{M}-site MPS, two brick-wall layers, inner bonds of BASELINE.json config "
+                                   f"{args.config} (N={N}, d={d}, chi={chi}), chi_max={chi_max}",
+                       "timing": "host wall clock around whole layers (tn_svd_truncate synchronises per gate)"},
+            "bond_dims_after": [int(x.numel()) for x in mps.lam], "discarded": [float(x) for x in disc]}
+    print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------------------------------- MPO pair path
 def run_pair(args, rank, world, local_rank):
     """One step = tn_theta2_plan (K1 on pair keys + tables) + tn_build_bs_unitary (K2) + tn_theta_exec
@@ -616,7 +680,9 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if args.pair is not None:
+        if args.layer is not None:
+            run_layer(args, rank, world, local_rank)
+        elif args.pair is not None:
             run_pair(args, rank, world, local_rank)
         elif args.config == 4:
             run_sweep(args, rank, world, local_rank)
