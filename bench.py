@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sectors", default="0,6,12,18,24,30")
-    ap.add_argument("--contraction", default="dmma", choices=["dmma", "int8"],
+    ap.add_argument("--contraction", default="dmma", choices=["dmma", "int8", "literal"],
                     help="K4 engine: FP64 DMMA (default) or the INT8 tcgen05 Ozaki emulation")
     ap.add_argument("--slices", type=int, default=6, help="INT8 emulation slice count (6: ≤1e-11 rel error)")
     ap.add_argument("--gates", type=int, default=32, help="config 4: gates of the brick-wall layer to time")

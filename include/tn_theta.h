@@ -139,8 +139,14 @@ TN_API tn_status tn_plan_kernel_times(const tn_plan* plan, float* ms5);
  *                            int32 TMEM per diagonal p+q ≤ slices+1 and are recombined in FP64.
  *                            Truncation error ≈ √K·2^(−7·slices) relative (slices = 7: ~1e-13).
  * slices ∈ [4, 8] (ignored for DMMA). Builds the slice layout (pooled workspace) and syncs once.
- * Errors: TN_ERR_DOMAIN (unknown mode / slices out of range), TN_ERR_OOM, TN_ERR_CUDA. */
-enum { TN_CONTRACT_F64_DMMA = 0, TN_CONTRACT_INT8_OZAKI = 1 };
+ * Errors: TN_ERR_DOMAIN (unknown mode / slices out of range), TN_ERR_OOM, TN_ERR_CUDA,
+ * TN_ERR_UNSUPPORTED (the literal engine on a pair plan).
+ *   TN_CONTRACT_PAPER_LITERAL — ABLATION only: the paper's kernel shape, one
+ *                            GEMM per Θ(c) over all its centre segments with the U element looked up per
+ *                            output element at every segment boundary, no product-once reformulation and
+ *                            no K5 (≈12× the flops at config 3). Same DMMA mainloop; single-charge plans.
+ */
+enum { TN_CONTRACT_F64_DMMA = 0, TN_CONTRACT_INT8_OZAKI = 1, TN_CONTRACT_PAPER_LITERAL = 2 };
 TN_API tn_status tn_plan_set_contraction(tn_plan* plan, int mode, int slices);
 TN_API tn_status tn_plan_get_contraction(const tn_plan* plan, int* mode, int* slices);
 
@@ -186,7 +192,7 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
  * canonical factors of bond k (Vidal form, R21): the new bond is ordered by charge
  * ascending, then value descending; for new bond a ↔ (c, s):
  *   q_new[a] = c,  lambda_new[a] = s_c[s]  (not renormalised),
- *   gamma_k_new [α × a] (complex, row-major, ld = chi_max, rows in the CALLER's α_{k−1} order)
+ *   gamma_k_new [α × a] (complex, row-major, ld = *chi_out, rows in the CALLER's α_{k−1} order)
  *                  = U_c[α, s] / λ^{[k−1]}[α] for α in Θ(c)'s rows, 0 elsewhere (x/0 := 0),
  *   gamma_k1_new[a × β] (complex, row-major, ld = χ_r, columns in the caller's α_{k+1} order)
  *                  = V_c†[s, β] / λ^{[k+1]}[β] for β in Θ(c)'s columns, 0 elsewhere.
@@ -194,9 +200,10 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
  *              SVD's input/workspace).
  *   lambda_l, lambda_r  DEVICE λ^{[k−1]}, λ^{[k+1]} (the ones passed to tn_theta_exec).
  *   q_new [chi_max] int32, lambda_new [chi_max] double, gamma_k_new [χ_l·chi_max] and
- *   gamma_k1_new [chi_max·χ_r] complex: DEVICE, caller-owned; entries beyond *chi_out are zero /
+ *   gamma_k1_new [chi_max·χ_r] complex: DEVICE, caller-owned capacity; the factors are written
+ *   compact for χ_new = *chi_out (Γk_new is χ_l × χ_new, Γk1_new is χ_new × χ_r), the rest is
  *   unspecified. *chi_out (HOST) = number kept, *discarded (HOST) = Σ of dropped s².
- * Synchronises the stream once (the kept count is returned on the host). Single-GPU single-charge
+ * Synchronises the stream once (the kept count is needed on the host). Single-GPU single-charge
  * plans only. Errors: TN_ERR_DIMENSION (NULL), TN_ERR_DOMAIN (chi_max < 1, cutoff < 0),
  * TN_ERR_UNSUPPORTED (sharded or pair plan), TN_ERR_OOM, TN_ERR_CUDA (incl. SVD non-convergence). */
 TN_API tn_status tn_svd_truncate(const tn_plan* plan, tn_stream stream, double* const* theta,

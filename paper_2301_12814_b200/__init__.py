@@ -121,14 +121,14 @@ class Plan:
 
     def set_contraction(self, mode, slices: int = 7):
         """tn_plan_set_contraction: "dmma" (FP64 tensor cores) or "int8" (tcgen05 INT8 emulation)."""
-        m = {"dmma": TN_CONTRACT_F64_DMMA, "int8": TN_CONTRACT_INT8_OZAKI}.get(mode, mode)
+        m = {"dmma": TN_CONTRACT_F64_DMMA, "int8": TN_CONTRACT_INT8_OZAKI, "literal": 2}.get(mode, mode)
         check(lib.tn_plan_set_contraction(self.handle, int(m), int(slices)), "tn_plan_set_contraction")
         return self
 
     def contraction(self):
         m, s = C.c_int(), C.c_int()
         check(lib.tn_plan_get_contraction(self.handle, C.byref(m), C.byref(s)), "tn_plan_get_contraction")
-        return ("dmma" if m.value == TN_CONTRACT_F64_DMMA else "int8"), s.value
+        return {TN_CONTRACT_F64_DMMA: "dmma", TN_CONTRACT_INT8_OZAKI: "int8", 2: "literal"}[m.value], s.value
 
     def kernel_times(self):
         """Device ms of the most recent K1 (plan), K2, K3, K4, K5 launched with this plan (−1: not run)."""

@@ -93,6 +93,7 @@ static void free_plan(tn_plan* p) {
   if (!p) return;
   const bool used = p->rec_exec;
   pool_release(p->blk_oz, p->last_stream, used);
+  pool_release(p->blk_lit, p->last_stream, used);
   pool_release(p->blk_work, p->last_stream, used);
   pool_release(p->blk_tab, p->last_stream, used);
   for (auto& e : p->ev)
@@ -583,7 +584,7 @@ tn_status tn_plan_flops(const tn_plan* p, int64_t* f_contract, int64_t* f_mix, i
   if (!p) return fail(TN_ERR_DIMENSION, "tn_plan_flops: NULL");
   if (f_contract) *f_contract = p->f_contract;
   if (f_mix) *f_mix = p->f_mix;
-  if (f_exec) *f_exec = p->f_exec;
+  if (f_exec) *f_exec = p->contraction == TN_CONTRACT_PAPER_LITERAL ? p->lit_flops : p->f_exec;
   if (f_contract_local) *f_contract_local = p->f_contract_local;
   if (f_mix_local) *f_mix_local = p->f_mix_local;
   return TN_OK;
@@ -604,6 +605,15 @@ tn_status tn_plan_workspace_bytes(const tn_plan* p, int64_t* bytes) {
 tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
   if (!p) return fail(TN_ERR_DIMENSION, "tn_plan_set_contraction: NULL plan");
   if (mode == TN_CONTRACT_F64_DMMA) {
+    p->contraction = mode;
+    return TN_OK;
+  }
+  if (mode == TN_CONTRACT_PAPER_LITERAL) {
+    if (p->pair) return fail(TN_ERR_UNSUPPORTED, "tn_plan_set_contraction: the literal ablation is single-charge only");
+    if (!p->blk_lit) {
+      const tn_status st = build_literal(p);
+      if (st != TN_OK) return st;
+    }
     p->contraction = mode;
     return TN_OK;
   }
@@ -755,6 +765,15 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   tn_status st = cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
+  if (p->contraction == TN_CONTRACT_PAPER_LITERAL) {  // ablation: K3L → K4L, no K5
+    st = cuda_check(launch_literal(p, sp, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                                   reinterpret_cast<const double2*>(gamma_k1), lambda_l, lambda_r,
+                                   reinterpret_cast<const double2*>(U), s, p->ev[5]),
+                    "literal launch");
+    if (st != TN_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
+    return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+  }
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
   st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
                                         reinterpret_cast<const double2*>(gamma_k1), s)

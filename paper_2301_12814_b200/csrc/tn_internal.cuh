@@ -42,6 +42,13 @@ struct TileDesc {
   int32_t g, mt, nt, pad;
 };
 
+struct LitSector {          // paper-literal ablation (k4l_literal.cu): one Θ(c) as one GEMM
+  int64_t a_off, b_off;     // complex offsets of its A / B panels
+  int64_t row0, col0;       // sorted positions of its first (local) row / column
+  int32_t c, R, C, K4;      // sector, local rows, cols, padded K (segments rounded up to BK)
+  int32_t nmt, nnt, seg0, nseg;  // tiles; its centre segments in the segment table
+};
+
 struct MixTile2 {           // K5P work unit (pair plans): one species' U mix over ≤ ~128 8-groups of one (l, r) block
   int32_t cl, n, lo, L;     // that species' left charge, U block n = l_s − r_s, first index lo, vector length L
   int32_t e0, ne, nr, ngr;  // as MixTile (8-groups row-major over the tile's rows of segment l)
@@ -170,6 +177,17 @@ struct tn_plan {
   int32_t* d_oea = nullptr;
   int32_t* d_oeb = nullptr;
   void* blk_oz = nullptr;
+  // paper-literal ablation engine (TN_CONTRACT_PAPER_LITERAL, k4l_literal.cu)
+  std::vector<tn::LitSector> lit_secs;
+  std::vector<tn::TileDesc> h_lit_tiles;
+  std::vector<char> h_lit_segs;
+  tn::LitSector* d_lit_secs = nullptr;
+  void* d_lit_segs = nullptr;
+  tn::TileDesc* d_lit_tiles = nullptr;
+  double2* d_lit_a = nullptr;
+  double2* d_lit_b = nullptr;
+  int64_t lit_ntiles = 0, lit_flops = 0;
+  void* blk_lit = nullptr;
   int64_t oz_macs = 0;                         // int8 MACs one exec issues
 };
 
@@ -204,6 +222,10 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
                        const double2* U, cudaStream_t s);
 void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out);
 tn_status build_pair_tables(tn_plan* p);
+tn_status build_literal(tn_plan* p);
+cudaError_t launch_literal(const tn_plan* p, const SectorParams& sp, const double2* gk, const double* lk,
+                           const double2* gk1, const double* ll, const double* lr, const double2* U, cudaStream_t s,
+                           cudaEvent_t mid);
 cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                             const double2* U, cudaStream_t s);
 cudaError_t launch_fused(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,

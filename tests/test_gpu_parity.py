@@ -385,3 +385,25 @@ def test_fused_k45_parity(tn, cfg, monkeypatch):
     ref, *_ = _oracle(cfg)
     _, _, got = gpu_theta(case)
     assert_sectors_close(got, ref, TOL, f"fused config{cfg}")
+
+
+# ------------------------------------------------------------------ paper-literal ablation engine
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_paper_literal_engine_parity(tn, cfg):
+    # one GEMM per Θ(c) with the per-element U lookup: the same Θ, so the same bar
+    case = _case(cfg)
+    ref, *_ = _oracle(cfg)
+    plan, _, got = gpu_theta(case, contraction=("literal", 0))
+    assert plan.contraction()[0] == "literal"
+    assert_sectors_close(got, ref, TOL, f"literal config{cfg}")
+    f = plan.flops()
+    assert f["f_exec"] > f["f_contract"] + f["f_mix"]     # it executes more work than the useful count
+
+
+def test_paper_literal_engine_edge_cases(tn):
+    for name in ("N0", "d_lt_N1", "ragged"):
+        e = EDGE[name]
+        case = synth.make_case(e["N"], e["d"], *e["chi"], seed=5, charges="uniform", lam="random")
+        ref, *_ = oracle_theta(case)
+        _, _, got = gpu_theta(case, contraction=("literal", 0))
+        assert_sectors_close(got, ref, 1e-12, f"literal {name}")
