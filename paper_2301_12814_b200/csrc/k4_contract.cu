@@ -113,20 +113,25 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
           for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks * 256 + mi * 32];
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
-          double bsum[2];
+          // the Gauss sums first, then all T1/T2 products (which do not need them), then the T3 products:
+          // every DMMA is issued well after the DADD that feeds it (no fixed-latency dependency stall)
+          double asum[4], bsum[2];
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) bsum[ni] = b[ni].x + b[ni].y;
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) {
-            const double asum = a[mi].x + a[mi].y;
+          for (int mi = 0; mi < 4; ++mi) asum[mi] = a[mi].x + a[mi].y;
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
             for (int ni = 0; ni < 2; ++ni) {
               double* c = acc[mi][ni];
               dmma(c[0], c[1], a[mi].x, b[ni].x);  // T1 += Ar·Br
               dmma(c[2], c[3], a[mi].y, b[ni].y);  // T2 += Ai·Bi
-              dmma(c[4], c[5], asum, bsum[ni]);    // T3 += (Ar+Ai)·(Br+Bi)
             }
-          }
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][4], acc[mi][ni][5], asum[mi], bsum[ni]);  // T3
         }
       }
       __syncwarp();
