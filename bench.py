@@ -294,6 +294,39 @@ def run_tn(args, rank, world, local_rank):
     ms_step = ms_max / args.steps
     value = f_useful / (ms_step * 1e-3) / 1e9
 
+    # ---- multi-GPU communication variants: exec only, then + operand broadcast,
+    # + SECTOR_OWNER gather, + ROOT gather, each timed on the device as the max over ranks
+    comm_variants = None
+    if world > 1:
+        try:
+            comm = tn.Comm(rank, world)
+            vplan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)
+            tn.build_bs_unitary(vplan, case.theta, case.phi, out=U)
+            comm_variants = {}
+            for name, bc, gm in (("exec_only", False, tn.TN_GATHER_NONE), ("bcast_operands", True, tn.TN_GATHER_NONE),
+                                 ("gather_sector_owner", False, tn.TN_GATHER_SECTOR_OWNER),
+                                 ("gather_root", False, tn.TN_GATHER_ROOT)):
+                vout = None
+                for it in range(4):                       # 1 warm-up + 3 timed
+                    barrier()
+                    torch.cuda.synchronize()
+                    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    v0.record(stream)
+                    vout = tn.theta_exec_sharded(vplan, comm, gk, lk, gk1, ll, lr, U, out=vout, bcast_operands=bc,
+                                                 gather_mode=gm)
+                    v1.record(stream)
+                    torch.cuda.synchronize()
+                    if it:
+                        comm_variants.setdefault(name, []).append(v0.elapsed_time(v1))
+                tv = torch.tensor([statistics.mean(comm_variants[name])], dtype=torch.float64, device=dev)
+                dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+                comm_variants[name] = round(float(tv.item()), 4)
+                del vout
+            vplan.destroy()
+            comm.destroy()
+        except Exception as e:  # keep the headline line even if a variant fails
+            comm_variants = {"error": repr(e)[:300]}
+
     # ---- end to end through the public API with host buffers (pinned H2D + Θ D2H inside the region).
     # Two slots on two streams: gate g+1's H2D and compute overlap gate g's D2H (independent gates, as in
     # a layer); every step still moves its full inputs in and its full Θ out.
@@ -415,6 +448,7 @@ def run_tn(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step_ms, 3),
                 "note": "pinned H2D of Γk, Γk1, λ's and charges + D2H of every Θ(c) per gate, 2 gates in flight"},
+        "comm_variants_ms": comm_variants,
         "gpu_launches": (LAUNCHES_PER_STEP + (2 if int8 else 0)) * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

@@ -62,7 +62,7 @@ typedef struct tn_comm tn_comm;   /* opaque; wraps an NCCL communicator */
 typedef void* tn_stream;          /* a cudaStream_t (0 = legacy default stream) */
 
 enum { TN_BOND_LEFT = 0, TN_BOND_CENTER = 1, TN_BOND_RIGHT = 2 };
-enum { TN_GATHER_NONE = 0, TN_GATHER_ROOT = 1 };
+enum { TN_GATHER_NONE = 0, TN_GATHER_ROOT = 1, TN_GATHER_SECTOR_OWNER = 2 };
 
 /* ------------------------------------------------------------------------------------------ */
 /* Plan: bond re-indexing (K1) + work decomposition. Not on the hot path; synchronises once.   */
@@ -112,6 +112,9 @@ TN_API tn_status tn_plan_perm(const tn_plan* plan, int bond, int32_t* host_out);
 TN_API tn_status tn_plan_offsets(const tn_plan* plan, int bond, int32_t* host_out);
 /* Sorted-left-position shard [r0, r1) of rank r (any r in [0, world_size)). */
 TN_API tn_status tn_plan_shard_rows(const tn_plan* plan, int r, int64_t* r0, int64_t* r1);
+/* Receiving rank of sector c under TN_GATHER_SECTOR_OWNER: longest-processing-time assignment of the
+ * sectors by element count R_c·C_c (largest first onto the least-loaded rank; ties → lower rank). */
+TN_API tn_status tn_plan_sector_owner(const tn_plan* plan, int c, int* owner);
 /* Useful work, 8 flops per complex MAC; any output pointer may be NULL.
  *   f_contract = 8 Σ_{allowed (c_l,c_c,c_r)} n_l n_c n_r  (whole problem),
  *   f_mix      = 8 Σ_{(c_l,c_r)} n_l n_r #c #c_c           (whole problem),
@@ -228,6 +231,9 @@ TN_API tn_status tn_comm_destroy(tn_comm* comm);
  *                 TN_GATHER_ROOT: on rank 0 theta_out holds the FULL Θ(c) (R_c×C_c) and every
  *                 rank's slab is sent to it with grouped ncclSend/ncclRecv; on other ranks
  *                 theta_out holds the local slabs.
+ *                 TN_GATHER_SECTOR_OWNER: Θ(c) goes to rank tn_plan_sector_owner(c)
+ *                 (sectors spread over ranks by element count — the hand-off to per-sector SVD); on the
+ *                 owner theta_out[c] holds the FULL Θ(c), elsewhere the local slab.
  * Other arguments as tn_theta_exec. Errors: as tn_theta_exec, plus TN_ERR_NCCL,
  * TN_ERR_CONSISTENCY. */
 TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn_comm* comm,
@@ -243,6 +249,8 @@ TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn
  * bounds[world_size]=χ_l. Errors: TN_ERR_DOMAIN. */
 TN_API tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_c,
                              const int64_t* n_r, int world_size, int64_t* bounds);
+/* The plan's sector-owner rule on host data: owners[0..n_sectors) from element counts sizes[]. */
+TN_API tn_status tn_sector_owners_host(int n_sectors, const int64_t* sizes, int world_size, int32_t* owners);
 
 TN_API /* Device memory: plan tables and staging workspace come from a library-owned pool. A destroyed
  * plan's blocks are reused by later plans once the work last enqueued with them has completed

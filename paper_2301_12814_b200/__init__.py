@@ -16,10 +16,11 @@ import numpy as np
 import torch
 
 from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT, TN_GATHER_NONE,
-                   TN_GATHER_ROOT, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH)
+                   TN_GATHER_ROOT, TN_GATHER_SECTOR_OWNER, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH)
 
 __all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Plan2", "Comm", "svd_truncate", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
-           "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT"]
+           "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT",
+           "TN_GATHER_SECTOR_OWNER", "sector_owners_host"]
 
 
 def _stream_ptr(stream) -> C.c_void_p:
@@ -108,6 +109,11 @@ class Plan:
         a, b = C.c_int64(), C.c_int64()
         check(lib.tn_plan_shard_rows(self.handle, int(r), C.byref(a), C.byref(b)), "tn_plan_shard_rows")
         return a.value, b.value
+
+    def sector_owner(self, c: int) -> int:
+        o = C.c_int()
+        check(lib.tn_plan_sector_owner(self.handle, int(c), C.byref(o)), "tn_plan_sector_owner")
+        return o.value
 
     def flops(self):
         v = [C.c_int64() for _ in range(5)]
@@ -267,6 +273,10 @@ def theta_exec_sharded(plan: Plan, comm: Comm, gk, lk, gk1, ll, lr, U, out=None,
     _check_inputs(plan, gk, lk, gk1, ll, lr, U)
     if out is None:
         out = alloc_theta(plan, full=(gather_mode == TN_GATHER_ROOT and plan.rank == 0))
+        if gather_mode == TN_GATHER_SECTOR_OWNER:
+            for c in range(plan.nsec):
+                if plan.sector_owner(c) == plan.rank:
+                    out[c] = torch.empty(plan.sector_shape(c), dtype=torch.complex128, device=out[c].device)
     ptrs = _theta_ptrs(out)
     check(lib.tn_theta_exec_sharded(plan.handle, _stream_ptr(stream), comm.handle, _ptr(gk), _ptr(lk), _ptr(gk1),
                                     _ptr(ll), _ptr(lr), _ptr(U), ptrs, int(bool(bcast_operands)), int(gather_mode)),
@@ -291,4 +301,13 @@ def shard_rows_host(d: int, N: int, n_l, n_c, n_r, world_size: int) -> np.ndarra
     i64p = C.POINTER(C.c_int64)
     check(lib.tn_shard_rows_host(int(d), int(N), *(x.ctypes.data_as(i64p) for x in a), int(world_size),
                                  out.ctypes.data_as(i64p)), "tn_shard_rows_host")
+    return out
+
+
+def sector_owners_host(sizes, world_size: int) -> np.ndarray:
+    """tn_sector_owners_host: the plan's TN_GATHER_SECTOR_OWNER assignment for element counts `sizes`."""
+    sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.int64))
+    out = np.empty(sz.shape[0], dtype=np.int32)
+    check(lib.tn_sector_owners_host(int(sz.shape[0]), sz.ctypes.data_as(C.POINTER(C.c_int64)), int(world_size),
+                                    out.ctypes.data_as(C.POINTER(C.c_int32))), "tn_sector_owners_host")
     return out

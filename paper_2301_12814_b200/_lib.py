@@ -17,7 +17,7 @@ lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 STATUS = {0: "TN_OK", 1: "TN_ERR_DOMAIN", 2: "TN_ERR_DIMENSION", 3: "TN_ERR_CONSISTENCY", 4: "TN_ERR_CUDA",
           5: "TN_ERR_OOM", 6: "TN_ERR_NCCL", 7: "TN_ERR_UNSUPPORTED"}
 TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT = 0, 1, 2
-TN_GATHER_NONE, TN_GATHER_ROOT = 0, 1
+TN_GATHER_NONE, TN_GATHER_ROOT, TN_GATHER_SECTOR_OWNER = 0, 1, 2
 TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI = 0, 1
 TN_MAX_N, TN_MAX_MIX = 100, 64
 
@@ -52,6 +52,8 @@ SIGNATURES = {
     "tn_comm_destroy": [_p],
     "tn_theta_exec_sharded": [_p, _p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p), C.c_int, C.c_int],
     "tn_shard_rows_host": [C.c_int, C.c_int, _i64p, _i64p, _i64p, C.c_int, _i64p],
+    "tn_sector_owners_host": [C.c_int, _i64p, C.c_int, _i32p],
+    "tn_plan_sector_owner": [_p, C.c_int, C.POINTER(C.c_int)],
     "tn_status_string": [C.c_int],
     "tn_last_error": [],
     "tn_version": [],

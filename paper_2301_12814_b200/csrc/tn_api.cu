@@ -181,6 +181,41 @@ tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_
   return TN_OK;
 }
 
+// Sector owners for TN_GATHER_SECTOR_OWNER: longest-processing-time assignment by
+// element count R_c·C_c (largest first onto the least-loaded rank, ties to the lower rank/sector).
+static void sector_owners(const std::vector<int64_t>& sizes, int world, std::vector<int32_t>& owner) {
+  const int n = (int)sizes.size();
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sizes[a] > sizes[b]; });
+  std::vector<int64_t> load(world, 0);
+  owner.assign(n, 0);
+  for (int c : order) {
+    int best = 0;
+    for (int r = 1; r < world; ++r)
+      if (load[r] < load[best]) best = r;
+    owner[c] = best;
+    load[best] += sizes[c];
+  }
+}
+
+tn_status tn_sector_owners_host(int n_sectors, const int64_t* sizes, int world_size, int32_t* owners) {
+  if (n_sectors < 0 || world_size < 1) return fail(TN_ERR_DOMAIN, "tn_sector_owners_host: bad n/world");
+  if ((n_sectors && (!sizes || !owners))) return fail(TN_ERR_DIMENSION, "tn_sector_owners_host: NULL");
+  std::vector<int64_t> sz(sizes, sizes + n_sectors);
+  std::vector<int32_t> o;
+  sector_owners(sz, world_size, o);
+  std::copy(o.begin(), o.end(), owners);
+  return TN_OK;
+}
+
+tn_status tn_plan_sector_owner(const tn_plan* p, int c, int* owner) {
+  if (!p || !owner) return fail(TN_ERR_DIMENSION, "tn_plan_sector_owner: NULL");
+  if (c < 0 || c >= p->nsec) return fail(TN_ERR_DOMAIN, "tn_plan_sector_owner: sector out of range");
+  *owner = p->owner.empty() ? 0 : p->owner[c];
+  return TN_OK;
+}
+
 // packed U layout (SURVEY.md §8(c) "Packed U")
 static void u_layout(tn_plan* p) {
   const int nmax = std::min(p->N, 2 * p->d - 2);
@@ -384,6 +419,11 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
         st = fail(TN_ERR_UNSUPPORTED, "sector dimension > INT32_MAX");
         goto done;
       }
+    }
+    {
+      std::vector<int64_t> sizes(N + 1);
+      for (int c = 0; c <= N; ++c) sizes[c] = p->R[c] * p->C[c];
+      sector_owners(sizes, world_size, p->owner);
     }
     // ---- useful flops of the whole problem ----
     for (int cl = 0; cl <= N; ++cl)

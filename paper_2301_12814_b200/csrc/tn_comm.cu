@@ -118,7 +118,7 @@ tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* com
   if (p->pair) return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_sharded: pair (MPO) plans are single-GPU in this build");
   if (p->world != comm->world || p->rank != comm->rank)
     return fail(TN_ERR_CONSISTENCY, "tn_theta_exec_sharded: plan world/rank differ from the communicator's");
-  if (gather_mode != TN_GATHER_NONE && gather_mode != TN_GATHER_ROOT)
+  if (gather_mode != TN_GATHER_NONE && gather_mode != TN_GATHER_ROOT && gather_mode != TN_GATHER_SECTOR_OWNER)
     return fail(TN_ERR_DOMAIN, "tn_theta_exec_sharded: unknown gather_mode");
   if (!theta_out) return fail(TN_ERR_DIMENSION, "tn_theta_exec_sharded: NULL theta_out");
   NcclApi& api = nccl();
@@ -140,13 +140,14 @@ tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* com
     st = nccl_check(r != ncclSuccess ? r : r2, "operand broadcast");
     if (st != TN_OK) return st;
   }
-  // Local slabs: on the gathering root the caller passed FULL sectors, so its slab starts at row
-  // (lrow0 − row0) of each sector.
-  const bool root_full = gather_mode == TN_GATHER_ROOT && p->rank == 0;
+  // Local slabs: where this rank receives a whole sector (ROOT: rank 0, SECTOR_OWNER: the sector's owner)
+  // the caller passed the FULL Θ(c), so this rank's slab starts at row (lrow0 − row0).
+  auto dest = [&](int c) { return gather_mode == TN_GATHER_ROOT ? 0 : p->owner[c]; };
   std::vector<double*> local(p->N + 1, nullptr);
   for (int c = 0; c <= p->N; ++c) {
     double* base = theta_out[c];
-    if (root_full && base) base += 2 * (p->lrow0[c] - p->row0[c]) * p->C[c];
+    if (gather_mode != TN_GATHER_NONE && p->world > 1 && dest(c) == p->rank && base)
+      base += 2 * (p->lrow0[c] - p->row0[c]) * p->C[c];
     local[c] = base;
   }
   st = tn_theta_exec(p, stream, gamma_k, lambda_k, gamma_k1, lambda_l, lambda_r, U, local.data());
@@ -156,19 +157,21 @@ tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* com
   ncclResult_t r = ncclSuccess;
   for (int c = 0; c <= p->N && r == ncclSuccess; ++c) {
     const int64_t a0 = p->row0[c], a1 = a0 + p->R[c], C = p->C[c];
-    if (p->rank == 0) {
-      for (int src = 1; src < p->world && r == ncclSuccess; ++src) {
+    const int to = dest(c);
+    if (p->rank == to) {
+      for (int src = 0; src < p->world && r == ncclSuccess; ++src) {
+        if (src == to) continue;
         const int64_t s0 = std::min(std::max(a0, p->bounds[src]), a1);
         const int64_t s1 = std::min(std::max(a0, p->bounds[src + 1]), a1);
         if (s1 > s0 && C > 0)
           r = api.Recv(theta_out[c] + 2 * (s0 - a0) * C, (size_t)(2 * (s1 - s0) * C), ncclFloat64, src, comm->comm, s);
       }
     } else if (p->lR[c] * C > 0) {
-      r = api.Send(theta_out[c], (size_t)(2 * p->lR[c] * C), ncclFloat64, 0, comm->comm, s);
+      r = api.Send(theta_out[c], (size_t)(2 * p->lR[c] * C), ncclFloat64, to, comm->comm, s);
     }
   }
   ncclResult_t r2 = api.GroupEnd();
-  return nccl_check(r != ncclSuccess ? r : r2, "Θ gather to root");
+  return nccl_check(r != ncclSuccess ? r : r2, gather_mode == TN_GATHER_ROOT ? "Θ gather to root" : "Θ gather to sector owners");
 }
 
 }  // extern "C"

@@ -117,6 +117,7 @@ struct tn_plan {
   int32_t* d_off[3] = {nullptr, nullptr, nullptr};   // device offset tables (N+2)
   double2* d_binom = nullptr;                  // (nmax+1)² exact binomials as double-double (K2)
   std::vector<int64_t> bounds;                 // world+1 shard bounds (sorted left positions)
+  std::vector<int32_t> owner;                  // TN_GATHER_SECTOR_OWNER: receiving rank of every sector
   int64_t r0 = 0, r1 = 0;                      // this rank's window
   // sectors
   std::vector<int64_t> R, C, row0, col0, lR, lrow0;   // global + local slab
