@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="tn", choices=["tn", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-alt-engine", action="store_true", help="skip timing the INT8 emulation engine")
     ap.add_argument("--cpu-sectors", default="0,6,12,18,24,30")
     ap.add_argument("--contraction", default="dmma", choices=["dmma", "int8", "literal"],
                     help="K4 engine: FP64 DMMA (default) or the INT8 tcgen05 Ozaki emulation")
@@ -294,6 +295,39 @@ def run_tn(args, rank, world, local_rank):
     ms_step = ms_max / args.steps
     value = f_useful / (ms_step * 1e-3) / 1e9
 
+    # ---- the optional INT8 tcgen05 emulation engine on the same gates (reported beside the FP64 line)
+    alt = None
+    if not int8 and not args.no_alt_engine:
+        try:
+            a_ms = []
+            for it in range(args.warmup + 5):
+                ap = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)
+                ap.set_contraction("int8", args.slices)
+                barrier()
+                torch.cuda.synchronize()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                tn.build_bs_unitary(ap, case.theta, case.phi, out=U)
+                tn.theta_exec(ap, gk, lk, gk1, ll, lr, U, out=outs)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                if it >= args.warmup:
+                    a_ms.append(a0.elapsed_time(a1))
+                kt8 = ap.kernel_times()
+                ap.destroy()
+            am = torch.tensor([statistics.mean(a_ms)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(am, op=dist.ReduceOp.MAX)
+            am = float(am.item())
+            alt = {"engine": f"INT8 tcgen05 Ozaki emulation, {args.slices} slices (≤1e-11 rel. error vs oracle)",
+                   "ms_per_gate_excl_plan": round(am, 4), "useful_gflops": round(f_useful / (am * 1e-3) / 1e9, 1),
+                   "pct_fp64_tc_peak": round(100.0 * f_useful / (am * 1e-3) / (FP64_TC_PEAK_TFLOPS * 1e12 * world), 2),
+                   "kernels_ms": {k: round(v, 4) for k, v in kt8.items() if k != "k1_sort"},
+                   "note": "U build + exec on resident inputs, plan excluded (it includes a host sync for the "
+                           "slice layout); the headline value above stays on FP64 DMMA"}
+        except Exception as e:
+            alt = {"error": repr(e)[:300]}
+
     # ---- multi-GPU communication variants: exec only, then + operand broadcast,
     # + SECTOR_OWNER gather, + ROOT gather, each timed on the device as the max over ranks
     comm_variants = None
@@ -449,6 +483,7 @@ def run_tn(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step_ms, 3),
                 "note": "pinned H2D of Γk, Γk1, λ's and charges + D2H of every Θ(c) per gate, 2 gates in flight"},
         "comm_variants_ms": comm_variants,
+        "alt_engine": alt,
         "gpu_launches": (LAUNCHES_PER_STEP + (2 if int8 else 0)) * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
