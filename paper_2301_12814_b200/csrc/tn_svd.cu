@@ -72,6 +72,25 @@ struct SvdParams {
   int nsec;
 };
 
+struct ThetaPtrs {          // the sectors' device pointers and element counts (kernel parameter)
+  const double2* p[SVD_MAXSEC];
+  int64_t n[SVD_MAXSEC];
+};
+
+// Frobenius² of every sector (blockIdx.y): the largest singular value of Θ(c) is ≤ ‖Θ(c)‖_F, which lets
+// the SVD skip sectors that cannot reach the global top χ (their whole weight is discarded)
+__global__ void k_sector_norm2(const ThetaPtrs tp, double* __restrict__ out) {
+  const int c = blockIdx.y;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tp.n[c]; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = tp.p[c][i];
+    acc += v.x * v.x + v.y * v.y;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(out + c, acc);
+}
+
 __global__ void k_svd_pack(const SvdParams sp, double* __restrict__ keys, int32_t* __restrict__ vals,
                            const int64_t* __restrict__ base) {
   const int c = blockIdx.y;
@@ -86,7 +105,8 @@ __global__ void __launch_bounds__(1024) k_svd_select(const SvdParams sp, const d
                                                       const int32_t* __restrict__ svals, int64_t total,
                                                       int64_t chi_max, double cutoff, int32_t* __restrict__ q_new,
                                                       double* __restrict__ lam_new, int32_t* __restrict__ off_new,
-                                                      int64_t* __restrict__ chi_out, double* __restrict__ disc_out) {
+                                                      int64_t* __restrict__ chi_out, double* __restrict__ disc_out,
+                                                      double disc_extra) {
   __shared__ int32_t kept[SVD_MAXSEC + 1];
   __shared__ double red[32];
   __shared__ int64_t nkeep_s;
@@ -116,7 +136,7 @@ __global__ void __launch_bounds__(1024) k_svd_select(const SvdParams sp, const d
   if (tid == 0) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    *disc_out = t;
+    *disc_out = t + disc_extra;  // + the whole weight of sectors skipped by the norm bound
     *chi_out = nkeep;
     int32_t o = 0;
     for (int c = 0; c < sp.nsec; ++c) {
@@ -236,16 +256,19 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     o_w[c] = take(wbytes);
     wsz[c] = wbytes;
   }
-  const int64_t total = base[ns];
+  const int64_t total_max = base[ns];
   const size_t o_info = take((size_t)ns * 4);
-  const size_t o_kin = take((size_t)std::max<int64_t>(total, 1) * 8), o_kout = take((size_t)std::max<int64_t>(total, 1) * 8);
-  const size_t o_vin = take((size_t)std::max<int64_t>(total, 1) * 4), o_vout = take((size_t)std::max<int64_t>(total, 1) * 4);
+  const size_t o_n2 = take((size_t)ns * 8);
+  const size_t o_kin = take((size_t)std::max<int64_t>(total_max, 1) * 8),
+               o_kout = take((size_t)std::max<int64_t>(total_max, 1) * 8);
+  const size_t o_vin = take((size_t)std::max<int64_t>(total_max, 1) * 4),
+               o_vout = take((size_t)std::max<int64_t>(total_max, 1) * 4);
   const size_t o_base = take((size_t)(ns + 1) * 8);
   const size_t o_off = take((size_t)(ns + 1) * 4);
   const size_t o_res = take(16);
   size_t sort_bytes = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const double*)nullptr, (double*)nullptr,
-                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(total, 1));
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(total_max, 1));
   const size_t o_sort = take(sort_bytes);
   if (off > X.cap) {
     if (X.buf) cudaFree(X.buf);
@@ -272,65 +295,129 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     S.s = reinterpret_cast<double*>(B + o_s[c]);
     order.push_back(c);
   }
-  // largest first, greedy onto the least-loaded lane (cost ~ R·C·min(R, C))
-  std::sort(order.begin(), order.end(), [&](int a, int b) {
-    return (double)p->R[a] * p->C[a] * std::min(p->R[a], p->C[a]) > (double)p->R[b] * p->C[b] * std::min(p->R[b], p->C[b]);
-  });
-  std::vector<std::vector<int>> lane(SVD_LANES);
-  {
+  tn_status st = cuda_check(cudaMemsetAsync(d_info, 0, ns * sizeof(int), s), "memset info");  // empty sectors
+  if (st != TN_OK) return st;
+  std::vector<std::string> errs(SVD_LANES);
+  // one wave of sector SVDs: largest first, greedy onto the least-loaded lane (cost ~ R·C·min(R, C))
+  auto run_wave = [&](std::vector<int> wave) -> tn_status {
+    if (wave.empty()) return TN_OK;
+    std::sort(wave.begin(), wave.end(), [&](int a, int b) {
+      return (double)p->R[a] * p->C[a] * std::min(p->R[a], p->C[a]) >
+             (double)p->R[b] * p->C[b] * std::min(p->R[b], p->C[b]);
+    });
+    std::vector<std::vector<int>> lane(SVD_LANES);
     double load[SVD_LANES] = {};
-    for (int c : order) {
+    for (int c : wave) {
       const int l = (int)(std::min_element(load, load + SVD_LANES) - load);
       lane[l].push_back(c);
       load[l] += (double)p->R[c] * p->C[c] * std::min(p->R[c], p->C[c]);
     }
-  }
-  tn_status st = cuda_check(cudaMemsetAsync(d_info, 0, ns * sizeof(int), s), "memset info");  // empty sectors
-  if (st != TN_OK) return st;
-  st = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
-  if (st != TN_OK) return st;
-  std::vector<std::string> errs(SVD_LANES);
-  auto work = [&](int l) {
-    if (cudaStreamWaitEvent(X.st[l], X.ev[SVD_LANES], 0) != cudaSuccess) {
-      errs[l] = "stream wait";
-      return;
-    }
-    std::vector<char> hbuf;
-    for (int c : lane[l]) {
-      const SvdSector& S = sp.sec[c];
-      const int R = S.R, C = S.C;
-      cusolverStatus_t r;
-      // X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
-      if (algo == 0) {
-        r = cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, reinterpret_cast<cuDoubleComplex*>(theta[c]), C,
-                              const_cast<double*>(S.s), reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)),
-                              C, reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
-                              reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c, X.params);
-      } else {
-        hbuf.resize(std::max<size_t>(hbytes[c], 1));
-        double herr = 0.0;
-        r = cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, CUDA_C_64F, theta[c], C, CUDA_R_64F,
-                              const_cast<double*>(S.s), CUDA_C_64F, const_cast<double2*>(S.ux), C, CUDA_C_64F,
-                              const_cast<double2*>(S.vx), R, CUDA_C_64F, B + o_w[c], wsz[c], hbuf.data(), hbytes[c],
-                              d_info + c, &herr);
-      }
-      if (r != CUSOLVER_STATUS_SUCCESS) {
-        errs[l] = "cuSOLVER SVD failed in sector " + std::to_string(c) + " (status " + std::to_string((int)r) + ")";
+    tn_status r0 = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
+    if (r0 != TN_OK) return r0;
+    auto work = [&](int l) {
+      if (cudaStreamWaitEvent(X.st[l], X.ev[SVD_LANES], 0) != cudaSuccess) {
+        errs[l] = "stream wait";
         return;
       }
+      std::vector<char> hbuf;
+      for (int c : lane[l]) {
+        const SvdSector& S = sp.sec[c];
+        const int R = S.R, C = S.C;
+        cusolverStatus_t r;
+        // X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
+        if (algo == 0) {
+          r = cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, reinterpret_cast<cuDoubleComplex*>(theta[c]),
+                                C, const_cast<double*>(S.s),
+                                reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)), C,
+                                reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
+                                reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c, X.params);
+        } else {
+          hbuf.resize(std::max<size_t>(hbytes[c], 1));
+          double herr = 0.0;
+          r = cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, CUDA_C_64F, theta[c], C,
+                                CUDA_R_64F, const_cast<double*>(S.s), CUDA_C_64F, const_cast<double2*>(S.ux), C,
+                                CUDA_C_64F, const_cast<double2*>(S.vx), R, CUDA_C_64F, B + o_w[c], wsz[c], hbuf.data(),
+                                hbytes[c], d_info + c, &herr);
+        }
+        if (r != CUSOLVER_STATUS_SUCCESS) {
+          errs[l] = "cuSOLVER SVD failed in sector " + std::to_string(c) + " (status " + std::to_string((int)r) + ")";
+          return;
+        }
+      }
+      if (cudaEventRecord(X.ev[l], X.st[l]) != cudaSuccess) errs[l] = "event record";
+    };
+    {
+      std::vector<std::thread> th;
+      for (int l = 1; l < SVD_LANES; ++l) th.emplace_back(work, l);
+      work(0);
+      for (auto& t : th) t.join();
     }
-    if (cudaEventRecord(X.ev[l], X.st[l]) != cudaSuccess) errs[l] = "event record";
+    for (int l = 0; l < SVD_LANES; ++l) {
+      if (!errs[l].empty()) return fail(TN_ERR_CUDA, "tn_svd_truncate: " + errs[l]);
+      if ((r0 = cuda_check(cudaStreamWaitEvent(s, X.ev[l], 0), "join SVD lanes")) != TN_OK) return r0;
+    }
+    return TN_OK;
   };
+  // ---- norm bound: SVD the heaviest sectors first; a sector with ‖Θ(c)‖_F below the χ-th largest singular
+  // value found so far cannot place any value in the global top χ (that threshold only grows), so its SVD
+  // is skipped and its whole weight ‖Θ(c)‖²_F is discarded — the result is identical ----
+  double disc_skipped = 0.0;
   {
-    std::vector<std::thread> th;
-    for (int l = 1; l < SVD_LANES; ++l) th.emplace_back(work, l);
-    work(0);
-    for (auto& t : th) t.join();
+    ThetaPtrs tp{};
+    for (int c = 0; c < ns; ++c) {
+      tp.p[c] = reinterpret_cast<const double2*>(theta[c]);
+      tp.n[c] = sp.sec[c].k ? (int64_t)p->R[c] * p->C[c] : 0;
+    }
+    double* d_n2 = reinterpret_cast<double*>(B + o_n2);
+    if ((st = cuda_check(cudaMemsetAsync(d_n2, 0, ns * sizeof(double), s), "memset norms")) != TN_OK) return st;
+    k_sector_norm2<<<dim3(32, ns), 256, 0, s>>>(tp, d_n2);
+    std::vector<double> n2(ns);
+    if ((st = cuda_check(cudaMemcpyAsync(n2.data(), d_n2, ns * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms")) !=
+        TN_OK)
+      return st;
+    if ((st = cuda_check(cudaStreamSynchronize(s), "norm sync")) != TN_OK) return st;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return n2[a] > n2[b]; });
+    std::vector<int> wave1, rest;
+    int64_t have = 0;
+    for (int c : order) {
+      if (have < 2 * chi_max) {
+        wave1.push_back(c);
+        have += sp.sec[c].k;
+      } else {
+        rest.push_back(c);
+      }
+    }
+    if ((st = run_wave(wave1)) != TN_OK) return st;
+    std::vector<int> wave2;
+    if (!rest.empty()) {
+      // the chi_max-th largest value of wave 1 (values of each sector come back descending)
+      std::vector<double> vals;
+      for (int c : wave1) {
+        std::vector<double> v(sp.sec[c].k);
+        if ((st = cuda_check(cudaMemcpyAsync(v.data(), sp.sec[c].s, v.size() * 8, cudaMemcpyDeviceToHost, s),
+                             "D2H wave-1 values")) != TN_OK)
+          return st;
+        if ((st = cuda_check(cudaStreamSynchronize(s), "wave-1 sync")) != TN_OK) return st;
+        vals.insert(vals.end(), v.begin(), v.end());
+      }
+      double T = -1.0;
+      if ((int64_t)vals.size() >= chi_max) {
+        std::nth_element(vals.begin(), vals.begin() + (chi_max - 1), vals.end(), std::greater<double>());
+        T = vals[chi_max - 1];
+      }
+      for (int c : rest) {
+        if (T > 0.0 && std::sqrt(n2[c]) < T) {
+          disc_skipped += n2[c];
+          sp.sec[c].k = 0;  // skipped: contributes no value, its whole weight is discarded
+        } else {
+          wave2.push_back(c);
+        }
+      }
+      if ((st = run_wave(wave2)) != TN_OK) return st;
+    }
+    for (int c = 0; c < ns; ++c) base[c + 1] = base[c] + sp.sec[c].k;
   }
-  for (int l = 0; l < SVD_LANES; ++l) {
-    if (!errs[l].empty()) return fail(TN_ERR_CUDA, "tn_svd_truncate: " + errs[l]);
-    if ((st = cuda_check(cudaStreamWaitEvent(s, X.ev[l], 0), "join SVD lanes")) != TN_OK) return st;
-  }
+  const int64_t total = base[ns];
   double* kin = reinterpret_cast<double*>(B + o_kin);
   double* kout = reinterpret_cast<double*>(B + o_kout);
   int32_t* vin = reinterpret_cast<int32_t*>(B + o_vin);
@@ -339,7 +426,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   int32_t* d_off = reinterpret_cast<int32_t*>(B + o_off);
   int64_t* d_chi = reinterpret_cast<int64_t*>(B + o_res);
   double* d_disc = reinterpret_cast<double*>(B + o_res + 8);
-  st = cuda_check(cudaMemcpyAsync(d_base, base.data(), (ns + 1) * 8, cudaMemcpyHostToDevice, s), "H2D bases");
+  st = cuda_check(cudaMemcpyAsync(d_base, base.data(), (ns + 1) * 8, cudaMemcpyHostToDevice, s), "H2D bases");  // after skips
   if (st != TN_OK) return st;
   if (total > 0) {
     k_svd_pack<<<dim3(8, ns), 256, 0, s>>>(sp, kin, vin, d_base);
@@ -348,7 +435,8 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
         cudaSuccess)
       return fail(TN_ERR_CUDA, "radix sort of singular values failed");
   }
-  k_svd_select<<<1, 1024, 0, s>>>(sp, kout, vout, total, chi_max, cutoff, q_new, lambda_new, d_off, d_chi, d_disc);
+  k_svd_select<<<1, 1024, 0, s>>>(sp, kout, vout, total, chi_max, cutoff, q_new, lambda_new, d_off, d_chi, d_disc,
+                                  disc_skipped);
   if ((st = cuda_check(cudaGetLastError(), "SVD select")) != TN_OK) return st;
   std::vector<int> info(ns, 0);
   int64_t res[2];
