@@ -562,8 +562,7 @@ def run_pair(args, rank, world, local_rank):
     import paper_2301_12814_b200 as tn
     import synth
 
-    if rank != 0:
-        return
+    import torch.distributed as dist
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     c = synth.make_pair_config(args.pair)
@@ -573,7 +572,7 @@ def run_pair(args, rank, world, local_rank):
     int8 = args.contraction == "int8"
 
     def mk():
-        p = tn.Plan2(c.d, c.N, *qs)
+        p = tn.Plan2(c.d, c.N, *qs, world, rank)   # row-sharded over the ranks (slabs stay local)
         if int8:
             p.set_contraction("int8", args.slices)
         return p
@@ -601,6 +600,9 @@ def run_pair(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     kt.clear()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
@@ -608,21 +610,29 @@ def run_pair(args, rank, world, local_rank):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     for p in keep:
         kt.append(p.kernel_times())
         p.destroy()
-    ms = e0.elapsed_time(e1) / args.steps
+    tms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+    ms = float(tms.item()) / args.steps
+    if rank != 0:
+        return
     km = {k: statistics.mean(x[k] for x in kt[-args.steps:]) for k in kt[0]}
     k4 = km["k4_contract"]
-    achieved = flops["f_contract"] / (k4 * 1e-3) / 1e12
+    achieved = flops["f_contract_local"] / (k4 * 1e-3) / 1e12
     line = {"metric": "Θ(c1,c2) MPO build useful complex FP64 GFLOP/s", "value": round(f_useful / (ms * 1e-3) / 1e9, 3),
-            "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (synth.PAIR_CONFIGS, seeded)",
             "gates_per_s": round(1000.0 / ms, 3),
             "config": {"workload": f"MPO pair config {args.pair}: N={c.N}, d={c.d}, chi={c.chi_l}, "
                                    f"{c.meta['charges']} charge pairs", "f_contract": flops["f_contract"],
                        "f_mix": flops["f_mix"], "contraction": args.contraction,
+                       "parallelism": f"rows{world}" if world > 1 else "single",
                        "step": "tn_theta2_plan + tn_build_bs_unitary + tn_theta_exec"},
             "roofline": {"bound": "tensor", "kernel": "k4_contract", "achieved": round(achieved, 3),
                          "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_TC_PEAK_TFLOPS, 4),

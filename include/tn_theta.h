@@ -93,12 +93,16 @@ TN_API tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64
  * Θ(c1,c2) is compact row-major, rows = sorted left positions with l1−c1, l2−c2 ∈ [0, d−1], columns
  * = sorted right positions with c1−r1, c2−r2 ∈ [0, d−1] (R16–R18). tn_build_bs_unitary and
  * tn_theta_exec are used unchanged (exec applies U to species 1 and conj(U) to species 2);
- * tn_plan_offsets returns (N+1)²+1 entries over the keys. Single GPU only (world_size 1).
+ * tn_plan_offsets returns (N+1)²+1 entries over the keys. world_size/rank shard the sorted left
+ * positions flop-balanced as in tn_theta_plan; a rank's slab of Θ(c1,c2) is the contiguous run of its
+ * rows inside [r0, r1) (tn_plan_local_sector_shape gives its first row). tn_theta_exec_sharded accepts
+ * pair plans with TN_GATHER_NONE only.
  * Errors: as tn_theta_plan, plus TN_ERR_UNSUPPORTED when (N+1)² exceeds this build's sector limit
- * (N ≤ 9). tn_theta_exec_sharded rejects pair plans with TN_ERR_UNSUPPORTED. */
+ * (N ≤ 9). */
 TN_API tn_status tn_theta2_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r,
                                 const int32_t* q1_l, const int32_t* q2_l, const int32_t* q1_c,
-                                const int32_t* q2_c, const int32_t* q1_r, const int32_t* q2_r, tn_plan** out);
+                                const int32_t* q2_c, const int32_t* q1_r, const int32_t* q2_r,
+                                int world_size, int rank, tn_plan** out);
 
 TN_API tn_status tn_plan_destroy(tn_plan* plan);  /* NULL is accepted. */
 

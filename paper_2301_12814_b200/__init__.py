@@ -152,14 +152,15 @@ class Plan2(Plan):
     """tn_theta2_plan: the MPO (doubled-charge) plan — every bond carries a charge pair (q1, q2); sectors are
     Θ(c1, c2), indexed s = c1·(N+1) + c2 (use `sector(c1, c2)`). theta_exec returns (N+1)² tensors."""
 
-    def __init__(self, d: int, N: int, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r):
+    def __init__(self, d: int, N: int, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r, world_size: int = 1, rank: int = 0):
         self._keep = [_charges(q) for q in (q1_l, q2_l, q1_c, q2_c, q1_r, q2_r)]
         k = self._keep
         self.d, self.N = int(d), int(N)
         self.chi = (int(k[0].shape[0]), int(k[2].shape[0]), int(k[4].shape[0]))
-        self.world_size, self.rank = 1, 0
+        self.world_size, self.rank = int(world_size), int(rank)
         h = C.c_void_p()
-        check(lib.tn_theta2_plan(self.d, self.N, *self.chi, *(_ptr(x) for x in k), C.byref(h)), "tn_theta2_plan")
+        check(lib.tn_theta2_plan(self.d, self.N, *self.chi, *(_ptr(x) for x in k), self.world_size, self.rank,
+                                 C.byref(h)), "tn_theta2_plan")
         self._h = h
         self.nsec = (self.N + 1) ** 2
         del self._keep

@@ -29,7 +29,8 @@ _i32p = C.POINTER(C.c_int32)
 SIGNATURES = {
     "tn_theta_plan": [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, _p, _p, _p, C.c_int, C.c_int,
                       C.POINTER(_p)],
-    "tn_theta2_plan": [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
+    "tn_theta2_plan": [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, _p, _p, _p, _p, _p, _p, C.c_int, C.c_int,
+                       C.POINTER(_p)],
     "tn_plan_destroy": [_p],
     "tn_plan_sector_shape": [_p, C.c_int, _i64p, _i64p],
     "tn_plan_local_sector_shape": [_p, C.c_int, _i64p, _i64p, _i64p],

@@ -246,7 +246,6 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     if (!q2[0] || !q2[1] || !q2[2]) return fail(TN_ERR_DIMENSION, "tn_theta2_plan: NULL charge array");
     if ((N + 1) * (N + 1) > MAXC)
       return fail(TN_ERR_UNSUPPORTED, "tn_theta2_plan: (N+1)^2 charge pairs exceed this build's sector limit (N <= 9)");
-    if (world_size != 1) return fail(TN_ERR_UNSUPPORTED, "tn_theta2_plan: row sharding of pair plans is not built");
   }
 
   tn_plan* p = new (std::nothrow) tn_plan();
@@ -569,10 +568,10 @@ tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_
 
 tn_status tn_theta2_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q1_l,
                          const int32_t* q2_l, const int32_t* q1_c, const int32_t* q2_c, const int32_t* q1_r,
-                         const int32_t* q2_r, tn_plan** out) {
+                         const int32_t* q2_r, int world_size, int rank, tn_plan** out) {
   if (!q1_l || !q1_c || !q1_r) return fail(TN_ERR_DIMENSION, "tn_theta2_plan: NULL charge array");
   const int32_t* q2[3] = {q2_l, q2_c, q2_r};
-  return plan_impl(d, N, chi_l, chi_c, chi_r, q1_l, q1_c, q1_r, q2, 1, 0, out);
+  return plan_impl(d, N, chi_l, chi_c, chi_r, q1_l, q1_c, q1_r, q2, world_size, rank, out);
 }
 
 tn_status tn_plan_destroy(tn_plan* plan) {

@@ -115,7 +115,8 @@ tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* com
                                 double* lambda_k, double* gamma_k1, double* lambda_l, double* lambda_r, double* U,
                                 double* const* theta_out, int bcast_operands, int gather_mode) {
   if (!p || !comm) return fail(TN_ERR_DIMENSION, "tn_theta_exec_sharded: NULL plan/comm");
-  if (p->pair) return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_sharded: pair (MPO) plans are single-GPU in this build");
+  if (p->pair && gather_mode != TN_GATHER_NONE)
+    return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_sharded: pair (MPO) plans support TN_GATHER_NONE only");
   if (p->world != comm->world || p->rank != comm->rank)
     return fail(TN_ERR_CONSISTENCY, "tn_theta_exec_sharded: plan world/rank differ from the communicator's");
   if (gather_mode != TN_GATHER_NONE && gather_mode != TN_GATHER_ROOT && gather_mode != TN_GATHER_SECTOR_OWNER)

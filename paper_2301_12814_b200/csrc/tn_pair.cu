@@ -53,17 +53,66 @@ tn_status build_pair_tables(tn_plan* p) {
   p->col0.assign(nq, 0);
   p->lR.assign(nq, 0);
   p->lrow0.assign(nq, 0);
-  p->bounds = {0, p->chi[0]};
-  p->r0 = 0;
-  p->r1 = p->chi[0];
+  // ---- flop-balanced row shards over sorted left positions (per-pair row cost: contraction + mix) ----
+  {
+    std::vector<double> cost(nq, 0.0);
+    for (int l = 0; l < nq; ++l) {
+      if (!cnt(ol, l)) continue;
+      const int l1 = l / nk, l2 = l % nk;
+      for (int r = 0; r < nq; ++r) {
+        const int64_t nr = cnt(orr, r);
+        if (!nr) continue;
+        const int r1 = r / nk, r2 = r % nk;
+        double L1 = 0, L2 = 0, mc = 0;
+        for (int x = 0; x <= N; ++x) L1 += ok(l1, x) && ok(x, r1);
+        for (int y = 0; y <= N; ++y) L2 += ok(l2, y) && ok(y, r2);
+        for (int m = 0; m < nq; ++m)
+          if (cnt(oc, m) && ok(l1, m / nk) && ok(m / nk, r1) && ok(l2, m % nk) && ok(m % nk, r2)) mc += (double)cnt(oc, m);
+        cost[l] += (double)nr * (mc + L1 * L1 * L2 + L1 * L2 * L2);
+      }
+    }
+    double total = 0.0;
+    for (int l = 0; l < nq; ++l) total += cost[l] * (double)cnt(ol, l);
+    const int W = p->world;
+    p->bounds.assign(W + 1, 0);
+    p->bounds[W] = p->chi[0];
+    double prefix = 0.0;
+    int64_t row = 0;
+    int rk = 1;
+    for (int l = 0; l < nq && rk < W; ++l)
+      for (int64_t i = 0; i < cnt(ol, l) && rk < W; ++i) {
+        while (rk < W && prefix >= total * (double)rk / W) p->bounds[rk++] = row;
+        prefix += cost[l];
+        ++row;
+      }
+    while (rk < W) p->bounds[rk++] = row;
+    p->r0 = p->bounds[p->rank];
+    p->r1 = p->bounds[p->rank + 1];
+  }
+  const int64_t R0 = p->r0, R1 = p->r1;
+  auto in_shard = [&](int l) {  // rows of left segment l inside [r0, r1): [first, count)
+    const int64_t a = std::max<int64_t>(ol[l], R0), b = std::min<int64_t>(ol[l + 1], R1);
+    return std::make_pair(a, std::max<int64_t>(0, b - a));
+  };
   for (int c1 = 0; c1 <= N; ++c1)
     for (int c2 = 0; c2 <= N; ++c2) {
       const int s = c1 * nk + c2;
-      int64_t r = 0, c = 0;
-      for (int l1 = c1; l1 <= std::min(N, c1 + d - 1); ++l1)  // keys ascend = sorted order
+      // rows of Θ(s): whole left segments in key (= sorted) order; this rank's slab = those in [r0, r1),
+      // one contiguous run of Θ(s)'s rows starting at a_s = #rows of Θ(s) before r0
+      int64_t r = 0, c = 0, a_s = 0, rl = 0;
+      for (int l1 = c1; l1 <= std::min(N, c1 + d - 1); ++l1)
         for (int l2 = c2; l2 <= std::min(N, c2 + d - 1); ++l2) {
-          rowoff[(size_t)s * nq + l1 * nk + l2] = (int32_t)r;
-          r += cnt(ol, l1 * nk + l2);
+          const int l = l1 * nk + l2;
+          a_s += std::min<int64_t>(std::max<int64_t>(R0 - ol[l], 0), cnt(ol, l));
+          rl += in_shard(l).second;
+        }
+      for (int l1 = c1; l1 <= std::min(N, c1 + d - 1); ++l1)
+        for (int l2 = c2; l2 <= std::min(N, c2 + d - 1); ++l2) {
+          const int l = l1 * nk + l2;
+          // slab-local row of segment l's first in-shard row
+          rowoff[(size_t)s * nq + l] =
+              (int32_t)(r + std::min<int64_t>(std::max<int64_t>(R0 - ol[l], 0), cnt(ol, l)) - a_s);
+          r += cnt(ol, l);
         }
       for (int r1 = std::max(0, c1 - d + 1); r1 <= c1; ++r1)
         for (int r2 = std::max(0, c2 - d + 1); r2 <= c2; ++r2) {
@@ -71,7 +120,9 @@ tn_status build_pair_tables(tn_plan* p) {
           c += cnt(orr, r1 * nk + r2);
         }
       if (r > INT32_MAX || c > INT32_MAX) return fail(TN_ERR_UNSUPPORTED, "sector dimension > INT32_MAX");
-      p->R[s] = p->lR[s] = r;
+      p->R[s] = r;
+      p->lR[s] = rl;
+      p->lrow0[s] = rl ? a_s : 0;  // pair plans: slab start as a row index of Θ(s) (row0 = 0)
       p->C[s] = c;
     }
   // ---- useful work (oracle.flop_counts2 definitions) ----
@@ -92,8 +143,24 @@ tn_status build_pair_tables(tn_plan* p) {
       if (L1 && L2) p->f_mix += 8 * nl * nr * (L1 * L1 * L2 + L1 * L2 * L2);
     }
   }
-  p->f_contract_local = p->f_contract;
-  p->f_mix_local = p->f_mix;
+  p->f_contract_local = p->f_mix_local = 0;
+  for (int l = 0; l < nq; ++l) {
+    const int64_t nl = in_shard(l).second;
+    if (!nl) continue;
+    const int l1 = l / nk, l2 = l % nk;
+    for (int r = 0; r < nq; ++r) {
+      const int64_t nr = cnt(orr, r);
+      if (!nr) continue;
+      const int r1 = r / nk, r2 = r % nk;
+      int64_t L1 = 0, L2 = 0;
+      for (int x = 0; x <= N; ++x) L1 += ok(l1, x) && ok(x, r1);
+      for (int y = 0; y <= N; ++y) L2 += ok(l2, y) && ok(y, r2);
+      for (int m = 0; m < nq; ++m)
+        if (cnt(oc, m) && ok(l1, m / nk) && ok(m / nk, r1) && ok(l2, m % nk) && ok(m % nk, r2))
+          p->f_contract_local += 8 * nl * cnt(oc, m) * nr;
+      if (L1 && L2) p->f_mix_local += 8 * nl * nr * (L1 * L1 * L2 + L1 * L2 * L2);
+    }
+  }
   // ---- groups: one per non-empty centre pair; rows / cols = those of Θ(m), gathered by position ----
   std::vector<int32_t>& rpos = p->h_rowperm_pos;
   std::vector<int32_t>& cpos = p->h_colperm_pos;
@@ -104,20 +171,22 @@ tn_status build_pair_tables(tn_plan* p) {
   p->f_exec = 0;
   for (int m = 0; m < nq; ++m) {
     const int64_t K = cnt(oc, m);
-    if (K == 0 || p->R[m] == 0 || p->C[m] == 0) continue;
+    if (K == 0 || p->lR[m] == 0 || p->C[m] == 0) continue;
     const int m1 = m / nk, m2 = m % nk;
     GroupDesc g{};
     g.cc = m;
     g.row0 = (int64_t)rpos.size();
     for (int l1 = m1; l1 <= std::min(N, m1 + d - 1); ++l1)
       for (int l2 = m2; l2 <= std::min(N, m2 + d - 1); ++l2)
-        for (int32_t q = ol[l1 * nk + l2]; q < ol[l1 * nk + l2 + 1]; ++q) rpos.push_back(q);
+        for (int32_t q = (int32_t)in_shard(l1 * nk + l2).first,
+                     qe = (int32_t)(in_shard(l1 * nk + l2).first + in_shard(l1 * nk + l2).second); q < qe; ++q)
+          rpos.push_back(q);
     g.col0 = (int64_t)cpos.size();
     for (int r1 = std::max(0, m1 - d + 1); r1 <= m1; ++r1)
       for (int r2 = std::max(0, m2 - d + 1); r2 <= m2; ++r2)
         for (int32_t q = orr[r1 * nk + r2]; q < orr[r1 * nk + r2 + 1]; ++q) cpos.push_back(q);
     g.k0 = oc[m];
-    g.R = (int32_t)p->R[m];
+    g.R = (int32_t)p->lR[m];
     g.C = (int32_t)p->C[m];
     g.K = (int32_t)K;
     g.K4 = (int32_t)((K + 3) / 4 * 4);
@@ -147,7 +216,7 @@ tn_status build_pair_tables(tn_plan* p) {
   int max_l = 1;
   for (int pass = 0; pass < 2; ++pass) {
     for (int l = 0; l < nq; ++l) {
-      const int64_t nl = cnt(ol, l);
+      const int64_t nl = in_shard(l).second, lfirst = in_shard(l).first;
       if (!nl) continue;
       const int l1 = l / nk, l2 = l % nk;
       for (int r = 0; r < nq; ++r) {
@@ -174,7 +243,7 @@ tn_status build_pair_tables(tn_plan* p) {
             t.ne = (int32_t)(rows * ngr);
             t.nr = (int32_t)nr;
             t.ngr = (int32_t)ngr;
-            t.pl0 = (int32_t)(ol[l] + band);
+            t.pl0 = (int32_t)(lfirst + band);
             t.pr0 = orr[r];
             t.lkey = l;
             t.rkey = r;

@@ -162,3 +162,35 @@ def test_pair_errors(tn):
     plan = tn.Plan2(4, 3, [0, 1], [1, 0], [0, 1], [0, 1], [0, 1], [1, 1])
     with pytest.raises(tn.TnError, match="DOMAIN"):
         plan.sector_shape(16)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_pair_sharded_equals_unsharded(tn, world):
+    # each rank's row slab of every Θ(c1,c2) (its plan run in turn on this one GPU, no collective needed):
+    # the slabs tile the sector rows and reproduce the unsharded Θ bit for bit
+    c = _pair(2)
+    _, full = gpu_theta2(tn, c)
+    dv = lambda a: _dev(a)
+    slabs = {k: [] for k in full}
+    f_loc = 0
+    for r in range(world):
+        pr = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r, world, r)
+        U = tn.build_bs_unitary(pr, c.theta, c.phi)
+        out = tn.theta_exec(pr, dv(c.gamma_k), dv(c.lam_k), dv(c.gamma_k1), dv(c.lam_l), dv(c.lam_r), U)
+        torch.cuda.synchronize()
+        f_loc += pr.flops()["f_contract_local"]
+        for (c1, c2) in full:
+            s = pr.sector(c1, c2)
+            R, Cc, row0 = pr.local_sector_shape(s)
+            assert tuple(out[s].shape) == (R, Cc)
+            slabs[(c1, c2)].append((row0, out[s].cpu().numpy()))
+    assert f_loc == pr.flops()["f_contract"]
+    for key, parts in slabs.items():
+        parts = sorted((p for p in parts if p[1].shape[0] > 0), key=lambda x: x[0])
+        pos = 0
+        for b, blk in parts:
+            assert b == pos
+            pos += blk.shape[0]
+        assert pos == full[key].shape[0]
+        if parts:
+            assert np.array_equal(np.concatenate([p for _, p in parts], axis=0), full[key]), key
