@@ -106,12 +106,14 @@ TN_API tn_status tn_theta2_plan(int d, int N, int64_t chi_l, int64_t chi_c, int6
 
 TN_API tn_status tn_plan_destroy(tn_plan* plan);  /* NULL is accepted. */
 
-/* Full Θ(c) shape R_c × C_c (all ranks). TN_ERR_DOMAIN for c ∉ [0,N]. */
+/* Full Θ(c) shape R_c × C_c (all ranks). c is a sector index: c ∈ [0, N], or s = c1·(N+1)+c2 ∈
+ * [0, (N+1)²) for pair plans. TN_ERR_DOMAIN for an index outside that range. */
 TN_API tn_status tn_plan_sector_shape(const tn_plan* plan, int c, int64_t* R, int64_t* C);
 /* This rank's slab of Θ(c): *R local rows × *C, its first row being row *row_begin of Θ(c). */
 TN_API tn_status tn_plan_local_sector_shape(const tn_plan* plan, int c, int64_t* R, int64_t* C,
                                      int64_t* row_begin);
-/* Copy perm_x (χ_x int32) / off_x (N+2 int32) of bond x into caller HOST memory. */
+/* Copy perm_x (χ_x int32) / off_x (N+2 int32; (N+1)²+1 over the pair keys for pair plans) of bond x
+ * into caller HOST memory. */
 TN_API tn_status tn_plan_perm(const tn_plan* plan, int bond, int32_t* host_out);
 TN_API tn_status tn_plan_offsets(const tn_plan* plan, int bond, int32_t* host_out);
 /* Sorted-left-position shard [r0, r1) of rank r (any r in [0, world_size)). */
@@ -121,8 +123,10 @@ TN_API tn_status tn_plan_shard_rows(const tn_plan* plan, int r, int64_t* r0, int
 TN_API tn_status tn_plan_sector_owner(const tn_plan* plan, int c, int* owner);
 /* Useful work, 8 flops per complex MAC; any output pointer may be NULL.
  *   f_contract = 8 Σ_{allowed (c_l,c_c,c_r)} n_l n_c n_r  (whole problem),
- *   f_mix      = 8 Σ_{(c_l,c_r)} n_l n_r #c #c_c           (whole problem),
- *   f_exec     = complex DMMA flops this rank's K4 executes incl. tile padding (8 per CMAC),
+ *   f_mix      = 8 Σ_{(c_l,c_r)} n_l n_r #c #c_c           (whole problem; pair plans: 8 Σ n_l n_r
+ *                (L1²L2 + L1L2²), the U⊗U* mix applied one species at a time, R19),
+ *   f_exec     = complex flops this rank's K4 executes incl. tile padding (8 per CMAC; for the
+ *                paper-literal engine its per-sector GEMMs),
  *   f_contract_local, f_mix_local = this rank's share (its rows [r0, r1)). */
 TN_API tn_status tn_plan_flops(const tn_plan* plan, int64_t* f_contract, int64_t* f_mix, int64_t* f_exec,
                                int64_t* f_contract_local, int64_t* f_mix_local);
@@ -133,8 +137,9 @@ TN_API tn_status tn_plan_workspace_bytes(const tn_plan* plan, int64_t* bytes);
 
 /* Per-kernel device times (CUDA events recorded on the launching streams) of the most recent
  * calls made with this plan: ms[0] K1 bond sort (inside tn_theta_plan), ms[1] K2 U build,
- * ms[2] K3 staging, ms[3] K4 contraction, ms[4] K5 U-mix. Waits for those events. Entries for
- * calls not yet made are −1. */
+ * ms[2] K3 staging, ms[3] K4 contraction, ms[4] K5 U-mix (pair plans: both K5P passes; the fused
+ * and paper-literal engines report their whole contraction as K4 and ~0 for K5). Waits for those
+ * events. Entries for calls not yet made are −1. */
 TN_API tn_status tn_plan_kernel_times(const tn_plan* plan, float* ms5);
 
 /* Contraction engine of tn_theta_exec (default TN_CONTRACT_F64_DMMA):
