@@ -407,3 +407,36 @@ def test_paper_literal_engine_edge_cases(tn):
         ref, *_ = oracle_theta(case)
         _, _, got = gpu_theta(case, contraction=("literal", 0))
         assert_sectors_close(got, ref, 1e-12, f"literal {name}")
+
+
+def test_theta_parity_config4_flat_per_block_sampled(tn):
+    # T9b for config 4 (gate 0, flat λ): elements sampled in random (c, c_l, c_r) blocks,
+    # each checked against the literal sum relative to its own block's RMS — with flat λ no block's
+    # contribution is hidden under the geometric decay
+    case = synth.flat_lambda(synth.make_config(4, gate=0))
+    plan, U, got = gpu_theta(case)
+    pl = plan.perm(0), plan.perm(1), plan.perm(2)
+    of = plan.offsets(0), plan.offsets(1), plan.offsets(2)
+    ub = [oracle.bs_unitary_block(n, case.theta, case.phi, case.d) for n in range(min(case.N, 2 * case.d - 2) + 1)]
+    rng = np.random.default_rng(44)
+    N, d = case.N, case.d
+    checked, worst = 0, 0.0
+    while checked < 200:
+        c = int(rng.integers(0, N + 1))
+        cl = int(rng.integers(c, min(N, c + d - 1) + 1))
+        cr = int(rng.integers(max(0, c - d + 1), c + 1))
+        (r0, _), (k0, _) = oracle.sector_ranges(of[0], of[2], N, d, c)
+        a0, a1 = int(of[0][cl]) - r0, int(of[0][cl + 1]) - r0
+        b0, b1 = int(of[2][cr]) - k0, int(of[2][cr + 1]) - k0
+        if a1 <= a0 or b1 <= b0:
+            continue
+        blk = got[c][a0:a1, b0:b1]
+        rms = np.linalg.norm(blk) / math.sqrt(blk.size)
+        if rms == 0.0:
+            continue
+        a, b = int(rng.integers(a0, a1)), int(rng.integers(b0, b1))
+        v = oracle.theta_element(N, d, c, a, b, case.q_l, case.q_c, case.q_r, case.gamma_k, case.lam_k,
+                                 case.gamma_k1, case.lam_l, case.lam_r, ub, (pl, of))
+        worst = max(worst, abs(got[c][a, b] - v) / rms)
+        checked += 1
+    assert worst <= 1e-10, worst
