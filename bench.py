@@ -356,6 +356,18 @@ def run_tn(args, rank, world, local_rank):
                 dist.all_reduce(tv, op=dist.ReduceOp.MAX)
                 comm_variants[name] = round(float(tv.item()), 4)
                 del vout
+            # the SECTOR_OWNER exchange fused into K5 (peer-memory stores over NVLink, tn_theta_exec_remote)
+            fx = []
+            for it in range(4):
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                tn.theta_exec_to_owners(vplan, gk, lk, gk1, ll, lr, U)
+                if it:
+                    fx.append((time.perf_counter() - t0) * 1e3)
+            tv = torch.tensor([statistics.mean(fx)], dtype=torch.float64, device=dev)
+            dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+            comm_variants["fused_sector_owner_wall"] = round(float(tv.item()), 4)
             vplan.destroy()
             comm.destroy()
         except Exception as e:  # keep the headline line even if a variant fails

@@ -250,6 +250,23 @@ TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn
                                 double* lambda_l, double* lambda_r, double* U,
                                 double* const* theta_out, int bcast_operands, int gather_mode);
 
+/* tn_theta_exec_remote — the SECTOR_OWNER exchange fused into the computation (SURVEY.md §8(e)
+ * "Optional fusion"): K4 writes this rank's P into a plan-owned LOCAL workspace, and K5 writes each row
+ * of this rank's slab of Θ(c) straight to theta_dst[c] — any device-accessible pointer, typically the
+ * owner rank's full Θ(c) buffer opened with tn_ipc_open (NVLink peer memory) offset to this rank's
+ * first row (tn_plan_local_sector_shape's row_begin × C_c complex). No collective runs inside: the
+ * caller orders consumers after every rank's stream (e.g. a barrier after synchronising). Other
+ * arguments as tn_theta_exec. Single-charge plans with the DMMA or INT8 engine; TN_ERR_UNSUPPORTED
+ * otherwise. */
+TN_API tn_status tn_theta_exec_remote(tn_plan* plan, tn_stream stream, const double* gamma_k,
+                                      const double* lambda_k, const double* gamma_k1, const double* lambda_l,
+                                      const double* lambda_r, const double* U, double* const* theta_dst);
+/* CUDA IPC for tn_theta_exec_remote: 64-byte handle + byte offset of dev_ptr inside its allocation;
+ * open a peer process's handle (peer access enabled lazily); close what tn_ipc_open returned. */
+TN_API tn_status tn_ipc_get_handle(const void* dev_ptr, void* handle64, int64_t* offset);
+TN_API tn_status tn_ipc_open(const void* handle64, void** dev_ptr);
+TN_API tn_status tn_ipc_close(void* dev_ptr);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Host-only helpers (no GPU needed) and diagnostics.                                          */
 /* ------------------------------------------------------------------------------------------ */

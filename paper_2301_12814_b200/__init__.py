@@ -20,7 +20,8 @@ from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN
 
 __all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Plan2", "Comm", "svd_truncate", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
            "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT",
-           "TN_GATHER_SECTOR_OWNER", "sector_owners_host"]
+           "TN_GATHER_SECTOR_OWNER", "sector_owners_host",
+           "theta_exec_to_owners", "ipc_handle"]
 
 
 def _stream_ptr(stream) -> C.c_void_p:
@@ -312,3 +313,61 @@ def sector_owners_host(sizes, world_size: int) -> np.ndarray:
     check(lib.tn_sector_owners_host(int(sz.shape[0]), sz.ctypes.data_as(C.POINTER(C.c_int64)), int(world_size),
                                     out.ctypes.data_as(C.POINTER(C.c_int32))), "tn_sector_owners_host")
     return out
+
+
+def ipc_handle(t: torch.Tensor):
+    """tn_ipc_get_handle: (64-byte handle, byte offset) exporting a CUDA tensor's memory to another process."""
+    h = (C.c_char * 64)()
+    off = C.c_int64()
+    check(lib.tn_ipc_get_handle(_ptr(t), h, C.byref(off)), "tn_ipc_get_handle")
+    return bytes(h), off.value
+
+
+def theta_exec_to_owners(plan: Plan, gk, lk, gk1, ll, lr, U, group=None, stream=None):
+    """The SECTOR_OWNER gather fused into the computation (tn_theta_exec_remote): every rank's K5 writes its
+    slab of Θ(c) straight into the owner's full Θ(c) (CUDA IPC / NVLink peer memory); handles are exchanged
+    with torch.distributed (any backend) and a barrier after the streams drain orders the owners' reads.
+    Returns {c: full Θ(c)} for the sectors this rank owns."""
+    import torch.distributed as dist
+    _check_inputs(plan, gk, lk, gk1, ll, lr, U)
+    world, rank = plan.world_size, plan.rank
+    dev = gk.device
+    owned = {}
+    for c in range(plan.nsec):
+        R, Cc = plan.sector_shape(c)
+        if plan.sector_owner(c) == rank and R * Cc > 0:
+            owned[c] = torch.empty((R, Cc), dtype=torch.complex128, device=dev)
+    mine = {c: ipc_handle(t) for c, t in owned.items()}
+    allh = [None] * world
+    if world > 1:
+        dist.all_gather_object(allh, mine, group=group)
+    else:
+        allh = [mine]
+    opened = {}
+    dst = (C.c_void_p * plan.nsec)()
+    try:
+        for c in range(plan.nsec):
+            R, Cc, row0 = plan.local_sector_shape(c)
+            if R * Cc == 0:
+                dst[c] = None
+                continue
+            o = plan.sector_owner(c)
+            if o == rank:
+                base = owned[c].data_ptr()
+            else:
+                hnd, off = allh[o][c]
+                if hnd not in opened:
+                    p = C.c_void_p()
+                    check(lib.tn_ipc_open(hnd, C.byref(p)), "tn_ipc_open")
+                    opened[hnd] = p.value
+                base = opened[hnd] + off
+            dst[c] = base + row0 * Cc * 16
+        check(lib.tn_theta_exec_remote(plan.handle, _stream_ptr(stream), _ptr(gk), _ptr(lk), _ptr(gk1), _ptr(ll),
+                                       _ptr(lr), _ptr(U), dst), "tn_theta_exec_remote")
+        (stream or torch.cuda.current_stream()).synchronize()
+        if world > 1:
+            dist.barrier(group=group)
+    finally:
+        for p in opened.values():
+            lib.tn_ipc_close(C.c_void_p(p))
+    return owned

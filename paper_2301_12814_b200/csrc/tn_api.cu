@@ -8,6 +8,8 @@
 
 #include <cstdlib>
 
+#include <dlfcn.h>
+
 #include "tn_internal.cuh"
 
 namespace tn {
@@ -94,6 +96,7 @@ static void free_plan(tn_plan* p) {
   const bool used = p->rec_exec;
   pool_release(p->blk_oz, p->last_stream, used);
   pool_release(p->blk_lit, p->last_stream, used);
+  pool_release(p->blk_p, p->last_stream, used);
   pool_release(p->blk_work, p->last_stream, used);
   pool_release(p->blk_tab, p->last_stream, used);
   for (auto& e : p->ev)
@@ -839,6 +842,97 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
     if (st != TN_OK) return st;
   }
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+}
+
+tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
+                               const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
+                               double* const* theta_dst) {
+  if (!p) return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL plan");
+  if (p->pair || p->fused || p->contraction == TN_CONTRACT_PAPER_LITERAL)
+    return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_remote: single-charge plans with the DMMA or INT8 engine only");
+  if (!gamma_k || !lambda_k || !gamma_k1 || !lambda_l || !lambda_r || !U || !theta_dst)
+    return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL input pointer");
+  for (int c = 0; c < p->nsec; ++c)
+    if (p->lR[c] * p->C[c] > 0 && !theta_dst[c])
+      return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL theta_dst[c] for a non-empty slab");
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_theta_exec_remote");
+  // local P workspace of this rank's slab shapes (pooled, kept by the plan)
+  std::vector<double*> pw(p->nsec, nullptr);
+  {
+    int64_t tot = 0;
+    std::vector<int64_t> off(p->nsec, 0);
+    for (int c = 0; c < p->nsec; ++c) {
+      off[c] = tot;
+      tot += (p->lR[c] * p->C[c] + 15) / 16 * 16;
+    }
+    if (!p->blk_p && tot > 0) {
+      cudaError_t aerr = cudaSuccess;
+      p->blk_p = pool_alloc((size_t)tot * sizeof(double2), &aerr);
+      if (aerr != cudaSuccess) return cuda_check(aerr, "pool alloc (remote P workspace)");
+      p->ws_bytes += tot * (int64_t)sizeof(double2);
+    }
+    for (int c = 0; c < p->nsec; ++c)
+      if (p->lR[c] * p->C[c] > 0) pw[c] = reinterpret_cast<double*>(static_cast<double2*>(p->blk_p) + off[c]);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const SectorParams sp4 = make_sector_params(p, pw.data());   // K4 writes P into the local workspace
+  SectorParams sp5 = make_sector_params(p, theta_dst);         // K5 reads it there, writes Θ to theta_dst
+  for (int c = 0; c < p->nsec; ++c) sp5.src[c] = reinterpret_cast<const double2*>(pw[c]);
+  p->last_stream = s;
+  p->rec_exec = true;
+  tn_status st = cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
+  if (st != TN_OK) return st;
+  if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
+  const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
+  st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                                        reinterpret_cast<const double2*>(gamma_k1), s)
+                      : launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
+                                     reinterpret_cast<const double2*>(gamma_k1), s),
+                  "K3 launch");
+  if (st != TN_OK) return st;
+  if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;
+  st = cuda_check(emu ? launch_oz_contract(p, sp4, s) : launch_contract(p, sp4, s), "K4 launch");
+  if (st != TN_OK) return st;
+  if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
+  st = cuda_check(launch_mix(p, sp5, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
+  if (st != TN_OK) return st;
+  return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+}
+
+// ---- CUDA IPC helpers: export a device buffer to another process, open a peer's buffer ----
+tn_status tn_ipc_get_handle(const void* dev_ptr, void* handle64, int64_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail(TN_ERR_DIMENSION, "tn_ipc_get_handle: NULL");
+  // the allocation base via the driver API, resolved at run time (the library must load without a GPU)
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<GetRange>(dlsym(h, "cuMemGetAddressRange_v2")) : nullptr;
+  }();
+  if (!get_range) return fail(TN_ERR_CUDA, "tn_ipc_get_handle: libcuda.so.1 / cuMemGetAddressRange_v2 unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+    return fail(TN_ERR_CUDA, "tn_ipc_get_handle: cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  tn_status st = cuda_check(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  if (st != TN_OK) return st;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)((unsigned long long)(uintptr_t)dev_ptr - base);
+  return TN_OK;
+}
+
+tn_status tn_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(TN_ERR_DIMENSION, "tn_ipc_open: NULL");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  return cuda_check(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+tn_status tn_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return TN_OK;
+  return cuda_check(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

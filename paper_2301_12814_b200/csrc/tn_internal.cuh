@@ -95,6 +95,7 @@ struct OzTile {
 // Per-sector tables passed BY VALUE as a kernel parameter (no device copy needed).
 struct SectorParams {
   double2* out[MAXC];       // this rank's slab of Θ(c) (row-major, ld = C_c)
+  const double2* src[MAXC]; // K5 reads P_{c_c} from here when set (tn_theta_exec_remote), else from out
   int64_t lrow0[MAXC];      // sorted left position of slab row 0
   int64_t col0[MAXC];       // sorted right position of column 0
   int32_t ld[MAXC];         // C_c
@@ -145,6 +146,7 @@ struct tn_plan {
   std::vector<tn::MixTile2> h_mix2;
   std::vector<int32_t> h_rowoff, h_coloff;
   std::vector<int32_t> h_rowperm_pos, h_colperm_pos;
+  void* blk_p = nullptr;                       // local P workspace of tn_theta_exec_remote (slab shapes)
   double2* d_apanel = nullptr;
   double2* d_bpanel = nullptr;
   int64_t a_elems = 0, b_elems = 0;

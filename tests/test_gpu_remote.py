@@ -1,0 +1,70 @@
+"""The SECTOR_OWNER exchange fused into K5 (tn_theta_exec_remote + CUDA IPC): two processes share the one
+GPU, each computes its row shard and writes its slab of every Θ(c) straight into the owning process's
+buffer; every owner then holds the full sectors it owns, bit-identical to the unsharded Θ. The ranks'
+kernels never wait on each other (the only synchronisation is a host barrier after each stream drains),
+so one GPU stands in for the NVLink peers without changing what the kernels do."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, engine, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        import paper_2301_12814_b200 as tn
+        import synth
+        from gpu_util import gpu_theta, to_dev
+        torch.cuda.set_device(0)
+        case = synth.make_config(cfg)
+        _, _, full = gpu_theta(case, contraction=engine)          # unsharded reference, same GPU path
+        plan = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r, world, rank)
+        if engine:
+            plan.set_contraction(*engine)
+        U = tn.build_bs_unitary(plan, case.theta, case.phi)
+        t = to_dev(case)
+        owned = tn.theta_exec_to_owners(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U)
+        ok = all(np.array_equal(v.cpu().numpy(), full[c]) for c, v in owned.items())
+        counts = [None] * world
+        dist.all_gather_object(counts, len(owned))
+        q.put((rank, "ok" if ok else "mismatch", sum(counts)))
+    except Exception as e:
+        q.put((rank, repr(e), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,engine", [(1, None), (2, None), (2, ("int8", 6))])
+def test_exec_to_owners_two_processes_one_gpu(cfg, engine, cuda_ok):
+    import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, engine, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    assert all(r[1] == "ok" for r in res), res
+    c = synth.CONFIGS[cfg]
+    assert res[0][2] >= 1
