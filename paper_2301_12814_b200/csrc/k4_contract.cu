@@ -167,12 +167,9 @@ cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream
   if (p->ntiles == 0) return cudaSuccess;
   constexpr int STAGES = K4_STAGES;
   const size_t smem = (size_t)STAGES * CHUNK * sizeof(double2) * 2 + 2 * STAGES * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k4_contract<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  // set on every launch (microseconds): the attribute is per device, and a process may drive several
+  cudaError_t e = cudaFuncSetAttribute(k4_contract<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   const int64_t grid = std::min<int64_t>(p->ntiles, (int64_t)p->sm_count);
   k4_contract<STAGES><<<(unsigned)grid, K4_THREADS, smem, s>>>(p->d_groups, p->d_tiles, (int)p->ntiles,
                                                                 p->d_apanel, p->d_bpanel, sp);

@@ -33,7 +33,8 @@ namespace tn {
 
 namespace {
 constexpr int SVD_LANES = 8;  // concurrent sector SVDs (one cuSOLVER handle + stream + host thread each)
-struct SvdCtx {  // cuSOLVER handles / streams + a grow-only device scratch, per process
+struct SvdCtx {  // cuSOLVER handles / streams + a grow-only device scratch, per process and bound to the
+                 // device current at first use (one process per GPU, as everywhere in this library)
   cusolverDnHandle_t h[SVD_LANES] = {};
   cudaStream_t st[SVD_LANES] = {};
   cudaEvent_t ev[SVD_LANES + 1] = {};
