@@ -68,3 +68,30 @@ def test_exec_to_owners_two_processes_one_gpu(cfg, engine, cuda_ok):
     assert all(r[1] == "ok" for r in res), res
     c = synth.CONFIGS[cfg]
     assert res[0][2] >= 1
+
+
+def test_exec_remote_single_rank_and_errors(cuda_ok):
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ctypes as C
+    import paper_2301_12814_b200 as tn
+    import synth
+    from gpu_util import gpu_theta, to_dev
+    case = synth.make_config(1)
+    _, _, full = gpu_theta(case)
+    plan = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r)
+    U = tn.build_bs_unitary(plan, case.theta, case.phi)
+    t = to_dev(case)
+    owned = tn.theta_exec_to_owners(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U)   # world 1: all local
+    assert set(owned) == {c for c in range(case.N + 1) if full[c].size}
+    for c, v in owned.items():
+        assert np.array_equal(v.cpu().numpy(), full[c])
+    nulls = (C.c_void_p * plan.nsec)()
+    with pytest.raises(tn.TnError, match="DIMENSION"):
+        tn.check(tn.lib.tn_theta_exec_remote(plan.handle, None, *(tn._ptr(t[k]) for k in ("gk", "lk", "gk1", "ll", "lr")),
+                                             tn._ptr(U), nulls), "tn_theta_exec_remote")
+    pc = synth.make_pair_config(0)
+    p2 = tn.Plan2(pc.d, pc.N, pc.q1_l, pc.q2_l, pc.q1_c, pc.q2_c, pc.q1_r, pc.q2_r)
+    with pytest.raises(tn.TnError, match="UNSUPPORTED"):
+        tn.check(tn.lib.tn_theta_exec_remote(p2.handle, None, *(tn._ptr(t[k]) for k in ("gk", "lk", "gk1", "ll", "lr")),
+                                             tn._ptr(U), nulls), "tn_theta_exec_remote")
