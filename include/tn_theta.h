@@ -198,7 +198,9 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
 /* ------------------------------------------------------------------------------------------ */
 /* SVD step after Θ: PAPER.md:67.                      */
 /* ------------------------------------------------------------------------------------------ */
-/* tn_svd_truncate — per-sector SVD Θ(c) = U_c diag(s_c) V_c† (cuSOLVER Jacobi), global ranking of
+/* tn_svd_truncate — per-sector SVD Θ(c) = U_c diag(s_c) V_c† (default: Gram eigensolver + Rayleigh–Ritz,
+ * accurate to rounding for every value that can enter the top χ; TN_SVD_ALGO=gesvdp /
+ * gesvdj select a full cuSOLVER SVD per sector), global ranking of
  * every singular value (value descending, then charge ascending, then index ascending),
  * keep the first min(chi_max, #{s > cutoff}) (SPEC.md:98 uses cutoff 1e−14), and write the new
  * canonical factors of bond k (Vidal form, R21): the new bond is ordered by charge
@@ -208,8 +210,8 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
  *                  = U_c[α, s] / λ^{[k−1]}[α] for α in Θ(c)'s rows, 0 elsewhere (x/0 := 0),
  *   gamma_k1_new[a × β] (complex, row-major, ld = χ_r, columns in the caller's α_{k+1} order)
  *                  = V_c†[s, β] / λ^{[k+1]}[β] for β in Θ(c)'s columns, 0 elsewhere.
- *   theta      HOST array of N+1 DEVICE sector pointers from tn_theta_exec — DESTROYED (used as the
- *              SVD's input/workspace).
+ *   theta      HOST array of N+1 DEVICE sector pointers from tn_theta_exec — may be DESTROYED (the
+ *              library SVD paths use it as workspace; the default path only reads it).
  *   lambda_l, lambda_r  DEVICE λ^{[k−1]}, λ^{[k+1]} (the ones passed to tn_theta_exec).
  *   q_new [chi_max] int32, lambda_new [chi_max] double, gamma_k_new [χ_l·chi_max] and
  *   gamma_k1_new [chi_max·χ_r] complex: DEVICE, caller-owned capacity; the factors are written

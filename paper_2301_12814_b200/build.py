@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if "spill" in (r.stderr or "") and "0 bytes spill" not in r.stderr:
             print(r.stderr, file=sys.stderr)
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", LIB] + objs + ["-ldl", "-lcusolver"]
+        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", LIB] + objs + ["-ldl", "-lcusolver", "-lcublas"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

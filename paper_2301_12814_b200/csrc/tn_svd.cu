@@ -17,6 +17,7 @@
 //  * K_fac: Γ^{[k]}_new[α, a] = U_c[α, s]/λl[α] and Γ^{[k+1]}_new[a, β] = V_c†[s, β]/λr[β] (x/0 := 0),
 //    written straight into the caller's bond order through perm_l / perm_r.
 #include <cub/device/device_radix_sort.cuh>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <cstring>
@@ -25,6 +26,8 @@
 #include <thread>
 #include <vector>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 
 #include "tn_internal.cuh"
@@ -36,26 +39,40 @@ constexpr int SVD_LANES = 8;  // concurrent sector SVDs (one cuSOLVER handle + s
 struct SvdCtx {  // cuSOLVER handles / streams + a grow-only device scratch, per process and bound to the
                  // device current at first use (one process per GPU, as everywhere in this library)
   cusolverDnHandle_t h[SVD_LANES] = {};
+  cublasHandle_t hb[SVD_LANES] = {};
   cudaStream_t st[SVD_LANES] = {};
   cudaEvent_t ev[SVD_LANES + 1] = {};
   gesvdjInfo_t params = nullptr;
   cusolverDnParams_t xparams = nullptr;
-  void* buf = nullptr;
+  void* buf = nullptr;   // common scratch (library-SVD outputs, ranking buffers)
   size_t cap = 0;
+  void* gbuf[2] = {};    // Gram path: phase A (Gram matrices → eigenvectors), phase C (Ritz SVDs)
+  size_t gcap[2] = {};
   std::mutex mu;
 };
 SvdCtx& ctx() {
   static SvdCtx c;
   return c;
 }
-// 1: polar-decomposition SVD (Xgesvdp, default: 0.95 s at config 3), 0: one-sided Jacobi (gesvdj, 1.98 s);
-// both meet the parity bar (tests/test_gpu_svd.py runs with either)
+// 2 (default): Gram eigensolver + Rayleigh–Ritz (svd_gram below; 0.1x s at config 3), 1: polar-decomposition
+// SVD per sector (TN_SVD_ALGO=gesvdp, 0.77 s), 0: one-sided Jacobi (TN_SVD_ALGO=gesvdj, 1.98 s); all three
+// meet the parity bar (tests/test_gpu_svd.py runs each)
 int svd_algo() {
-  static const int v = [] {
-    const char* e = getenv("TN_SVD_ALGO");
-    return (e && std::string(e) == "gesvdj") ? 0 : 1;
-  }();
-  return v;
+  const char* e = getenv("TN_SVD_ALGO");
+  if (e && std::string(e) == "gesvdj") return 0;
+  if (e && std::string(e) == "gesvdp") return 1;
+  return 2;
+}
+tn_status grow(void*& buf, size_t& cap, size_t need, char** out) {  // grow-only device scratch
+  if (need > cap) {
+    if (buf) cudaFree(buf);
+    buf = nullptr;
+    cap = 0;
+    if (cudaMalloc(&buf, need) != cudaSuccess) return fail(TN_ERR_OOM, "tn_svd_truncate: scratch allocation");
+    cap = need;
+  }
+  *out = static_cast<char*>(buf);
+  return TN_OK;
 }
 }  // namespace
 
@@ -186,6 +203,261 @@ __global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ of
   }
 }
 
+// Run job(lane, c, host_workspace) for every sector of `wave` on the SVD lanes (largest cost first onto the
+// least-loaded lane; one host thread per lane, each lane's stream joined back into `s`).
+template <class Cost, class Job>
+tn_status run_lanes(SvdCtx& X, cudaStream_t s, std::vector<int> wave, Cost cost, Job job) {
+  if (wave.empty()) return TN_OK;
+  std::sort(wave.begin(), wave.end(), [&](int a, int b) { return cost(a) > cost(b); });
+  std::vector<std::vector<int>> lane(SVD_LANES);
+  double load[SVD_LANES] = {};
+  for (int c : wave) {
+    const int l = (int)(std::min_element(load, load + SVD_LANES) - load);
+    lane[l].push_back(c);
+    load[l] += cost(c);
+  }
+  tn_status r0 = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
+  if (r0 != TN_OK) return r0;
+  std::vector<std::string> errs(SVD_LANES);
+  auto work = [&](int l) {
+    if (lane[l].empty()) return;
+    if (cudaStreamWaitEvent(X.st[l], X.ev[SVD_LANES], 0) != cudaSuccess) {
+      errs[l] = "stream wait";
+      return;
+    }
+    std::vector<char> hbuf;
+    for (int c : lane[l]) {
+      errs[l] = job(l, c, hbuf);
+      if (!errs[l].empty()) return;
+    }
+    if (cudaEventRecord(X.ev[l], X.st[l]) != cudaSuccess) errs[l] = "event record";
+  };
+  {
+    std::vector<std::thread> th;
+    for (int l = 1; l < SVD_LANES; ++l) th.emplace_back(work, l);
+    work(0);
+    for (auto& t : th) t.join();
+  }
+  for (int l = 0; l < SVD_LANES; ++l) {
+    if (!errs[l].empty()) return fail(TN_ERR_CUDA, "tn_svd_truncate: " + errs[l]);
+    if (!lane[l].empty() && (r0 = cuda_check(cudaStreamWaitEvent(s, X.ev[l], 0), "join SVD lanes")) != TN_OK) return r0;
+  }
+  return TN_OK;
+}
+
+// ---- Gram eigensolver + Rayleigh–Ritz SVD step (default) ----
+// The column-major view of Θ(c) is Z = Θᵀ (C × R, ld C). With n_g = min(R, C):
+//  A. G = ZᴴZ (R ≤ C, "tall") or ZZᴴ (R > C), n_g × n_g, by ZGEMM on the DMMA pipe; Hermitian eigensolver
+//     (Xsyevd): eigenvalues w ≈ s² with absolute error ≲ n_g·ε·‖G‖, eigenvectors E (ascending).
+//  B. (host) approximate global χ-th value T² from every sector's w; a sector keeps its k' top eigenvectors
+//     with w ≥ T² − 2Δ (Δ = the largest error bound 16·n_g·ε·w_max over sectors) and w ≥ cutoff² − Δ_c, so
+//     every value that can make the exact top χ (or pass the cutoff) is inside E_k'. The norm bound of the
+//     library path skips whole sectors the same way (‖Θ(c)‖²_F < T² − Δ).
+//  C. Rayleigh–Ritz: Y = Z·E_k' (tall) or Zᴴ·E_k' (max(R,C) × k', ZGEMM), exact SVD Y = P S Wᴴ (Xgesvdp),
+//     then Z ≈ P S (E_k' W)ᴴ (tall) or (E_k' W) S Pᴴ. Ritz values are accurate to second order in the
+//     subspace error, i.e. to ~ε relative, and both factors are orthonormal to ~ε. The weight outside the
+//     computed values, ‖Θ(c)‖²_F − Σ S², joins the discarded weight. Θ(c) is read, not destroyed.
+tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& sp, const std::vector<double>& n2,
+                   const std::vector<int>& wave1, const std::vector<int>& rest, int64_t chi_max, double cutoff,
+                   double& disc_skipped) {
+  const int ns = sp.nsec;
+  struct Geo {
+    int R, C, ng, mt;
+    bool tall;
+  };
+  std::vector<Geo> g(ns);
+  for (int c = 0; c < ns; ++c) {
+    const int R = sp.sec[c].R, C = sp.sec[c].C;
+    const bool tall = C >= R;
+    g[c] = Geo{R, C, tall ? R : C, tall ? C : R, tall};
+  }
+  auto cost = [&](int c) { return (double)g[c].ng * g[c].ng * ((double)g[c].mt + 3.0 * g[c].ng); };
+  // phase-A scratch for every candidate sector
+  std::vector<size_t> oG(ns, 0), oW(ns, 0), oWs(ns, 0), wsA(ns, 0), hsA(ns, 0);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  std::vector<int> cand(wave1);
+  cand.insert(cand.end(), rest.begin(), rest.end());
+  for (int c : cand) {
+    const int64_t n = g[c].ng;
+    if (cusolverDnXsyevd_bufferSize(X.h[0], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F,
+                                    nullptr, n, CUDA_R_64F, nullptr, CUDA_C_64F, &wsA[c], &hsA[c]) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return fail(TN_ERR_CUDA, "cusolverDnXsyevd_bufferSize failed");
+    oG[c] = take((size_t)n * n * 16);
+    oW[c] = take((size_t)n * 8);
+    oWs[c] = take(wsA[c]);
+  }
+  const size_t oInfo = take((size_t)2 * ns * 4);
+  char* A = nullptr;
+  tn_status st = grow(X.gbuf[0], X.gcap[0], off, &A);
+  if (st != TN_OK) return st;
+  int* infoA = reinterpret_cast<int*>(A + oInfo);
+  int* infoC = infoA + ns;
+  if ((st = cuda_check(cudaMemsetAsync(infoA, 0, 2 * ns * sizeof(int), s), "memset info")) != TN_OK) return st;
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  auto jobA = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
+    const Geo& q = g[c];
+    const auto* Z = reinterpret_cast<const cuDoubleComplex*>(theta[c]);
+    auto* G = reinterpret_cast<cuDoubleComplex*>(A + oG[c]);
+    const cublasStatus_t b =
+        q.tall ? cublasZgemm(X.hb[l], CUBLAS_OP_C, CUBLAS_OP_N, q.R, q.R, q.C, &one, Z, q.C, Z, q.C, &zero, G, q.R)
+               : cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_C, q.C, q.C, q.R, &one, Z, q.C, Z, q.C, &zero, G, q.C);
+    if (b != CUBLAS_STATUS_SUCCESS) return "cuBLAS Gram matrix failed in sector " + std::to_string(c);
+    hbuf.resize(std::max<size_t>(hsA[c], 1));
+    const cusolverStatus_t r =
+        cusolverDnXsyevd(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, q.ng, CUDA_C_64F, G, q.ng,
+                         CUDA_R_64F, A + oW[c], CUDA_C_64F, A + oWs[c], wsA[c], hbuf.data(), hsA[c], infoA + c);
+    return r == CUSOLVER_STATUS_SUCCESS ? std::string() : "cuSOLVER Xsyevd failed in sector " + std::to_string(c);
+  };
+  std::vector<std::vector<double>> w(ns);
+  auto fetch = [&](const std::vector<int>& secs) -> tn_status {
+    std::vector<int> info(ns, 0);
+    for (int c : secs) {
+      w[c].resize(g[c].ng);
+      tn_status r = cuda_check(cudaMemcpyAsync(w[c].data(), A + oW[c], w[c].size() * 8, cudaMemcpyDeviceToHost, s), "D2H w");
+      if (r != TN_OK) return r;
+    }
+    tn_status r = cuda_check(cudaMemcpyAsync(info.data(), infoA, ns * 4, cudaMemcpyDeviceToHost, s), "D2H info");
+    if (r == TN_OK) r = cuda_check(cudaStreamSynchronize(s), "Gram sync");
+    if (r != TN_OK) return r;
+    for (int c : secs)
+      if (info[c] != 0) return fail(TN_ERR_CUDA, "tn_svd_truncate: the eigensolver failed in sector " + std::to_string(c));
+    return TN_OK;
+  };
+  const double eps = std::ldexp(1.0, -53);
+  auto delta = [&](int c) { return 16.0 * g[c].ng * eps * std::max(w[c].back(), 0.0); };
+  // approximate χ-th largest s² over `secs` (−1 if fewer than χ values) and the largest error bound
+  auto kth = [&](const std::vector<int>& secs, double& dmax) {
+    std::vector<double> v;
+    dmax = 0.0;
+    for (int c : secs) {
+      for (double x : w[c]) v.push_back(std::max(x, 0.0));
+      dmax = std::max(dmax, delta(c));
+    }
+    if ((int64_t)v.size() < chi_max) return -1.0;
+    std::nth_element(v.begin(), v.begin() + (chi_max - 1), v.end(), std::greater<double>());
+    return v[chi_max - 1];
+  };
+  const bool prof = getenv("TN_SVD_PROFILE") != nullptr;
+  auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t0 = now();
+  if ((st = run_lanes(X, s, wave1, cost, jobA)) != TN_OK) return st;
+  if ((st = fetch(wave1)) != TN_OK) return st;
+  const double t1 = now();
+  double d1 = 0.0;
+  const double T1 = kth(wave1, d1);
+  std::vector<int> wave2, done(wave1);
+  for (int c : rest) {
+    if (T1 > 0.0 && n2[c] < T1 - d1) {
+      disc_skipped += n2[c];
+      sp.sec[c].k = 0;
+    } else {
+      wave2.push_back(c);
+    }
+  }
+  if ((st = run_lanes(X, s, wave2, cost, jobA)) != TN_OK) return st;
+  if ((st = fetch(wave2)) != TN_OK) return st;
+  done.insert(done.end(), wave2.begin(), wave2.end());
+  const double t2 = now();
+  double dmax = 0.0;
+  const double T2 = kth(done, dmax);
+  const double tau = T2 > 0.0 ? T2 - 2.0 * dmax : -1.0;
+  // phase C: k' per sector and its scratch
+  std::vector<int> kp(ns, 0), waveC;
+  std::vector<size_t> oT(ns), oP(ns), oWm(ns), oS(ns), oEW(ns), oWc(ns), wsC(ns), hsC(ns);
+  off = 0;
+  for (int c : done) {
+    const double lo = std::max(tau, cutoff * cutoff - delta(c));
+    int k = 0;
+    for (int i = g[c].ng - 1; i >= 0 && w[c][i] >= lo; --i) ++k;
+    kp[c] = k;
+    if (k == 0) {
+      disc_skipped += n2[c];
+      sp.sec[c].k = 0;
+      continue;
+    }
+    waveC.push_back(c);
+    const Geo& q = g[c];
+    if (cusolverDnXgesvdp_bufferSize(X.h[0], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, q.mt, k, CUDA_C_64F, nullptr, q.mt,
+                                     CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, q.mt, CUDA_C_64F, nullptr, k, CUDA_C_64F,
+                                     &wsC[c], &hsC[c]) != CUSOLVER_STATUS_SUCCESS)
+      return fail(TN_ERR_CUDA, "cusolverDnXgesvdp_bufferSize failed");
+    oT[c] = take((size_t)q.mt * k * 16);
+    oP[c] = take((size_t)q.mt * k * 16);
+    oWm[c] = take((size_t)k * k * 16);
+    oS[c] = take((size_t)k * 8);
+    oEW[c] = take((size_t)q.ng * k * 16);
+    oWc[c] = take(wsC[c]);
+  }
+  char* Cb = nullptr;
+  if ((st = grow(X.gbuf[1], X.gcap[1], std::max<size_t>(off, 256), &Cb)) != TN_OK) return st;
+  auto jobC = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
+    const Geo& q = g[c];
+    const int k = kp[c];
+    const auto* Z = reinterpret_cast<const cuDoubleComplex*>(theta[c]);
+    const auto* E = reinterpret_cast<const cuDoubleComplex*>(A + oG[c]) + (size_t)(q.ng - k) * q.ng;
+    auto* T = reinterpret_cast<cuDoubleComplex*>(Cb + oT[c]);
+    auto* Wm = reinterpret_cast<cuDoubleComplex*>(Cb + oWm[c]);
+    cublasStatus_t b =
+        q.tall ? cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.C, k, q.R, &one, Z, q.C, E, q.R, &zero, T, q.C)
+               : cublasZgemm(X.hb[l], CUBLAS_OP_C, CUBLAS_OP_N, q.R, k, q.C, &one, Z, q.C, E, q.C, &zero, T, q.R);
+    if (b != CUBLAS_STATUS_SUCCESS) return "cuBLAS Ritz projection failed in sector " + std::to_string(c);
+    hbuf.resize(std::max<size_t>(hsC[c], 1));
+    double herr = 0.0;
+    const cusolverStatus_t r =
+        cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, q.mt, k, CUDA_C_64F, T, q.mt, CUDA_R_64F,
+                          Cb + oS[c], CUDA_C_64F, Cb + oP[c], q.mt, CUDA_C_64F, Wm, k, CUDA_C_64F, Cb + oWc[c], wsC[c],
+                          hbuf.data(), hsC[c], infoC + c, &herr);
+    if (r != CUSOLVER_STATUS_SUCCESS) return "cuSOLVER Ritz SVD failed in sector " + std::to_string(c);
+    b = cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.ng, k, k, &one, E, q.ng, Wm, k, &zero,
+                    reinterpret_cast<cuDoubleComplex*>(Cb + oEW[c]), q.ng);
+    return b == CUBLAS_STATUS_SUCCESS ? std::string() : "cuBLAS Ritz rotation failed in sector " + std::to_string(c);
+  };
+  if ((st = run_lanes(X, s, waveC, cost, jobC)) != TN_OK) return st;
+  std::vector<int> info(ns, 0);
+  std::vector<std::vector<double>> sv(ns);
+  for (int c : waveC) {
+    sv[c].resize(kp[c]);
+    if ((st = cuda_check(cudaMemcpyAsync(sv[c].data(), Cb + oS[c], kp[c] * 8, cudaMemcpyDeviceToHost, s), "D2H S")) != TN_OK)
+      return st;
+  }
+  if ((st = cuda_check(cudaMemcpyAsync(info.data(), infoC, ns * 4, cudaMemcpyDeviceToHost, s), "D2H info")) != TN_OK)
+    return st;
+  if ((st = cuda_check(cudaStreamSynchronize(s), "Ritz sync")) != TN_OK) return st;
+  if (prof) {
+    int64_t sk = 0, sn = 0;
+    int kmax = 0;
+    for (int c : waveC) {
+      sk += kp[c];
+      sn += g[c].ng;
+      kmax = std::max(kmax, kp[c]);
+    }
+    fprintf(stderr, "[svd_gram] gram+eig wave1 %.1f ms (%zu sectors), wave2 %.1f ms (%zu), ritz %.1f ms (%zu sectors, sum k' %lld of %lld, max k' %d)\n",
+            t1 - t0, wave1.size(), t2 - t1, wave2.size(), now() - t2, waveC.size(), (long long)sk, (long long)sn, kmax);
+  }
+  for (int c : waveC) {
+    if (info[c] != 0) return fail(TN_ERR_CUDA, "tn_svd_truncate: the Ritz SVD failed in sector " + std::to_string(c));
+    if (kp[c] < g[c].ng) {  // the weight outside the computed values (none when all n_g were computed)
+      double kept2 = 0.0;
+      for (double x : sv[c]) kept2 += x * x;
+      disc_skipped += std::max(n2[c] - kept2, 0.0);
+    }
+    SvdSector& S = sp.sec[c];
+    const double2* P = reinterpret_cast<const double2*>(Cb + oP[c]);
+    const double2* EW = reinterpret_cast<const double2*>(Cb + oEW[c]);
+    S.ux = g[c].tall ? P : EW;   // C × k', ld C
+    S.vx = g[c].tall ? EW : P;   // R × k', ld R
+    S.s = reinterpret_cast<const double*>(Cb + oS[c]);
+    S.k = kp[c];
+  }
+  return TN_OK;
+}
+
 }  // namespace tn
 
 using namespace tn;
@@ -209,6 +481,8 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
       if (cudaStreamCreateWithFlags(&X.st[i], cudaStreamNonBlocking) != cudaSuccess)
         return fail(TN_ERR_CUDA, "SVD stream create failed");
       cusolverDnSetStream(X.h[i], X.st[i]);
+      if (cublasCreate(&X.hb[i]) != CUBLAS_STATUS_SUCCESS) return fail(TN_ERR_CUDA, "cublasCreate failed");
+      cublasSetStream(X.hb[i], X.st[i]);
     }
     for (auto& e : X.ev)
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(TN_ERR_CUDA, "event");
@@ -220,7 +494,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   }
   const int algo = svd_algo();
   const int ns = p->nsec;
-  // ---- scratch layout: per sector U_x, V_x, S, workspace; then sort buffers ----
+  // ---- scratch layout: per sector U_x, V_x, S, workspace (library SVD paths); then sort buffers ----
   SvdParams sp{};
   sp.nsec = ns;
   std::vector<size_t> o_ux(ns), o_vx(ns), o_s(ns), o_w(ns);
@@ -236,7 +510,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   for (int c = 0; c < ns; ++c) {
     const int R = (int)p->R[c], C = (int)p->C[c], k = std::min(R, C);
     base[c + 1] = base[c] + k;
-    if (k == 0) continue;
+    if (k == 0 || algo == 2) continue;
     size_t wbytes = 0;
     if (algo == 0) {
       if (cusolverDnZgesvdj_bufferSize(X.h[0], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, nullptr, C, nullptr, nullptr, C,
@@ -271,14 +545,9 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const double*)nullptr, (double*)nullptr,
                                             (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(total_max, 1));
   const size_t o_sort = take(sort_bytes);
-  if (off > X.cap) {
-    if (X.buf) cudaFree(X.buf);
-    X.buf = nullptr;
-    X.cap = 0;
-    if (cudaMalloc(&X.buf, off) != cudaSuccess) return fail(TN_ERR_OOM, "tn_svd_truncate: scratch allocation");
-    X.cap = off;
-  }
-  char* B = static_cast<char*>(X.buf);
+  char* B = nullptr;
+  tn_status st = grow(X.buf, X.cap, off, &B);
+  if (st != TN_OK) return st;
   int* d_info = reinterpret_cast<int*>(B + o_info);
   std::vector<int> order;
   for (int c = 0; c < ns; ++c) {
@@ -291,78 +560,43 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     S.col0 = p->col0[c];
     if (k == 0) continue;
     if (!theta[c]) return fail(TN_ERR_DIMENSION, "tn_svd_truncate: NULL Θ(c) for a non-empty sector");
-    S.ux = reinterpret_cast<double2*>(B + o_ux[c]);
-    S.vx = reinterpret_cast<double2*>(B + o_vx[c]);
-    S.s = reinterpret_cast<double*>(B + o_s[c]);
+    if (algo != 2) {
+      S.ux = reinterpret_cast<double2*>(B + o_ux[c]);
+      S.vx = reinterpret_cast<double2*>(B + o_vx[c]);
+      S.s = reinterpret_cast<double*>(B + o_s[c]);
+    }
     order.push_back(c);
   }
-  tn_status st = cuda_check(cudaMemsetAsync(d_info, 0, ns * sizeof(int), s), "memset info");  // empty sectors
+  st = cuda_check(cudaMemsetAsync(d_info, 0, ns * sizeof(int), s), "memset info");  // empty sectors
   if (st != TN_OK) return st;
-  std::vector<std::string> errs(SVD_LANES);
-  // one wave of sector SVDs: largest first, greedy onto the least-loaded lane (cost ~ R·C·min(R, C))
-  auto run_wave = [&](std::vector<int> wave) -> tn_status {
-    if (wave.empty()) return TN_OK;
-    std::sort(wave.begin(), wave.end(), [&](int a, int b) {
-      return (double)p->R[a] * p->C[a] * std::min(p->R[a], p->C[a]) >
-             (double)p->R[b] * p->C[b] * std::min(p->R[b], p->C[b]);
-    });
-    std::vector<std::vector<int>> lane(SVD_LANES);
-    double load[SVD_LANES] = {};
-    for (int c : wave) {
-      const int l = (int)(std::min_element(load, load + SVD_LANES) - load);
-      lane[l].push_back(c);
-      load[l] += (double)p->R[c] * p->C[c] * std::min(p->R[c], p->C[c]);
+  auto cost = [&](int c) { return (double)p->R[c] * p->C[c] * std::min(p->R[c], p->C[c]); };
+  // one library SVD (paths 0/1): X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
+  auto lib_svd = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
+    const SvdSector& S = sp.sec[c];
+    const int R = S.R, C = S.C;
+    cusolverStatus_t r;
+    if (algo == 0) {
+      r = cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, reinterpret_cast<cuDoubleComplex*>(theta[c]), C,
+                            const_cast<double*>(S.s), reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)), C,
+                            reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
+                            reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c, X.params);
+    } else {
+      hbuf.resize(std::max<size_t>(hbytes[c], 1));
+      double herr = 0.0;
+      r = cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, CUDA_C_64F, theta[c], C, CUDA_R_64F,
+                            const_cast<double*>(S.s), CUDA_C_64F, const_cast<double2*>(S.ux), C, CUDA_C_64F,
+                            const_cast<double2*>(S.vx), R, CUDA_C_64F, B + o_w[c], wsz[c], hbuf.data(), hbytes[c],
+                            d_info + c, &herr);
     }
-    tn_status r0 = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
-    if (r0 != TN_OK) return r0;
-    auto work = [&](int l) {
-      if (cudaStreamWaitEvent(X.st[l], X.ev[SVD_LANES], 0) != cudaSuccess) {
-        errs[l] = "stream wait";
-        return;
-      }
-      std::vector<char> hbuf;
-      for (int c : lane[l]) {
-        const SvdSector& S = sp.sec[c];
-        const int R = S.R, C = S.C;
-        cusolverStatus_t r;
-        // X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
-        if (algo == 0) {
-          r = cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, reinterpret_cast<cuDoubleComplex*>(theta[c]),
-                                C, const_cast<double*>(S.s),
-                                reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)), C,
-                                reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
-                                reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c, X.params);
-        } else {
-          hbuf.resize(std::max<size_t>(hbytes[c], 1));
-          double herr = 0.0;
-          r = cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, CUDA_C_64F, theta[c], C,
-                                CUDA_R_64F, const_cast<double*>(S.s), CUDA_C_64F, const_cast<double2*>(S.ux), C,
-                                CUDA_C_64F, const_cast<double2*>(S.vx), R, CUDA_C_64F, B + o_w[c], wsz[c], hbuf.data(),
-                                hbytes[c], d_info + c, &herr);
-        }
-        if (r != CUSOLVER_STATUS_SUCCESS) {
-          errs[l] = "cuSOLVER SVD failed in sector " + std::to_string(c) + " (status " + std::to_string((int)r) + ")";
-          return;
-        }
-      }
-      if (cudaEventRecord(X.ev[l], X.st[l]) != cudaSuccess) errs[l] = "event record";
-    };
-    {
-      std::vector<std::thread> th;
-      for (int l = 1; l < SVD_LANES; ++l) th.emplace_back(work, l);
-      work(0);
-      for (auto& t : th) t.join();
-    }
-    for (int l = 0; l < SVD_LANES; ++l) {
-      if (!errs[l].empty()) return fail(TN_ERR_CUDA, "tn_svd_truncate: " + errs[l]);
-      if ((r0 = cuda_check(cudaStreamWaitEvent(s, X.ev[l], 0), "join SVD lanes")) != TN_OK) return r0;
-    }
-    return TN_OK;
+    return r == CUSOLVER_STATUS_SUCCESS ? std::string()
+                                        : "cuSOLVER SVD failed in sector " + std::to_string(c) + " (status " +
+                                              std::to_string((int)r) + ")";
   };
-  // ---- norm bound: SVD the heaviest sectors first; a sector with ‖Θ(c)‖_F below the χ-th largest singular
-  // value found so far cannot place any value in the global top χ (that threshold only grows), so its SVD
-  // is skipped and its whole weight ‖Θ(c)‖²_F is discarded — the result is identical ----
+  // ---- norm bound: the largest singular value of Θ(c) is ≤ ‖Θ(c)‖_F, so a sector whose norm is below the
+  // χ-th largest value found among the heaviest sectors cannot place any value in the global top χ (that
+  // threshold only grows): its SVD is skipped and its whole weight ‖Θ(c)‖²_F is discarded ----
   double disc_skipped = 0.0;
+  std::vector<double> n2(ns, 0.0);
   {
     ThetaPtrs tp{};
     for (int c = 0; c < ns; ++c) {
@@ -372,13 +606,14 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     double* d_n2 = reinterpret_cast<double*>(B + o_n2);
     if ((st = cuda_check(cudaMemsetAsync(d_n2, 0, ns * sizeof(double), s), "memset norms")) != TN_OK) return st;
     k_sector_norm2<<<dim3(32, ns), 256, 0, s>>>(tp, d_n2);
-    std::vector<double> n2(ns);
     if ((st = cuda_check(cudaMemcpyAsync(n2.data(), d_n2, ns * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H norms")) !=
         TN_OK)
       return st;
     if ((st = cuda_check(cudaStreamSynchronize(s), "norm sync")) != TN_OK) return st;
-    std::sort(order.begin(), order.end(), [&](int a, int b) { return n2[a] > n2[b]; });
-    std::vector<int> wave1, rest;
+  }
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return n2[a] > n2[b]; });
+  std::vector<int> wave1, rest;
+  {
     int64_t have = 0;
     for (int c : order) {
       if (have < 2 * chi_max) {
@@ -388,7 +623,11 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
         rest.push_back(c);
       }
     }
-    if ((st = run_wave(wave1)) != TN_OK) return st;
+  }
+  if (algo == 2) {
+    if ((st = svd_gram(X, s, theta, sp, n2, wave1, rest, chi_max, cutoff, disc_skipped)) != TN_OK) return st;
+  } else {
+    if ((st = run_lanes(X, s, wave1, cost, lib_svd)) != TN_OK) return st;
     std::vector<int> wave2;
     if (!rest.empty()) {
       // the chi_max-th largest value of wave 1 (values of each sector come back descending)
@@ -414,10 +653,10 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
           wave2.push_back(c);
         }
       }
-      if ((st = run_wave(wave2)) != TN_OK) return st;
+      if ((st = run_lanes(X, s, wave2, cost, lib_svd)) != TN_OK) return st;
     }
-    for (int c = 0; c < ns; ++c) base[c + 1] = base[c] + sp.sec[c].k;
   }
+  for (int c = 0; c < ns; ++c) base[c + 1] = base[c] + sp.sec[c].k;
   const int64_t total = base[ns];
   double* kin = reinterpret_cast<double*>(B + o_kin);
   double* kout = reinterpret_cast<double*>(B + o_kout);

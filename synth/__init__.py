@@ -91,6 +91,8 @@ def _lam(rng, kind: str, chi: int) -> np.ndarray:
         v = np.sort(1.0 - rng.random(chi))[::-1].copy()   # values in (0, 1], descending
     elif kind == "geometric":
         v = 0.995 ** np.arange(chi, dtype=np.float64)     # SURVEY.md G12 (no draws)
+    elif kind == "steep":
+        v = 0.97 ** np.arange(chi, dtype=np.float64)      # a wide Schmidt spectrum (no draws)
     elif kind == "flat":
         v = np.ones(chi)
     else:

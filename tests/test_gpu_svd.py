@@ -45,8 +45,13 @@ def _recon(case, res, c):
     return (A * res["lam_new"][a][None, :]) @ B, A, B
 
 
+ALGOS = ["gram", "gesvdp", "gesvdj"]   # TN_SVD_ALGO: Gram eigensolver + Rayleigh–Ritz (default), library SVDs
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("cfg,chi", [(0, 5), (1, 64), (1, 100000), (2, 1024), (2, 300)])
-def test_svd_truncate_parity(tn, cfg, chi):
+def test_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
     case = synth.make_config(cfg)
     got, res = _run(tn, case, chi)
     ref_secs, *_ = oracle_theta(case)
@@ -69,7 +74,34 @@ def test_svd_truncate_parity(tn, cfg, chi):
             assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
 
 
-def test_svd_no_truncation_reconstructs_theta(tn):
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("chi", [40, 250, 100000])
+def test_svd_wide_spectrum(tn, chi, algo, monkeypatch):
+    # λ = 0.97^i on every bond: Θ's singular values span many decades, the regime where an eigen-
+    # decomposition of the Gram matrix alone loses the small kept values (the Ritz step must recover them)
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    case = synth.make_case(6, 7, 300, 280, 320, seed=44, charges="uniform", lam="steep")
+    got, res = _run(tn, case, chi)
+    ref_secs, *_ = oracle_theta(case)
+    ref = osvd.truncate_update(case.N, case.d, case.q_l, case.q_r, ref_secs, case.lam_l, case.lam_r, chi)
+    assert res["chi"] == ref["chi"]
+    assert np.array_equal(res["q_new"], ref["q_new"])
+    smax = max(float(s.max()) for s in ref["svals"] if s.size)
+    assert np.max(np.abs(res["lam_new"] - ref["lam_new"])) <= 1e-12 * smax
+    for c in range(case.N + 1):
+        if ref_secs[c].size == 0:
+            continue
+        rg, A, B = _recon(case, res, c)
+        rr, *_ = _recon(case, ref, c)
+        assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), c
+        if A.shape[1]:
+            assert np.allclose(A.conj().T @ A, np.eye(A.shape[1]), atol=1e-12)
+            assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_svd_no_truncation_reconstructs_theta(tn, algo, monkeypatch):
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
     case = synth.make_config(1)
     got, res = _run(tn, case, 10 ** 6)
     assert res["discarded"] <= 1e-24
