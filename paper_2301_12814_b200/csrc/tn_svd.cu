@@ -46,8 +46,8 @@ struct SvdCtx {  // cuSOLVER handles / streams + a grow-only device scratch, per
   cusolverDnParams_t xparams = nullptr;
   void* buf = nullptr;   // common scratch (library-SVD outputs, ranking buffers)
   size_t cap = 0;
-  void* gbuf[2] = {};    // Gram path: phase A (Gram matrices → eigenvectors), phase C (Ritz SVDs)
-  size_t gcap[2] = {};
+  void* gbuf[3] = {};    // Gram path: phase A (Gram matrices → eigenvectors), phase C (Ritz SVDs), tests
+  size_t gcap[3] = {};
   std::mutex mu;
 };
 SvdCtx& ctx() {
@@ -300,19 +300,27 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   int* infoC = infoA + ns;
   if ((st = cuda_check(cudaMemsetAsync(infoA, 0, 2 * ns * sizeof(int), s), "memset info")) != TN_OK) return st;
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-  auto jobA = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
+  auto gram = [&](int l, int c) -> std::string {
     const Geo& q = g[c];
     const auto* Z = reinterpret_cast<const cuDoubleComplex*>(theta[c]);
     auto* G = reinterpret_cast<cuDoubleComplex*>(A + oG[c]);
     const cublasStatus_t b =
         q.tall ? cublasZgemm(X.hb[l], CUBLAS_OP_C, CUBLAS_OP_N, q.R, q.R, q.C, &one, Z, q.C, Z, q.C, &zero, G, q.R)
                : cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_C, q.C, q.C, q.R, &one, Z, q.C, Z, q.C, &zero, G, q.C);
-    if (b != CUBLAS_STATUS_SUCCESS) return "cuBLAS Gram matrix failed in sector " + std::to_string(c);
+    return b == CUBLAS_STATUS_SUCCESS ? std::string() : "cuBLAS Gram matrix failed in sector " + std::to_string(c);
+  };
+  auto eig = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
+    const Geo& q = g[c];
     hbuf.resize(std::max<size_t>(hsA[c], 1));
     const cusolverStatus_t r =
-        cusolverDnXsyevd(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, q.ng, CUDA_C_64F, G, q.ng,
-                         CUDA_R_64F, A + oW[c], CUDA_C_64F, A + oWs[c], wsA[c], hbuf.data(), hsA[c], infoA + c);
+        cusolverDnXsyevd(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, q.ng, CUDA_C_64F,
+                         A + oG[c], q.ng, CUDA_R_64F, A + oW[c], CUDA_C_64F, A + oWs[c], wsA[c], hbuf.data(), hsA[c],
+                         infoA + c);
     return r == CUSOLVER_STATUS_SUCCESS ? std::string() : "cuSOLVER Xsyevd failed in sector " + std::to_string(c);
+  };
+  auto jobA = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
+    std::string e = gram(l, c);
+    return e.empty() ? eig(l, c, hbuf) : e;
   };
   std::vector<std::vector<double>> w(ns);
   auto fetch = [&](const std::vector<int>& secs) -> tn_status {
@@ -351,14 +359,74 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   const double t1 = now();
   double d1 = 0.0;
   const double T1 = kth(wave1, d1);
-  std::vector<int> wave2, done(wave1);
+  // sectors at least this large get the trace-power test (TN_SVD_TEST_MIN_NG lets tests reach it at small sizes)
+  const int test_min_ng = getenv("TN_SVD_TEST_MIN_NG") ? atoi(getenv("TN_SVD_TEST_MIN_NG")) : 256;
+  std::vector<int> wave2, done(wave1), tested;
   for (int c : rest) {
     if (T1 > 0.0 && n2[c] < T1 - d1) {
       disc_skipped += n2[c];
       sp.sec[c].k = 0;
+    } else if (T1 - d1 > 0.0 && g[c].ng >= test_min_ng) {
+      tested.push_back(c);
     } else {
       wave2.push_back(c);
     }
+  }
+  // Trace-power test for the remaining large sectors: with τ = T1 − d1 ≤ the exact χ-th s², every
+  // eigenvalue λ ≥ τ of G contributes ≥ 1 to tr((G/τ)^16) = ‖(G/τ)^8‖²_F (three ZGEMM squarings), so a
+  // sector with tr < 1/2 has no value that can enter the top χ and is skipped without its eigensolver
+  // (an overflow or NaN fails the test, i.e. the sector is solved).
+  if (!tested.empty()) {
+    const double tau1 = T1 - d1;
+    std::vector<size_t> oH(ns, 0);
+    size_t hoff = 0;
+    for (int c : tested) {
+      oH[c] = hoff;
+      hoff += (((size_t)g[c].ng * g[c].ng * 16 + 255) & ~(size_t)255) * 2;
+    }
+    char* Hb = nullptr;
+    if ((st = grow(X.gbuf[2], X.gcap[2], hoff + 256 * (size_t)ns, &Hb)) != TN_OK) return st;
+    double* d_tr = reinterpret_cast<double*>(Hb + hoff);
+    const cuDoubleComplex inv2 = make_cuDoubleComplex(1.0 / (tau1 * tau1), 0.0);
+    auto jobT = [&](int l, int c, std::vector<char>&) -> std::string {
+      std::string e = gram(l, c);
+      if (!e.empty()) return e;
+      const int n = g[c].ng;
+      const auto* G = reinterpret_cast<const cuDoubleComplex*>(A + oG[c]);
+      auto* H1 = reinterpret_cast<cuDoubleComplex*>(Hb + oH[c]);
+      auto* H2 = reinterpret_cast<cuDoubleComplex*>(Hb + oH[c] + (((size_t)n * n * 16 + 255) & ~(size_t)255));
+      cublasStatus_t b = cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &inv2, G, n, G, n, &zero, H1, n);  // (G/τ)²
+      if (b == CUBLAS_STATUS_SUCCESS)
+        b = cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, H1, n, H1, n, &zero, H2, n);              // ^4
+      if (b == CUBLAS_STATUS_SUCCESS)
+        b = cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, H2, n, H2, n, &zero, H1, n);              // ^8
+      return b == CUBLAS_STATUS_SUCCESS ? std::string() : "cuBLAS trace-power test failed in sector " + std::to_string(c);
+    };
+    if ((st = run_lanes(X, s, tested, cost, jobT)) != TN_OK) return st;
+    ThetaPtrs tp{};
+    for (int c : tested) {
+      tp.p[c] = reinterpret_cast<const double2*>(Hb + oH[c]);
+      tp.n[c] = (int64_t)g[c].ng * g[c].ng;
+    }
+    if ((st = cuda_check(cudaMemsetAsync(d_tr, 0, ns * sizeof(double), s), "memset tr")) != TN_OK) return st;
+    k_sector_norm2<<<dim3(32, ns), 256, 0, s>>>(tp, d_tr);
+    std::vector<double> tr(ns, 0.0);
+    if ((st = cuda_check(cudaMemcpyAsync(tr.data(), d_tr, ns * 8, cudaMemcpyDeviceToHost, s), "D2H tr")) != TN_OK) return st;
+    if ((st = cuda_check(cudaStreamSynchronize(s), "trace-power sync")) != TN_OK) return st;
+    std::vector<int> solve;
+    for (int c : tested) {
+      if (tr[c] < 0.5) {
+        disc_skipped += n2[c];
+        sp.sec[c].k = 0;
+      } else {
+        solve.push_back(c);
+      }
+    }
+    if (prof)
+      for (int c : tested) fprintf(stderr, "[svd_gram]   trace-power test sector %d: tr((G/τ)^16) = %.3g\n", c, tr[c]);
+    if ((st = run_lanes(X, s, solve, cost, eig)) != TN_OK) return st;
+    if ((st = fetch(solve)) != TN_OK) return st;
+    done.insert(done.end(), solve.begin(), solve.end());
   }
   if ((st = run_lanes(X, s, wave2, cost, jobA)) != TN_OK) return st;
   if ((st = fetch(wave2)) != TN_OK) return st;
@@ -439,6 +507,10 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
     }
     fprintf(stderr, "[svd_gram] gram+eig wave1 %.1f ms (%zu sectors), wave2 %.1f ms (%zu), ritz %.1f ms (%zu sectors, sum k' %lld of %lld, max k' %d)\n",
             t1 - t0, wave1.size(), t2 - t1, wave2.size(), now() - t2, waveC.size(), (long long)sk, (long long)sn, kmax);
+    for (int c : done)
+      fprintf(stderr, "[svd_gram]   sector %d: %dx%d n_g %d k' %d  |Θ|²/T² %.1f  wave %d\n", c, g[c].R, g[c].C, g[c].ng,
+              kp[c], T2 > 0 ? n2[c] / T2 : -1.0,
+              std::find(wave1.begin(), wave1.end(), c) != wave1.end() ? 1 : 2);
   }
   for (int c : waveC) {
     if (info[c] != 0) return fail(TN_ERR_CUDA, "tn_svd_truncate: the Ritz SVD failed in sector " + std::to_string(c));

@@ -48,10 +48,13 @@ def _recon(case, res, c):
 ALGOS = ["gram", "gesvdp", "gesvdj"]   # TN_SVD_ALGO: Gram eigensolver + Rayleigh–Ritz (default), library SVDs
 
 
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", ALGOS + ["gram-tested"])
 @pytest.mark.parametrize("cfg,chi", [(0, 5), (1, 64), (1, 100000), (2, 1024), (2, 300)])
 def test_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
-    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    # "gram-tested": the trace-power sector test (normally only for n_g ≥ 256) applied to every candidate
+    monkeypatch.setenv("TN_SVD_ALGO", algo.split("-")[0])
+    if algo == "gram-tested":
+        monkeypatch.setenv("TN_SVD_TEST_MIN_NG", "1")
     case = synth.make_config(cfg)
     got, res = _run(tn, case, chi)
     ref_secs, *_ = oracle_theta(case)
@@ -74,12 +77,14 @@ def test_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
             assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
 
 
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", ALGOS + ["gram-tested"])
 @pytest.mark.parametrize("chi", [40, 250, 100000])
 def test_svd_wide_spectrum(tn, chi, algo, monkeypatch):
     # λ = 0.97^i on every bond: Θ's singular values span many decades, the regime where an eigen-
     # decomposition of the Gram matrix alone loses the small kept values (the Ritz step must recover them)
-    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    monkeypatch.setenv("TN_SVD_ALGO", algo.split("-")[0])
+    if algo == "gram-tested":
+        monkeypatch.setenv("TN_SVD_TEST_MIN_NG", "1")
     case = synth.make_case(6, 7, 300, 280, 320, seed=44, charges="uniform", lam="steep")
     got, res = _run(tn, case, chi)
     ref_secs, *_ = oracle_theta(case)
