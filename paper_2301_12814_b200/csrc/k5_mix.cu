@@ -23,15 +23,22 @@
 //    one row α is swept across consecutive c_r blocks, 2.8–3.5 TB/s when tiles are block-major,
 //    whatever the per-instruction shape: tools/probe_mix_bw.cu, profiles/r01_probe_mix_bw.jsonl).
 //  * P_{c_c} of an empty center segment is zero and never read.
+//  * Register classes: the warp loop's registers grow with ⌈L/8⌉, and one kernel sized for the largest L
+//    (128 registers at L = 32) capped every tile at 16 warps per SM. Tiles are therefore issued as up to
+//    four launches by L (≤ 8: 56 registers, 8 CTAs/SM; ≤ 16: 72, 7 CTAs/SM; ≤ 32: 128; larger), each
+//    keeping the band-major order: config 3 0.78 → 0.72 ms, config 4 6.05 → 4.30 ms.
 #include "k5_mix.cuh"
 
 namespace tn {
 
 constexpr int MIX_THREADS = 128;
 constexpr int MIX_WARPS = MIX_THREADS / 32;
+#ifndef K5_SMALL_MINB
+#define K5_SMALL_MINB 7   // CTAs per SM for the L ≤ 16 instantiations (≤ 72 registers, no spills)
+#endif
 
 template <int NTMAX>
-__global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
+__global__ void __launch_bounds__(MIX_THREADS, (NTMAX == 1 ? 8 : NTMAX == 2 ? K5_SMALL_MINB : NTMAX <= 4 ? 4 : 2))
     k5_mix(const SectorParams sp, const MixTile* __restrict__ tiles, const int32_t* __restrict__ perm_l,
            const int32_t* __restrict__ perm_r, const double* __restrict__ ll, const double* __restrict__ lr,
            const double2* __restrict__ U, int us_elems) {
@@ -64,11 +71,12 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX <= 4 ? 4 : 2))
 // staging is amortised), tiles issued band-major (row band, then c_r): concurrently running CTAs cover
 // the same rows across consecutive c_r blocks, i.e. the sector rows are swept contiguously
 // (tools/probe_mix_bw.cu: 5.2–5.4 TB/s row-major vs 2.8–3.5 TB/s block-major for a pure copy).
-void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out) {
+void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out) {
   out.clear();
+  std::vector<MixTile> mid, big, huge;  // L ≤ 8 → out, ≤ 16 → mid, ≤ 32 → big, > 32: one launch per register class
   const auto& ol = p->off[0];
   const auto& orr = p->off[2];
-  constexpr int BAND = 4;
+  constexpr int BAND = 4;  // 2 / 8 / 16 measured: 0.714 / 0.763 / 0.779 ms at config 3, 4.34 / 4.31 / 4.28 at config 4
   for (int cl = 0; cl <= p->N; ++cl) {
     const int64_t a0 = std::max<int64_t>(ol[cl], p->r0), a1 = std::min<int64_t>(ol[cl + 1], p->r1);
     for (int64_t band = a0, rows = 0; band < a1; band += rows) {
@@ -90,20 +98,30 @@ void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out) {
           t.ngr = (int32_t)ngr;
           t.pl0 = (int32_t)band;
           t.pr0 = (int32_t)orr[cr];
-          out.push_back(t);
+          const int L = std::min(cl, cr + p->d - 1) - std::max(cr, cl - p->d + 1) + 1;
+          (L <= 8 ? out : L <= 16 ? mid : L <= 32 ? big : huge).push_back(t);
         }
       }
     }
   }
+  p->nmix_cls[0] = (int64_t)out.size();
+  p->nmix_cls[1] = (int64_t)mid.size();
+  p->nmix_cls[2] = (int64_t)big.size();
+  out.insert(out.end(), mid.begin(), mid.end());
+  out.insert(out.end(), big.begin(), big.end());
+  out.insert(out.end(), huge.begin(), huge.end());
 }
 
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s) {
   if (p->nmix == 0) return cudaSuccess;
-  const unsigned grid = (unsigned)p->nmix;
-  const int L = p->max_mix;
-  const int NT = (L + 7) >> 3;
-  const int smax = mix_us_elems(L);
+  // one launch per register class: L ≤ 8 (56 registers → 8 CTAs per SM), L ≤ 16 (72 → 7), L ≤ 32 (128 → 4),
+  // the rest (NT 6/8 instantiations)
+  auto one = [&](const MixTile* tiles, int64_t n, int L) -> cudaError_t {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)n;
+    const int NT = (L + 7) >> 3;
+    const int smax = mix_us_elems(L);
 #define TN_MIX_LAUNCH(M)                                                                                       \
   do {                                                                                                         \
     const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * sizeof(SecRef);     \
@@ -111,20 +129,28 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
       cudaError_t e = cudaFuncSetAttribute(k5_mix<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
       if (e != cudaSuccess) return e;                                                                          \
     }                                                                                                          \
-    k5_mix<M><<<grid, MIX_THREADS, smem, s>>>(sp, p->d_mix, p->d_perm[0], p->d_perm[2], ll, lr, U, smax);      \
+    k5_mix<M><<<grid, MIX_THREADS, smem, s>>>(sp, tiles, p->d_perm[0], p->d_perm[2], ll, lr, U, smax);         \
   } while (0)
-  if (NT <= 1)
-    TN_MIX_LAUNCH(1);
-  else if (NT <= 2)
-    TN_MIX_LAUNCH(2);
-  else if (NT <= 4)
-    TN_MIX_LAUNCH(4);
-  else if (NT <= 6)
-    TN_MIX_LAUNCH(6);
-  else
-    TN_MIX_LAUNCH(8);
+    if (NT <= 1)
+      TN_MIX_LAUNCH(1);
+    else if (NT <= 2)
+      TN_MIX_LAUNCH(2);
+    else if (NT <= 4)
+      TN_MIX_LAUNCH(4);
+    else if (NT <= 6)
+      TN_MIX_LAUNCH(6);
+    else
+      TN_MIX_LAUNCH(8);
 #undef TN_MIX_LAUNCH
-  return cudaGetLastError();
+    return cudaGetLastError();
+  };
+  const int L = p->max_mix;
+  const int64_t n0 = p->nmix_cls[0], n1 = p->nmix_cls[1], n2 = p->nmix_cls[2];
+  cudaError_t e = one(p->d_mix, n0, std::min(L, 8));
+  if (e == cudaSuccess) e = one(p->d_mix + n0, n1, std::min(L, 16));
+  if (e == cudaSuccess) e = one(p->d_mix + n0 + n1, n2, std::min(L, 32));
+  if (e != cudaSuccess) return e;
+  return one(p->d_mix + n0 + n1 + n2, p->nmix - n0 - n1 - n2, L);
 }
 
 }  // namespace tn

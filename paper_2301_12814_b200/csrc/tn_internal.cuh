@@ -129,6 +129,7 @@ struct tn_plan {
   int64_t ntiles = 0;
   tn::MixTile* d_mix = nullptr;
   int64_t nmix = 0;                            // K5 tiles
+  int64_t nmix_cls[3] = {0, 0, 0};             // of which the first [0] have L ≤ 8, the next [1] L ≤ 16, [2] L ≤ 32
   bool fused = false;                          // K4 + K5 in one kernel (k45_fused.cu)
   int64_t nbands = 0;                          // K45_BAND-row bands of this rank's rows
   std::vector<int32_t> h_band_need;            // K4 tiles touching each band
@@ -223,7 +224,7 @@ cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* l
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s);
-void build_mix_tiles(const tn_plan* p, std::vector<MixTile>& out);
+void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out);
 tn_status build_pair_tables(tn_plan* p);
 tn_status build_literal(tn_plan* p);
 cudaError_t launch_literal(const tn_plan* p, const SectorParams& sp, const double2* gk, const double* lk,
