@@ -113,7 +113,7 @@ void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out) {
 }
 
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                       const double2* U, cudaStream_t s) {
+                       const double2* U, cudaStream_t s, int first_class) {
   if (p->nmix == 0) return cudaSuccess;
   // one launch per register class: L ≤ 8 (56 registers → 8 CTAs per SM), L ≤ 16 (72 → 7), L ≤ 32 (128 → 4),
   // the rest (NT 6/8 instantiations)
@@ -146,9 +146,10 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
   };
   const int L = p->max_mix;
   const int64_t n0 = p->nmix_cls[0], n1 = p->nmix_cls[1], n2 = p->nmix_cls[2];
-  cudaError_t e = one(p->d_mix, n0, std::min(L, 8));
-  if (e == cudaSuccess) e = one(p->d_mix + n0, n1, std::min(L, 16));
-  if (e == cudaSuccess) e = one(p->d_mix + n0 + n1, n2, std::min(L, 32));
+  cudaError_t e = cudaSuccess;
+  if (first_class <= 0) e = one(p->d_mix, n0, std::min(L, 8));
+  if (e == cudaSuccess && first_class <= 1) e = one(p->d_mix + n0, n1, std::min(L, 16));
+  if (e == cudaSuccess && first_class <= 2) e = one(p->d_mix + n0 + n1, n2, std::min(L, 32));
   if (e != cudaSuccess) return e;
   return one(p->d_mix + n0 + n1 + n2, p->nmix - n0 - n1 - n2, L);
 }

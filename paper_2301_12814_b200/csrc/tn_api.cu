@@ -516,11 +516,18 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     std::vector<MixTile>& mix = p->h_mix;
     build_mix_tiles(p, mix);
     p->nmix = (int64_t)mix.size();
+    std::vector<MixItem>& items = p->h_items;
+    build_mix_items(p, items);
+    {
+      const char* env = getenv("TN_K5T");
+      p->k5t = env && env[0] == '1' && !items.empty();
+    }
     if (!p->groups.empty() || !mix.empty()) {
       Carver cw;
       const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
       const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
       const size_t o_m = cw.take<MixTile>((int64_t)mix.size());
+      const size_t o_i = cw.take<MixItem>((int64_t)items.size());
       const size_t o_bn = cw.take<int32_t>(p->nbands);
       const size_t o_bd = cw.take<int32_t>(p->nbands);
       const size_t o_a = cw.take<double2>(p->a_elems);
@@ -531,6 +538,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
       p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
       p->d_mix = reinterpret_cast<MixTile*>(base + o_m);
+      p->d_items = reinterpret_cast<MixItem*>(base + o_i);
       p->d_band_need = reinterpret_cast<int32_t*>(base + o_bn);
       p->d_band_done = reinterpret_cast<int32_t*>(base + o_bd);
       if (p->nbands)
@@ -547,6 +555,9 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       if (!mix.empty())
         TN_TRY(cudaMemcpyAsync(p->d_mix, mix.data(), mix.size() * sizeof(MixTile), cudaMemcpyHostToDevice,
                                p->plan_stream), "H2D mix tiles");
+      if (!items.empty())
+        TN_TRY(cudaMemcpyAsync(p->d_items, items.data(), items.size() * sizeof(MixItem), cudaMemcpyHostToDevice,
+                               p->plan_stream), "H2D mix items");
       // no host sync: tn_theta_exec's stream waits for ev_ready (the host vectors stay alive in the plan)
       p->ws_bytes = (int64_t)cw.off;
     }
@@ -838,7 +849,13 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
     st = cuda_check(emu ? launch_oz_contract(p, sp, s) : launch_contract(p, sp, s), "K4 launch");
     if (st != TN_OK) return st;
     if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
-    st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
+    if (p->k5t) {  // K5T (TMA runs) for the L ≤ 32 blocks, k5_mix for the rest
+      st = cuda_check(launch_mix_tma(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5T launch");
+      if (st == TN_OK)
+        st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, 3), "K5 launch");
+    } else {
+      st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
+    }
     if (st != TN_OK) return st;
   }
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");

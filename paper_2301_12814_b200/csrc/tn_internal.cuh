@@ -65,6 +65,13 @@ struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive c
   int32_t pl0, pr0;         // sorted positions of the block's first (local) row / first column
 };
 
+struct MixItem {            // K5T work unit: nrows rows × w columns of one (c_l, c_r) block, all its L sectors
+  int32_t cl, cr;
+  int32_t pl, nrows;        // sorted left position of the first row; rows
+  int32_t pc, w;            // sorted right position of the first column; columns
+  int32_t stride, pad;      // shared-memory run stride (complex elements)
+};
+
 constexpr int MAXC = TN_MAX_N + 1;
 
 // ---------------------------------------------------------------------------------------------
@@ -166,6 +173,10 @@ struct tn_plan {
   cudaEvent_t ev_ready = nullptr;
   std::vector<tn::TileDesc> h_tiles;           // host sources of the async uploads (kept alive)
   std::vector<tn::MixTile> h_mix;
+  std::vector<tn::MixItem> h_items;            // K5T items (L ≤ 32 blocks), classes L ≤ 8 / 16 / 32
+  tn::MixItem* d_items = nullptr;
+  int64_t nitem_cls[3] = {0, 0, 0};
+  bool k5t = false;                            // U-mix by K5T (TMA runs) for the L ≤ 32 blocks
   std::vector<tn::OzTile> h_oz_tiles;
   mutable bool rec_k1 = false, rec_k2 = false, rec_exec = false;
   mutable cudaStream_t last_stream = nullptr;  // stream of the last exec (pool release fence)
@@ -223,8 +234,11 @@ cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* l
                             cudaStream_t s);
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                       const double2* U, cudaStream_t s);
+                       const double2* U, cudaStream_t s, int first_class = 0);
 void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out);
+void build_mix_items(tn_plan* p, std::vector<MixItem>& out);
+cudaError_t launch_mix_tma(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
+                           const double2* U, cudaStream_t s);
 tn_status build_pair_tables(tn_plan* p);
 tn_status build_literal(tn_plan* p);
 cudaError_t launch_literal(const tn_plan* p, const SectorParams& sp, const double2* gk, const double* lk,
