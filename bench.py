@@ -509,15 +509,17 @@ def run_layer(args, rank, world, local_rank):
     have the shape of BASELINE.json config `--config` (N, d, χ, Gaussian charges, 0.995^i λ): each gate is
     tn_theta_plan + U + tn_theta_exec + tn_svd_truncate, the next gate consuming the previous one's output.
     Γ is drawn on the device (same distribution, δ-masked). Reports gates/s (host wall clock: the SVD step
-    synchronises once per gate to learn the kept bond dimension)."""
+    synchronises once per gate to learn the kept bond dimension). Under torchrun every rank builds the same
+    replica and the gates of each layer are dealt to the ranks (mps.MPS.apply_layer(group=…)),
+    results broadcast over NCCL; the time is the max over ranks."""
     import numpy as np
     import torch
 
     import synth
     from paper_2301_12814_b200.mps import MPS
 
-    if rank != 0:
-        return
+    import torch.distributed as dist
+    group = dist.group.WORLD if world > 1 else None
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = synth.CONFIGS[args.config]
@@ -548,18 +550,27 @@ def run_layer(args, rank, world, local_rank):
     th = rng.uniform(0, math.pi / 2, M)
     ph = rng.uniform(0, 2 * math.pi, M)
     torch.cuda.synchronize()
+    if group is not None:
+        dist.barrier()
     t0 = time.perf_counter()
-    disc = mps.apply_layer(0, th, ph, chi_max) + mps.apply_layer(1, th, ph, chi_max)
+    disc = mps.apply_layer(0, th, ph, chi_max, group=group) + mps.apply_layer(1, th, ph, chi_max, group=group)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if group is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        if rank != 0:
+            return
     ngates = len(disc)
     line = {"metric": "brick-wall TEBD gates/s (Θ + per-sector SVD + truncation per gate)",
-            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": 1, "steps": ngates, "warmup": 0,
+            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": world, "steps": ngates, "warmup": 0,
             "ms_per_step": round(dt / ngates * 1e3, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-drawn Γ, config-shaped bonds)",
             "config": {"workload": f"{M}-site MPS, two brick-wall layers, inner bonds of BASELINE.json config "
                                    f"{args.config} (N={N}, d={d}, chi={chi}), chi_max={chi_max}",
-                       "timing": "host wall clock around whole layers (tn_svd_truncate synchronises per gate)"},
+                       "timing": "host wall clock around whole layers (tn_svd_truncate synchronises per gate), max over ranks",
+                       "parallelism": f"layer-parallel over {world} GPU(s): gates dealt by LPT, results broadcast (NCCL)"},
             "bond_dims_after": [int(x.numel()) for x in mps.lam], "discarded": [float(x) for x in disc]}
     print(json.dumps(line), flush=True)
 

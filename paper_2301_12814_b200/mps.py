@@ -7,8 +7,13 @@ site k carries Γ^{[k]} [χ_k × χ_{k+1}] (complex128, rows/columns in the bond
 carries λ (float64) and its charges (int32, photons to the right); bond 0 is one bond of charge N,
 bond M one bond of charge 0. A gate on sites (k, k+1) uses bonds k, k+1, k+2 as the left, centre and
 right bonds of Eq. S5 and replaces Γ^{[k]}, λ^{[k+1]}, q^{[k+1]}, Γ^{[k+1]} (oracle: oracle/layer.py).
-Gates of one layer act on disjoint site pairs ("beam splitter updates within a layer are
-parallel"); here they run one after another on the current device.
+
+Layer parallelism ("beam splitter updates within a layer are parallel"; PAPER.md:96-103
+first-level parallelism): with a torch.distributed process group, every rank holds a replica of the MPS,
+the gates of a layer (disjoint site pairs, so independent) are dealt to ranks by longest-processing-time
+on their Θ flop estimate (χ_k·χ_{k+1}·χ_{k+2}, identical on every rank), each rank runs its own gates
+on its GPU, and the owner of each gate broadcasts the four updated tensors (NCCL over NVLink; ~1 ms
+per config-3 Γ at 900 GB/s against ~0.35 s of SVD per gate), so every replica ends the layer identical.
 """
 from __future__ import annotations
 
@@ -18,16 +23,34 @@ import torch
 from . import Plan, build_bs_unitary, svd_truncate, theta_exec
 
 
+def layer_owners(costs, world: int):
+    """Longest-processing-time assignment of independent gates to `world` ranks: gates in decreasing
+    cost (ties: lower gate index first) each go to the currently least-loaded rank (ties: lower rank).
+    Deterministic, so every rank computes the same table without communication."""
+    order = sorted(range(len(costs)), key=lambda g: (-costs[g], g))
+    load = [0.0] * world
+    owner = [0] * len(costs)
+    for g in order:
+        r = min(range(world), key=lambda x: (load[x], x))
+        owner[g] = r
+        load[r] += costs[g]
+    return owner
+
+
 class MPS:
     def __init__(self, N: int, d: int, q, gam, lam, device="cuda"):
         dev = torch.device(device)
         as_t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
             dev, dt).contiguous()
         self.N, self.d = int(N), int(d)
+        self.device = dev
         self.q = [as_t(x, torch.int32) for x in q]
         self.gam = [as_t(x, torch.complex128) for x in gam]
         self.lam = [as_t(x, torch.float64) for x in lam]
         self.M = len(self.gam)
+        # test hook only: host-logic tests of the layer exchange (gloo, CPU) replace the gate by the CPU
+        # oracle's; the product path always runs the C ABI below and raises if the library is missing
+        self._gate_impl = None
         if len(self.q) != self.M + 1 or len(self.lam) != self.M + 1:
             raise ValueError("an MPS of M sites needs M+1 bonds of charges and λ")
 
@@ -43,6 +66,8 @@ class MPS:
         """One TEBD update of sites (k, k+1); returns the discarded weight Σ dropped s²."""
         if not 0 <= k < self.M - 1:
             raise ValueError("gate sites out of range")
+        if self._gate_impl is not None:
+            return self._gate_impl(self, k, theta, phi, chi_max, cutoff)
         plan = Plan(self.d, self.N, self.q[k], self.q[k + 1], self.q[k + 2])
         if contraction is not None:
             plan.set_contraction(*contraction)
@@ -56,7 +81,60 @@ class MPS:
         plan.destroy()
         return res["discarded"]
 
-    def apply_layer(self, parity: int, thetas, phis, chi_max: int, cutoff: float = 1e-14, contraction=None):
-        """Gates on (k, k+1) for k = parity, parity+2, … < M−1; returns their discarded weights."""
-        return [self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction)
-                for g, k in enumerate(range(parity, self.M - 1, 2))]
+    def gate_cost(self, k: int) -> float:
+        """Θ-build flop estimate of the gate on (k, k+1) used to balance a layer: χ_k·χ_{k+1}·χ_{k+2}."""
+        return float(self.q[k].numel()) * float(self.q[k + 1].numel()) * float(self.q[k + 2].numel())
+
+    def apply_layer(self, parity: int, thetas, phis, chi_max: int, cutoff: float = 1e-14, contraction=None,
+                    group=None):
+        """Gates on (k, k+1) for k = parity, parity+2, … < M−1; returns their discarded weights.
+
+        With `group` (a torch.distributed process group of size > 1) the gates are spread over its ranks
+        (layer_owners) and the results broadcast, leaving every rank's replica identical."""
+        ks = list(range(parity, self.M - 1, 2))
+        world = 1
+        if group is not None:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+        if world == 1:
+            return [self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction) for g, k in enumerate(ks)]
+        import torch.distributed as dist
+        me = dist.get_rank(group)
+        owner = layer_owners([self.gate_cost(k) for k in ks], world)
+        disc = torch.zeros(len(ks), dtype=torch.float64, device=self.device)
+        for g, k in enumerate(ks):
+            if owner[g] == me:
+                disc[g] = float(self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction))
+        for g, k in enumerate(ks):   # every rank walks the gates in the same order
+            self._bcast_gate(k, owner[g], owner[g] == me, group)
+        dist.all_reduce(disc, group=group)   # each entry has exactly one non-zero contributor
+        return [float(x) for x in disc.cpu()]
+
+    def _bcast_gate(self, k: int, src: int, mine: bool, group):
+        """Broadcast the tensors gate (k, k+1) replaced — q^{[k+1]}, λ^{[k+1]}, Γ^{[k]}, Γ^{[k+1]} — from
+        group rank `src`."""
+        import torch.distributed as dist
+        dev = self.device
+        bc = lambda t: dist.broadcast(t, group=group, group_src=src)
+        if mine:  # the owner's freshly written tensors are sent as they are (contiguous)
+            self.gam[k], self.gam[k + 1] = self.gam[k].contiguous(), self.gam[k + 1].contiguous()
+            self.lam[k + 1] = self.lam[k + 1].contiguous()
+        n = torch.tensor([self.q[k + 1].numel() if mine else 0], dtype=torch.int64, device=dev)
+        bc(n)
+        chi = int(n.item())
+        chi_l, chi_r = self.q[k].numel(), self.q[k + 2].numel()
+        if not mine:
+            self.q[k + 1] = torch.empty(chi, dtype=torch.int32, device=dev)
+            self.lam[k + 1] = torch.empty(chi, dtype=torch.float64, device=dev)
+            self.gam[k] = torch.empty((chi_l, chi), dtype=torch.complex128, device=dev)
+            self.gam[k + 1] = torch.empty((chi, chi_r), dtype=torch.complex128, device=dev)
+        if chi == 0:
+            return
+        q64 = self.q[k + 1].to(torch.int64)   # int32 broadcast is not available on every backend
+        bc(q64)
+        bc(self.lam[k + 1])
+        for t in (self.gam[k], self.gam[k + 1]):
+            if t.numel():
+                bc(torch.view_as_real(t))
+        if not mine:
+            self.q[k + 1] = q64.to(torch.int32)
