@@ -16,7 +16,8 @@ Every function is a plain, slow, obviously-correct transcription of PAPER.md (Su
                          conserved charges) by the literal loop over three charge PAIRS (oracle/theta2.py)
   * `sort_pair_bonds`, `pair_sector_rows/cols`, `flop_counts2` — its tables and useful work
   * `svd.truncate_update` — per-sector SVD (numpy) + global top-χ
-                         + the new canonical factors Γ^{[k]}, λ^{[k]}, Γ^{[k+1]} (oracle/svd.py)
+                         + the new canonical factors Γ^{[k]}, λ^{[k]}, Γ^{[k+1]} (oracle/svd.py);
+                         `svd.truncate_update2` the same step for MPO pair-charge sectors
 
 Pins (tests/test_oracle_pins.py, `-m "not gpu"`): dense δ-tensor brute force (tiny inputs), scipy
 expm of the block generator, HOM dip, θ=0 identity, θ=π/2 swap closed form, Wigner-d (sympy),
@@ -26,7 +27,10 @@ factorisation Θ2(c1,c2)[(α,α'),(β,β')] = Θ(c1)[α,β]·conj(Θ(c2)[α',β'
 oracle, a dense brute force with the doubled gate built from scipy expm and explicit δ tensors per
 species, identity gate == two-site product, and Σ‖Θ2‖² invariance; for the SVD step
 (tests/test_oracle_svd_pins.py): SPEC.md's worked example, known spectra, Eckart–Young on the
-block-diagonal Θ, exact reconstruction without truncation, orthonormal factors, the tie-break rule.
+block-diagonal Θ, exact reconstruction without truncation, orthonormal factors, the tie-break rule;
+for the pair step: the Kronecker closed form on a vectorized pure state (singular values = products
+s_i(c1)·s_j(c2)), the reduction to the single-charge step when the second species is absent, and exact
+reconstruction of Θ2 without truncation.
 No function here is "parity unpinned".
 """
 from .theta import (sort_bonds, bs_unitary_block, packed_u, packed_u_offsets, theta_sectors,

@@ -50,35 +50,63 @@ def global_top_chi(svals, chi_max: int, cutoff: float = 1e-14):
     return kept, disc
 
 
-def truncate_update(N, d, q_l, q_r, sectors, lam_l, lam_r, chi_max, cutoff=1e-14):
-    """The whole step on host. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
-    [chi × χ_r], kept, discarded, svals)."""
-    perm_l, off_l = sort_bonds(q_l, N)
-    perm_r, off_r = sort_bonds(q_r, N)
+def truncate_update_rows(sectors, rows, cols, chi_l, chi_r, lam_l, lam_r, chi_max, cutoff=1e-14):
+    """The whole step on host for sectors given with their row / column bond lists: `rows[c]`, `cols[c]`
+    are the CALLER indices of Θ(c)'s rows / columns (sector c = its position in `sectors`, which is the
+    charge order of the ranking). Returns dict(chi, q_new (sector index per new bond), lam_new,
+    gamma_k_new [χ_l × chi], gamma_k1_new [chi × χ_r], kept, discarded, svals)."""
     svd = sector_svds(sectors)
     kept, disc = global_top_chi([s for _, s, _ in svd], chi_max, cutoff)
     chi = sum(kept)
-    gk = np.zeros((len(q_l), chi), dtype=np.complex128)
-    gk1 = np.zeros((chi, len(q_r)), dtype=np.complex128)
+    gk = np.zeros((chi_l, chi), dtype=np.complex128)
+    gk1 = np.zeros((chi, chi_r), dtype=np.complex128)
     q_new = np.zeros(chi, dtype=np.int32)
     lam_new = np.zeros(chi)
     a = 0
-    for c in range(N + 1):
+    for c in range(len(sectors)):
         k = kept[c]
         if k == 0:
             continue
         U, s, Vh = svd[c]
-        (r0, r1), (k0, k1) = sector_ranges(off_l, off_r, N, d, c)
-        rows = perm_l[r0:r1]                    # caller indices of Θ(c)'s rows
-        cols = perm_r[k0:k1]
-        ll = np.asarray(lam_l)[rows]
-        lr = np.asarray(lam_r)[cols]
+        ll = np.asarray(lam_l)[rows[c]]
+        lr = np.asarray(lam_r)[cols[c]]
         inv_l = np.divide(1.0, ll, out=np.zeros_like(ll), where=ll != 0)
         inv_r = np.divide(1.0, lr, out=np.zeros_like(lr), where=lr != 0)
-        gk[rows, a:a + k] = U[:, :k] * inv_l[:, None]
-        gk1[a:a + k][:, cols] = Vh[:k, :] * inv_r[None, :]
+        gk[rows[c], a:a + k] = U[:, :k] * inv_l[:, None]
+        gk1[a:a + k][:, cols[c]] = Vh[:k, :] * inv_r[None, :]
         q_new[a:a + k] = c
         lam_new[a:a + k] = s[:k]
         a += k
     return dict(chi=chi, q_new=q_new, lam_new=lam_new, gamma_k_new=gk, gamma_k1_new=gk1, kept=kept,
                 discarded=disc, svals=[s for _, s, _ in svd])
+
+
+def truncate_update(N, d, q_l, q_r, sectors, lam_l, lam_r, chi_max, cutoff=1e-14):
+    """Single-charge plans: Θ(c) rows are the sorted left bonds with c_l − c ∈ [0, d−1], columns the sorted
+    right bonds with c − c_r ∈ [0, d−1] (oracle.theta.sector_ranges)."""
+    perm_l, off_l = sort_bonds(q_l, N)
+    perm_r, off_r = sort_bonds(q_r, N)
+    rows, cols = [], []
+    for c in range(N + 1):
+        (r0, r1), (k0, k1) = sector_ranges(off_l, off_r, N, d, c)
+        rows.append(perm_l[r0:r1])
+        cols.append(perm_r[k0:k1])
+    return truncate_update_rows(sectors, rows, cols, len(q_l), len(q_r), lam_l, lam_r, chi_max, cutoff)
+
+
+def truncate_update2(N, d, q1_l, q2_l, q1_r, q2_r, sectors2, lam_l, lam_r, chi_max, cutoff=1e-14):
+    """MPO (pair-charge) plans: sector (c1, c2) has index c1·(N+1) + c2 — the ranking's
+    charge order is the lexicographic pair order — and its rows / columns are the admissible
+    sorted bonds of oracle.theta2 (l − c ∈ [0, d−1]², c − r ∈ [0, d−1]²). `sectors2[(c1, c2)]` as returned by
+    oracle.theta2_sectors. Adds q1_new, q2_new (the kept values' charge pair)."""
+    from .theta2 import pair_sector_cols, pair_sector_rows, sort_pair_bonds
+    pl, pr = sort_pair_bonds(q1_l, q2_l), sort_pair_bonds(q1_r, q2_r)
+    secs, rows, cols = [], [], []
+    for c1 in range(N + 1):
+        for c2 in range(N + 1):
+            secs.append(sectors2[(c1, c2)])
+            rows.append(pl[pair_sector_rows(np.asarray(q1_l)[pl], np.asarray(q2_l)[pl], d, c1, c2)])
+            cols.append(pr[pair_sector_cols(np.asarray(q1_r)[pr], np.asarray(q2_r)[pr], d, c1, c2)])
+    res = truncate_update_rows(secs, rows, cols, len(q1_l), len(q1_r), lam_l, lam_r, chi_max, cutoff)
+    res["q1_new"], res["q2_new"] = np.divmod(res["q_new"], N + 1)
+    return res

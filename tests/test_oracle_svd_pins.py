@@ -78,3 +78,82 @@ def test_no_truncation_is_exact():
         if secs[c].size:
             rec, _ = _reconstruct(case, res, c)
             assert np.linalg.norm(secs[c] - rec) <= 1e-12 * np.linalg.norm(secs[c])
+
+
+# ------------------------------------------------------------------ MPO (pair-charge) truncation
+def _theta2(c):
+    return oracle.theta2_sectors(c.N, c.d, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r, c.gamma_k, c.lam_k,
+                                 c.gamma_k1, c.lam_l, c.lam_r, c.theta, c.phi)[0]
+
+
+@pytest.mark.parametrize("chi", [7, 40, 10 ** 6])
+def test_pair_truncation_kronecker_closed_form(chi):
+    # vectorized pure state: Θ2(c1,c2) = Θ(c1) ⊗ conj(Θ(c2)) up to row/column order, so its singular values
+    # are exactly the products s_i(c1)·s_j(c2) (SVD of a Kronecker product); the kept λ are the top-χ
+    # products, and the kept count of every unordered pair {c1, c2} is fixed by them (the ordered split of
+    # an exact tie between (c1,c2) and (c2,c1) is decided by rounding, so only the sum is compared)
+    base = synth.make_case(3, 4, 9, 8, 10, seed=12, charges="uniform", lam="random")
+    vec = synth.vectorize_pure(base)
+    single = oracle.theta_sectors(base.N, base.d, base.q_l, base.q_c, base.q_r, base.gamma_k, base.lam_k,
+                                  base.gamma_k1, base.lam_l, base.lam_r, base.theta, base.phi)[0]
+    sv = [np.linalg.svd(t, compute_uv=False) if t.size else np.zeros(0) for t in single]
+    prods = sorted(((a * b, c1, c2) for c1 in range(base.N + 1) for c2 in range(base.N + 1)
+                    for a in sv[c1] for b in sv[c2] if a * b > 1e-14), key=lambda x: -x[0])
+    top = prods[:chi]
+    res = osvd.truncate_update2(vec.N, vec.d, vec.q1_l, vec.q2_l, vec.q1_r, vec.q2_r, _theta2(vec), vec.lam_l,
+                                vec.lam_r, chi)
+    assert res["chi"] == len(top)
+    smax = top[0][0]
+    assert np.max(np.abs(np.sort(res["lam_new"])[::-1] - np.array([t[0] for t in top]))) <= 1e-13 * smax
+    want, got = {}, {}
+    for _, c1, c2 in top:
+        want[frozenset((c1, c2))] = want.get(frozenset((c1, c2)), 0) + 1
+    for c1, c2 in zip(res["q1_new"], res["q2_new"]):
+        got[frozenset((int(c1), int(c2)))] = got.get(frozenset((int(c1), int(c2))), 0) + 1
+    assert got == want
+
+
+def test_pair_truncation_reduces_to_single_charge():
+    # a second species that is identically zero: Θ2(c1, 0) = Θ(c1) (U_0 = 1), every other sector empty,
+    # so the pair step must return the pinned single-charge step exactly (sector index c1·(N+1) = charge c1)
+    base = synth.make_config(1)
+    z = lambda q: np.zeros_like(q)
+    secs = _theta2(synth.PairCase("q2=0", base.N, base.d, base.q_l, z(base.q_l), base.q_c, z(base.q_c), base.q_r,
+                                  z(base.q_r), base.gamma_k, base.gamma_k1, base.lam_l, base.lam_k, base.lam_r,
+                                  base.theta, base.phi))
+    single = oracle.theta_sectors(base.N, base.d, base.q_l, base.q_c, base.q_r, base.gamma_k, base.lam_k,
+                                  base.gamma_k1, base.lam_l, base.lam_r, base.theta, base.phi)[0]
+    for c1 in range(base.N + 1):
+        assert np.allclose(secs[(c1, 0)], single[c1], rtol=0, atol=1e-13 * max(1.0, np.abs(single[c1]).max(initial=0)))
+    for chi in (30, 10 ** 6):
+        r2 = osvd.truncate_update2(base.N, base.d, base.q_l, z(base.q_l), base.q_r, z(base.q_r), secs, base.lam_l,
+                                   base.lam_r, chi)
+        r1 = osvd.truncate_update(base.N, base.d, base.q_l, base.q_r, single, base.lam_l, base.lam_r, chi)
+        assert r2["chi"] == r1["chi"]
+        assert np.array_equal(r2["q1_new"], r1["q_new"]) and not r2["q2_new"].any()
+        assert np.allclose(r2["lam_new"], r1["lam_new"], rtol=1e-12, atol=0)
+        # the factors agree up to one phase per kept vector: compare the phase-free products
+        P2 = r2["gamma_k_new"] * r2["lam_new"][None, :] @ r2["gamma_k1_new"]
+        P1 = r1["gamma_k_new"] * r1["lam_new"][None, :] @ r1["gamma_k1_new"]
+        assert np.linalg.norm(P2 - P1) <= 1e-12 * np.linalg.norm(P1)
+
+
+def test_pair_no_truncation_reconstructs_theta2():
+    c = synth.make_pair_config(0)
+    secs = _theta2(c)
+    res = osvd.truncate_update2(c.N, c.d, c.q1_l, c.q2_l, c.q1_r, c.q2_r, secs, c.lam_l, c.lam_r, 10 ** 6)
+    pl, pr = oracle.sort_pair_bonds(c.q1_l, c.q2_l), oracle.sort_pair_bonds(c.q1_r, c.q2_r)
+    key = res["q1_new"] * (c.N + 1) + res["q2_new"]
+    for c1 in range(c.N + 1):
+        for c2 in range(c.N + 1):
+            th = secs[(c1, c2)]
+            if th.size == 0:
+                continue
+            rows = pl[oracle.pair_sector_rows(c.q1_l[pl], c.q2_l[pl], c.d, c1, c2)]
+            cols = pr[oracle.pair_sector_cols(c.q1_r[pr], c.q2_r[pr], c.d, c1, c2)]
+            a = np.nonzero(key == c1 * (c.N + 1) + c2)[0]
+            A = c.lam_l[rows][:, None] * res["gamma_k_new"][np.ix_(rows, a)]
+            B = res["gamma_k1_new"][np.ix_(a, cols)] * c.lam_r[cols][None, :]
+            rec = (A * res["lam_new"][a][None, :]) @ B
+            assert np.linalg.norm(rec - th) <= 1e-12 * max(np.linalg.norm(th), 1e-300), (c1, c2)
+    assert res["discarded"] <= 1e-24
