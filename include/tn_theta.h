@@ -217,9 +217,12 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
  *   gamma_k1_new [chi_max·χ_r] complex: DEVICE, caller-owned capacity; the factors are written
  *   compact for χ_new = *chi_out (Γk_new is χ_l × χ_new, Γk1_new is χ_new × χ_r), the rest is
  *   unspecified. *chi_out (HOST) = number kept, *discarded (HOST) = Σ of dropped s².
- * Synchronises the stream once (the kept count is needed on the host). Single-GPU single-charge
- * plans only. Errors: TN_ERR_DIMENSION (NULL), TN_ERR_DOMAIN (chi_max < 1, cutoff < 0),
- * TN_ERR_UNSUPPORTED (sharded or pair plan), TN_ERR_OOM, TN_ERR_CUDA (incl. SVD non-convergence). */
+ * MPO pair plans (tn_theta2_plan): the sectors are Θ(c1,c2) (index c1·(N+1)+c2, the
+ * ranking's charge order), q_new holds the pair key c1·(N+1)+c2, and Θ(c1,c2)'s rows/columns are its
+ * admissible pair segments in sorted order (the layout tn_theta_exec wrote).
+ * Synchronises the stream a few times (the kept count is needed on the host). Single-GPU plans only.
+ * Errors: TN_ERR_DIMENSION (NULL), TN_ERR_DOMAIN (chi_max < 1, cutoff < 0), TN_ERR_UNSUPPORTED
+ * (sharded plan), TN_ERR_OOM, TN_ERR_CUDA (incl. SVD non-convergence). */
 TN_API tn_status tn_svd_truncate(const tn_plan* plan, tn_stream stream, double* const* theta,
                                  const double* lambda_l, const double* lambda_r, int64_t chi_max,
                                  double cutoff, int32_t* q_new, double* lambda_new, double* gamma_k_new,

@@ -225,8 +225,8 @@ def theta_exec(plan: Plan, gk, lk, gk1, ll, lr, U, out=None, stream=None):
 
 
 def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None):
-    """tn_svd_truncate: per-sector SVD + global top-χ + new canonical factors. `theta` (the list from
-    theta_exec) is DESTROYED. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
+    """tn_svd_truncate: per-sector SVD + global top-χ + new canonical factors (single-charge or MPO pair
+    plans). `theta` (the list from theta_exec) may be DESTROYED. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
     [chi × χ_r], discarded) as contiguous CUDA tensors (views of chi_max-capacity buffers)."""
     chi_l, _, chi_r = plan.chi
     dev = ll.device
@@ -239,8 +239,11 @@ def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14,
                               float(cutoff), _ptr(q_new), _ptr(lam_new), _ptr(gk), _ptr(gk1), C.byref(chi_out),
                               C.byref(disc)), "tn_svd_truncate")
     k = chi_out.value
-    return dict(chi=k, q_new=q_new[:k], lam_new=lam_new[:k], gamma_k_new=gk.view(-1)[:chi_l * k].view(chi_l, k),
-                gamma_k1_new=gk1[:k], discarded=disc.value)
+    res = dict(chi=k, q_new=q_new[:k], lam_new=lam_new[:k], gamma_k_new=gk.view(-1)[:chi_l * k].view(chi_l, k),
+               gamma_k1_new=gk1[:k], discarded=disc.value)
+    if isinstance(plan, Plan2):  # q_new holds the pair key c1·(N+1) + c2
+        res["q1_new"], res["q2_new"] = q_new[:k] // (plan.N + 1), q_new[:k] % (plan.N + 1)
+    return res
 
 
 class Comm:

@@ -80,7 +80,9 @@ struct SvdSector {          // device views of one sector's SVD
   const double2* ux;        // C × k column-major (ld C)
   const double2* vx;        // R × k column-major (ld R)
   const double* s;          // k values, descending
-  int64_t row0, col0;       // sorted positions of Θ(c)'s first row / column
+  int64_t row0, col0;       // sorted positions of Θ(c)'s first row / column (single-charge plans)
+  const int32_t* rpos;      // pair plans: sorted position of every row / column of Θ(c) (else nullptr:
+  const int32_t* cpos;      //   rows row0 + r, columns col0 + j)
   int32_t R, C, k;
 };
 
@@ -186,7 +188,7 @@ __global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ of
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < na) {  // U_Θ[r, s] = conj(V_x[r, s]); consecutive threads → consecutive new-bond columns
       const int r = (int)(i / kc), s = (int)(i - (int64_t)r * kc);
-      const int32_t al = perm_l[S.row0 + r];
+      const int32_t al = perm_l[S.rpos ? (int64_t)S.rpos[r] : S.row0 + r];
       const double l = lam_l[al];
       const double2 v = S.vx[r + (int64_t)s * S.R];
       const double inv = l != 0.0 ? 1.0 / l : 0.0;
@@ -194,7 +196,7 @@ __global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ of
     } else {       // V_Θ†[s, col] = U_x[col, s]
       const int64_t j = i - na;
       const int s = (int)(j / S.C), col = (int)(j - (int64_t)s * S.C);
-      const int32_t be = perm_r[S.col0 + col];
+      const int32_t be = perm_r[S.cpos ? (int64_t)S.cpos[col] : S.col0 + col];
       const double l = lam_r[be];
       const double2 u = S.ux[col + (int64_t)s * S.C];
       const double inv = l != 0.0 ? 1.0 / l : 0.0;
@@ -542,8 +544,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   if (!p || !theta || !lambda_l || !lambda_r || !q_new || !lambda_new || !gamma_k_new || !gamma_k1_new || !chi_out ||
       !discarded)
     return fail(TN_ERR_DIMENSION, "tn_svd_truncate: NULL argument");
-  if (p->world != 1 || p->pair)
-    return fail(TN_ERR_UNSUPPORTED, "tn_svd_truncate: needs a single-GPU, single-charge plan (full sectors)");
+  if (p->world != 1) return fail(TN_ERR_UNSUPPORTED, "tn_svd_truncate: needs a single-GPU plan (full sectors)");
   cudaStream_t s = (cudaStream_t)stream;
   SvdCtx& X = ctx();
   std::lock_guard<std::mutex> lock(X.mu);
@@ -613,6 +614,29 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   const size_t o_base = take((size_t)(ns + 1) * 8);
   const size_t o_off = take((size_t)(ns + 1) * 4);
   const size_t o_res = take(16);
+  // pair plans: Θ(c1,c2)'s rows are whole left pair segments (l1 ∈ [c1, c1+d−1], l2 ∈ [c2, c2+d−1], key order)
+  // and its columns whole right segments (r1 ∈ [c1−d+1, c1], r2 ∈ [c2−d+1, c2]) — tn_pair.cu's layout
+  std::vector<int32_t> hpos;
+  std::vector<int64_t> rpos_at(ns, 0), cpos_at(ns, 0);
+  if (p->pair) {
+    const int N = p->N, d = p->d, nk = N + 1;
+    const auto& ol = p->off[0];
+    const auto& orr = p->off[2];
+    for (int c = 0; c < ns; ++c) {
+      const int c1 = c / nk, c2 = c % nk;
+      rpos_at[c] = (int64_t)hpos.size();
+      for (int l1 = c1; l1 <= std::min(N, c1 + d - 1); ++l1)
+        for (int l2 = c2; l2 <= std::min(N, c2 + d - 1); ++l2)
+          for (int32_t x = ol[l1 * nk + l2]; x < ol[l1 * nk + l2 + 1]; ++x) hpos.push_back(x);
+      if ((int64_t)hpos.size() - rpos_at[c] != p->R[c]) return fail(TN_ERR_CONSISTENCY, "tn_svd_truncate: pair rows");
+      cpos_at[c] = (int64_t)hpos.size();
+      for (int r1 = std::max(0, c1 - d + 1); r1 <= c1; ++r1)
+        for (int r2 = std::max(0, c2 - d + 1); r2 <= c2; ++r2)
+          for (int32_t x = orr[r1 * nk + r2]; x < orr[r1 * nk + r2 + 1]; ++x) hpos.push_back(x);
+      if ((int64_t)hpos.size() - cpos_at[c] != p->C[c]) return fail(TN_ERR_CONSISTENCY, "tn_svd_truncate: pair cols");
+    }
+  }
+  const size_t o_pos = take(std::max<size_t>(hpos.size(), 1) * 4);
   size_t sort_bytes = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const double*)nullptr, (double*)nullptr,
                                             (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(total_max, 1));
@@ -630,6 +654,8 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     S.k = k;
     S.row0 = p->row0[c];
     S.col0 = p->col0[c];
+    S.rpos = p->pair ? reinterpret_cast<const int32_t*>(B + o_pos) + rpos_at[c] : nullptr;
+    S.cpos = p->pair ? reinterpret_cast<const int32_t*>(B + o_pos) + cpos_at[c] : nullptr;
     if (k == 0) continue;
     if (!theta[c]) return fail(TN_ERR_DIMENSION, "tn_svd_truncate: NULL Θ(c) for a non-empty sector");
     if (algo != 2) {
@@ -641,6 +667,10 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   }
   st = cuda_check(cudaMemsetAsync(d_info, 0, ns * sizeof(int), s), "memset info");  // empty sectors
   if (st != TN_OK) return st;
+  if (!hpos.empty() &&
+      (st = cuda_check(cudaMemcpyAsync(B + o_pos, hpos.data(), hpos.size() * 4, cudaMemcpyHostToDevice, s),
+                       "H2D pair positions")) != TN_OK)
+    return st;
   auto cost = [&](int c) { return (double)p->R[c] * p->C[c] * std::min(p->R[c], p->C[c]); };
   // one library SVD (paths 0/1): X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
   auto lib_svd = [&](int l, int c, std::vector<char>& hbuf) -> std::string {

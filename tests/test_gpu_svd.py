@@ -126,3 +126,47 @@ def test_svd_errors(tn):
     sharded = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r, 2, 0)
     with pytest.raises(tn.TnError, match="UNSUPPORTED"):
         tn.svd_truncate(sharded, t, ll, lr, 4)
+
+
+# ------------------------------------------------------------------ MPO pair plans (oracle.svd.truncate_update2)
+def _recon2(c, res, c1, c2, key):
+    pl, pr = oracle.sort_pair_bonds(c.q1_l, c.q2_l), oracle.sort_pair_bonds(c.q1_r, c.q2_r)
+    rows = pl[oracle.pair_sector_rows(c.q1_l[pl], c.q2_l[pl], c.d, c1, c2)]
+    cols = pr[oracle.pair_sector_cols(c.q1_r[pr], c.q2_r[pr], c.d, c1, c2)]
+    a = np.nonzero(key == c1 * (c.N + 1) + c2)[0]
+    A = c.lam_l[rows][:, None] * res["gamma_k_new"][np.ix_(rows, a)]
+    B = res["gamma_k1_new"][np.ix_(a, cols)] * c.lam_r[cols][None, :]
+    return (A * res["lam_new"][a][None, :]) @ B, A, B
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("cfg,chi", [(0, 10), (1, 200), (1, 10 ** 6)])
+def test_pair_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    from test_gpu_pair import gpu_theta2
+    c = synth.make_pair_config(cfg)
+    plan, got = gpu_theta2(tn, c)
+    N = c.N
+    t = [torch.from_numpy(np.ascontiguousarray(got[(s // (N + 1), s % (N + 1))])).cuda() for s in range((N + 1) ** 2)]
+    ll, lr = torch.from_numpy(c.lam_l).cuda(), torch.from_numpy(c.lam_r).cuda()
+    res = tn.svd_truncate(plan, t, ll, lr, chi)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
+    ref = osvd.truncate_update2(N, c.d, c.q1_l, c.q2_l, c.q1_r, c.q2_r, got, c.lam_l, c.lam_r, chi)
+    assert res["chi"] == ref["chi"]
+    assert np.array_equal(res["q_new"], ref["q_new"])
+    assert np.array_equal(res["q1_new"], ref["q1_new"]) and np.array_equal(res["q2_new"], ref["q2_new"])
+    smax = max(float(s.max()) for s in ref["svals"] if s.size)
+    assert np.max(np.abs(res["lam_new"] - ref["lam_new"]), initial=0.0) <= 1e-12 * smax
+    tot = sum(np.linalg.norm(x) ** 2 for x in got.values())
+    assert abs(res["discarded"] - ref["discarded"]) <= 1e-12 * tot
+    for c1 in range(N + 1):
+        for c2 in range(N + 1):
+            if got[(c1, c2)].size == 0:
+                continue
+            rg, A, B = _recon2(c, res, c1, c2, res["q_new"])
+            rr, *_ = _recon2(c, ref, c1, c2, ref["q_new"])
+            assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), (c1, c2)
+            if A.shape[1]:
+                assert np.allclose(A.conj().T @ A, np.eye(A.shape[1]), atol=1e-12)
+                assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
