@@ -30,7 +30,9 @@ species, identity gate == two-site product, and Σ‖Θ2‖² invariance; for th
 block-diagonal Θ, exact reconstruction without truncation, orthonormal factors, the tie-break rule;
 for the pair step: the Kronecker closed form on a vectorized pure state (singular values = products
 s_i(c1)·s_j(c2)), the reduction to the single-charge step when the second species is absent, and exact
-reconstruction of Θ2 without truncation.
+reconstruction of Θ2 without truncation; for layers (tests/test_oracle_layer_pins.py): dense state-vector
+evolution (MPS) and dense ρ → (U⊗U*)ρ evolution (MPO, `layer.apply_gate2`), both against scipy expm, and
+the vectorized pure state evolving like its MPS.
 No function here is "parity unpinned".
 """
 from .theta import (sort_bonds, bs_unitary_block, packed_u, packed_u_offsets, theta_sectors,

@@ -98,3 +98,93 @@ def random_mps(M, N, d, chi, seed):
 def copy_state(s):
     return dict(N=s["N"], d=s["d"], q=[x.copy() for x in s["q"]], gam=[x.copy() for x in s["gam"]],
                 lam=[x.copy() for x in s["lam"]])
+
+
+# ---------------------------------------------------------------------------------------------------------
+# MPO (vectorized density matrix, two conserved charges) — PAPER.md:101, :105-107: "MPOs are vectorized into
+# the MPS form, U → U⊗U*, and two conserved charges are present". Bond k carries charge PAIRS (q1, q2) (ket,
+# bra photons to the right); site k's physical pair (i, i') is implied by i = q1_k − q1_{k+1}, i' = q2_k − q2_{k+1}.
+# A gate is Θ(c1, c2) (oracle.theta2_sectors) followed by the pair SVD update (oracle.svd.truncate_update2).
+# ---------------------------------------------------------------------------------------------------------
+def apply_gate2(state, k, theta, phi, chi_max, cutoff=1e-14):
+    """In-place TEBD update of MPO sites (k, k+1). `state` = dict(N, d, q1, q2: [M+1 int arrays], gam: [M],
+    lam: [M+1]). Returns the discarded weight."""
+    from .svd import truncate_update2
+    from .theta2 import theta2_sectors
+    N, d = state["N"], state["d"]
+    q1, q2, gam, lam = state["q1"], state["q2"], state["gam"], state["lam"]
+    secs, *_ = theta2_sectors(N, d, q1[k], q2[k], q1[k + 1], q2[k + 1], q1[k + 2], q2[k + 2], gam[k], lam[k + 1],
+                              gam[k + 1], lam[k], lam[k + 2], theta, phi)
+    res = truncate_update2(N, d, q1[k], q2[k], q1[k + 2], q2[k + 2], secs, lam[k], lam[k + 2], chi_max, cutoff)
+    q1[k + 1], q2[k + 1] = res["q1_new"].astype(np.int32), res["q2_new"].astype(np.int32)
+    lam[k + 1] = res["lam_new"]
+    gam[k] = res["gamma_k_new"]
+    gam[k + 1] = res["gamma_k1_new"]
+    return res["discarded"]
+
+
+def apply_layer2(state, parity, thetas, phis, chi_max, cutoff=1e-14):
+    M = len(state["gam"])
+    return [apply_gate2(state, k, thetas[g], phis[g], chi_max, cutoff) for g, k in enumerate(range(parity, M - 1, 2))]
+
+
+def vectorize_mps(state):
+    """|ψ⟩⟨ψ| of a Vidal MPS as a vectorized MPO: pair bond (α, α') with charges (q[α], q[α']),
+    Γ2 = Γ ⊗ conj(Γ), λ2 = λ ⊗ λ (row-major pair index)."""
+    pq = lambda q: (np.repeat(q, len(q)).astype(np.int32), np.tile(q, len(q)).astype(np.int32))
+    q1, q2 = zip(*(pq(q) for q in state["q"]))
+    return dict(N=state["N"], d=state["d"], q1=list(q1), q2=list(q2),
+                gam=[np.kron(g, np.conj(g)) for g in state["gam"]], lam=[np.kron(l, l) for l in state["lam"]])
+
+
+def dense_state2(state):
+    """ρ[i_0..i_{M−1}, i'_0..i'_{M−1}] of a small vectorized MPO: the chain contracted like dense_state with
+    the physical pair (i, i') = (q1_k − q1_{k+1}, q2_k − q2_{k+1}) ∈ [0, d−1]² (both δ's written out)."""
+    N, d = state["N"], state["d"]
+    q1, q2, gam, lam = state["q1"], state["q2"], state["gam"], state["lam"]
+    M = len(gam)
+    vec = np.asarray(lam[0], dtype=np.complex128).copy()
+    for k in range(M):
+        G = gam[k] * lam[k + 1][None, :]
+        new = np.zeros((len(q1[k + 1]),) + (d * d,) * (k + 1), dtype=np.complex128)
+        for a in range(len(q1[k])):
+            for b in range(len(q1[k + 1])):
+                i, ip = int(q1[k][a]) - int(q1[k + 1][b]), int(q2[k][a]) - int(q2[k + 1][b])
+                if 0 <= i <= d - 1 and 0 <= ip <= d - 1 and G[a, b] != 0:
+                    new[(b,) + (slice(None),) * k + (i * d + ip,)] += vec[a] * G[a, b]
+        vec = new
+    x = vec.sum(axis=0).reshape((d, d) * M)              # axes (i_0, i'_0, i_1, i'_1, …)
+    return np.transpose(x, list(range(0, 2 * M, 2)) + list(range(1, 2 * M, 2)))
+
+
+def random_mpo(M, N, d, chi, seed):
+    """A random vectorized-MPO-shaped state with two independent charge species per bond (each in the
+    reachable window of random_mps), Γ masked to blocks allowed for BOTH species; bonds sorted by pair key."""
+    rng = np.random.default_rng(seed)
+    q1, q2 = [], []
+    for k in range(M + 1):
+        if k == 0:
+            a = b = np.array([N], dtype=np.int32)
+        elif k == M:
+            a = b = np.array([0], dtype=np.int32)
+        else:
+            lo, hi = max(0, N - k * (d - 1)), min(N, (M - k) * (d - 1))
+            a = rng.integers(lo, hi + 1, size=chi)
+            b = rng.integers(lo, hi + 1, size=chi)
+            o = np.lexsort((b, a))
+            a, b = a[o].astype(np.int32), b[o].astype(np.int32)
+        q1.append(a)
+        q2.append(b)
+    gam = []
+    for k in range(M):
+        g = (rng.standard_normal((len(q1[k]), len(q1[k + 1]))) + 1j * rng.standard_normal((len(q1[k]), len(q1[k + 1])))) / np.sqrt(2)
+        d1 = q1[k][:, None].astype(np.int64) - q1[k + 1][None, :]
+        d2 = q2[k][:, None].astype(np.int64) - q2[k + 1][None, :]
+        gam.append(g * ((d1 >= 0) & (d1 <= d - 1) & (d2 >= 0) & (d2 <= d - 1)))
+    lam = [np.ones(1)] + [np.sort(rng.uniform(0.2, 1.0, size=len(q1[k])))[::-1].copy() for k in range(1, M)] + [np.ones(1)]
+    return dict(N=N, d=d, q1=q1, q2=q2, gam=gam, lam=lam)
+
+
+def copy_state2(s):
+    return dict(N=s["N"], d=s["d"], q1=[x.copy() for x in s["q1"]], q2=[x.copy() for x in s["q2"]],
+                gam=[x.copy() for x in s["gam"]], lam=[x.copy() for x in s["lam"]])

@@ -46,3 +46,46 @@ def test_truncation_reports_discarded_weight():
     disc = L.apply_layer(st, 0, [0.6, 1.1], [0.3, 2.0], chi_max=3)
     assert sum(disc) > 0 and min(disc) >= 0
     assert all(len(st["lam"][k]) <= 3 for k in (1, 3))
+
+
+# ------------------------------------------------------------------ MPO (vectorized density matrix) layers
+def test_vectorized_pure_mpo_is_outer_product():
+    st = L.random_mps(4, 2, 3, 4, 5)
+    psi = L.dense_state(st)
+    rho = L.dense_state2(L.vectorize_mps(st))
+    assert np.allclose(rho, np.multiply.outer(psi, psi.conj()), rtol=0, atol=1e-13 * np.abs(psi).max() ** 2)
+
+
+@pytest.mark.parametrize("M,N,d,chi,seed", [(4, 2, 3, 5, 0), (4, 3, 3, 6, 1), (3, 2, 3, 6, 2)])
+def test_mpo_layer_without_truncation_is_dense_evolution(M, N, d, chi, seed):
+    # ρ → (U⊗U*) ρ on the ket pair (i_k, i_{k+1}) and the bra pair (i'_k, i'_{k+1}) (U → U⊗U*),
+    # the dense side built from scipy expm like the single-charge pin above
+    st = L.random_mpo(M, N, d, chi, seed)
+    rho = L.dense_state2(st)
+    rng = np.random.default_rng(seed + 20)
+    for parity in (0, 1, 0):
+        gates = list(range(parity, M - 1, 2))
+        th = rng.uniform(0, np.pi / 2, len(gates))
+        ph = rng.uniform(0, 2 * np.pi, len(gates))
+        disc = L.apply_layer2(st, parity, th, ph, chi_max=10 ** 6)
+        assert max(disc, default=0.0) < 1e-20
+        for g, k in enumerate(gates):
+            U4 = _u4(th[g], ph[g], d, N)
+            rho = L.dense_gate(rho, k, U4)
+            rho = L.dense_gate(rho, M + k, U4.conj())
+        got = L.dense_state2(st)
+        assert np.linalg.norm(got - rho) <= 1e-12 * np.linalg.norm(rho), parity
+
+
+def test_mpo_layer_on_vectorized_pure_state_matches_mps_layer():
+    st = L.random_mps(5, 3, 3, 5, 7)
+    mpo = L.vectorize_mps(st)
+    rng = np.random.default_rng(70)
+    for parity in (0, 1):
+        n = len(range(parity, 4, 2))
+        th, ph = rng.uniform(0, np.pi / 2, n), rng.uniform(0, 2 * np.pi, n)
+        L.apply_layer(st, parity, th, ph, chi_max=10 ** 6)
+        L.apply_layer2(mpo, parity, th, ph, chi_max=10 ** 6)
+    psi = L.dense_state(st)
+    rho = L.dense_state2(mpo)
+    assert np.linalg.norm(rho - np.multiply.outer(psi, psi.conj())) <= 1e-11 * np.linalg.norm(rho)
