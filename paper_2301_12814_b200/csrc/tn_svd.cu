@@ -26,6 +26,7 @@
 #include <thread>
 #include <vector>
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -63,6 +64,8 @@ int svd_algo() {
   if (e && std::string(e) == "gesvdp") return 1;
   return 2;
 }
+// largest h_err_sigma accepted from Xgesvdp in the Ritz step before it is redone by one-sided Jacobi
+constexpr double kRitzHerrMax = 1e-13;
 tn_status grow(void*& buf, size_t& cap, size_t need, char** out) {  // grow-only device scratch
   if (need > cap) {
     if (buf) cudaFree(buf);
@@ -466,6 +469,7 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   }
   char* Cb = nullptr;
   if ((st = grow(X.gbuf[1], X.gcap[1], std::max<size_t>(off, 256), &Cb)) != TN_OK) return st;
+  std::atomic<int> n_jacobi{0};
   auto jobC = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
     const Geo& q = g[c];
     const int k = kp[c];
@@ -484,11 +488,46 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
                           Cb + oS[c], CUDA_C_64F, Cb + oP[c], q.mt, CUDA_C_64F, Wm, k, CUDA_C_64F, Cb + oWc[c], wsC[c],
                           hbuf.data(), hsC[c], infoC + c, &herr);
     if (r != CUSOLVER_STATUS_SUCCESS) return "cuSOLVER Ritz SVD failed in sector " + std::to_string(c);
+    if (getenv("TN_SVD_PROFILE")) fprintf(stderr, "[svd] ritz sector %d %dx%d h_err_sigma %.3e\n", c, q.mt, k, herr);
+    if (!(herr <= kRitzHerrMax)) {
+      // the polar-decomposition SVD reports a large backward error (seen up to 5e-8 on small rank-deficient
+      // matrices): recompute Y and take the one-sided Jacobi SVD instead (accurate to rounding, slower)
+      ++n_jacobi;
+      b = q.tall ? cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.C, k, q.R, &one, Z, q.C, E, q.R, &zero, T, q.C)
+                 : cublasZgemm(X.hb[l], CUBLAS_OP_C, CUBLAS_OP_N, q.R, k, q.C, &one, Z, q.C, E, q.C, &zero, T, q.R);
+      if (b != CUBLAS_STATUS_SUCCESS) return "cuBLAS Ritz projection failed in sector " + std::to_string(c);
+      gesvdjInfo_t jp = nullptr;
+      if (cusolverDnCreateGesvdjInfo(&jp) != CUSOLVER_STATUS_SUCCESS) return "cusolverDnCreateGesvdjInfo failed";
+      cusolverDnXgesvdjSetTolerance(jp, 0.0);
+      cusolverDnXgesvdjSetMaxSweeps(jp, 100);
+      int lw = 0;
+      std::string err;
+      if (cusolverDnZgesvdj_bufferSize(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, q.mt, k, T, q.mt,
+                                       reinterpret_cast<double*>(Cb + oS[c]), reinterpret_cast<cuDoubleComplex*>(Cb + oP[c]),
+                                       q.mt, Wm, k, &lw, jp) != CUSOLVER_STATUS_SUCCESS) {
+        err = "cusolverDnZgesvdj_bufferSize failed";
+      } else {
+        void* wj = nullptr;
+        if (cudaMallocAsync(&wj, (size_t)std::max(lw, 1) * 16, X.st[l]) != cudaSuccess) {
+          err = "Jacobi workspace allocation failed";
+        } else {
+          if (cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, q.mt, k, T, q.mt,
+                                reinterpret_cast<double*>(Cb + oS[c]), reinterpret_cast<cuDoubleComplex*>(Cb + oP[c]),
+                                q.mt, Wm, k, reinterpret_cast<cuDoubleComplex*>(wj), lw, infoC + c, jp) !=
+              CUSOLVER_STATUS_SUCCESS)
+            err = "cuSOLVER Jacobi Ritz SVD failed in sector " + std::to_string(c);
+          cudaFreeAsync(wj, X.st[l]);
+        }
+      }
+      cusolverDnDestroyGesvdjInfo(jp);
+      if (!err.empty()) return err;
+    }
     b = cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.ng, k, k, &one, E, q.ng, Wm, k, &zero,
                     reinterpret_cast<cuDoubleComplex*>(Cb + oEW[c]), q.ng);
     return b == CUBLAS_STATUS_SUCCESS ? std::string() : "cuBLAS Ritz rotation failed in sector " + std::to_string(c);
   };
   if ((st = run_lanes(X, s, waveC, cost, jobC)) != TN_OK) return st;
+  if (prof && n_jacobi.load()) fprintf(stderr, "[svd_gram] Jacobi fallback in %d Ritz SVDs\n", n_jacobi.load());
   std::vector<int> info(ns, 0);
   std::vector<std::vector<double>> sv(ns);
   for (int c : waveC) {
@@ -689,6 +728,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
                             const_cast<double*>(S.s), CUDA_C_64F, const_cast<double2*>(S.ux), C, CUDA_C_64F,
                             const_cast<double2*>(S.vx), R, CUDA_C_64F, B + o_w[c], wsz[c], hbuf.data(), hbytes[c],
                             d_info + c, &herr);
+      if (getenv("TN_SVD_PROFILE")) fprintf(stderr, "[svd] gesvdp sector %d %dx%d h_err_sigma %.3e\n", c, R, C, herr);
     }
     return r == CUSOLVER_STATUS_SUCCESS ? std::string()
                                         : "cuSOLVER SVD failed in sector " + std::to_string(c) + " (status " +

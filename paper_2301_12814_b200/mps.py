@@ -20,7 +20,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import Plan, build_bs_unitary, svd_truncate, theta_exec
+from . import Plan, Plan2, build_bs_unitary, svd_truncate, theta_exec
 
 
 def layer_owners(costs, world: int):
@@ -138,3 +138,56 @@ class MPS:
                 bc(torch.view_as_real(t))
         if not mine:
             self.q[k + 1] = q64.to(torch.int32)
+
+
+class MPO:
+    """A vectorized density matrix on the device ("MPOs are vectorized into the MPS
+    form, U → U⊗U*, and two conserved charges are present"): bond k carries charge PAIRS (q1, q2) (ket, bra
+    photons to the right, int32 each), λ (float64); site k carries Γ^{[k]} [χ_k × χ_{k+1}] complex128. A gate
+    on sites (k, k+1) is tn_theta2_plan → U → tn_theta_exec (Θ(c1, c2), two-pass U⊗U* mix) →
+    tn_svd_truncate on the pair plan (oracle: oracle/layer.py apply_gate2)."""
+
+    def __init__(self, N: int, d: int, q1, q2, gam, lam, device="cuda"):
+        dev = torch.device(device)
+        as_t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
+            dev, dt).contiguous()
+        self.N, self.d, self.device = int(N), int(d), dev
+        self.q1 = [as_t(x, torch.int32) for x in q1]
+        self.q2 = [as_t(x, torch.int32) for x in q2]
+        self.gam = [as_t(x, torch.complex128) for x in gam]
+        self.lam = [as_t(x, torch.float64) for x in lam]
+        self.M = len(self.gam)
+        if not (len(self.q1) == len(self.q2) == len(self.lam) == self.M + 1):
+            raise ValueError("an MPO of M sites needs M+1 bonds of charge pairs and λ")
+
+    @classmethod
+    def from_state(cls, st: dict, device="cuda"):
+        return cls(st["N"], st["d"], st["q1"], st["q2"], st["gam"], st["lam"], device)
+
+    def to_state(self) -> dict:
+        c = lambda xs: [x.cpu().numpy() for x in xs]
+        return dict(N=self.N, d=self.d, q1=c(self.q1), q2=c(self.q2), gam=c(self.gam), lam=c(self.lam))
+
+    def apply_gate(self, k: int, theta: float, phi: float, chi_max: int, cutoff: float = 1e-14, contraction=None):
+        """One TEBD update of sites (k, k+1) with U⊗U*; returns the discarded weight."""
+        if not 0 <= k < self.M - 1:
+            raise ValueError("gate sites out of range")
+        plan = Plan2(self.d, self.N, self.q1[k], self.q2[k], self.q1[k + 1], self.q2[k + 1], self.q1[k + 2],
+                     self.q2[k + 2])
+        if contraction is not None:
+            plan.set_contraction(*contraction)
+        U = build_bs_unitary(plan, theta, phi)
+        out = theta_exec(plan, self.gam[k], self.lam[k + 1], self.gam[k + 1], self.lam[k], self.lam[k + 2], U)
+        res = svd_truncate(plan, out, self.lam[k], self.lam[k + 2], chi_max, cutoff)
+        self.q1[k + 1] = res["q1_new"].to(torch.int32).contiguous()
+        self.q2[k + 1] = res["q2_new"].to(torch.int32).contiguous()
+        self.lam[k + 1] = res["lam_new"]
+        self.gam[k] = res["gamma_k_new"]
+        self.gam[k + 1] = res["gamma_k1_new"]
+        plan.destroy()
+        return res["discarded"]
+
+    def apply_layer(self, parity: int, thetas, phis, chi_max: int, cutoff: float = 1e-14, contraction=None):
+        """Gates on (k, k+1) for k = parity, parity+2, … < M−1; returns their discarded weights."""
+        return [self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction)
+                for g, k in enumerate(range(parity, self.M - 1, 2))]

@@ -37,3 +37,36 @@ def test_layers_match_oracle(tn, M, N, d, chi, chi_max, seed):
             assert abs(x - y) <= 1e-10 * max(y, 1e-30) + 1e-28
     psi_ref, psi = L.dense_state(ref), L.dense_state(got)
     assert np.linalg.norm(psi - psi_ref) <= 1e-10 * np.linalg.norm(psi_ref)
+
+
+# ------------------------------------------------------------------ MPO (vectorized density matrix) layers
+# TN_SVD_ALGO=gesvdp is left out: cuSOLVER's polar-decomposition SVD reports h_err_sigma up to 5e-8 on the
+# small rank-deficient sectors the no-truncation case produces; the default Gram
+# path guards its own Xgesvdp call with a Jacobi fallback
+@pytest.mark.parametrize("algo", ["gram", "gesvdj"])
+@pytest.mark.parametrize("M,N,d,chi,chi_max,seed", [(4, 2, 3, 6, 10 ** 6, 0), (5, 2, 3, 8, 10, 1), (4, 3, 3, 9, 14, 2)])
+def test_mpo_layers_match_oracle(tn, M, N, d, chi, chi_max, seed, algo, monkeypatch):
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    from paper_2301_12814_b200.mps import MPO
+    st = L.random_mpo(M, N, d, chi, seed)
+    ref = L.copy_state2(st)
+    mpo = MPO.from_state(st)
+    rng = np.random.default_rng(seed + 200)
+    # the bond dimension grows without truncation, so some Θ(c1,c2) are rank-deficient: their "zero" singular
+    # values are rounding noise ~ ε‖Θ‖ on both sides (with this unnormalised state near SPEC.md's absolute
+    # 1e-14), and the Vidal update divides by λ, so a kept λ ~ 1e-9 amplifies rounding to ~1e-8 in the next
+    # gate on EITHER side (gesvdp and the Gram path alike); a cutoff of 1e-5 keeps both effects below the bar
+    cut = 1e-5
+    for parity in (0, 1, 0, 1):
+        gates = list(range(parity, M - 1, 2))
+        th, ph = rng.uniform(0, np.pi / 2, len(gates)), rng.uniform(0, 2 * np.pi, len(gates))
+        d_ref = L.apply_layer2(ref, parity, th, ph, chi_max, cut)
+        d_gpu = mpo.apply_layer(parity, th, ph, chi_max, cut)
+        got = mpo.to_state()
+        for b in range(M + 1):
+            assert np.array_equal(got["q1"][b], ref["q1"][b]) and np.array_equal(got["q2"][b], ref["q2"][b]), (parity, b)
+            assert np.max(np.abs(got["lam"][b] - ref["lam"][b]), initial=0.0) <= 1e-10 * ref["lam"][b].max(), (parity, b)
+        for x, y in zip(d_gpu, d_ref):
+            assert abs(x - y) <= 1e-10 * max(y, 1e-30) + 1e-16
+    rho_ref, rho = L.dense_state2(ref), L.dense_state2(got)
+    assert np.linalg.norm(rho - rho_ref) <= 1e-10 * np.linalg.norm(rho_ref)
