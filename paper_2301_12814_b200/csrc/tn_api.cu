@@ -517,10 +517,11 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     build_mix_tiles(p, mix);
     p->nmix = (int64_t)mix.size();
     std::vector<MixItem>& items = p->h_items;
-    build_mix_items(p, items);
     {
+      // the K5T experiment's item list is built only when it is selected (host time is on the step's path)
       const char* env = getenv("TN_K5T");
-      p->k5t = env && env[0] == '1' && !items.empty();
+      if (env && env[0] == '1') build_mix_items(p, items);
+      p->k5t = !items.empty();
     }
     if (!p->groups.empty() || !mix.empty()) {
       Carver cw;
