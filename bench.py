@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Θ-build useful complex FP64 GFLOP/s & gates/s at d=32,χ=4096; % FP64 TC peak"
 FP64_TC_PEAK_TFLOPS = 37.2   # measured: DMMA.8x8x4 loop, 148 SMs @ 1965 MHz (profiles/r01_fp64_peaks.jsonl)
-LAUNCHES_PER_STEP = 6        # K1 (1 launch, 3 CTAs), K2, K3a, K3b, K4, K5 (INT8 engine: K3O is 4 launches)
+# kernel launches per step = K1 (plan) + K2 (U) + tn_plan_exec_launches (K3, K4, one K5 launch per register
+# class of the mix; INT8 engine: 4 K3O launches + K4O), counted from the plan
 INT8_UMMA_PEAK_TOPS = 4347.9  # measured tcgen05 kind::i8 M=128 N=256 (profiles/r01_umma_i8_test.log)
 
 
@@ -229,6 +230,7 @@ def run_tn(args, rank, world, local_rank):
     if int8:
         probe.set_contraction("int8", args.slices)
     k1_isolated_ms = probe.kernel_times()["k1_sort"]   # K1 on an idle GPU (in the timed loop it overlaps)
+    launches_per_step = 2 + probe.exec_launches()
     flops = probe.flops()
     f_useful = flops["f_contract"] + flops["f_mix"]
     int8_ops = 0   # INT8 tensor ops (2 per MAC) one K4O launch executes, incl. tile padding
@@ -496,7 +498,7 @@ def run_tn(args, rank, world, local_rank):
                 "note": "pinned H2D of Γk, Γk1, λ's and charges + D2H of every Θ(c) per gate, 2 gates in flight"},
         "comm_variants_ms": comm_variants,
         "alt_engine": alt,
-        "gpu_launches": (LAUNCHES_PER_STEP + (2 if int8 else 0)) * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
@@ -601,6 +603,7 @@ def run_pair(args, rank, world, local_rank):
         return p
 
     probe = mk()
+    launches_per_step = 2 + probe.exec_launches()
     flops = probe.flops()
     f_useful = flops["f_contract"] + flops["f_mix"]
     outs = tn.alloc_theta(probe, device=dev)
@@ -662,7 +665,7 @@ def run_pair(args, rank, world, local_rank):
                          "achieved_def": "F_contract (useful, 8/CMAC) / mean K4 launch time"},
             "kernels_ms": {k: round(v, 4) for k, v in km.items()},
             "mix_hbm_gbs": round(2 * 2 * 16 * sum(o.numel() for o in outs) / (km["k5_mix"] * 1e-3) / 1e9, 1),
-            "gpu_launches": 7 * args.steps, "clocks": clk.summary()}
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 
 
@@ -724,9 +727,10 @@ def run_sweep(args, rank, world, local_rank):
                 for c in range(N + 1)]
         tn.build_bs_unitary(plan, gt["theta"], gt["phi"], out=U)
         tn.theta_exec(plan, gt["gk"], lam, gt["gk1"], lam, lam, U, out=outs)
+        launches.append(2 + plan.exec_launches())
         keep.append(plan)
 
-    keep = []
+    keep, launches = [], []
     for i in range(args.warmup):
         step(gates[i % len(gates)], keep)
     torch.cuda.synchronize()
@@ -738,6 +742,7 @@ def run_sweep(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ktimes = []
+    launches.clear()
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
         for gt in gates:
@@ -778,7 +783,7 @@ def run_sweep(args, rank, world, local_rank):
                        "step": "per gate: tn_theta_plan + tn_build_bs_unitary + tn_theta_exec",
                        "l2": "inputs larger than L2 (Γ 1.07 GB each per gate; Θ up to 7.5 GB)"},
             "kernels_mean_ms": {k: round(statistics.mean(kt[k] for kt in ktimes), 4) for k in ktimes[0]},
-            "gpu_launches": (LAUNCHES_PER_STEP + (2 if args.contraction == "int8" else 0)) * len(mine),
+            "gpu_launches": sum(launches),
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 

@@ -121,6 +121,12 @@ class Plan:
         check(lib.tn_plan_flops(self.handle, *(C.byref(x) for x in v)), "tn_plan_flops")
         return dict(zip(("f_contract", "f_mix", "f_exec", "f_contract_local", "f_mix_local"), (x.value for x in v)))
 
+    def exec_launches(self) -> int:
+        """tn_plan_exec_launches: kernel launches of one tn_theta_exec with the current engine."""
+        n = C.c_int64()
+        check(lib.tn_plan_exec_launches(self.handle, C.byref(n)), "tn_plan_exec_launches")
+        return n.value
+
     def u_size(self) -> int:
         n = C.c_int64()
         check(lib.tn_plan_u_size(self.handle, C.byref(n)), "tn_plan_u_size")

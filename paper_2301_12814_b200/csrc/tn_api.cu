@@ -766,6 +766,27 @@ tn_status tn_plan_get_contraction(const tn_plan* p, int* mode, int* slices) {
   return TN_OK;
 }
 
+tn_status tn_plan_exec_launches(const tn_plan* p, int64_t* n_launches) {
+  if (!p || !n_launches) return fail(TN_ERR_DIMENSION, "tn_plan_exec_launches: NULL");
+  int64_t n = 0;
+  if (p->contraction == TN_CONTRACT_PAPER_LITERAL) {
+    n = p->lit_secs.empty() ? 0 : 2 + (p->lit_ntiles > 0);                 // K3L a/b, K4L
+  } else {
+    const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
+    if (emu) n += (p->oz_groups.empty() ? 0 : 4) + (p->oz_ntiles > 0);      // K3O ×4, K4O
+    else n += (p->groups.empty() ? 0 : 2) + ((p->fused && !p->pair) ? 1 : (p->ntiles > 0));  // K3 a/b, K4 (or K45)
+    if (p->pair) {
+      n += (p->nmix2[0] > 0) + (p->nmix2[1] > 0);                            // K5P, two passes
+    } else if (emu || !p->fused) {
+      const int64_t c0 = p->nmix_cls[0], c1 = p->nmix_cls[1], c2 = p->nmix_cls[2], c3 = p->nmix - c0 - c1 - c2;
+      if (p->k5t) n += (p->nitem_cls[0] > 0) + (p->nitem_cls[1] > 0) + (p->nitem_cls[2] > 0) + (c3 > 0);
+      else n += (c0 > 0) + (c1 > 0) + (c2 > 0) + (c3 > 0);                  // K5, one launch per L class
+    }
+  }
+  *n_launches = n;
+  return TN_OK;
+}
+
 tn_status tn_plan_kernel_times(const tn_plan* p, float* ms) {
   if (!p || !ms) return fail(TN_ERR_DIMENSION, "tn_plan_kernel_times: NULL");
   for (int i = 0; i < 5; ++i) ms[i] = -1.0f;
