@@ -214,8 +214,8 @@ TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,
  *                  = U_c[α, s] / λ^{[k−1]}[α] for α in Θ(c)'s rows, 0 elsewhere (x/0 := 0),
  *   gamma_k1_new[a × β] (complex, row-major, ld = χ_r, columns in the caller's α_{k+1} order)
  *                  = V_c†[s, β] / λ^{[k+1]}[β] for β in Θ(c)'s columns, 0 elsewhere.
- *   theta      HOST array of N+1 DEVICE sector pointers from tn_theta_exec — may be DESTROYED (the
- *              library SVD paths use it as workspace; the default path only reads it).
+ *   theta      HOST array of N+1 DEVICE sector pointers from tn_theta_exec — read only (every
+ *              path factorises a copy or a projection; Θ(c) is left intact).
  *   lambda_l, lambda_r  DEVICE λ^{[k−1]}, λ^{[k+1]} (the ones passed to tn_theta_exec).
  *   q_new [chi_max] int32, lambda_new [chi_max] double, gamma_k_new [χ_l·chi_max] and
  *   gamma_k1_new [chi_max·χ_r] complex: DEVICE, caller-owned capacity; the factors are written

@@ -232,7 +232,7 @@ def theta_exec(plan: Plan, gk, lk, gk1, ll, lr, U, out=None, stream=None):
 
 def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None):
     """tn_svd_truncate: per-sector SVD + global top-χ + new canonical factors (single-charge or MPO pair
-    plans). `theta` (the list from theta_exec) may be DESTROYED. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
+    plans). `theta` (the list from theta_exec) is only read. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
     [chi × χ_r], discarded) as contiguous CUDA tensors (views of chi_max-capacity buffers)."""
     chi_l, _, chi_r = plan.chi
     dev = ll.device

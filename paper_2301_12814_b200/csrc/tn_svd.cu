@@ -44,6 +44,7 @@ struct SvdCtx {  // cuSOLVER handles / streams + a grow-only device scratch, per
   cudaStream_t st[SVD_LANES] = {};
   cudaEvent_t ev[SVD_LANES + 1] = {};
   gesvdjInfo_t params = nullptr;
+  gesvdjInfo_t pj[SVD_LANES] = {};  // per-lane Jacobi settings (the info object also carries results)
   cusolverDnParams_t xparams = nullptr;
   void* buf = nullptr;   // common scratch (library-SVD outputs, ranking buffers)
   size_t cap = 0;
@@ -64,8 +65,9 @@ int svd_algo() {
   if (e && std::string(e) == "gesvdp") return 1;
   return 2;
 }
-// largest h_err_sigma accepted from Xgesvdp in the Ritz step before it is redone by one-sided Jacobi
-constexpr double kRitzHerrMax = 1e-13;
+// largest h_err_sigma accepted from Xgesvdp (Ritz step and TN_SVD_ALGO=gesvdp) before Jacobi redoes it:
+// healthy config-2/3 sectors report 0 … 3.9e-13, the failure seen on small rank-deficient sectors 5.1e-8
+constexpr double kRitzHerrMax = 1e-11;
 tn_status grow(void*& buf, size_t& cap, size_t need, char** out) {  // grow-only device scratch
   if (need > cap) {
     if (buf) cudaFree(buf);
@@ -602,6 +604,11 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
       return fail(TN_ERR_CUDA, "cusolverDnCreateGesvdjInfo failed");
     cusolverDnXgesvdjSetTolerance(X.params, 0.0);      // 0 → machine accuracy
     cusolverDnXgesvdjSetMaxSweeps(X.params, 100);
+    for (auto& q : X.pj) {
+      if (cusolverDnCreateGesvdjInfo(&q) != CUSOLVER_STATUS_SUCCESS) return fail(TN_ERR_CUDA, "gesvdj info");
+      cusolverDnXgesvdjSetTolerance(q, 0.0);
+      cusolverDnXgesvdjSetMaxSweeps(q, 100);
+    }
     if (cusolverDnCreateParams(&X.xparams) != CUSOLVER_STATUS_SUCCESS) return fail(TN_ERR_CUDA, "cusolver params");
   }
   const int algo = svd_algo();
@@ -613,7 +620,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
   std::vector<int> lwork(ns, 0);
   std::vector<size_t> hbytes(ns, 0), wsz(ns, 0);
   std::vector<int64_t> base(ns + 1, 0);
-  size_t off = 0;
+  size_t off = 0, copy_max = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
     off += (bytes + 255) & ~(size_t)255;
@@ -624,10 +631,12 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     base[c + 1] = base[c] + k;
     if (k == 0 || algo == 2) continue;
     size_t wbytes = 0;
+    // Jacobi workspace: the gesvdj path, and the gesvdp path's fallback
+    if (cusolverDnZgesvdj_bufferSize(X.h[0], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, nullptr, C, nullptr, nullptr, C,
+                                     nullptr, R, &lwork[c], X.params) != CUSOLVER_STATUS_SUCCESS)
+      return fail(TN_ERR_CUDA, "cusolverDnZgesvdj_bufferSize failed");
+    copy_max = std::max(copy_max, (size_t)R * C * 16);
     if (algo == 0) {
-      if (cusolverDnZgesvdj_bufferSize(X.h[0], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, nullptr, C, nullptr, nullptr, C,
-                                       nullptr, R, &lwork[c], X.params) != CUSOLVER_STATUS_SUCCESS)
-        return fail(TN_ERR_CUDA, "cusolverDnZgesvdj_bufferSize failed");
       wbytes = (size_t)lwork[c] * 16;
     } else {
       size_t hb = 0;
@@ -636,6 +645,7 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
                                        &wbytes, &hb) != CUSOLVER_STATUS_SUCCESS)
         return fail(TN_ERR_CUDA, "cusolverDnXgesvdp_bufferSize failed");
       hbytes[c] = hb;
+      wbytes = std::max(wbytes, (size_t)lwork[c] * 16);
     }
     o_ux[c] = take((size_t)C * k * 16);
     o_vx[c] = take((size_t)R * k * 16);
@@ -644,6 +654,8 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     wsz[c] = wbytes;
   }
   const int64_t total_max = base[ns];
+  // library paths: each lane factorises a copy of Θ(c) (the routines overwrite their input; Θ stays intact)
+  const size_t o_copy = take(copy_max * SVD_LANES);
   const size_t o_info = take((size_t)ns * 4);
   const size_t o_n2 = take((size_t)ns * 8);
   const size_t o_kin = take((size_t)std::max<int64_t>(total_max, 1) * 8),
@@ -711,24 +723,38 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
                        "H2D pair positions")) != TN_OK)
     return st;
   auto cost = [&](int c) { return (double)p->R[c] * p->C[c] * std::min(p->R[c], p->C[c]); };
-  // one library SVD (paths 0/1): X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ; Θ(c) is destroyed
+  // one library SVD (paths 0/1) of a lane-private copy of Θ(c): X = Θᵀ (column-major C × R, ld C) = U_x S V_xᴴ.
+  // Xgesvdp (path 1) reports its backward error; above kLibHerrMax the sector is redone by Jacobi (seen:
+  // 5e-8 on small rank-deficient sectors), so both paths are accurate to rounding
   auto lib_svd = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
     const SvdSector& S = sp.sec[c];
     const int R = S.R, C = S.C;
+    auto* Zc = reinterpret_cast<cuDoubleComplex*>(B + o_copy + (size_t)l * copy_max);
+    auto copy_in = [&] {
+      return cudaMemcpyAsync(Zc, theta[c], (size_t)R * C * 16, cudaMemcpyDeviceToDevice, X.st[l]) == cudaSuccess;
+    };
+    auto jacobi = [&] {
+      return cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, Zc, C, const_cast<double*>(S.s),
+                               reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)), C,
+                               reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
+                               reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c, X.pj[l]);
+    };
+    if (!copy_in()) return "copy of sector " + std::to_string(c) + " failed";
     cusolverStatus_t r;
     if (algo == 0) {
-      r = cusolverDnZgesvdj(X.h[l], CUSOLVER_EIG_MODE_VECTOR, 1, C, R, reinterpret_cast<cuDoubleComplex*>(theta[c]), C,
-                            const_cast<double*>(S.s), reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.ux)), C,
-                            reinterpret_cast<cuDoubleComplex*>(const_cast<double2*>(S.vx)), R,
-                            reinterpret_cast<cuDoubleComplex*>(B + o_w[c]), lwork[c], d_info + c, X.params);
+      r = jacobi();
     } else {
       hbuf.resize(std::max<size_t>(hbytes[c], 1));
       double herr = 0.0;
-      r = cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, CUDA_C_64F, theta[c], C, CUDA_R_64F,
+      r = cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, C, R, CUDA_C_64F, Zc, C, CUDA_R_64F,
                             const_cast<double*>(S.s), CUDA_C_64F, const_cast<double2*>(S.ux), C, CUDA_C_64F,
                             const_cast<double2*>(S.vx), R, CUDA_C_64F, B + o_w[c], wsz[c], hbuf.data(), hbytes[c],
                             d_info + c, &herr);
       if (getenv("TN_SVD_PROFILE")) fprintf(stderr, "[svd] gesvdp sector %d %dx%d h_err_sigma %.3e\n", c, R, C, herr);
+      if (r == CUSOLVER_STATUS_SUCCESS && !(herr <= kRitzHerrMax)) {
+        if (!copy_in()) return "copy of sector " + std::to_string(c) + " failed";
+        r = jacobi();
+      }
     }
     return r == CUSOLVER_STATUS_SUCCESS ? std::string()
                                         : "cuSOLVER SVD failed in sector " + std::to_string(c) + " (status " +

@@ -40,10 +40,9 @@ def test_layers_match_oracle(tn, M, N, d, chi, chi_max, seed):
 
 
 # ------------------------------------------------------------------ MPO (vectorized density matrix) layers
-# TN_SVD_ALGO=gesvdp is left out: cuSOLVER's polar-decomposition SVD reports h_err_sigma up to 5e-8 on the
-# small rank-deficient sectors the no-truncation case produces; the default Gram
-# path guards its own Xgesvdp call with a Jacobi fallback
-@pytest.mark.parametrize("algo", ["gram", "gesvdj"])
+# every SVD algorithm: the no-truncation case produces small rank-deficient sectors on which cuSOLVER's
+# polar-decomposition SVD reports h_err_sigma up to 5e-8 — both Xgesvdp uses fall back to Jacobi there
+@pytest.mark.parametrize("algo", ["gram", "gesvdp", "gesvdj"])
 @pytest.mark.parametrize("M,N,d,chi,chi_max,seed", [(4, 2, 3, 6, 10 ** 6, 0), (5, 2, 3, 8, 10, 1), (4, 3, 3, 9, 14, 2)])
 def test_mpo_layers_match_oracle(tn, M, N, d, chi, chi_max, seed, algo, monkeypatch):
     monkeypatch.setenv("TN_SVD_ALGO", algo)

@@ -170,3 +170,15 @@ def test_pair_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
             if A.shape[1]:
                 assert np.allclose(A.conj().T @ A, np.eye(A.shape[1]), atol=1e-12)
                 assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_svd_leaves_theta_intact(tn, algo, monkeypatch):
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    case = synth.make_config(1)
+    plan, U, got = gpu_theta(case)
+    t = [torch.from_numpy(np.ascontiguousarray(g)).cuda() for g in got]
+    before = [x.clone() for x in t]
+    tn.svd_truncate(plan, t, torch.from_numpy(case.lam_l).cuda(), torch.from_numpy(case.lam_r).cuda(), 50)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(t, before))
