@@ -9,24 +9,27 @@
 // B200 design (DESIGN.md §4 "K4"): sm_100a has no tcgen05 FP64 MMA (`kind::f64` does not exist),
 // so the FP64 tensor path is the warp-level DMMA.8x8x4 (mma.sync.m8n8k4.f64), measured at 37.2
 // TFLOP/s. A persistent grid (one CTA per SM) walks a heavy-first tile list; one producer warp
-// streams each 64×16 operand chunk with a single cp.async.bulk (TMA 1-D) copy into a K4_STAGES-deep
-// mbarrier ring; eight consumer warps (2×4, 32×16 complex outputs each) read fragments with
+// streams each 64×32 operand stage (two 64×16 chunks) with a single cp.async.bulk (TMA 1-D) copy per
+// operand into a 3-deep mbarrier ring; eight consumer warps (2×4, 32×16 complex outputs each) read fragments with
 // conflict-free 128-bit LDS (K3 wrote the panels in fragment order). The complex product uses the
 // 3-multiplication (Gauss) form, 3 real DMMAs per complex 8×8×4 step instead of 4:
 //   T1 = Ar·Br, T2 = Ai·Bi, T3 = (Ar+Ai)·(Br+Bi);  Re = T1 − T2,  Im = T3 − T1 − T2
 // (error bound ~ eps·|Ar+Ai||Br+Bi| per term, same order as the 4-product form).
+#include <cstdlib>
+
 #include "k4_device.cuh"
 
 namespace tn {
 
-template <int STAGES>
+template <int STAGES, int CPS>  // CPS: BK-chunks per ring stage (one bulk copy per operand per stage)
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_contract(const GroupDesc* __restrict__ groups, const TileDesc* __restrict__ tiles, int ntiles,
                 const double2* __restrict__ ap, const double2* __restrict__ bp, const SectorParams sp) {
   extern __shared__ __align__(128) uint8_t smem[];
   double2* sA = reinterpret_cast<double2*>(smem);
-  double2* sB = sA + STAGES * CHUNK;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * CHUNK);
+  constexpr int SCH = CPS * CHUNK, SBK = CPS * BK;  // elements / K per stage
+  double2* sB = sA + STAGES * SCH;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * SCH);
   uint64_t* empty = full + STAGES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -55,13 +58,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         }
         const double2* a = ap + g.a_off + (int64_t)td.mt * BM * g.K4;
         const double2* b = bp + g.b_off + (int64_t)td.nt * BN * g.K4;
-        for (int kc = 0; kc * BK < g.K4; ++kc) {
+        for (int kc = 0; kc * SBK < g.K4; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t kcnt = (uint32_t)min(BK, g.K4 - kc * BK);
+          const uint32_t kcnt = (uint32_t)min(SBK, g.K4 - kc * SBK);
           const uint32_t bytes = kcnt * BM * (uint32_t)sizeof(double2);
           mbar_expect_tx(&full[stage], 2 * bytes);
-          bulk_g2s(sA + stage * CHUNK, a + (int64_t)kc * CHUNK, bytes, &full[stage]);
-          bulk_g2s(sB + stage * CHUNK, b + (int64_t)kc * CHUNK, bytes, &full[stage]);
+          bulk_g2s(sA + stage * SCH, a + (int64_t)kc * SCH, bytes, &full[stage]);
+          bulk_g2s(sB + stage * SCH, b + (int64_t)kc * SCH, bytes, &full[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -100,13 +103,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < 6; ++q) acc[mi][ni][q] = 0.0;
 
-    for (int kc = 0; kc * BK < g.K4; ++kc) {
+    for (int kc = 0; kc * SBK < g.K4; ++kc) {
       mbar_wait(&full[stage], phase);
-      const int nks = min(BK, g.K4 - kc * BK) >> 2;
-      const double2* As = sA + stage * CHUNK + wm * 128 + lane;
-      const double2* Bs = sB + stage * CHUNK + wn * 64 + lane;
+      const int nks = min(SBK, g.K4 - kc * SBK) >> 2;
+      const double2* As = sA + stage * SCH + wm * 128 + lane;
+      const double2* Bs = sB + stage * SCH + wn * 64 + lane;
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
+      for (int ks = 0; ks < 4 * CPS; ++ks) {
         if (ks < nks) {
           double2 a[4], b[2];
 #pragma unroll
@@ -163,17 +166,26 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   }
 }
 
-cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
-  if (p->ntiles == 0) return cudaSuccess;
-  constexpr int STAGES = K4_STAGES;
-  const size_t smem = (size_t)STAGES * CHUNK * sizeof(double2) * 2 + 2 * STAGES * sizeof(uint64_t);
+template <int STAGES, int CPS>
+static cudaError_t contract_cfg(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
+  const size_t smem = (size_t)STAGES * CPS * CHUNK * sizeof(double2) * 2 + 2 * STAGES * sizeof(uint64_t);
   // set on every launch (microseconds): the attribute is per device, and a process may drive several
-  cudaError_t e = cudaFuncSetAttribute(k4_contract<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(k4_contract<STAGES, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t grid = std::min<int64_t>(p->ntiles, (int64_t)p->sm_count);
-  k4_contract<STAGES><<<(unsigned)grid, K4_THREADS, smem, s>>>(p->d_groups, p->d_tiles, (int)p->ntiles,
-                                                                p->d_apanel, p->d_bpanel, sp);
+  k4_contract<STAGES, CPS><<<(unsigned)grid, K4_THREADS, smem, s>>>(p->d_groups, p->d_tiles, (int)p->ntiles,
+                                                                     p->d_apanel, p->d_bpanel, sp);
   return cudaGetLastError();
+}
+
+cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
+  if (p->ntiles == 0) return cudaSuccess;
+  // 3 stages of 2 chunks (32-deep K per barrier round trip) by default: 2.533 vs 2.558 ms for 6 stages of
+  // one chunk at config 3, 18.88 vs 19.03 ms at config 4 (TN_K4_CPS=1 selects the latter)
+  static const int cps = getenv("TN_K4_CPS") ? atoi(getenv("TN_K4_CPS")) : 2;
+  if (cps == 1) return contract_cfg<K4_STAGES, 1>(p, sp, s);
+  return contract_cfg<3, 2>(p, sp, s);
 }
 
 }  // namespace tn
