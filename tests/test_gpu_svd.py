@@ -182,3 +182,25 @@ def test_svd_leaves_theta_intact(tn, algo, monkeypatch):
     tn.svd_truncate(plan, t, torch.from_numpy(case.lam_l).cuda(), torch.from_numpy(case.lam_r).cuda(), 50)
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for a, b in zip(t, before))
+
+
+@pytest.mark.parametrize("name,N,d,chi,chi_max", [("N0", 0, 2, (5, 4, 6), 3), ("chi1", 2, 3, (20, 18, 22), 1),
+                                                  ("ragged", 3, 2, (37, 29, 41), 25)])
+def test_pair_svd_edge_cases(tn, name, N, d, chi, chi_max):
+    from test_gpu_pair import gpu_theta2
+    c = synth.make_pair_case(N, d, *chi, seed=17, charges="uniform", lam="random")
+    plan, got = gpu_theta2(tn, c)
+    t = [torch.from_numpy(np.ascontiguousarray(got[(s // (N + 1), s % (N + 1))])).cuda() for s in range((N + 1) ** 2)]
+    res = tn.svd_truncate(plan, t, torch.from_numpy(c.lam_l).cuda(), torch.from_numpy(c.lam_r).cuda(), chi_max)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
+    ref = osvd.truncate_update2(N, c.d, c.q1_l, c.q2_l, c.q1_r, c.q2_r, got, c.lam_l, c.lam_r, chi_max)
+    assert res["chi"] == ref["chi"] and np.array_equal(res["q_new"], ref["q_new"]), name
+    smax = max((float(s.max()) for s in ref["svals"] if s.size), default=1.0)
+    assert np.max(np.abs(res["lam_new"] - ref["lam_new"]), initial=0.0) <= 1e-12 * smax
+    for c1 in range(N + 1):
+        for c2 in range(N + 1):
+            if got[(c1, c2)].size:
+                rg, _, _ = _recon2(c, res, c1, c2, res["q_new"])
+                rr, *_ = _recon2(c, ref, c1, c2, ref["q_new"])
+                assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), (name, c1, c2)
