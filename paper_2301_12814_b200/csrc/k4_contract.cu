@@ -108,34 +108,39 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
       const int nks = min(SBK, g.K4 - kc * SBK) >> 2;
       const double2* As = sA + stage * SCH + wm * 128 + lane;
       const double2* Bs = sB + stage * SCH + wn * 64 + lane;
+      // one 8×8×4 complex step: the Gauss sums first, then all T1/T2 products (which do not need them), then
+      // the T3 products — every DMMA is issued well after the DADD that feeds it
+      auto kstep = [&](int ks) {
+        double2 a[4], b[2];
 #pragma unroll
-      for (int ks = 0; ks < 4 * CPS; ++ks) {
-        if (ks < nks) {
-          double2 a[4], b[2];
+        for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks * 256 + mi * 32];
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks * 256 + mi * 32];
+        for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
+        double asum[4], bsum[2];
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
-          // the Gauss sums first, then all T1/T2 products (which do not need them), then the T3 products:
-          // every DMMA is issued well after the DADD that feeds it (no fixed-latency dependency stall)
-          double asum[4], bsum[2];
+        for (int ni = 0; ni < 2; ++ni) bsum[ni] = b[ni].x + b[ni].y;
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) bsum[ni] = b[ni].x + b[ni].y;
+        for (int mi = 0; mi < 4; ++mi) asum[mi] = a[mi].x + a[mi].y;
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) asum[mi] = a[mi].x + a[mi].y;
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
+          for (int ni = 0; ni < 2; ++ni) {
+            double* c = acc[mi][ni];
+            dmma(c[0], c[1], a[mi].x, b[ni].x);  // T1 += Ar·Br
+            dmma(c[2], c[3], a[mi].y, b[ni].y);  // T2 += Ai·Bi
+          }
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-              double* c = acc[mi][ni];
-              dmma(c[0], c[1], a[mi].x, b[ni].x);  // T1 += Ar·Br
-              dmma(c[2], c[3], a[mi].y, b[ni].y);  // T2 += Ai·Bi
-            }
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
+          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][4], acc[mi][ni][5], asum[mi], bsum[ni]);  // T3
+      };
+      if (nks == 4 * CPS) {  // full stage: no guards, so the fragment loads of step ks+1 can overlap step ks
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][4], acc[mi][ni][5], asum[mi], bsum[ni]);  // T3
-        }
+        for (int ks = 0; ks < 4 * CPS; ++ks) kstep(ks);
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < 4 * CPS; ++ks)
+          if (ks < nks) kstep(ks);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
