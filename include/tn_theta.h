@@ -96,7 +96,7 @@ TN_API tn_status tn_theta_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64
  * tn_plan_offsets returns (N+1)²+1 entries over the keys. world_size/rank shard the sorted left
  * positions flop-balanced as in tn_theta_plan; a rank's slab of Θ(c1,c2) is the contiguous run of its
  * rows inside [r0, r1) (tn_plan_local_sector_shape gives its first row). tn_theta_exec_sharded accepts
- * pair plans with TN_GATHER_NONE only.
+ * pair plans with every gather mode (sector owners by the same LPT rule over the (N+1)² sectors).
  * Errors: as tn_theta_plan, plus TN_ERR_UNSUPPORTED when (N+1)² exceeds this build's sector limit
  * (N ≤ 9). */
 TN_API tn_status tn_theta2_plan(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r,
@@ -240,6 +240,10 @@ TN_API tn_status tn_comm_unique_id(void* id128);
 /* Bootstrap a communicator; NCCL is loaded at run time (dlopen "libnccl.so.2", or $TN_NCCL_LIB). */
 TN_API tn_status tn_comm_init(const void* id128, int rank, int world_size, tn_comm** out);
 TN_API tn_status tn_comm_destroy(tn_comm* comm);
+/* Where rank `rank`'s slab of sector c lies inside the FULL Θ(c): its first row and row count (HOST
+ * outputs; what the ROOT / SECTOR_OWNER gathers use to place each rank's rows, for single-charge and
+ * pair plans). Errors: DIMENSION (NULL), DOMAIN (c or rank out of range). */
+TN_API tn_status tn_plan_slab_rows(const tn_plan* plan, int c, int rank, int64_t* row_begin, int64_t* rows);
 
 /* tn_theta_exec_sharded — this rank's rows of every Θ(c), plus optional exchange.
  *   plan          built with the communicator's world_size and rank (else TN_ERR_CONSISTENCY).

@@ -121,6 +121,12 @@ class Plan:
         check(lib.tn_plan_flops(self.handle, *(C.byref(x) for x in v)), "tn_plan_flops")
         return dict(zip(("f_contract", "f_mix", "f_exec", "f_contract_local", "f_mix_local"), (x.value for x in v)))
 
+    def slab_rows(self, c: int, rank: int):
+        """tn_plan_slab_rows: (first row, rows) of rank `rank`'s slab inside the full Θ(c)."""
+        b, n = C.c_int64(), C.c_int64()
+        check(lib.tn_plan_slab_rows(self.handle, int(c), int(rank), C.byref(b), C.byref(n)), "tn_plan_slab_rows")
+        return b.value, n.value
+
     def exec_launches(self) -> int:
         """tn_plan_exec_launches: kernel launches of one tn_theta_exec with the current engine."""
         n = C.c_int64()

@@ -40,6 +40,7 @@ SIGNATURES = {
     "tn_plan_flops": [_p, _i64p, _i64p, _i64p, _i64p, _i64p],
     "tn_plan_u_size": [_p, _i64p],
     "tn_plan_exec_launches": [_p, _i64p],
+    "tn_plan_slab_rows": [_p, C.c_int, C.c_int, _i64p, _i64p],
     "tn_plan_workspace_bytes": [_p, _i64p],
     "tn_plan_kernel_times": [_p, _p],
     "tn_plan_set_contraction": [_p, C.c_int, C.c_int],

@@ -371,6 +371,11 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     // ---- MPO pair plan: sectors, groups, two-pass mix (tn_pair.cu) ----
     st = build_pair_tables(p);
     if (st != TN_OK) goto done;
+    {
+      std::vector<int64_t> sizes(p->nsec);
+      for (int c = 0; c < p->nsec; ++c) sizes[c] = p->R[c] * p->C[c];
+      sector_owners(sizes, world_size, p->owner);
+    }
     p->ws_bytes += (int64_t)ct.off;
     TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     u_layout(p);

@@ -111,12 +111,35 @@ tn_status tn_comm_destroy(tn_comm* comm) {
   return st;
 }
 
+// Rows of Θ(c) whose sorted left position is < pos: its rows are [row0, row0+R) for single-charge plans,
+// and for MPO pair plans whole left pair segments l = (l1, l2), l − (c1, c2) ∈ [0, d−1]², in key order
+static int64_t sector_rows_before(const tn_plan* p, int c, int64_t pos) {
+  if (!p->pair) return std::min(std::max(pos, p->row0[c]), p->row0[c] + p->R[c]) - p->row0[c];
+  const int nk = p->N + 1, c1 = c / nk, c2 = c % nk;
+  const auto& ol = p->off[0];
+  int64_t n = 0;
+  for (int l1 = c1; l1 <= std::min(p->N, c1 + p->d - 1); ++l1)
+    for (int l2 = c2; l2 <= std::min(p->N, c2 + p->d - 1); ++l2) {
+      const int l = l1 * nk + l2;
+      n += std::min<int64_t>(std::max<int64_t>(pos - ol[l], 0), (int64_t)ol[l + 1] - ol[l]);
+    }
+  return n;
+}
+
+tn_status tn_plan_slab_rows(const tn_plan* p, int c, int rank, int64_t* row_begin, int64_t* rows) {
+  if (!p || !row_begin || !rows) return fail(TN_ERR_DIMENSION, "tn_plan_slab_rows: NULL");
+  if (c < 0 || c >= p->nsec) return fail(TN_ERR_DOMAIN, "tn_plan_slab_rows: sector out of range");
+  if (rank < 0 || rank >= p->world) return fail(TN_ERR_DOMAIN, "tn_plan_slab_rows: rank out of range");
+  const int64_t b = sector_rows_before(p, c, p->bounds[rank]), e = sector_rows_before(p, c, p->bounds[rank + 1]);
+  *row_begin = b;
+  *rows = e - b;
+  return TN_OK;
+}
+
 tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* comm, double* gamma_k,
                                 double* lambda_k, double* gamma_k1, double* lambda_l, double* lambda_r, double* U,
                                 double* const* theta_out, int bcast_operands, int gather_mode) {
   if (!p || !comm) return fail(TN_ERR_DIMENSION, "tn_theta_exec_sharded: NULL plan/comm");
-  if (p->pair && gather_mode != TN_GATHER_NONE)
-    return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_sharded: pair (MPO) plans support TN_GATHER_NONE only");
   if (p->world != comm->world || p->rank != comm->rank)
     return fail(TN_ERR_CONSISTENCY, "tn_theta_exec_sharded: plan world/rank differ from the communicator's");
   if (gather_mode != TN_GATHER_NONE && gather_mode != TN_GATHER_ROOT && gather_mode != TN_GATHER_SECTOR_OWNER)
@@ -141,14 +164,15 @@ tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* com
     st = nccl_check(r != ncclSuccess ? r : r2, "operand broadcast");
     if (st != TN_OK) return st;
   }
+  auto rows_before = [&](int c, int64_t pos) { return sector_rows_before(p, c, pos); };
   // Local slabs: where this rank receives a whole sector (ROOT: rank 0, SECTOR_OWNER: the sector's owner)
-  // the caller passed the FULL Θ(c), so this rank's slab starts at row (lrow0 − row0).
+  // the caller passed the FULL Θ(c), so this rank's slab starts at row rows_before(c, r0).
   auto dest = [&](int c) { return gather_mode == TN_GATHER_ROOT ? 0 : p->owner[c]; };
-  std::vector<double*> local(p->N + 1, nullptr);
-  for (int c = 0; c <= p->N; ++c) {
+  std::vector<double*> local(p->nsec, nullptr);
+  for (int c = 0; c < p->nsec; ++c) {
     double* base = theta_out[c];
     if (gather_mode != TN_GATHER_NONE && p->world > 1 && dest(c) == p->rank && base)
-      base += 2 * (p->lrow0[c] - p->row0[c]) * p->C[c];
+      base += 2 * rows_before(c, p->r0) * p->C[c];
     local[c] = base;
   }
   st = tn_theta_exec(p, stream, gamma_k, lambda_k, gamma_k1, lambda_l, lambda_r, U, local.data());
@@ -156,16 +180,15 @@ tn_status tn_theta_exec_sharded(const tn_plan* p, tn_stream stream, tn_comm* com
   st = nccl_check(api.GroupStart(), "ncclGroupStart");
   if (st != TN_OK) return st;
   ncclResult_t r = ncclSuccess;
-  for (int c = 0; c <= p->N && r == ncclSuccess; ++c) {
-    const int64_t a0 = p->row0[c], a1 = a0 + p->R[c], C = p->C[c];
+  for (int c = 0; c < p->nsec && r == ncclSuccess; ++c) {
+    const int64_t C = p->C[c];
     const int to = dest(c);
     if (p->rank == to) {
       for (int src = 0; src < p->world && r == ncclSuccess; ++src) {
         if (src == to) continue;
-        const int64_t s0 = std::min(std::max(a0, p->bounds[src]), a1);
-        const int64_t s1 = std::min(std::max(a0, p->bounds[src + 1]), a1);
+        const int64_t s0 = rows_before(c, p->bounds[src]), s1 = rows_before(c, p->bounds[src + 1]);
         if (s1 > s0 && C > 0)
-          r = api.Recv(theta_out[c] + 2 * (s0 - a0) * C, (size_t)(2 * (s1 - s0) * C), ncclFloat64, src, comm->comm, s);
+          r = api.Recv(theta_out[c] + 2 * s0 * C, (size_t)(2 * (s1 - s0) * C), ncclFloat64, src, comm->comm, s);
       }
     } else if (p->lR[c] * C > 0) {
       r = api.Send(theta_out[c], (size_t)(2 * p->lR[c] * C), ncclFloat64, to, comm->comm, s);

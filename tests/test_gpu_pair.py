@@ -194,3 +194,31 @@ def test_pair_sharded_equals_unsharded(tn, world):
         assert pos == full[key].shape[0]
         if parts:
             assert np.array_equal(np.concatenate([p for _, p in parts], axis=0), full[key]), key
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_gather_placement_and_owners(tn, world):
+    # what tn_theta_exec_sharded's ROOT / SECTOR_OWNER gathers use for every source rank: tn_plan_slab_rows
+    # must place rank r's slab exactly where rank r's own plan says it starts (tn_plan_local_sector_shape),
+    # for MPO pair plans and single-charge plans; pair-plan owners follow the LPT rule over (N+1)² sectors
+    c = _pair(2)
+    plans = [tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r, world, r) for r in range(world)]
+    s1 = synth.make_config(2)
+    singles = [tn.Plan(s1.d, s1.N, s1.q_l, s1.q_c, s1.q_r, world, r) for r in range(world)]
+    for ps in (plans, singles):
+        for s in range(ps[0].nsec):
+            R, _ = ps[0].sector_shape(s)
+            pos = 0
+            for r in range(world):
+                Rl, _, b = ps[r].local_sector_shape(s)
+                got = ps[0].slab_rows(s, r)
+                if Rl:
+                    assert got == (b, Rl), (s, r)
+                    assert b == pos
+                    pos += Rl
+                else:
+                    assert got[1] == 0
+            assert pos == R, s
+    sizes = [int(np.prod(plans[0].sector_shape(s))) for s in range(plans[0].nsec)]
+    want = tn.sector_owners_host(sizes, world)
+    assert [plans[0].sector_owner(s) for s in range(plans[0].nsec)] == list(want)
