@@ -2,7 +2,9 @@
 
 Every output buffer the library writes — each Θ(c) slab, the SVD step's q/λ/Γ outputs — is carved out of one
 allocation with guard zones before and after it, all filled with a sentinel bit pattern; after the call
-every guard must still hold the sentinel, and the read-only inputs (Γ, λ, U) must be unchanged. Covers the
+every guard must still hold the sentinel, and the read-only inputs (Γ, λ, U) must be unchanged. The
+inputs themselves sit between NaN guard zones, and the result must equal a run on plain buffers bit for
+bit (an out-of-bounds READ reaching a guard would turn it into NaN). Covers the
 FP64 DMMA, INT8-emulation and paper-literal engines, MPO pair plans, sharded slabs, edge shapes and the SVD
 step."""
 import ctypes as C
@@ -44,19 +46,35 @@ def _check_guards(big, guards, sent=SENT, what=""):
         assert bool((big[a:b] == sent).all().item()), f"{what}: guard [{a}, {b}) overwritten"
 
 
+def _nan_guarded(t):
+    """A copy of device tensor t inside an allocation whose guard zones hold NaN (an out-of-bounds READ
+    that reaches them turns the result into NaN)."""
+    nan = complex("nan+nanj") if t.is_complex() else float("nan")
+    big, (v,), _ = _guarded([tuple(t.shape)], dtype=t.dtype, sent=nan)
+    v.copy_(t)
+    return big, v
+
+
 def _exec_guarded(tn, plan, case, U):
     shapes = [plan.local_sector_shape(c)[:2] for c in range(plan.nsec)]
     big, views, guards = _guarded(shapes)
     t = to_dev(case)
-    before = {k: v.clone() for k, v in t.items()}
-    Ub = U.clone()
+    ref = tn.theta_exec(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U)   # plain buffers
+    keep, g = [], {}
+    for k, v in t.items():
+        b, g[k] = _nan_guarded(v)
+        keep.append(b)
+    bu, Ug = _nan_guarded(U)
     out = [v if v is not None else torch.empty((0, 0), dtype=torch.complex128, device="cuda") for v in views]
-    tn.theta_exec(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U, out=out)
+    tn.theta_exec(plan, g["gk"], g["lk"], g["gk1"], g["ll"], g["lr"], Ug, out=out)
     torch.cuda.synchronize()
     _check_guards(big, guards, what="Θ slabs")
     for k, v in t.items():
-        assert torch.equal(v, before[k]), f"input {k} modified"
-    assert torch.equal(U, Ub), "U modified"
+        assert torch.equal(g[k], v), f"input {k} modified"
+    assert torch.equal(Ug, U), "U modified"
+    for c, (a, r) in enumerate(zip(out, ref)):   # NaN guards never reached: identical results
+        if a.numel() or r.numel():
+            assert torch.equal(a, r), f"sector {c} differs with NaN-guarded inputs"
     return out
 
 
