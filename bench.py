@@ -551,11 +551,27 @@ def run_layer(args, rank, world, local_rank):
     mps = MPS(N, d, qd, gam, lam, device=dev)
     th = rng.uniform(0, math.pi / 2, M)
     ph = rng.uniform(0, 2 * math.pi, M)
+    # warm-up: `--warmup` full-size gates on a throw-away copy (library handles, SVD scratch, memory pool)
+    kw = M // 2 - 1
+    for _ in range(args.warmup):
+        w = MPS(N, d, [x.clone() for x in qd], [x.clone() for x in gam], [x.clone() for x in lam], device=dev)
+        w.apply_gate(kw, th[0], ph[0], chi_max)
+        del w
     torch.cuda.synchronize()
     if group is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    disc = mps.apply_layer(0, th, ph, chi_max, group=group) + mps.apply_layer(1, th, ph, chi_max, group=group)
+    gate_ms = []
+    if group is None:   # one GPU: the same gates as apply_layer, timed one by one
+        disc = []
+        for parity in (0, 1):
+            for g, k in enumerate(range(parity, M - 1, 2)):
+                tg = time.perf_counter()
+                disc.append(mps.apply_gate(k, th[g], ph[g], chi_max))
+                torch.cuda.synchronize()
+                gate_ms.append(round((time.perf_counter() - tg) * 1e3, 1))
+    else:
+        disc = mps.apply_layer(0, th, ph, chi_max, group=group) + mps.apply_layer(1, th, ph, chi_max, group=group)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     if group is not None:
@@ -566,14 +582,15 @@ def run_layer(args, rank, world, local_rank):
             return
     ngates = len(disc)
     line = {"metric": "brick-wall TEBD gates/s (Θ + per-sector SVD + truncation per gate)",
-            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": world, "steps": ngates, "warmup": 0,
+            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": world, "steps": ngates, "warmup": args.warmup,
             "ms_per_step": round(dt / ngates * 1e3, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-drawn Γ, config-shaped bonds)",
             "config": {"workload": f"{M}-site MPS, two brick-wall layers, inner bonds of BASELINE.json config "
                                    f"{args.config} (N={N}, d={d}, chi={chi}), chi_max={chi_max}",
                        "timing": "host wall clock around whole layers (tn_svd_truncate synchronises per gate), max over ranks",
                        "parallelism": f"layer-parallel over {world} GPU(s): gates dealt by LPT, results broadcast (NCCL)"},
-            "bond_dims_after": [int(x.numel()) for x in mps.lam], "discarded": [float(x) for x in disc]}
+            "bond_dims_after": [int(x.numel()) for x in mps.lam], "discarded": [float(x) for x in disc],
+            "gate_ms": gate_ms}
     print(json.dumps(line), flush=True)
 
 

@@ -70,11 +70,19 @@ int svd_algo() {
 constexpr double kRitzHerrMax = 1e-11;
 tn_status grow(void*& buf, size_t& cap, size_t need, char** out) {  // grow-only device scratch
   if (need > cap) {
+    // 25% headroom: the sector shapes of consecutive gates differ, and every regrowth is a synchronising
+    // cudaFree + cudaMalloc on the gate's critical path
+    const size_t want = need + need / 4;
     if (buf) cudaFree(buf);
     buf = nullptr;
     cap = 0;
-    if (cudaMalloc(&buf, need) != cudaSuccess) return fail(TN_ERR_OOM, "tn_svd_truncate: scratch allocation");
-    cap = need;
+    if (cudaMalloc(&buf, want) != cudaSuccess) {
+      cudaGetLastError();
+      if (cudaMalloc(&buf, need) != cudaSuccess) return fail(TN_ERR_OOM, "tn_svd_truncate: scratch allocation");
+      cap = need;
+    } else {
+      cap = want;
+    }
   }
   *out = static_cast<char*>(buf);
   return TN_OK;
