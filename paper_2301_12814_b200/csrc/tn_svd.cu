@@ -268,7 +268,7 @@ tn_status run_lanes(SvdCtx& X, cudaStream_t s, std::vector<int> wave, Cost cost,
 //     with w ≥ T² − 2Δ (Δ = the largest error bound 16·n_g·ε·w_max over sectors) and w ≥ cutoff² − Δ_c, so
 //     every value that can make the exact top χ (or pass the cutoff) is inside E_k'. The norm bound of the
 //     library path skips whole sectors the same way (‖Θ(c)‖²_F < T² − Δ).
-//  C. Rayleigh–Ritz: Y = Z·E_k' (tall) or Zᴴ·E_k' (max(R,C) × k', ZGEMM), exact SVD Y = P S Wᴴ (Xgesvdp),
+//  C. Rayleigh–Ritz: Y = Z·E_k' (tall) or Zᴴ·E_k' (max(R,C) × k', ZGEMM), exact SVD Y = P S Wᴴ (one-sided Jacobi),
 //     then Z ≈ P S (E_k' W)ᴴ (tall) or (E_k' W) S Pᴴ. Ritz values are accurate to second order in the
 //     subspace error, i.e. to ~ε relative, and both factors are orthonormal to ~ε. The weight outside the
 //     computed values, ‖Θ(c)‖²_F − Σ S², joins the discarded weight. Θ(c) is read, not destroyed.
@@ -491,15 +491,21 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
         q.tall ? cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.C, k, q.R, &one, Z, q.C, E, q.R, &zero, T, q.C)
                : cublasZgemm(X.hb[l], CUBLAS_OP_C, CUBLAS_OP_N, q.R, k, q.C, &one, Z, q.C, E, q.C, &zero, T, q.R);
     if (b != CUBLAS_STATUS_SUCCESS) return "cuBLAS Ritz projection failed in sector " + std::to_string(c);
-    hbuf.resize(std::max<size_t>(hsC[c], 1));
+    // one-sided Jacobi by default: Y = Z·E_k' already has nearly orthogonal columns (E_k' are eigenvectors of
+    // ZᴴZ), so it converges in a few sweeps and is accurate to rounding (config 3: Ritz 89 vs 110 ms with the
+    // polar-decomposition Xgesvdp, which TN_RITZ_POLAR=1 selects, guarded by its backward-error report)
+    static const bool ritz_jacobi = getenv("TN_RITZ_POLAR") == nullptr;
     double herr = 0.0;
-    const cusolverStatus_t r =
-        cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, q.mt, k, CUDA_C_64F, T, q.mt, CUDA_R_64F,
-                          Cb + oS[c], CUDA_C_64F, Cb + oP[c], q.mt, CUDA_C_64F, Wm, k, CUDA_C_64F, Cb + oWc[c], wsC[c],
-                          hbuf.data(), hsC[c], infoC + c, &herr);
-    if (r != CUSOLVER_STATUS_SUCCESS) return "cuSOLVER Ritz SVD failed in sector " + std::to_string(c);
-    if (getenv("TN_SVD_PROFILE")) fprintf(stderr, "[svd] ritz sector %d %dx%d h_err_sigma %.3e\n", c, q.mt, k, herr);
-    if (!(herr <= kRitzHerrMax)) {
+    if (!ritz_jacobi) {
+      hbuf.resize(std::max<size_t>(hsC[c], 1));
+      const cusolverStatus_t r =
+          cusolverDnXgesvdp(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, 1, q.mt, k, CUDA_C_64F, T, q.mt, CUDA_R_64F,
+                            Cb + oS[c], CUDA_C_64F, Cb + oP[c], q.mt, CUDA_C_64F, Wm, k, CUDA_C_64F, Cb + oWc[c], wsC[c],
+                            hbuf.data(), hsC[c], infoC + c, &herr);
+      if (r != CUSOLVER_STATUS_SUCCESS) return "cuSOLVER Ritz SVD failed in sector " + std::to_string(c);
+      if (getenv("TN_SVD_PROFILE")) fprintf(stderr, "[svd] ritz sector %d %dx%d h_err_sigma %.3e\n", c, q.mt, k, herr);
+    }
+    if (ritz_jacobi || !(herr <= kRitzHerrMax)) {
       // the polar-decomposition SVD reports a large backward error (seen up to 5e-8 on small rank-deficient
       // matrices): recompute Y and take the one-sided Jacobi SVD instead (accurate to rounding, slower)
       ++n_jacobi;
