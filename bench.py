@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--layer", type=int, default=None, metavar="M",
                     help="time brick-wall layers (Θ + SVD per gate) on an M-site MPS with config-N bonds")
     ap.add_argument("--chi-max", type=int, default=None, help="layer mode: truncation χ (default: the config's χ)")
+    ap.add_argument("--mpo", type=int, default=None, metavar="K",
+                    help="layer mode on an MPO (vectorized density matrix, pair charges) shaped like synth.PAIR_CONFIGS[K]")
     ap.add_argument("--pair", type=int, default=None,
                     help="time the MPO doubled-charge path on synth.PAIR_CONFIGS[k] instead (tn_theta2_plan)")
     return ap.parse_args()
@@ -518,28 +520,48 @@ def run_layer(args, rank, world, local_rank):
     import torch
 
     import synth
-    from paper_2301_12814_b200.mps import MPS
+    from paper_2301_12814_b200.mps import MPO, MPS
 
     import torch.distributed as dist
-    group = dist.group.WORLD if world > 1 else None
+    mpo = args.mpo is not None
+    if mpo and rank != 0:
+        return                      # MPO layers run on rank 0 (layer parallelism is implemented for MPS)
+    group = dist.group.WORLD if world > 1 and not mpo else None
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg = synth.CONFIGS[args.config]
+    cfg = synth.PAIR_CONFIGS[args.mpo] if mpo else synth.CONFIGS[args.config]
     N, d, chi, M = cfg["N"], cfg["d"], cfg["chi"], args.layer
     chi_max = args.chi_max or chi
     rng = np.random.default_rng(cfg["seed"] + 77)
     gen = torch.Generator(device=dev)
     gen.manual_seed(cfg["seed"] + 77)
-    q = [np.array([N], np.int32)]
-    for k in range(1, M):
+
+    def bond_charges(k):   # Gaussian charges in bond k's reachable window (photons to the right)
         lo, hi = max(0, N - k * (d - 1)), min(N, (M - k) * (d - 1))
-        q.append(np.sort(np.clip(np.rint(rng.normal(N / 2, N / 4, chi)), lo, hi)).astype(np.int32))
-    q.append(np.array([0], np.int32))
-    qd = [torch.from_numpy(x).to(dev) for x in q]
+        return np.clip(np.rint(rng.normal(N / 2, N / 4, chi)), lo, hi).astype(np.int32)
+
+    def ends():
+        return np.array([N], np.int32), np.array([0], np.int32)
+    if mpo:   # two independent species per bond, lexicographic order (synth's pair recipe)
+        q1, q2 = [ends()[0]], [ends()[0]]
+        for k in range(1, M):
+            a, b = bond_charges(k), bond_charges(k)
+            o = np.lexsort((b, a))
+            q1.append(a[o])
+            q2.append(b[o])
+        q1.append(ends()[1])
+        q2.append(ends()[1])
+        qs = [[torch.from_numpy(x).to(dev) for x in q1], [torch.from_numpy(x).to(dev) for x in q2]]
+    else:
+        q = [ends()[0]] + [np.sort(bond_charges(k)) for k in range(1, M)] + [ends()[1]]
+        qs = [[torch.from_numpy(x).to(dev) for x in q]]
     gam = []
     for k in range(M):
-        a, b = qd[k].long(), qd[k + 1].long()
-        m = ((a[:, None] - b[None, :]) >= 0) & ((a[:, None] - b[None, :]) <= d - 1)
+        m = None
+        for qq in qs:
+            a, b = qq[k].long(), qq[k + 1].long()
+            mk = ((a[:, None] - b[None, :]) >= 0) & ((a[:, None] - b[None, :]) <= d - 1)
+            m = mk if m is None else m & mk
         x = torch.randn(tuple(m.shape), generator=gen, device=dev, dtype=torch.float64)
         y = torch.randn(tuple(m.shape), generator=gen, device=dev, dtype=torch.float64)
         gam.append(torch.complex(x, y) / math.sqrt(2) * m)
@@ -548,13 +570,19 @@ def run_layer(args, rank, world, local_rank):
         v = torch.from_numpy(0.995 ** np.arange(chi)).to(dev)
         lam.append(v / torch.linalg.vector_norm(v))
     lam.append(torch.ones(1, dtype=torch.float64, device=dev))
-    mps = MPS(N, d, qd, gam, lam, device=dev)
+
+    def make_state(clone=False):
+        cp = (lambda xs: [x.clone() for x in xs]) if clone else (lambda xs: xs)
+        if mpo:
+            return MPO(N, d, cp(qs[0]), cp(qs[1]), cp(gam), cp(lam), device=dev)
+        return MPS(N, d, cp(qs[0]), cp(gam), cp(lam), device=dev)
+    mps = make_state()
     th = rng.uniform(0, math.pi / 2, M)
     ph = rng.uniform(0, 2 * math.pi, M)
     # warm-up: `--warmup` full-size gates on a throw-away copy (library handles, SVD scratch, memory pool)
     kw = M // 2 - 1
     for _ in range(args.warmup):
-        w = MPS(N, d, [x.clone() for x in qd], [x.clone() for x in gam], [x.clone() for x in lam], device=dev)
+        w = make_state(clone=True)
         w.apply_gate(kw, th[0], ph[0], chi_max)
         del w
     torch.cuda.synchronize()
@@ -581,14 +609,18 @@ def run_layer(args, rank, world, local_rank):
         if rank != 0:
             return
     ngates = len(disc)
-    line = {"metric": "brick-wall TEBD gates/s (Θ + per-sector SVD + truncation per gate)",
-            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": world, "steps": ngates, "warmup": args.warmup,
+    line = {"metric": ("MPO " if mpo else "") + "brick-wall TEBD gates/s (Θ + per-sector SVD + truncation per gate)",
+            "value": round(ngates / dt, 4), "unit": "gates/s", "n_gpus": world if group is not None else 1, "steps": ngates,
+            "warmup": args.warmup,
             "ms_per_step": round(dt / ngates * 1e3, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-drawn Γ, config-shaped bonds)",
-            "config": {"workload": f"{M}-site MPS, two brick-wall layers, inner bonds of BASELINE.json config "
-                                   f"{args.config} (N={N}, d={d}, chi={chi}), chi_max={chi_max}",
+            "config": {"workload": (f"{M}-site MPO (vectorized density matrix, pair charges, U⊗U*), two brick-wall layers, "
+                                    f"inner bonds shaped like synth.PAIR_CONFIGS[{args.mpo}]" if mpo else
+                                    f"{M}-site MPS, two brick-wall layers, inner bonds of BASELINE.json config {args.config}")
+                                   + f" (N={N}, d={d}, chi={chi}), chi_max={chi_max}",
                        "timing": "host wall clock around whole layers (tn_svd_truncate synchronises per gate), max over ranks",
-                       "parallelism": f"layer-parallel over {world} GPU(s): gates dealt by LPT, results broadcast (NCCL)"},
+                       "parallelism": "single GPU" if group is None else
+                       f"layer-parallel over {world} GPU(s): gates dealt by LPT, results broadcast (NCCL)"},
             "bond_dims_after": [int(x.numel()) for x in mps.lam], "discarded": [float(x) for x in disc],
             "gate_ms": gate_ms}
     print(json.dumps(line), flush=True)
