@@ -23,7 +23,11 @@ __global__ void fill(double2* a, int n, unsigned seed) {
   }
 }
 
+static bool use_j = false;
 struct Job {
+  syevjInfo_t jp = nullptr;
+  int lwj = 0;
+  double2* wj = nullptr;
   cusolverDnHandle_t h;
   cudaStream_t s;
   cusolverDnParams_t prm;
@@ -39,6 +43,7 @@ static double now() { return std::chrono::duration<double, std::milli>(std::chro
 
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 2000, J = 4;
+  use_j = argc > 2 && argv[2][0] == 'j';
   std::vector<Job> jobs(J);
   cusolverDnParams_t shared;
   cusolverDnCreateParams(&shared);
@@ -57,20 +62,29 @@ int main(int argc, char** argv) {
                                 CUDA_R_64F, b.W, CUDA_C_64F, &b.wd, &b.wh);
     CK(cudaMalloc(&b.work, b.wd + 16));
     b.hw.resize(b.wh + 16);
+    cusolverDnCreateSyevjInfo(&b.jp);
+    cusolverDnXsyevjSetTolerance(b.jp, 0.0);
+    cusolverDnXsyevjSetMaxSweeps(b.jp, 100);
+    cusolverDnZheevj_bufferSize(b.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, (cuDoubleComplex*)b.A, n, b.W, &b.lwj, b.jp);
+    CK(cudaMalloc(&b.wj, (size_t)b.lwj * 16 + 16));
   }
   CK(cudaDeviceSynchronize());
   auto run = [&](int j, cusolverDnParams_t p) {
     Job& b = jobs[j];
     cudaMemcpyAsync(b.A, b.A0, (size_t)n * n * 16, cudaMemcpyDeviceToDevice, b.s);
-    cusolverDnXsyevd(b.h, p, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F, b.A, n, CUDA_R_64F, b.W,
-                     CUDA_C_64F, b.work, b.wd, b.hw.data(), b.wh, b.info);
+    if (use_j)
+      cusolverDnZheevj(b.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, (cuDoubleComplex*)b.A, n, b.W,
+                       (cuDoubleComplex*)b.wj, b.lwj, b.info, b.jp);
+    else
+      cusolverDnXsyevd(b.h, p, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F, b.A, n, CUDA_R_64F, b.W,
+                       CUDA_C_64F, b.work, b.wd, b.hw.data(), b.wh, b.info);
   };
   run(0, jobs[0].prm);
   CK(cudaDeviceSynchronize());
   double t = now();
   run(0, jobs[0].prm);
   CK(cudaDeviceSynchronize());
-  printf("{\"n\": %d, \"single_ms\": %.1f", n, now() - t);
+  printf("{\"n\": %d, \"solver\": \"%s\", \"single_ms\": %.1f", n, use_j ? "heevj" : "syevd", now() - t);
   t = now();
   for (int j = 0; j < J; ++j) { Job& b = jobs[j]; cusolverDnSetStream(b.h, jobs[0].s); run(j, b.prm); cusolverDnSetStream(b.h, b.s); }
   CK(cudaDeviceSynchronize());
