@@ -37,7 +37,7 @@ INT8_UMMA_PEAK_TOPS = 4347.9  # measured tcgen05 kind::i8 M=128 N=256 (profiles/
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="tn", choices=["tn", "reference"])
@@ -86,6 +86,7 @@ class ClockSampler:
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
+        self.period = float(os.environ.get("TN_BENCH_NVML_PERIOD_S", "0.005"))
         self.rows = []
         self._stop = threading.Event()
         self._t = None
@@ -109,7 +110,7 @@ class ClockSampler:
                 self.rows.append((sm, mx, pw, rs))
             except Exception:
                 pass
-            self._stop.wait(0.005)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         if self._nv is not None:
