@@ -525,9 +525,7 @@ def run_layer(args, rank, world, local_rank):
 
     import torch.distributed as dist
     mpo = args.mpo is not None
-    if mpo and rank != 0:
-        return                      # MPO layers run on rank 0 (layer parallelism is implemented for MPS)
-    group = dist.group.WORLD if world > 1 and not mpo else None
+    group = dist.group.WORLD if world > 1 else None
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = synth.PAIR_CONFIGS[args.mpo] if mpo else synth.CONFIGS[args.config]

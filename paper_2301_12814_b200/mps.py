@@ -37,7 +37,77 @@ def layer_owners(costs, world: int):
     return owner
 
 
-class MPS:
+class _Chain:
+    """Layer logic shared by MPS and MPO: `_charges()` lists the per-bond charge lists (one species for an
+    MPS, two for an MPO), `apply_gate` updates sites (k, k+1)."""
+
+    def _charges(self):
+        raise NotImplementedError
+
+    def gate_cost(self, k: int) -> float:
+        """Θ-build flop estimate of the gate on (k, k+1) used to balance a layer: χ_k·χ_{k+1}·χ_{k+2}."""
+        q = self._charges()[0]
+        return float(q[k].numel()) * float(q[k + 1].numel()) * float(q[k + 2].numel())
+
+    def apply_layer(self, parity: int, thetas, phis, chi_max: int, cutoff: float = 1e-14, contraction=None,
+                    group=None):
+        """Gates on (k, k+1) for k = parity, parity+2, … < M−1; returns their discarded weights.
+
+        With `group` (a torch.distributed process group of size > 1) the gates are spread over its ranks
+        (layer_owners) and the results broadcast, leaving every rank's replica identical."""
+        ks = list(range(parity, self.M - 1, 2))
+        world = 1
+        if group is not None:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+        if world == 1:
+            return [self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction) for g, k in enumerate(ks)]
+        import torch.distributed as dist
+        me = dist.get_rank(group)
+        owner = layer_owners([self.gate_cost(k) for k in ks], world)
+        disc = torch.zeros(len(ks), dtype=torch.float64, device=self.device)
+        for g, k in enumerate(ks):
+            if owner[g] == me:
+                disc[g] = float(self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction))
+        for g, k in enumerate(ks):   # every rank walks the gates in the same order
+            self._bcast_gate(k, owner[g], owner[g] == me, group)
+        dist.all_reduce(disc, group=group)   # each entry has exactly one non-zero contributor
+        return [float(x) for x in disc.cpu()]
+
+    def _bcast_gate(self, k: int, src: int, mine: bool, group):
+        """Broadcast the tensors gate (k, k+1) replaced — the charges of bond k+1 (every species), λ^{[k+1]},
+        Γ^{[k]}, Γ^{[k+1]} — from group rank `src`."""
+        import torch.distributed as dist
+        dev = self.device
+        qs = self._charges()
+        bc = lambda t: dist.broadcast(t, group=group, group_src=src)
+        if mine:  # the owner's freshly written tensors are sent as they are (contiguous)
+            self.gam[k], self.gam[k + 1] = self.gam[k].contiguous(), self.gam[k + 1].contiguous()
+            self.lam[k + 1] = self.lam[k + 1].contiguous()
+        n = torch.tensor([qs[0][k + 1].numel() if mine else 0], dtype=torch.int64, device=dev)
+        bc(n)
+        chi = int(n.item())
+        chi_l, chi_r = qs[0][k].numel(), qs[0][k + 2].numel()
+        if not mine:
+            for q in qs:
+                q[k + 1] = torch.empty(chi, dtype=torch.int32, device=dev)
+            self.lam[k + 1] = torch.empty(chi, dtype=torch.float64, device=dev)
+            self.gam[k] = torch.empty((chi_l, chi), dtype=torch.complex128, device=dev)
+            self.gam[k + 1] = torch.empty((chi, chi_r), dtype=torch.complex128, device=dev)
+        if chi == 0:
+            return
+        for q in qs:
+            q64 = q[k + 1].to(torch.int64)   # int32 broadcast is not available on every backend
+            bc(q64)
+            if not mine:
+                q[k + 1] = q64.to(torch.int32)
+        bc(self.lam[k + 1])
+        for t in (self.gam[k], self.gam[k + 1]):
+            if t.numel():
+                bc(torch.view_as_real(t))
+
+
+class MPS(_Chain):
     def __init__(self, N: int, d: int, q, gam, lam, device="cuda"):
         dev = torch.device(device)
         as_t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
@@ -81,66 +151,11 @@ class MPS:
         plan.destroy()
         return res["discarded"]
 
-    def gate_cost(self, k: int) -> float:
-        """Θ-build flop estimate of the gate on (k, k+1) used to balance a layer: χ_k·χ_{k+1}·χ_{k+2}."""
-        return float(self.q[k].numel()) * float(self.q[k + 1].numel()) * float(self.q[k + 2].numel())
-
-    def apply_layer(self, parity: int, thetas, phis, chi_max: int, cutoff: float = 1e-14, contraction=None,
-                    group=None):
-        """Gates on (k, k+1) for k = parity, parity+2, … < M−1; returns their discarded weights.
-
-        With `group` (a torch.distributed process group of size > 1) the gates are spread over its ranks
-        (layer_owners) and the results broadcast, leaving every rank's replica identical."""
-        ks = list(range(parity, self.M - 1, 2))
-        world = 1
-        if group is not None:
-            import torch.distributed as dist
-            world = dist.get_world_size(group)
-        if world == 1:
-            return [self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction) for g, k in enumerate(ks)]
-        import torch.distributed as dist
-        me = dist.get_rank(group)
-        owner = layer_owners([self.gate_cost(k) for k in ks], world)
-        disc = torch.zeros(len(ks), dtype=torch.float64, device=self.device)
-        for g, k in enumerate(ks):
-            if owner[g] == me:
-                disc[g] = float(self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction))
-        for g, k in enumerate(ks):   # every rank walks the gates in the same order
-            self._bcast_gate(k, owner[g], owner[g] == me, group)
-        dist.all_reduce(disc, group=group)   # each entry has exactly one non-zero contributor
-        return [float(x) for x in disc.cpu()]
-
-    def _bcast_gate(self, k: int, src: int, mine: bool, group):
-        """Broadcast the tensors gate (k, k+1) replaced — q^{[k+1]}, λ^{[k+1]}, Γ^{[k]}, Γ^{[k+1]} — from
-        group rank `src`."""
-        import torch.distributed as dist
-        dev = self.device
-        bc = lambda t: dist.broadcast(t, group=group, group_src=src)
-        if mine:  # the owner's freshly written tensors are sent as they are (contiguous)
-            self.gam[k], self.gam[k + 1] = self.gam[k].contiguous(), self.gam[k + 1].contiguous()
-            self.lam[k + 1] = self.lam[k + 1].contiguous()
-        n = torch.tensor([self.q[k + 1].numel() if mine else 0], dtype=torch.int64, device=dev)
-        bc(n)
-        chi = int(n.item())
-        chi_l, chi_r = self.q[k].numel(), self.q[k + 2].numel()
-        if not mine:
-            self.q[k + 1] = torch.empty(chi, dtype=torch.int32, device=dev)
-            self.lam[k + 1] = torch.empty(chi, dtype=torch.float64, device=dev)
-            self.gam[k] = torch.empty((chi_l, chi), dtype=torch.complex128, device=dev)
-            self.gam[k + 1] = torch.empty((chi, chi_r), dtype=torch.complex128, device=dev)
-        if chi == 0:
-            return
-        q64 = self.q[k + 1].to(torch.int64)   # int32 broadcast is not available on every backend
-        bc(q64)
-        bc(self.lam[k + 1])
-        for t in (self.gam[k], self.gam[k + 1]):
-            if t.numel():
-                bc(torch.view_as_real(t))
-        if not mine:
-            self.q[k + 1] = q64.to(torch.int32)
+    def _charges(self):
+        return [self.q]
 
 
-class MPO:
+class MPO(_Chain):
     """A vectorized density matrix on the device ("MPOs are vectorized into the MPS
     form, U → U⊗U*, and two conserved charges are present"): bond k carries charge PAIRS (q1, q2) (ket, bra
     photons to the right, int32 each), λ (float64); site k carries Γ^{[k]} [χ_k × χ_{k+1}] complex128. A gate
@@ -157,6 +172,7 @@ class MPO:
         self.gam = [as_t(x, torch.complex128) for x in gam]
         self.lam = [as_t(x, torch.float64) for x in lam]
         self.M = len(self.gam)
+        self._gate_impl = None   # test hook only (as MPS._gate_impl)
         if not (len(self.q1) == len(self.q2) == len(self.lam) == self.M + 1):
             raise ValueError("an MPO of M sites needs M+1 bonds of charge pairs and λ")
 
@@ -172,6 +188,8 @@ class MPO:
         """One TEBD update of sites (k, k+1) with U⊗U*; returns the discarded weight."""
         if not 0 <= k < self.M - 1:
             raise ValueError("gate sites out of range")
+        if self._gate_impl is not None:
+            return self._gate_impl(self, k, theta, phi, chi_max, cutoff)
         plan = Plan2(self.d, self.N, self.q1[k], self.q2[k], self.q1[k + 1], self.q2[k + 1], self.q1[k + 2],
                      self.q2[k + 2])
         if contraction is not None:
@@ -187,7 +205,5 @@ class MPO:
         plan.destroy()
         return res["discarded"]
 
-    def apply_layer(self, parity: int, thetas, phis, chi_max: int, cutoff: float = 1e-14, contraction=None):
-        """Gates on (k, k+1) for k = parity, parity+2, … < M−1; returns their discarded weights."""
-        return [self.apply_gate(k, thetas[g], phis[g], chi_max, cutoff, contraction)
-                for g, k in enumerate(range(parity, self.M - 1, 2))]
+    def _charges(self):
+        return [self.q1, self.q2]

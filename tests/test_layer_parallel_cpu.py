@@ -38,6 +38,52 @@ def _oracle_gate(mps, k, theta, phi, chi_max, cutoff):
     return disc
 
 
+def _oracle_gate2(mpo, k, theta, phi, chi_max, cutoff):
+    import oracle.layer as L
+    st = dict(N=mpo.N, d=mpo.d, q1=[x.numpy() for x in mpo.q1], q2=[x.numpy() for x in mpo.q2],
+              gam=[x.numpy() for x in mpo.gam], lam=[x.numpy() for x in mpo.lam])
+    disc = L.apply_gate2(st, k, theta, phi, chi_max, cutoff)
+    mpo.q1[k + 1] = torch.from_numpy(np.ascontiguousarray(st["q1"][k + 1]).astype(np.int32))
+    mpo.q2[k + 1] = torch.from_numpy(np.ascontiguousarray(st["q2"][k + 1]).astype(np.int32))
+    mpo.lam[k + 1] = torch.from_numpy(np.ascontiguousarray(st["lam"][k + 1]))
+    for s in (k, k + 1):
+        mpo.gam[s] = torch.from_numpy(np.ascontiguousarray(st["gam"][s]))
+    return disc
+
+
+def _worker_mpo(rank, world, port, M, N, d, chi, chi_max, seed, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle.layer as L
+        from paper_2301_12814_b200.mps import MPO
+        st = L.random_mpo(M, N, d, chi, seed)
+        ref = L.copy_state2(st)
+        mpo = MPO.from_state(st, device="cpu")
+        mpo._gate_impl = _oracle_gate2
+        rng = np.random.default_rng(seed + 9)
+        for parity in (0, 1, 0):
+            n = len(range(parity, M - 1, 2))
+            th, ph = rng.uniform(0, np.pi / 2, n), rng.uniform(0, 2 * np.pi, n)
+            d_ref = L.apply_layer2(ref, parity, th, ph, chi_max)
+            d_par = mpo.apply_layer(parity, th, ph, chi_max, group=dist.group.WORLD)
+            assert d_par == [float(x) for x in d_ref], (rank, parity)
+            got = mpo.to_state()
+            for b in range(M + 1):
+                assert np.array_equal(got["q1"][b], ref["q1"][b]) and np.array_equal(got["q2"][b], ref["q2"][b])
+                assert np.array_equal(got["lam"][b], ref["lam"][b]), (rank, parity, b)
+            for s_ in range(M):
+                assert np.array_equal(got["gam"][s_], ref["gam"][s_]), (rank, parity, s_)
+        q.put((rank, "ok"))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
 def _worker(rank, world, port, M, N, d, chi, chi_max, seed, q):
     import sys
     sys.path.insert(0, ROOT)
@@ -77,6 +123,22 @@ def test_layer_parallel_matches_serial(world, M):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, M, 3, 4, 12, 9, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}:\n{msg}"
+
+
+def test_mpo_layer_parallel_matches_serial():
+    # the same exchange for MPO layers (two charge species per bond, U⊗U* gates): oracle apply_gate2 injected
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_mpo, args=(r, world, port, 5, 2, 3, 6, 8, 3, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
