@@ -90,3 +90,8 @@ def test_set_contraction_errors(tn):
         plan.set_contraction(5, 7)
     plan.set_contraction("dmma")
     assert plan.contraction() == ("dmma", 0)
+    # the int32 diagonal accumulators are exact only for K ≤ 2048 (OZ_KMAX): a longer centre segment is refused
+    big = tn.Plan(4, 3, [1, 2, 3], np.zeros(2100, dtype=np.int32), [0, 1])
+    with pytest.raises(tn.TnError, match="UNSUPPORTED"):
+        big.set_contraction("int8", 6)
+    assert big.contraction() == ("dmma", 0)      # the plan stays usable on the FP64 engine
