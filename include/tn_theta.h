@@ -269,8 +269,8 @@ TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn
  * owner rank's full Θ(c) buffer opened with tn_ipc_open (NVLink peer memory) offset to this rank's
  * first row (tn_plan_local_sector_shape's row_begin × C_c complex). No collective runs inside: the
  * caller orders consumers after every rank's stream (e.g. a barrier after synchronising). Other
- * arguments as tn_theta_exec. Single-charge plans with the DMMA or INT8 engine; TN_ERR_UNSUPPORTED
- * otherwise. */
+ * arguments as tn_theta_exec. Single-charge and MPO pair plans (K5P: first pass in place on the local
+ * workspace, second pass into theta_dst) with the DMMA or INT8 engine; TN_ERR_UNSUPPORTED otherwise. */
 TN_API tn_status tn_theta_exec_remote(tn_plan* plan, tn_stream stream, const double* gamma_k,
                                       const double* lambda_k, const double* gamma_k1, const double* lambda_l,
                                       const double* lambda_r, const double* U, double* const* theta_dst);

@@ -892,8 +892,8 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
                                const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
                                double* const* theta_dst) {
   if (!p) return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL plan");
-  if (p->pair || p->fused || p->contraction == TN_CONTRACT_PAPER_LITERAL)
-    return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_remote: single-charge plans with the DMMA or INT8 engine only");
+  if (p->fused || p->contraction == TN_CONTRACT_PAPER_LITERAL)
+    return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_remote: the DMMA or INT8 engine only");
   if (!gamma_k || !lambda_k || !gamma_k1 || !lambda_l || !lambda_r || !U || !theta_dst)
     return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL input pointer");
   for (int c = 0; c < p->nsec; ++c)
@@ -939,7 +939,11 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
   st = cuda_check(emu ? launch_oz_contract(p, sp4, s) : launch_contract(p, sp4, s), "K4 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
-  st = cuda_check(launch_mix(p, sp5, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
+  if (p->pair)  // K5P: pass 1 in place on the local workspace, pass 2 from it into the destination buffers
+    st = cuda_check(launch_pair_mix(p, sp4, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, &sp5),
+                    "K5P launch");
+  else
+    st = cuda_check(launch_mix(p, sp5, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
   if (st != TN_OK) return st;
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");
 }

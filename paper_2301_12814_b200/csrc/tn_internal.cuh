@@ -245,7 +245,7 @@ cudaError_t launch_literal(const tn_plan* p, const SectorParams& sp, const doubl
                            const double2* gk1, const double* ll, const double* lr, const double2* U, cudaStream_t s,
                            cudaEvent_t mid);
 cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                            const double2* U, cudaStream_t s);
+                            const double2* U, cudaStream_t s, const SectorParams* sp2 = nullptr);
 cudaError_t launch_fused(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                          const double2* U, cudaStream_t s);
 size_t k45_smem_bytes(int stages, int max_mix);

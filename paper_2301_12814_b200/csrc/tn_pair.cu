@@ -331,9 +331,12 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
   for (int u = threadIdx.x; u < L; u += K5P_THREADS) {
     // pass 1: sectors (lo+u, fixed), sources P valid only for a non-empty centre pair; pass 2: (fixed, lo+u)
     const int s = pass2 ? t.fixed * nk + t.lo + u : (t.lo + u) * nk + t.fixed;
-    const double2* base = sp.out[s] + (int64_t)(rowoff[s * nq + t.lkey] + t.band) * sp.ld[s] + coloff[s * nq + t.rkey];
+    const int64_t off = (int64_t)(rowoff[s * nq + t.lkey] + t.band) * sp.ld[s] + coloff[s * nq + t.rkey];
+    const double2* base = sp.out[s] + off;
     const bool valid = pass2 || ((sp.cc_mask[s >> 5] >> (s & 31)) & 1u);
-    ld_sec[u] = SecRef{valid ? base : nullptr, (int64_t)sp.ld[s]};
+    // the source is Θ(s) itself, or a local workspace when Θ goes elsewhere (tn_theta_exec_remote, pass 2)
+    const double2* lbase = sp.src[s] ? sp.src[s] + off : base;
+    ld_sec[u] = SecRef{valid ? lbase : nullptr, (int64_t)sp.ld[s]};
     st_sec[u] = SecRef{base, (int64_t)sp.ld[s]};
   }
   // Us[t][u] = U_n[i = cl − (lo+t)][j = cl − (lo+u)]  (conjugated for the bra species), padded to TP × UP
@@ -378,8 +381,9 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
   }
 }
 
-cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                            const double2* U, cudaStream_t s) {
+cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp1, const double* ll, const double* lr,
+                            const double2* U, cudaStream_t s, const SectorParams* sp2_in) {
+  const SectorParams& sp2 = sp2_in ? *sp2_in : sp1;   // pass 2 may read one set of buffers and write another
   const int L = p->max_mix;
   const int NT = (L + 7) >> 3;
   const int smax = mix_us_elems(L);
@@ -387,6 +391,7 @@ cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const doub
     const int64_t n = p->nmix2[pass];
     if (n == 0) continue;
     const MixTile2* tiles = p->d_mix2 + (pass ? p->nmix2[0] : 0);
+    const SectorParams& sp = pass ? sp2 : sp1;
 #define TN_P_LAUNCH(M)                                                                                        \
   do {                                                                                                        \
     const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * sizeof(SecRef);    \

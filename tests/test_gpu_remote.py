@@ -7,6 +7,7 @@ import os
 import socket
 
 import numpy as np
+import torch
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -21,6 +22,34 @@ def _port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def _worker_pair(rank, world, port, cfg, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        import paper_2301_12814_b200 as tn
+        import synth
+        torch.cuda.set_device(0)
+        c = synth.make_pair_config(cfg)
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        args = [dv(x) for x in (c.gamma_k, c.lam_k, c.gamma_k1, c.lam_l, c.lam_r)]
+        full_plan = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
+        full = [x.clone() for x in tn.theta_exec(full_plan, *args, tn.build_bs_unitary(full_plan, c.theta, c.phi))]
+        plan = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r, world, rank)
+        owned = tn.theta_exec_to_owners(plan, *args, tn.build_bs_unitary(plan, c.theta, c.phi))
+        ok = all(torch.equal(v, full[s_]) for s_, v in owned.items())
+        counts = [None] * world
+        dist.all_gather_object(counts, len(owned))
+        q.put((rank, "ok" if ok else "mismatch", sum(counts)))
+    except Exception as e:
+        q.put((rank, repr(e), None))
+    finally:
+        dist.destroy_process_group()
 
 
 def _worker(rank, world, port, cfg, engine, q):
@@ -70,6 +99,32 @@ def test_exec_to_owners_two_processes_one_gpu(cfg, engine, cuda_ok):
     assert res[0][2] >= 1
 
 
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_exec_to_owners_pair_two_processes_one_gpu(cfg, cuda_ok):
+    # MPO pair plans: each of two processes writes its row slabs of every Θ(c1,c2) into the owner's buffer
+    # through CUDA IPC; the owners' sectors equal the unsharded pair exec bit for bit
+    import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_pair, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    assert all(r[1] == "ok" for r in res), res
+    c = synth.make_pair_config(cfg)
+    full = tn_full_sector_count(c)
+    assert res[0][2] == full
+
+
+def tn_full_sector_count(c):
+    import paper_2301_12814_b200 as tn
+    p = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
+    return sum(1 for s in range(p.nsec) if p.sector_shape(s)[0] * p.sector_shape(s)[1] > 0)
+
+
 def test_exec_remote_single_rank_and_errors(cuda_ok):
     import sys
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -90,8 +145,18 @@ def test_exec_remote_single_rank_and_errors(cuda_ok):
     with pytest.raises(tn.TnError, match="DIMENSION"):
         tn.check(tn.lib.tn_theta_exec_remote(plan.handle, None, *(tn._ptr(t[k]) for k in ("gk", "lk", "gk1", "ll", "lr")),
                                              tn._ptr(U), nulls), "tn_theta_exec_remote")
-    pc = synth.make_pair_config(0)
+    # MPO pair plans: K5P's first pass runs in place on the local workspace, the second writes the owners' Θ
+    pc = synth.make_pair_config(1)
     p2 = tn.Plan2(pc.d, pc.N, pc.q1_l, pc.q2_l, pc.q1_c, pc.q2_c, pc.q1_r, pc.q2_r)
+    U2 = tn.build_bs_unitary(p2, pc.theta, pc.phi)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    args2 = [dv(x) for x in (pc.gamma_k, pc.lam_k, pc.gamma_k1, pc.lam_l, pc.lam_r)]
+    ref2 = [x.clone() for x in tn.theta_exec(p2, *args2, U2)]
+    owned2 = tn.theta_exec_to_owners(p2, *args2, U2)
+    assert set(owned2) == {s_ for s_ in range(p2.nsec) if ref2[s_].numel()}
+    for s_, v in owned2.items():
+        assert torch.equal(v, ref2[s_]), s_
+    lit = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r).set_contraction("literal")
     with pytest.raises(tn.TnError, match="UNSUPPORTED"):
-        tn.check(tn.lib.tn_theta_exec_remote(p2.handle, None, *(tn._ptr(t[k]) for k in ("gk", "lk", "gk1", "ll", "lr")),
+        tn.check(tn.lib.tn_theta_exec_remote(lit.handle, None, *(tn._ptr(t[k]) for k in ("gk", "lk", "gk1", "ll", "lr")),
                                              tn._ptr(U), nulls), "tn_theta_exec_remote")
