@@ -56,7 +56,7 @@ SvdCtx& ctx() {
   static SvdCtx c;
   return c;
 }
-// 2 (default): Gram eigensolver + Rayleigh–Ritz (svd_gram below; 0.1x s at config 3), 1: polar-decomposition
+// 2 (default): Gram eigensolver + Rayleigh–Ritz (svd_gram below; 0.26–0.30 s at config 3), 1: polar-decomposition
 // SVD per sector (TN_SVD_ALGO=gesvdp, 0.77 s), 0: one-sided Jacobi (TN_SVD_ALGO=gesvdj, 1.98 s); all three
 // meet the parity bar (tests/test_gpu_svd.py runs each)
 int svd_algo() {
@@ -234,8 +234,14 @@ tn_status run_lanes(SvdCtx& X, cudaStream_t s, std::vector<int> wave, Cost cost,
   tn_status r0 = cuda_check(cudaEventRecord(X.ev[SVD_LANES], s), "Θ ready");
   if (r0 != TN_OK) return r0;
   std::vector<std::string> errs(SVD_LANES);
+  int dev = 0;
+  cudaGetDevice(&dev);   // lane threads must run on the caller's device (one process per GPU, any local rank)
   auto work = [&](int l) {
     if (lane[l].empty()) return;
+    if (cudaSetDevice(dev) != cudaSuccess) {
+      errs[l] = "set device";
+      return;
+    }
     if (cudaStreamWaitEvent(X.st[l], X.ev[SVD_LANES], 0) != cudaSuccess) {
       errs[l] = "stream wait";
       return;
