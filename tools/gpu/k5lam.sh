@@ -1,0 +1,3 @@
+for c in 3 4; do echo "cfg $c $(timeout 300 python tools/run_step.py --config $c --reps 4 2>&1 | tail -1 | grep -o '"k5_mix[^,]*')"; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "theta_parity or edge or sharded or metamorphic or padding" 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_remote.py tests/test_gpu_guards.py -q -x 2>&1 | tail -2
