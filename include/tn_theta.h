@@ -291,7 +291,7 @@ TN_API tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int6
 /* The plan's sector-owner rule on host data: owners[0..n_sectors) from element counts sizes[]. */
 TN_API tn_status tn_sector_owners_host(int n_sectors, const int64_t* sizes, int world_size, int32_t* owners);
 
-TN_API /* Device memory: plan tables and staging workspace come from a library-owned pool. A destroyed
+/* Device memory: plan tables and staging workspace come from a library-owned pool. A destroyed
  * plan's blocks are reused by later plans once the work last enqueued with them has completed
  * (an event recorded on the last exec stream), so per-gate planning does not call cudaMalloc.
  * tn_release_cached_memory frees every idle block (waiting for its event) and reports the bytes
