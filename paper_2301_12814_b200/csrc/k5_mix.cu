@@ -27,6 +27,8 @@
 //    (128 registers at L = 32) capped every tile at 16 warps per SM. Tiles are therefore issued as up to
 //    four launches by L (≤ 8: 56 registers, 8 CTAs/SM; ≤ 16: 72, 7 CTAs/SM; ≤ 32: 128; larger), each
 //    keeping the band-major order: config 3 0.78 → 0.72 ms, config 4 6.05 → 4.30 ms.
+#include <cstdlib>
+
 #include "k5_mix.cuh"
 
 namespace tn {
@@ -117,7 +119,7 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
   if (p->nmix == 0) return cudaSuccess;
   // one launch per register class: L ≤ 8 (56 registers → 8 CTAs per SM), L ≤ 16 (72 → 7), L ≤ 32 (128 → 4),
   // the rest (NT 6/8 instantiations)
-  auto one = [&](const MixTile* tiles, int64_t n, int L) -> cudaError_t {
+  auto one = [&](const MixTile* tiles, int64_t n, int L, cudaStream_t s) -> cudaError_t {
     if (n == 0) return cudaSuccess;
     const unsigned grid = (unsigned)n;
     const int NT = (L + 7) >> 3;
@@ -145,13 +147,45 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
     return cudaGetLastError();
   };
   const int L = p->max_mix;
-  const int64_t n0 = p->nmix_cls[0], n1 = p->nmix_cls[1], n2 = p->nmix_cls[2];
-  cudaError_t e = cudaSuccess;
-  if (first_class <= 0) e = one(p->d_mix, n0, std::min(L, 8));
-  if (e == cudaSuccess && first_class <= 1) e = one(p->d_mix + n0, n1, std::min(L, 16));
-  if (e == cudaSuccess && first_class <= 2) e = one(p->d_mix + n0 + n1, n2, std::min(L, 32));
-  if (e != cudaSuccess) return e;
-  return one(p->d_mix + n0 + n1 + n2, p->nmix - n0 - n1 - n2, L);
+  const int64_t n0 = p->nmix_cls[0], n1 = p->nmix_cls[1], n2 = p->nmix_cls[2], n3 = p->nmix - n0 - n1 - n2;
+  const MixTile* t[4] = {p->d_mix, p->d_mix + n0, p->d_mix + n0 + n1, p->d_mix + n0 + n1 + n2};
+  const int64_t n[4] = {first_class <= 0 ? n0 : 0, first_class <= 1 ? n1 : 0, first_class <= 2 ? n2 : 0, n3};
+  const int Lc[4] = {std::min(L, 8), std::min(L, 16), std::min(L, 32), L};
+  static const bool concurrent = getenv("TN_K5_SERIAL") == nullptr;
+  if (!concurrent) {
+    for (int c = 0; c < 4; ++c) {
+      cudaError_t e = one(t[c], n[c], Lc[c], s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  // the classes touch disjoint elements: run them concurrently (their tails and occupancy overlap) on
+  // per-thread auxiliary streams forked from and joined back into s
+  struct Aux {
+    int dev = -1;
+    cudaStream_t st[3] = {};
+    cudaEvent_t fork = nullptr, join[3] = {};
+  };
+  thread_local Aux aux;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (aux.dev != dev) {
+    for (auto& x : aux.st) if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return cudaGetLastError();
+    if (cudaEventCreateWithFlags(&aux.fork, cudaEventDisableTiming) != cudaSuccess) return cudaGetLastError();
+    for (auto& x : aux.join) if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) return cudaGetLastError();
+    aux.dev = dev;
+  }
+  cudaError_t e = cudaEventRecord(aux.fork, s);
+  for (int c = 1; c < 4 && e == cudaSuccess; ++c) {
+    if (n[c] == 0) continue;
+    e = cudaStreamWaitEvent(aux.st[c - 1], aux.fork, 0);
+    if (e == cudaSuccess) e = one(t[c], n[c], Lc[c], aux.st[c - 1]);
+    if (e == cudaSuccess) e = cudaEventRecord(aux.join[c - 1], aux.st[c - 1]);
+  }
+  if (e == cudaSuccess) e = one(t[0], n[0], Lc[0], s);
+  for (int c = 1; c < 4 && e == cudaSuccess; ++c)
+    if (n[c]) e = cudaStreamWaitEvent(s, aux.join[c - 1], 0);
+  return e;
 }
 
 }  // namespace tn
