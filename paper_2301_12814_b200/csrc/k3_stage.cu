@@ -84,13 +84,21 @@ cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, 
     int64_t cap = std::max<int64_t>(1, target * 4 / ng);
     return (unsigned)std::max<int64_t>(1, std::min(b, cap));
   };
+  // the A and B panels are disjoint: stage B on an auxiliary stream beside A (both HBM-bound, they share the
+  // bandwidth but overlap each other's launch tails)
+  AuxStreams* aux = nullptr;
+  cudaError_t e = aux_streams(&aux);
+  if (e == cudaSuccess) e = cudaEventRecord(aux->fork, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(aux->st[0], aux->fork, 0);
+  if (e != cudaSuccess) return e;
+  k3_stage_b<<<dim3(blocks(bmax), ng), 256, 0, aux->st[0]>>>(p->d_groups, p->d_perm[1], p->d_colperm, gk1,
+                                                              p->chi[2], p->d_bpanel);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(aux->join[0], aux->st[0])) != cudaSuccess) return e;
   k3_stage_a<<<dim3(blocks(amax), ng), 256, 0, s>>>(p->d_groups, p->d_rowperm, p->d_perm[1], gk, p->chi[1],
                                                      lk, p->d_apanel);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k3_stage_b<<<dim3(blocks(bmax), ng), 256, 0, s>>>(p->d_groups, p->d_perm[1], p->d_colperm, gk1, p->chi[2],
-                                                     p->d_bpanel);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaStreamWaitEvent(s, aux->join[0], 0);
 }
 
 }  // namespace tn

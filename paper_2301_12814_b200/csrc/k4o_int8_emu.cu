@@ -574,15 +574,26 @@ static cudaError_t stage_s(const tn_plan* p, const double2* gk, const double* lk
     maxa = std::max(maxa, g.nmt * g.nkc);
     maxb = std::max(maxb, g.nnt * ((g.nkc + 3) / 4));
   }
+  // the A chain (row exponents → A slices) and the B chain (column exponents → B slices) are independent:
+  // the B chain runs on an auxiliary stream beside the A chain
+  AuxStreams* aux = nullptr;
+  cudaError_t e = aux_streams(&aux);
+  if (e == cudaSuccess) e = cudaEventRecord(aux->fork, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(aux->st[0], aux->fork, 0);
+  if (e != cudaSuccess) return e;
+  cudaStream_t sb = aux->st[0];
+  if (maxc > 0) k3o_col_exp<<<dim3((maxc + 63) / 64, ng), 256, 0, sb>>>(p->d_oz_groups, p->d_perm[1], p->d_colperm,
+                                                                          gk1, p->chi[2], p->d_oeb);
+  k3o_cols<S><<<dim3(maxb, ng), 4 * OZ_BN, 0, sb>>>(p->d_oz_groups, p->d_perm[1], p->d_colperm, gk1, p->chi[2], p->d_oeb,
+                                                p->d_ob);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(aux->join[0], sb)) != cudaSuccess) return e;
   if (maxr > 0) k3o_row_exp<<<dim3((maxr + 7) / 8, ng), 256, 0, s>>>(p->d_oz_groups, p->d_rowperm, p->d_perm[1], gk,
                                                                      p->chi[1], lk, p->d_oea);
-  if (maxc > 0) k3o_col_exp<<<dim3((maxc + 63) / 64, ng), 256, 0, s>>>(p->d_oz_groups, p->d_perm[1], p->d_colperm,
-                                                                         gk1, p->chi[2], p->d_oeb);
   k3o_rows<S><<<dim3(maxa, ng), OZ_BM, 0, s>>>(p->d_oz_groups, p->d_rowperm, p->d_perm[1], gk, p->chi[1], lk, p->d_oea,
                                                p->d_oa);
-  k3o_cols<S><<<dim3(maxb, ng), 4 * OZ_BN, 0, s>>>(p->d_oz_groups, p->d_perm[1], p->d_colperm, gk1, p->chi[2], p->d_oeb,
-                                               p->d_ob);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaStreamWaitEvent(s, aux->join[0], 0);
 }
 
 cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1, cudaStream_t s) {

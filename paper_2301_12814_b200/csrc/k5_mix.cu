@@ -161,20 +161,9 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
   }
   // the classes touch disjoint elements: run them concurrently (their tails and occupancy overlap) on
   // per-thread auxiliary streams forked from and joined back into s
-  struct Aux {
-    int dev = -1;
-    cudaStream_t st[3] = {};
-    cudaEvent_t fork = nullptr, join[3] = {};
-  };
-  thread_local Aux aux;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (aux.dev != dev) {
-    for (auto& x : aux.st) if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return cudaGetLastError();
-    if (cudaEventCreateWithFlags(&aux.fork, cudaEventDisableTiming) != cudaSuccess) return cudaGetLastError();
-    for (auto& x : aux.join) if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) return cudaGetLastError();
-    aux.dev = dev;
-  }
+  AuxStreams* ap = nullptr;
+  if (cudaError_t ea = aux_streams(&ap); ea != cudaSuccess) return ea;
+  AuxStreams& aux = *ap;
   cudaError_t e = cudaEventRecord(aux.fork, s);
   for (int c = 1; c < 4 && e == cudaSuccess; ++c) {
     if (n[c] == 0) continue;

@@ -233,6 +233,30 @@ cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream
 cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
                             cudaStream_t s);
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
+// Per-thread auxiliary streams on the current device for launches that touch disjoint data (K3 a/b,
+// K3O's two exponent→slice chains, K5's register classes): fork from s, run, join back into s.
+struct AuxStreams {
+  int dev = -1;
+  cudaStream_t st[3] = {};
+  cudaEvent_t fork = nullptr, join[3] = {};
+};
+inline cudaError_t aux_streams(AuxStreams** out) {
+  thread_local AuxStreams aux;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (aux.dev != dev) {
+    for (auto& x : aux.st)
+      if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&aux.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (auto& x : aux.join)
+      if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+    aux.dev = dev;
+  }
+  *out = &aux;
+  return cudaSuccess;
+}
+
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s, int first_class = 0);
 void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out);
