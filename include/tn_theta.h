@@ -191,7 +191,9 @@ TN_API tn_status tn_build_bs_unitary(const tn_plan* plan, double theta, double p
  *             slab of Θ(c) (R×C from tn_plan_local_sector_shape), row-major, ld = C. Entries
  *             with R·C = 0 may be NULL. Buffers must not alias the inputs or each other.
  * Γ entries outside δ-allowed charge blocks are never read. Stream-ordered, no host sync.
- * The plan's workspace is reused: one exec per plan in flight at a time.
+ * The plan's workspace is reused: one exec per plan in flight at a time. Capturable into a CUDA graph
+ * (independent launches fork onto per-thread auxiliary streams and join back) once the plan's table
+ * upload has completed — after any earlier exec with the plan or a synchronisation.
  * Errors: TN_ERR_DIMENSION (a NULL input, or NULL theta_out[c] for a non-empty slab),
  * TN_ERR_CUDA (launch failure, or a sticky error from earlier work). */
 TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,

@@ -827,6 +827,16 @@ tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_str
   return st;
 }
 
+// The exec stream waits for the plan's asynchronous table upload. Under CUDA graph capture that event lies
+// outside the capture (waiting on it would invalidate it): a captured exec requires the tables to be ready
+// already (any earlier exec or a synchronisation), which the header documents.
+static tn_status wait_tables(const tn_plan* p, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) cs = cudaStreamCaptureStatusNone;
+  if (cs != cudaStreamCaptureStatusNone) return TN_OK;
+  return cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
+}
+
 tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
                         const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
                         double* const* theta_out) {
@@ -842,7 +852,7 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   const SectorParams sp = make_sector_params(p, theta_out);
   p->last_stream = s;
   p->rec_exec = true;  // the workspace is in use from here on (pool release fence)
-  tn_status st = cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
+  tn_status st = wait_tables(p, s);
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
   if (p->contraction == TN_CONTRACT_PAPER_LITERAL) {  // ablation: K3L → K4L, no K5
@@ -925,7 +935,7 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
   for (int c = 0; c < p->nsec; ++c) sp5.src[c] = reinterpret_cast<const double2*>(pw[c]);
   p->last_stream = s;
   p->rec_exec = true;
-  tn_status st = cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
+  tn_status st = wait_tables(p, s);
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;

@@ -8,6 +8,7 @@ import math
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 import synth
@@ -468,3 +469,28 @@ def test_exec_launch_count(tn):
     c = synth.make_pair_config(1)
     p2 = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
     assert p2.exec_launches() == 5                   # K3 a/b, K4, K5P ×2
+
+
+def test_exec_captured_in_cuda_graph(tn):
+    # tn_theta_exec is stream-ordered, so it can be captured into a CUDA graph (its K3/K5 launches fork onto
+    # auxiliary streams and join back, which capture records as graph branches) and replayed bit-identically
+    case = _case(2)
+    plan = tn.Plan(case.d, case.N, case.q_l, case.q_c, case.q_r)
+    U = tn.build_bs_unitary(plan, case.theta, case.phi)
+    t = to_dev(case)
+    ref = [x.clone() for x in tn.theta_exec(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U)]
+    out = tn.alloc_theta(plan)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):          # warm-up outside capture (lazy per-thread stream creation)
+        tn.theta_exec(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U, out=out, stream=s)
+    torch.cuda.synchronize()
+    for o in out:
+        o.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tn.theta_exec(plan, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U, out=out, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(out, ref):
+        assert torch.equal(a, b)
