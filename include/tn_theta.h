@@ -72,7 +72,9 @@ enum { TN_GATHER_NONE = 0, TN_GATHER_ROOT = 1, TN_GATHER_SECTOR_OWNER = 2 };
  *   N        total photon number; charges lie in [0, N]; 0 ≤ N ≤ TN_MAX_N.
  *   chi_*    bond dimensions of α_{k−1} (l), α_k (c), α_{k+1} (r); each ≥ 1.
  *   q_*      int32 charge per bond index, in the caller's bond order; host OR device pointers
- *            (told apart with cudaPointerGetAttributes). Read during the call only.
+ *            (told apart with cudaPointerGetAttributes). Read during the call only. Device charges are
+ *            read on the plan's own stream, unordered with the caller's streams: the caller makes them
+ *            ready first (e.g. synchronises the producing stream; the Python binding does).
  *   world_size, rank   row sharding of Θ over ranks (1, 0 for a single GPU). The plan computes
  *            flop-balanced shards of the sorted left positions and keeps the work for `rank`.
  *   out      receives the new plan; free with tn_plan_destroy.
@@ -192,8 +194,9 @@ TN_API tn_status tn_build_bs_unitary(const tn_plan* plan, double theta, double p
  *             with R·C = 0 may be NULL. Buffers must not alias the inputs or each other.
  * Γ entries outside δ-allowed charge blocks are never read. Stream-ordered, no host sync.
  * The plan's workspace is reused: one exec per plan in flight at a time. Capturable into a CUDA graph
- * (independent launches fork onto per-thread auxiliary streams and join back) once the plan's table
- * upload has completed — after any earlier exec with the plan or a synchronisation.
+ * (independent launches fork onto per-thread auxiliary streams and join back): a captured call waits on the
+ * host for the plan's table upload, and the plan must outlive every graph (and replay) that contains it —
+ * tn_plan_destroy of a captured plan synchronises the device before its memory is reused.
  * Errors: TN_ERR_DIMENSION (a NULL input, or NULL theta_out[c] for a non-empty slab),
  * TN_ERR_CUDA (launch failure, or a sticky error from earlier work). */
 TN_API tn_status tn_theta_exec(const tn_plan* plan, tn_stream stream,

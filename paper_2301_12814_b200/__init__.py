@@ -52,11 +52,19 @@ def _charges(q):
     return np.ascontiguousarray(np.asarray(q, dtype=np.int32))
 
 
+def _ready(qs):
+    # the plan reads device charges on its own stream (include/tn_theta.h): the producing work — typically on
+    # the current stream (a dtype cast above, an SVD step's q_new) — must have finished
+    if any(isinstance(q, torch.Tensor) and q.is_cuda for q in qs):
+        torch.cuda.current_stream().synchronize()
+
+
 class Plan:
     """tn_theta_plan: bond re-indexing (K1) and work decomposition for one gate's bond charges."""
 
     def __init__(self, d: int, N: int, q_l, q_c, q_r, world_size: int = 1, rank: int = 0):
         self._keep = [_charges(q) for q in (q_l, q_c, q_r)]
+        _ready(self._keep)
         ql, qc, qr = self._keep
         self.d, self.N = int(d), int(N)
         self.chi = (int(ql.shape[0]), int(qc.shape[0]), int(qr.shape[0]))
@@ -167,6 +175,7 @@ class Plan2(Plan):
 
     def __init__(self, d: int, N: int, q1_l, q2_l, q1_c, q2_c, q1_r, q2_r, world_size: int = 1, rank: int = 0):
         self._keep = [_charges(q) for q in (q1_l, q2_l, q1_c, q2_c, q1_r, q2_r)]
+        _ready(self._keep)
         k = self._keep
         self.d, self.N = int(d), int(N)
         self.chi = (int(k[0].shape[0]), int(k[2].shape[0]), int(k[4].shape[0]))
@@ -352,6 +361,9 @@ def theta_exec_to_owners(plan: Plan, gk, lk, gk1, ll, lr, U, group=None, stream=
         R, Cc = plan.sector_shape(c)
         if plan.sector_owner(c) == rank and R * Cc > 0:
             owned[c] = torch.empty((R, Cc), dtype=torch.complex128, device=dev)
+    # the caching allocator may hand out blocks that this rank's pending kernels still use: peers write into
+    # them through NVLink outside this stream's order, so drain the stream before publishing the handles
+    (stream or torch.cuda.current_stream()).synchronize()
     mine = {c: ipc_handle(t) for c, t in owned.items()}
     allh = [None] * world
     if world > 1:

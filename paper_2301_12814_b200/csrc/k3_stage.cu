@@ -87,7 +87,7 @@ cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, 
   // the A and B panels are disjoint: stage B on an auxiliary stream beside A (both HBM-bound, they share the
   // bandwidth but overlap each other's launch tails)
   AuxStreams* aux = nullptr;
-  cudaError_t e = aux_streams(&aux);
+  cudaError_t e = aux_streams(s, &aux);
   if (e == cudaSuccess) e = cudaEventRecord(aux->fork, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(aux->st[0], aux->fork, 0);
   if (e != cudaSuccess) return e;

@@ -1,5 +1,5 @@
-// Device helpers of the K4 contraction shared by k4_contract.cu and the fused K4+K5 kernel (k45_fused.cu):
-// mbarrier ring primitives, the 1-D TMA bulk copy and the DMMA.8x8x4 wrapper.
+// Device helpers of the K4 contraction (k4_contract.cu, k4l_literal.cu; the retired fused K4+K5 experiment in
+// tools/experiments/ used them too): mbarrier ring primitives, the 1-D TMA bulk copy and the DMMA.8x8x4 wrapper.
 #pragma once
 #include "tn_internal.cuh"
 

@@ -286,8 +286,7 @@ template <int S, int OZ_STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-partition → ≤ 168 registers
     k4o_contract(const OzGroup* __restrict__ groups, const OzTile* __restrict__ tiles, int ntiles,
                  const int8_t* __restrict__ oa, const int8_t* __restrict__ ob, const int32_t* __restrict__ oea,
-                 const int32_t* __restrict__ oeb, const SectorParams sp, const int dbg,
-                 unsigned long long* __restrict__ prof) {
+                 const int32_t* __restrict__ oeb, const SectorParams sp) {
   constexpr int A_HS = S * OZ_A_TILE, B_HS = S * OZ_B_TILE;   // one plane of one K step
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
@@ -334,15 +333,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               ob_sleep_wait(&empty[stage], phase ^ 1);
-              if (dbg & 2) {  // ablation: no operand traffic
-                ob_arrive(&full[stage]);
-              } else {
-                ob_expect_tx(&full[stage], A_HS + B_HS);
-                ob_bulk(sA + stage * A_HS, a_t + (int64_t)(kc * 2 + h) * A_HS, A_HS, &full[stage]);
-                // B planes [Br, −Bi, Bi]: Re pass (Br, −Bi), Im pass (Bi, Br)
-                const int bp = pass == 0 ? h : (h == 0 ? 2 : 0);
-                ob_bulk(sB + stage * B_HS, b_t + (int64_t)(kc * 3 + bp) * B_HS, B_HS, &full[stage]);
-              }
+              ob_expect_tx(&full[stage], A_HS + B_HS);
+              ob_bulk(sA + stage * A_HS, a_t + (int64_t)(kc * 2 + h) * A_HS, A_HS, &full[stage]);
+              // B planes [Br, −Bi, Bi]: Re pass (Br, −Bi), Im pass (Bi, Br)
+              const int bp = pass == 0 ? h : (h == 0 ? 2 : 0);
+              ob_bulk(sB + stage * B_HS, b_t + (int64_t)(kc * 3 + bp) * B_HS, B_HS, &full[stage]);
               if (++stage == OZ_STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -358,8 +353,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
     // half steps stay in the ring (not released) and are replayed for it once the slot frees, so the
     // MMA issue never stalls on the epilogue while operand stages remain.
     if (lane == 0) {
-      long long t_full = 0, t_slot = 0, n_block = 0, n_defer = 0;
-      const long long t_start = clock64();
       int stage = 0;
       uint32_t phase = 0, slot_uses = 0;  // 2 bits per slot: parity of its use count
       int base = 0;
@@ -390,14 +383,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
           int held = 0;               // half steps of this pass kept in the ring (not yet released)
           const int st0 = stage;      // ring stage of the pass's first half step
           for (int hs = 0; hs < nhs; ++hs) {
-            const long long tw0 = clock64();
             ob_wait(&full[stage], phase);
-            t_full += clock64() - tw0;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const bool last = hs == nhs - 1;
-            if (dbg & 1) {  // ablation: no MMAs
-              commit(&empty[stage]);
-            } else if (acq != ALL) {
+            if (acq != ALL) {
               // block for a slot only when deferring further would exhaust the ring, or at the last step
               const bool must = last || held + 2 > OZ_STAGES;
 #pragma unroll
@@ -409,12 +398,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
                 }
                 const int sl = (base + i) & (OZ_SLOTS - 1);
                 const uint32_t u = (slot_uses >> (2 * sl)) & 3u;
-                bool ok = u == 0 || (dbg & 4) || ob_test(&slot_empty[sl], (u - 1) & 1);
+                bool ok = u == 0 || ob_test(&slot_empty[sl], (u - 1) & 1);
                 if (!ok && must) {
-                  const long long ts0 = clock64();
                   ob_spin(&slot_empty[sl], (u - 1) & 1);
-                  t_slot += clock64() - ts0;
-                  ++n_block;
                   ok = true;
                 }
                 if (ok) {
@@ -440,7 +426,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
                   for (int i = 0; i < S; ++i) commit(&slot_full[(base + i) & (OZ_SLOTS - 1)]);
               } else {
                 ++held;
-                ++n_defer;
               }
             } else if (last) {
               // last half step: diagonal by diagonal in slot order, each committed to its own slot_full
@@ -469,13 +454,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
           base = (base + S) & (OZ_SLOTS - 1);
         }
       }
-      if (dbg & 32) {
-        prof[blockIdx.x * 5 + 0] = clock64() - t_start;
-        prof[blockIdx.x * 5 + 1] = t_full;
-        prof[blockIdx.x * 5 + 2] = t_slot;
-        prof[blockIdx.x * 5 + 3] = n_block;
-        prof[blockIdx.x * 5 + 4] = n_defer;
-      }
     }
   } else {
     // ---------------- epilogue: warps 2..9 ----------------
@@ -483,7 +461,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
     const int half = (warp - 2) >> 2;       // columns 32·half .. +31
     uint32_t slot_seen = 0;  // 2 bits per slot: parity of how many times it has been drained
     int ebase = 0;
-    for (int t = (dbg & 4) ? ntiles : blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const OzTile td = tiles[t];
       const OzGroup g = groups[td.g];
       const int row = td.mt * OZ_BM + quad * 32 + lane;
@@ -513,11 +491,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
             ob_sleep_wait(&slot_full[sl], u & 1);
             slot_seen = (slot_seen & ~(3u << (2 * sl))) | ((u == 3 ? 2u : u + 1) << (2 * sl));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          }
-          if (dbg & 8) {  // ablation: no TMEM drain
-            __syncwarp();
-            if (lane == 0) ob_arrive(&slot_empty[sl]);
-            continue;
           }
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -553,7 +526,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
           double x;
           if constexpr (S <= 6) x = __ll2double_rn(hacc[j]) * srow * oz_pow2(ecj);
           else x = v[j] * srow * oz_pow2(ecj);
-          if (row < g.R && col < g.C && !(dbg & 16)) orow[2 * col] = x;
+          if (row < g.R && col < g.C) orow[2 * col] = x;
         }
       }
     }
@@ -577,7 +550,7 @@ static cudaError_t stage_s(const tn_plan* p, const double2* gk, const double* lk
   // the A chain (row exponents → A slices) and the B chain (column exponents → B slices) are independent:
   // the B chain runs on an auxiliary stream beside the A chain
   AuxStreams* aux = nullptr;
-  cudaError_t e = aux_streams(&aux);
+  cudaError_t e = aux_streams(s, &aux);
   if (e == cudaSuccess) e = cudaEventRecord(aux->fork, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(aux->st[0], aux->fork, 0);
   if (e != cudaSuccess) return e;
@@ -608,38 +581,14 @@ cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* l
   return cudaErrorInvalidValue;
 }
 
-static int oz_debug() {
-  static const int v = [] {
-    // bit mask, timing studies only (results are garbage): 1 skip MMAs, 2 skip operand loads,
-    // 4 MMA ignores TMEM slot reuse and the epilogue does nothing, 8 epilogue skips the TMEM drain,
-    // 16 epilogue skips the global stores
-    const char* e = getenv("TN_K4O_ABLATE");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <int S, int STG>
 static cudaError_t contract_st(const tn_plan* p, const SectorParams& sp, cudaStream_t s) {
   const size_t smem = (size_t)STG * S * (OZ_A_TILE + OZ_B_TILE) + 8 * (2 * STG + 2 * OZ_SLOTS) + 16;
   cudaError_t e = cudaFuncSetAttribute(k4o_contract<S, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p->oz_ntiles, p->sm_count);
-  const int dbg = oz_debug();
-  unsigned long long* prof = nullptr;
-  if (dbg & 32) cudaMalloc(&prof, sizeof(unsigned long long) * 5 * grid);
   k4o_contract<S, STG><<<grid, OZ_THREADS, smem, s>>>(p->d_oz_groups, p->d_oz_tiles, (int)p->oz_ntiles, p->d_oa,
-                                                      p->d_ob, p->d_oea, p->d_oeb, sp, dbg, prof);
-  if (dbg & 32) {  // timing study: per-CTA MMA-issuer cycle breakdown
-    std::vector<unsigned long long> h(5 * grid);
-    cudaMemcpy(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    double a[5] = {0, 0, 0, 0, 0};
-    for (int b = 0; b < grid; ++b)
-      for (int k = 0; k < 5; ++k) a[k] += (double)h[b * 5 + k] / grid;
-    fprintf(stderr, "k4o mma-issuer per CTA: total %.0f clk, full-wait %.0f, slot-wait %.0f, blocks %.1f, defers %.1f\n",
-            a[0], a[1], a[2], a[3], a[4]);
-    cudaFree(prof);
-  }
+                                                      p->d_ob, p->d_oea, p->d_oeb, sp);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;

@@ -82,9 +82,7 @@ void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out) {
   for (int cl = 0; cl <= p->N; ++cl) {
     const int64_t a0 = std::max<int64_t>(ol[cl], p->r0), a1 = std::min<int64_t>(ol[cl + 1], p->r1);
     for (int64_t band = a0, rows = 0; band < a1; band += rows) {
-      // ≤ BAND rows, never crossing a K45_BAND boundary (the fused kernel waits per band)
-      const int64_t next = p->r0 + ((band - p->r0) / K45_BAND + 1) * K45_BAND;
-      rows = std::min<int64_t>(std::min<int64_t>(BAND, a1 - band), next - band);
+      rows = std::min<int64_t>(BAND, a1 - band);
       for (int cr = std::max(0, cl - 2 * p->d + 2); cr <= cl; ++cr) {
         const int64_t nr = orr[cr + 1] - orr[cr];
         if (nr == 0) continue;
@@ -162,7 +160,7 @@ cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* l
   // the classes touch disjoint elements: run them concurrently (their tails and occupancy overlap) on
   // per-thread auxiliary streams forked from and joined back into s
   AuxStreams* ap = nullptr;
-  if (cudaError_t ea = aux_streams(&ap); ea != cudaSuccess) return ea;
+  if (cudaError_t ea = aux_streams(s, &ap); ea != cudaSuccess) return ea;
   AuxStreams& aux = *ap;
   cudaError_t e = cudaEventRecord(aux.fork, s);
   for (int c = 1; c < 4 && e == cudaSuccess; ++c) {

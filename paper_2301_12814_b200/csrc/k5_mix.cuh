@@ -1,5 +1,5 @@
-// Device code of the U-mix (K5) shared by the stand-alone K5 kernel (k5_mix.cu) and the mixer warps
-// of the fused K4+K5 kernel (k45_fused.cu). See k5_mix.cu for the design.
+// Device code of the U-mix (K5, k5_mix.cu) and of the pair-plan mix K5P (tn_pair.cu). See k5_mix.cu for
+// the design.
 #pragma once
 #include "tn_internal.cuh"
 
@@ -36,7 +36,7 @@ __device__ __forceinline__ void load_group(double2 (&a)[KSM], const SecRef* __re
   }
 }
 
-// L2ONLY: P was written by other SMs during this kernel (fused K4+K5) → bypass L1 (ld.global.cg)
+// L2ONLY: P was written by other SMs during the same kernel → bypass L1 (ld.global.cg)
 // PF: groups further ahead (beyond the one held in registers) whose P lines are prefetched into L2
 // (PF = 2 measured slower at configs 3 and 4: 0.82 vs 0.78 ms, 6.57 vs 6.05 ms)
 template <int NT, int NW, bool L2ONLY = false, int PF = 0>  // NT = ⌈L/8⌉ output tiles of 8 sectors; NW warps per tile

@@ -94,6 +94,8 @@ static void shard_bounds(const Counts& k, int world, std::vector<int64_t>& bound
 static void free_plan(tn_plan* p) {
   if (!p) return;
   const bool used = p->rec_exec;
+  // a captured exec may be replayed on any stream: wait for every replay before the blocks are reused
+  if (p->captured) cudaDeviceSynchronize();
   pool_release(p->blk_oz, p->last_stream, used);
   pool_release(p->blk_lit, p->last_stream, used);
   pool_release(p->blk_p, p->last_stream, used);
@@ -484,58 +486,14 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
         for (int nt = 0; nt < g.nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
     }
     p->ntiles = (int64_t)tiles.size();
-    // ---- fused K4+K5 (k45_fused.cu): band-major tile order + per-band tile counts ----
-    {
-      const char* env = getenv("TN_FUSED");
-      // opt-in (TN_FUSED=1): measured slower than K4 + K5 (4.79 vs 3.35 ms at config 3)
-      p->fused = (env && env[0] == '1') && k45_smem_bytes(5, p->max_mix) <= 227 * 1024 && p->r1 > p->r0;
-      p->nbands = (p->r1 - p->r0 + K45_BAND - 1) / K45_BAND;
-      p->h_band_need.assign((size_t)p->nbands, 0);
-      auto band_span = [&](const TileDesc& t, int64_t* b0, int64_t* b1) {
-        const auto& g = p->groups[t.g];
-        const int64_t a0 = g.row0 + (int64_t)t.mt * BM - p->r0;
-        const int64_t a1 = std::min<int64_t>(g.row0 + g.R, g.row0 + (int64_t)t.mt * BM + BM) - p->r0;
-        *b0 = a0 / K45_BAND;
-        *b1 = (a1 - 1) / K45_BAND;
-      };
-      for (const auto& t : tiles) {
-        int64_t b0, b1;
-        band_span(t, &b0, &b1);
-        for (int64_t b = b0; b <= b1; ++b) ++p->h_band_need[(size_t)b];
-      }
-      if (p->fused) {  // band of the first row, then the heavy-first order above
-        std::vector<int64_t> key(tiles.size());
-        for (size_t i = 0; i < tiles.size(); ++i) {
-          int64_t b0, b1;
-          band_span(tiles[i], &b0, &b1);
-          key[i] = b0;
-        }
-        std::vector<size_t> idx(tiles.size());
-        std::iota(idx.begin(), idx.end(), 0);
-        std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return key[x] < key[y]; });
-        std::vector<TileDesc> sorted(tiles.size());
-        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = tiles[idx[i]];
-        tiles.swap(sorted);
-      }
-    }
     std::vector<MixTile>& mix = p->h_mix;
     build_mix_tiles(p, mix);
     p->nmix = (int64_t)mix.size();
-    std::vector<MixItem>& items = p->h_items;
-    {
-      // the K5T experiment's item list is built only when it is selected (host time is on the step's path)
-      const char* env = getenv("TN_K5T");
-      if (env && env[0] == '1') build_mix_items(p, items);
-      p->k5t = !items.empty();
-    }
     if (!p->groups.empty() || !mix.empty()) {
       Carver cw;
       const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
       const size_t o_t = cw.take<TileDesc>((int64_t)tiles.size());
       const size_t o_m = cw.take<MixTile>((int64_t)mix.size());
-      const size_t o_i = cw.take<MixItem>((int64_t)items.size());
-      const size_t o_bn = cw.take<int32_t>(p->nbands);
-      const size_t o_bd = cw.take<int32_t>(p->nbands);
       const size_t o_a = cw.take<double2>(p->a_elems);
       const size_t o_b = cw.take<double2>(p->b_elems);
       p->blk_work = pool_alloc(cw.off, &aerr);
@@ -544,12 +502,6 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
       p->d_tiles = reinterpret_cast<TileDesc*>(base + o_t);
       p->d_mix = reinterpret_cast<MixTile*>(base + o_m);
-      p->d_items = reinterpret_cast<MixItem*>(base + o_i);
-      p->d_band_need = reinterpret_cast<int32_t*>(base + o_bn);
-      p->d_band_done = reinterpret_cast<int32_t*>(base + o_bd);
-      if (p->nbands)
-        TN_TRY(cudaMemcpyAsync(p->d_band_need, p->h_band_need.data(), p->nbands * sizeof(int32_t),
-                               cudaMemcpyHostToDevice, p->plan_stream), "H2D band counts");
       p->d_apanel = reinterpret_cast<double2*>(base + o_a);
       p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
       if (!p->groups.empty()) {
@@ -561,9 +513,6 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       if (!mix.empty())
         TN_TRY(cudaMemcpyAsync(p->d_mix, mix.data(), mix.size() * sizeof(MixTile), cudaMemcpyHostToDevice,
                                p->plan_stream), "H2D mix tiles");
-      if (!items.empty())
-        TN_TRY(cudaMemcpyAsync(p->d_items, items.data(), items.size() * sizeof(MixItem), cudaMemcpyHostToDevice,
-                               p->plan_stream), "H2D mix items");
       // no host sync: tn_theta_exec's stream waits for ev_ready (the host vectors stay alive in the plan)
       p->ws_bytes = (int64_t)cw.off;
     }
@@ -779,13 +728,12 @@ tn_status tn_plan_exec_launches(const tn_plan* p, int64_t* n_launches) {
   } else {
     const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
     if (emu) n += (p->oz_groups.empty() ? 0 : 4) + (p->oz_ntiles > 0);      // K3O ×4, K4O
-    else n += (p->groups.empty() ? 0 : 2) + ((p->fused && !p->pair) ? 1 : (p->ntiles > 0));  // K3 a/b, K4 (or K45)
+    else n += (p->groups.empty() ? 0 : 2) + (p->ntiles > 0);                  // K3 a/b, K4
     if (p->pair) {
       n += (p->nmix2[0] > 0) + (p->nmix2[1] > 0);                            // K5P, two passes
-    } else if (emu || !p->fused) {
+    } else {
       const int64_t c0 = p->nmix_cls[0], c1 = p->nmix_cls[1], c2 = p->nmix_cls[2], c3 = p->nmix - c0 - c1 - c2;
-      if (p->k5t) n += (p->nitem_cls[0] > 0) + (p->nitem_cls[1] > 0) + (p->nitem_cls[2] > 0) + (c3 > 0);
-      else n += (c0 > 0) + (c1 > 0) + (c2 > 0) + (c3 > 0);                  // K5, one launch per L class
+      n += (c0 > 0) + (c1 > 0) + (c2 > 0) + (c3 > 0);                        // K5, one launch per L class
     }
   }
   *n_launches = n;
@@ -828,12 +776,21 @@ tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_str
 }
 
 // The exec stream waits for the plan's asynchronous table upload. Under CUDA graph capture that event lies
-// outside the capture (waiting on it would invalidate it): a captured exec requires the tables to be ready
-// already (any earlier exec or a synchronisation), which the header documents.
+// outside the capture (waiting on it would invalidate the capture), and a replay may run on any stream, so
+// the host waits for the upload instead and marks the plan captured: its blocks then go back to the pool
+// only after a device-wide synchronisation (free_plan), because a replay's stream is unknown to the plan.
 static tn_status wait_tables(const tn_plan* p, cudaStream_t s) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) cs = cudaStreamCaptureStatusNone;
-  if (cs != cudaStreamCaptureStatusNone) return TN_OK;
+  if (cs != cudaStreamCaptureStatusNone) {
+    p->captured = true;
+    // a host wait is a "potentially unsafe" call under global capture mode: relax this thread's mode for it
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    const cudaError_t e = cudaEventSynchronize(p->ev_ready);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    return cuda_check(e, "plan tables (captured exec)");
+  }
   return cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
 }
 
@@ -878,21 +835,11 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
     if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
     st = cuda_check(launch_pair_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5P launch");
     if (st != TN_OK) return st;
-  } else if (!emu && p->fused) {  // K4 + K5 in one kernel; its time is reported as K4's, K5's as 0
-    st = cuda_check(launch_fused(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K45 launch");
-    if (st != TN_OK) return st;
-    if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
   } else {
     st = cuda_check(emu ? launch_oz_contract(p, sp, s) : launch_contract(p, sp, s), "K4 launch");
     if (st != TN_OK) return st;
     if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
-    if (p->k5t) {  // K5T (TMA runs) for the L ≤ 32 blocks, k5_mix for the rest
-      st = cuda_check(launch_mix_tma(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5T launch");
-      if (st == TN_OK)
-        st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s, 3), "K5 launch");
-    } else {
-      st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
-    }
+    st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
     if (st != TN_OK) return st;
   }
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");
@@ -902,7 +849,7 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
                                const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
                                double* const* theta_dst) {
   if (!p) return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL plan");
-  if (p->fused || p->contraction == TN_CONTRACT_PAPER_LITERAL)
+  if (p->contraction == TN_CONTRACT_PAPER_LITERAL)
     return fail(TN_ERR_UNSUPPORTED, "tn_theta_exec_remote: the DMMA or INT8 engine only");
   if (!gamma_k || !lambda_k || !gamma_k1 || !lambda_l || !lambda_r || !U || !theta_dst)
     return fail(TN_ERR_DIMENSION, "tn_theta_exec_remote: NULL input pointer");

@@ -25,7 +25,6 @@ constexpr int CHUNK = BM * BK;        // complex elements per full operand chunk
 constexpr int K4_STAGES = 6;
 constexpr int K4_CONSUMER_WARPS = 8;
 constexpr int K4_THREADS = (K4_CONSUMER_WARPS + 1) * 32;
-constexpr int K45_BAND = 256;         // rows (sorted left positions) per band of the fused K4+K5 kernel
 
 struct GroupDesc {          // one center charge c_c: P_{c_c} = A_{c_c} · B_{c_c}
   int64_t a_off;            // complex offset of this group's A panel in the A workspace
@@ -63,13 +62,6 @@ struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive c
   int32_t e0, ne;           // first 8-group (row-major within the block) and count
   int32_t nr, ngr;          // columns of the block (n_r(c_r)) and 8-groups per row ⌈nr/8⌉
   int32_t pl0, pr0;         // sorted positions of the block's first (local) row / first column
-};
-
-struct MixItem {            // K5T work unit: nrows rows × w columns of one (c_l, c_r) block, all its L sectors
-  int32_t cl, cr;
-  int32_t pl, nrows;        // sorted left position of the first row; rows
-  int32_t pc, w;            // sorted right position of the first column; columns
-  int32_t stride, pad;      // shared-memory run stride (complex elements)
 };
 
 constexpr int MAXC = TN_MAX_N + 1;
@@ -137,11 +129,6 @@ struct tn_plan {
   tn::MixTile* d_mix = nullptr;
   int64_t nmix = 0;                            // K5 tiles
   int64_t nmix_cls[3] = {0, 0, 0};             // of which the first [0] have L ≤ 8, the next [1] L ≤ 16, [2] L ≤ 32
-  bool fused = false;                          // K4 + K5 in one kernel (k45_fused.cu)
-  int64_t nbands = 0;                          // K45_BAND-row bands of this rank's rows
-  std::vector<int32_t> h_band_need;            // K4 tiles touching each band
-  int32_t* d_band_need = nullptr;
-  int32_t* d_band_done = nullptr;
   // row / column index lists K3 and K3O gather through: perm_l / perm_r themselves for single-charge
   // plans (group rows are contiguous sorted positions), per-group gathered lists for pair plans
   const int32_t* d_rowperm = nullptr;
@@ -173,13 +160,10 @@ struct tn_plan {
   cudaEvent_t ev_ready = nullptr;
   std::vector<tn::TileDesc> h_tiles;           // host sources of the async uploads (kept alive)
   std::vector<tn::MixTile> h_mix;
-  std::vector<tn::MixItem> h_items;            // K5T items (L ≤ 32 blocks), classes L ≤ 8 / 16 / 32
-  tn::MixItem* d_items = nullptr;
-  int64_t nitem_cls[3] = {0, 0, 0};
-  bool k5t = false;                            // U-mix by K5T (TMA runs) for the L ≤ 32 blocks
   std::vector<tn::OzTile> h_oz_tiles;
   mutable bool rec_k1 = false, rec_k2 = false, rec_exec = false;
   mutable cudaStream_t last_stream = nullptr;  // stream of the last exec (pool release fence)
+  mutable bool captured = false;               // an exec was captured into a CUDA graph (free_plan syncs the device)
   // contraction mode (TN_CONTRACT_*) and the INT8-emulation layout (built by tn_plan_set_contraction)
   int contraction = TN_CONTRACT_F64_DMMA;
   int oz_slices = 0;
@@ -233,36 +217,63 @@ cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream
 cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
                             cudaStream_t s);
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
-// Per-thread auxiliary streams on the current device for launches that touch disjoint data (K3 a/b,
-// K3O's two exponent→slice chains, K5's register classes): fork from s, run, join back into s.
+// Per-thread auxiliary streams for launches that touch disjoint data (K3 a/b, K3O's two exponent→slice
+// chains, K5's register classes): fork from s, run, join back into s. One set per (device, caller stream),
+// so gates in flight on different caller streams of one thread share no auxiliary stream (no false
+// cross-gate dependencies); a thread keeps at most AUX_SETS sets and recycles the least recently used one
+// (reuse only adds ordering, never a hazard).
 struct AuxStreams {
   int dev = -1;
+  cudaStream_t owner = nullptr;  // the caller stream this set serves
+  uint64_t used = 0;             // LRU stamp
   cudaStream_t st[3] = {};
   cudaEvent_t fork = nullptr, join[3] = {};
 };
-inline cudaError_t aux_streams(AuxStreams** out) {
-  thread_local AuxStreams aux;
+constexpr int AUX_SETS = 8;
+inline cudaError_t aux_streams(cudaStream_t s, AuxStreams** out) {
+  thread_local AuxStreams sets[AUX_SETS];
+  thread_local uint64_t clock = 0;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (aux.dev != dev) {
-    for (auto& x : aux.st)
-      if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&aux.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    for (auto& x : aux.join)
-      if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
-    aux.dev = dev;
+  AuxStreams* hit = nullptr;
+  AuxStreams* lru = &sets[0];
+  for (auto& a : sets) {
+    if (a.dev == dev && a.owner == s) {
+      hit = &a;
+      break;
+    }
+    if (a.used < lru->used) lru = &a;
   }
-  *out = &aux;
+  if (!hit) {
+    hit = lru;
+    if (hit->dev != dev) {  // (re)create on this device; release the old device's handles first
+      if (hit->dev >= 0) {
+        int cur = dev;
+        cudaSetDevice(hit->dev);
+        for (auto& x : hit->st) cudaStreamDestroy(x);
+        cudaEventDestroy(hit->fork);
+        for (auto& x : hit->join) cudaEventDestroy(x);
+        cudaSetDevice(cur);
+        hit->dev = -1;
+      }
+      for (auto& x : hit->st)
+        if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&hit->fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+      for (auto& x : hit->join)
+        if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+      hit->dev = dev;
+    }
+    hit->owner = s;
+  }
+  hit->used = ++clock;
+  *out = hit;
   return cudaSuccess;
 }
 
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                        const double2* U, cudaStream_t s, int first_class = 0);
 void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out);
-void build_mix_items(tn_plan* p, std::vector<MixItem>& out);
-cudaError_t launch_mix_tma(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                           const double2* U, cudaStream_t s);
 tn_status build_pair_tables(tn_plan* p);
 tn_status build_literal(tn_plan* p);
 cudaError_t launch_literal(const tn_plan* p, const SectorParams& sp, const double2* gk, const double* lk,
@@ -270,9 +281,6 @@ cudaError_t launch_literal(const tn_plan* p, const SectorParams& sp, const doubl
                            cudaEvent_t mid);
 cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
                             const double2* U, cudaStream_t s, const SectorParams* sp2 = nullptr);
-cudaError_t launch_fused(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,
-                         const double2* U, cudaStream_t s);
-size_t k45_smem_bytes(int stages, int max_mix);
 
 // ---- double-double arithmetic (K2): error-free transforms, ~106-bit significand ----
 struct dd {

@@ -5,9 +5,11 @@
 // PAPER.md:192 (SVD "takes up the majority" of GPU time); contract SPEC.md:70-78, tie-break SPEC.md:97.
 //
 // B200 design (DESIGN.md §4 "SVD step"):
-//  * Per-sector SVD with cuSOLVER (polar-decomposition Xgesvdp by default, one-sided Jacobi gesvdj with
-//    TN_SVD_ALGO=gesvdj), econ: a library routine, as the paper treats SVD ("a well-researched and
-//    optimized routine"). Sectors run concurrently on 8 lanes (handle + stream + host
+//  * Per-sector spectrum by default from the Gram eigensolver + Rayleigh–Ritz path (only the
+//    values that can enter the global top χ are computed exactly); a full cuSOLVER SVD per sector
+//    (polar-decomposition Xgesvdp with TN_SVD_ALGO=gesvdp, one-sided Jacobi gesvdj with TN_SVD_ALGO=gesvdj)
+//    is selectable — the SVD itself being a library routine, as the paper treats it ("a well-researched
+//    and optimized routine"). Sectors run concurrently on 8 lanes (handle + stream + host
 //    thread each), largest first onto the least-loaded lane. Θ(c) is row-major, i.e. the column-major
 //    C×R matrix X = Θᵀ = U_x S V_xᴴ, so Θ = conj(V_x) S U_xᵀ.
 //  * Global ranking on the device: one stable radix sort (cub) of all singular values, descending, whose
@@ -896,6 +898,9 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
         sp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, lambda_r, chi_new, p->chi[2],
         reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
     if ((st = cuda_check(cudaGetLastError(), "SVD factors")) != TN_OK) return st;
+    // k_svd_factors reads the process-wide scratch (X.buf, gbuf): drain it before another call (on any stream
+    // or thread) may overwrite that scratch — negligible next to the SVD itself
+    if ((st = cuda_check(cudaStreamSynchronize(s), "SVD factors sync")) != TN_OK) return st;
   }
   *chi_out = res[0];
   std::memcpy(discarded, &res[1], 8);

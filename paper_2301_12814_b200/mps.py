@@ -118,9 +118,6 @@ class MPS(_Chain):
         self.gam = [as_t(x, torch.complex128) for x in gam]
         self.lam = [as_t(x, torch.float64) for x in lam]
         self.M = len(self.gam)
-        # test hook only: host-logic tests of the layer exchange (gloo, CPU) replace the gate by the CPU
-        # oracle's; the product path always runs the C ABI below and raises if the library is missing
-        self._gate_impl = None
         if len(self.q) != self.M + 1 or len(self.lam) != self.M + 1:
             raise ValueError("an MPS of M sites needs M+1 bonds of charges and λ")
 
@@ -136,8 +133,6 @@ class MPS(_Chain):
         """One TEBD update of sites (k, k+1); returns the discarded weight Σ dropped s²."""
         if not 0 <= k < self.M - 1:
             raise ValueError("gate sites out of range")
-        if self._gate_impl is not None:
-            return self._gate_impl(self, k, theta, phi, chi_max, cutoff)
         plan = Plan(self.d, self.N, self.q[k], self.q[k + 1], self.q[k + 2])
         if contraction is not None:
             plan.set_contraction(*contraction)
@@ -172,7 +167,6 @@ class MPO(_Chain):
         self.gam = [as_t(x, torch.complex128) for x in gam]
         self.lam = [as_t(x, torch.float64) for x in lam]
         self.M = len(self.gam)
-        self._gate_impl = None   # test hook only (as MPS._gate_impl)
         if not (len(self.q1) == len(self.q2) == len(self.lam) == self.M + 1):
             raise ValueError("an MPO of M sites needs M+1 bonds of charge pairs and λ")
 
@@ -188,8 +182,6 @@ class MPO(_Chain):
         """One TEBD update of sites (k, k+1) with U⊗U*; returns the discarded weight."""
         if not 0 <= k < self.M - 1:
             raise ValueError("gate sites out of range")
-        if self._gate_impl is not None:
-            return self._gate_impl(self, k, theta, phi, chi_max, cutoff)
         plan = Plan2(self.d, self.N, self.q1[k], self.q2[k], self.q1[k + 1], self.q2[k + 1], self.q1[k + 2],
                      self.q2[k + 2])
         if contraction is not None:

@@ -376,30 +376,6 @@ def test_padding_invariance(tn, cfg, extra):
         assert rel_err(sub, a[c][np.ix_(ra, ca)]) < 1e-13, c
 
 
-# ------------------------------------------------------------------ experimental fused K4+K5 (opt-in)
-@pytest.mark.parametrize("cfg", [1, 2])
-def test_fused_k45_parity(tn, cfg, monkeypatch):
-    # TN_FUSED=1 (read at plan time) runs K4 and K5 in one kernel (k45_fused.cu, band-ordered handoff
-    # through global counters); same arithmetic, so the same ≤ 1e-10 bar against the oracle.
-    monkeypatch.setenv("TN_FUSED", "1")
-    case = _case(cfg)
-    ref, *_ = _oracle(cfg)
-    _, _, got = gpu_theta(case)
-    assert_sectors_close(got, ref, TOL, f"fused config{cfg}")
-
-
-# ------------------------------------------------------------------ experimental TMA-fed mix K5T (opt-in)
-@pytest.mark.parametrize("cfg", [0, 1, 2])
-def test_k5t_parity(tn, cfg, monkeypatch):
-    # TN_K5T=1 (read at plan time): the L ≤ 32 blocks are mixed by k5t_mix (bulk-copy ring); same
-    # arithmetic as k5_mix, so the same ≤ 1e-10 bar against the oracle
-    monkeypatch.setenv("TN_K5T", "1")
-    case = _case(cfg)
-    ref, *_ = _oracle(cfg)
-    _, _, got = gpu_theta(case)
-    assert_sectors_close(got, ref, TOL, f"k5t config{cfg}")
-
-
 # ------------------------------------------------------------------ paper-literal ablation engine
 @pytest.mark.parametrize("cfg", [0, 1, 2])
 def test_paper_literal_engine_parity(tn, cfg):

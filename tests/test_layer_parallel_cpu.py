@@ -3,8 +3,8 @@
 
 Every rank holds a replica of the MPS; MPS.apply_layer(group=…) deals the gates by longest-processing-
 time (layer_owners), runs its own and broadcasts the updated q, λ, Γ^{[k]}, Γ^{[k+1]}. The GPU gate is
-replaced by the CPU oracle's gate (oracle/layer.py, the test hook MPS._gate_impl), so the distributed
-run must reproduce the serial oracle layer bit for bit on every rank."""
+replaced by the CPU oracle's gate (oracle/layer.py) in a test-only subclass that overrides apply_gate, so
+the distributed run must reproduce the serial oracle layer bit for bit on every rank."""
 import os
 import socket
 
@@ -61,8 +61,11 @@ def _worker_mpo(rank, world, port, M, N, d, chi, chi_max, seed, q):
         from paper_2301_12814_b200.mps import MPO
         st = L.random_mpo(M, N, d, chi, seed)
         ref = L.copy_state2(st)
-        mpo = MPO.from_state(st, device="cpu")
-        mpo._gate_impl = _oracle_gate2
+        class OracleMPO(MPO):  # test subclass: the GPU gate replaced by the oracle's
+            def apply_gate(self, k, theta, phi, chi_max, cutoff=1e-14, contraction=None):
+                return _oracle_gate2(self, k, theta, phi, chi_max, cutoff)
+
+        mpo = OracleMPO.from_state(st, device="cpu")
         rng = np.random.default_rng(seed + 9)
         for parity in (0, 1, 0):
             n = len(range(parity, M - 1, 2))
@@ -94,8 +97,11 @@ def _worker(rank, world, port, M, N, d, chi, chi_max, seed, q):
         from paper_2301_12814_b200.mps import MPS
         st = L.random_mps(M, N, d, chi, seed)
         ref = L.copy_state(st)
-        mps = MPS.from_state(st, device="cpu")
-        mps._gate_impl = _oracle_gate
+        class OracleMPS(MPS):  # test subclass: the GPU gate replaced by the oracle's
+            def apply_gate(self, k, theta, phi, chi_max, cutoff=1e-14, contraction=None):
+                return _oracle_gate(self, k, theta, phi, chi_max, cutoff)
+
+        mps = OracleMPS.from_state(st, device="cpu")
         rng = np.random.default_rng(seed + 7)
         for parity in (0, 1, 0, 1):
             n = len(range(parity, M - 1, 2))
