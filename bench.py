@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--chi-max", type=int, default=None, help="layer mode: truncation χ (default: the config's χ)")
     ap.add_argument("--mpo", type=int, default=None, metavar="K",
                     help="layer mode on an MPO (vectorized density matrix, pair charges) shaped like synth.PAIR_CONFIGS[K]")
+    ap.add_argument("--emulate-ranks", type=int, default=8, metavar="R",
+                    help="N=1 only: run every rank's row-sharded step of a world-R job in turn on this GPU and "
+                         "report per-rank device times and the projected strong-scaling speedup (0: skip)")
     ap.add_argument("--pair", type=int, default=None,
                     help="time the MPO doubled-charge path on synth.PAIR_CONFIGS[k] instead (tn_theta2_plan)")
     return ap.parse_args()
@@ -223,7 +226,10 @@ def run_tn(args, rank, world, local_rank):
     h = lambda a: torch.from_numpy(np.ascontiguousarray(a))
     gk, gk1 = h(case.gamma_k).to(dev), h(case.gamma_k1).to(dev)
     lk, ll, lr = h(case.lam_k).to(dev), h(case.lam_l).to(dev), h(case.lam_r).to(dev)
-    ql, qc, qr = (h(q).to(dev) for q in (case.q_l, case.q_c, case.q_r))
+    # bond charges stay on the host (48 KB of plan metadata): tn_theta_plan counts them there and uploads them
+    # for K1 (which sorts on the device), so planning never waits for the GPU (include/tn_theta.h)
+    hq = [np.ascontiguousarray(q) for q in (case.q_l, case.q_c, case.q_r)]
+    ql, qc, qr = hq
 
     torch.cuda.synchronize()
     tn.Plan(case.d, case.N, ql, qc, qr, world, rank).destroy()   # warm the module / pool
@@ -250,8 +256,12 @@ def run_tn(args, rank, world, local_rank):
     del probe
     stream = torch.cuda.current_stream(dev)
 
+    plan_host_ms = []
+
     def step(keep):
+        t_p = time.perf_counter()
         plan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)          # K1 + decomposition
+        plan_host_ms.append((time.perf_counter() - t_p) * 1e3)
         if int8:
             plan.set_contraction("int8", args.slices)                      # slice layout (K3O/K4O)
         tn.build_bs_unitary(plan, case.theta, case.phi, out=U)            # K2
@@ -340,18 +350,23 @@ def run_tn(args, rank, world, local_rank):
         try:
             comm = tn.Comm(rank, world)
             vplan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)
+            gk_scratch = torch.empty_like(gk)
             tn.build_bs_unitary(vplan, case.theta, case.phi, out=U)
             comm_variants = {}
-            for name, bc, gm in (("exec_only", False, tn.TN_GATHER_NONE), ("bcast_operands", True, tn.TN_GATHER_NONE),
-                                 ("gather_sector_owner", False, tn.TN_GATHER_SECTOR_OWNER),
-                                 ("gather_root", False, tn.TN_GATHER_ROOT)):
+            for name, bc, gm in (("exec_only", tn.TN_BCAST_NONE, tn.TN_GATHER_NONE),
+                                 ("bcast_slabs", tn.TN_BCAST_SLABS, tn.TN_GATHER_NONE),
+                                 ("bcast_full", tn.TN_BCAST_FULL, tn.TN_GATHER_NONE),
+                                 ("gather_sector_owner", tn.TN_BCAST_NONE, tn.TN_GATHER_SECTOR_OWNER),
+                                 ("gather_root", tn.TN_BCAST_NONE, tn.TN_GATHER_ROOT)):
                 vout = None
                 for it in range(4):                       # 1 warm-up + 3 timed
                     barrier()
                     torch.cuda.synchronize()
                     v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     v0.record(stream)
-                    vout = tn.theta_exec_sharded(vplan, comm, gk, lk, gk1, ll, lr, U, out=vout, bcast_operands=bc,
+                    # TN_BCAST_SLABS overwrites a rank > 0's gk with its packed slab: use a scratch copy
+                    g_in = gk if bc != tn.TN_BCAST_SLABS or rank == 0 else gk_scratch
+                    vout = tn.theta_exec_sharded(vplan, comm, g_in, lk, gk1, ll, lr, U, out=vout, bcast_operands=bc,
                                                  gather_mode=gm)
                     v1.record(stream)
                     torch.cuda.synchronize()
@@ -436,6 +451,11 @@ def run_tn(args, rank, world, local_rank):
     e2e_step_ms = float(te.item()) / args.e2e_steps
     e2e_value = f_useful / (e2e_step_ms * 1e-3) / 1e9
 
+    projection = None
+    if world == 1 and args.emulate_ranks > 1 and not int8:
+        projection = emulate_ranks(tn, case, args.emulate_ranks, args.steps, args.warmup, dev, stream, hq,
+                                   (gk, lk, gk1, ll, lr), U, ms_step)
+
     if rank != 0:
         return
     kmean = {k: (statistics.mean(v) if v else None) for k, v in ktimes.items()}
@@ -500,12 +520,72 @@ def run_tn(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step_ms, 3),
                 "note": "pinned H2D of Γk, Γk1, λ's and charges + D2H of every Θ(c) per gate, 2 gates in flight"},
         "comm_variants_ms": comm_variants,
+        "plan_host_ms": round(statistics.median(plan_host_ms), 4) if plan_host_ms else None,
+        "multi_gpu_projection": projection,
         "alt_engine": alt,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, U, wall1_ms):
+    """A PROJECTION of the world-R row-sharded step (compute only, operands
+    pre-replicated, Θ left sharded), measured on this one GPU: every rank's own step — tn_theta_plan(R, r) with
+    host charges + U + tn_theta_exec of its flop-balanced row shard — runs back to back `steps` times in turn,
+    timed with CUDA events exactly like the N=1 line; a rank on its own B200 would see this device time (same
+    SM count and HBM), while the host-side plan time per rank is what could keep it from staying GPU-bound.
+    projected_speedup = wall(1) / max_r wall(r)."""
+    import torch
+    gk, lk, gk1, ll, lr = ops
+    per, host, kern = [], [], []
+    for r in range(R):
+        probe = tn.Plan(case.d, case.N, *hq, R, r)
+        outs = tn.alloc_theta(probe, device=dev)
+        probe.destroy()
+        hms = []
+
+        def step(keep):
+            t0 = time.perf_counter()
+            p = tn.Plan(case.d, case.N, *hq, R, r)
+            hms.append((time.perf_counter() - t0) * 1e3)
+            tn.build_bs_unitary(p, case.theta, case.phi, out=U)
+            tn.theta_exec(p, gk, lk, gk1, ll, lr, U, out=outs)
+            keep.append(p)
+        keep = []
+        for _ in range(warmup):
+            step(keep)
+        torch.cuda.synchronize()
+        for p in keep:
+            p.destroy()
+        keep.clear()
+        hms.clear()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kt = []
+        e0.record(stream)
+        for _ in range(steps):
+            step(keep)
+            if len(keep) > 2:
+                old = keep.pop(0)
+                kt.append(old.kernel_times())
+                old.destroy()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        for p in keep:
+            kt.append(p.kernel_times())
+            p.destroy()
+        per.append(e0.elapsed_time(e1) / steps)
+        host.append(statistics.median(hms))
+        kern.append({k: round(statistics.mean(x[k] for x in kt), 4) for k in ("k3_stage", "k4_contract", "k5_mix")})
+        del outs
+    mx, mean = max(per), statistics.mean(per)
+    return {"kind": "projection (not a multi-GPU measurement): each rank's step timed alone on this GPU",
+            "ranks": R, "per_rank_ms": [round(x, 4) for x in per], "max_ms": round(mx, 4),
+            "imbalance_max_over_mean": round(mx / mean, 4), "wall1_ms": round(wall1_ms, 4),
+            "projected_speedup": round(wall1_ms / mx, 3), "plan_host_ms_per_rank": [round(x, 4) for x in host],
+            "kernels_ms_rank0": kern[0], "kernels_ms_slowest": kern[per.index(mx)],
+            "excludes": "operand distribution and Θ gathers (comm_variants_ms at N>1 measures those)"}
 
 
 # --------------------------------------------------------------------------------------------- brick-wall layer

@@ -63,6 +63,14 @@ typedef void* tn_stream;          /* a cudaStream_t (0 = legacy default stream) 
 
 enum { TN_BOND_LEFT = 0, TN_BOND_CENTER = 1, TN_BOND_RIGHT = 2 };
 enum { TN_GATHER_NONE = 0, TN_GATHER_ROOT = 1, TN_GATHER_SECTOR_OWNER = 2 };
+enum { TN_BCAST_NONE = 0, TN_BCAST_SLABS = 1, TN_BCAST_FULL = 2 };
+
+/* One entry of a Θ gather schedule (tn_plan_gather_schedule / tn_gather_schedule_host): rank `src`'s slab
+ * of sector `sector` — `rows` × `cols` complex, row-major — lands at row `row_begin` of the FULL Θ(sector)
+ * on rank `dst`. Entries with src == dst are placed in place by the exec (no transfer). */
+typedef struct {
+  int64_t sector, src, dst, row_begin, rows, cols;
+} tn_transfer;
 
 /* ------------------------------------------------------------------------------------------ */
 /* Plan: bond re-indexing (K1) + work decomposition. Not on the hot path; synchronises once.   */
@@ -250,10 +258,50 @@ TN_API tn_status tn_comm_destroy(tn_comm* comm);
  * pair plans). Errors: DIMENSION (NULL), DOMAIN (c or rank out of range). */
 TN_API tn_status tn_plan_slab_rows(const tn_plan* plan, int c, int rank, int64_t* row_begin, int64_t* rows);
 
-/* tn_theta_exec_sharded — this rank's rows of every Θ(c), plus optional exchange.
+/* The exact transfer list tn_theta_exec_sharded executes for gather_mode: one entry per
+ * (sector, source rank) with a non-empty slab, sectors ascending then source rank ascending, destination
+ * rank 0 (TN_GATHER_ROOT) or tn_plan_sector_owner(sector) (TN_GATHER_SECTOR_OWNER); none for
+ * TN_GATHER_NONE. Identical on every rank. HOST outputs: *n_out = number of entries; the first
+ * min(capacity, *n_out) are written to out (out may be NULL with capacity 0 to query the count).
+ * Errors: DIMENSION (NULL plan/n_out, or capacity < *n_out with out != NULL), DOMAIN (gather_mode). */
+TN_API tn_status tn_plan_gather_schedule(const tn_plan* plan, int gather_mode, int64_t capacity, tn_transfer* out,
+                                         int64_t* n_out);
+/* The same schedule without a plan or a GPU (single-charge layout, R2): from host offset tables
+ * off_l / off_r (N+2 int32 each, as tn_plan_offsets returns) and row-shard bounds (world_size+1 int64, as
+ * tn_shard_rows_host returns); sector owners by the tn_sector_owners_host rule. Errors as above, plus
+ * DOMAIN for decreasing offsets or bounds. */
+TN_API tn_status tn_gather_schedule_host(int d, int N, const int32_t* off_l, const int32_t* off_r, int world_size,
+                                         const int64_t* bounds, int gather_mode, int64_t capacity,
+                                         tn_transfer* out, int64_t* n_out);
+/* The communicator's asynchronous error state (ncclCommGetAsyncError): TN_OK, or TN_ERR_NCCL with the NCCL
+ * error in tn_last_error(). tn_theta_exec_sharded checks it before and after each grouped call. */
+TN_API tn_status tn_comm_async_error(tn_comm* comm);
+
+/* Row-slab operands (the TN_BCAST_SLABS distribution, usable on its own when the caller moves the slabs):
+ * tn_pack_row_slab writes rank `rank`'s rows of Γk — sorted left positions [r0, r1) of that rank's shard
+ * (tn_plan_shard_rows) — packed in sorted order: slab_out[(p − r0)·χ_c + k] = Γk[perm_l[p]][k]
+ * (K6 `k6_pack_rows`; gamma_k DEVICE complex [χ_l × χ_c] caller order, slab_out DEVICE complex of
+ * (r1−r0)·χ_c entries, caller-owned). tn_theta_exec_slab is tn_theta_exec for the plan's own rank with Γk
+ * given as that packed slab (gamma_k_slab; every other argument as tn_theta_exec), so a rank never holds
+ * the rows of other shards. Stream-ordered, no host sync. Errors: DIMENSION (NULL), DOMAIN (rank),
+ * UNSUPPORTED (the paper-literal ablation engine), CUDA. */
+TN_API tn_status tn_pack_row_slab(const tn_plan* plan, tn_stream stream, const double* gamma_k, int rank,
+                                  double* slab_out);
+TN_API tn_status tn_theta_exec_slab(const tn_plan* plan, tn_stream stream, const double* gamma_k_slab,
+                                    const double* lambda_k, const double* gamma_k1, const double* lambda_l,
+                                    const double* lambda_r, const double* U, double* const* theta_out);
+
+/* tn_theta_exec_sharded — this rank's rows of every Θ(c), plus optional exchange (PAPER.md:96-103).
  *   plan          built with the communicator's world_size and rank (else TN_ERR_CONSISTENCY).
- *   bcast_operands if non-zero, first ncclBroadcast Γk, λk, Γk1, λl, λr and U from rank 0 into
- *                 the same (full-size, every rank) device buffers.
+ *   bcast_operands operand distribution from rank 0 before the compute:
+ *                 TN_BCAST_NONE  — every rank already holds its operands (full-size, caller order).
+ *                 TN_BCAST_SLABS — rank 0 holds Γk (caller order); each other rank receives ONLY its row
+ *                   slab: rank 0 packs the other ranks' rows in sorted order (tn_pack_row_slab's K6) and
+ *                   sends each rank its run, which lands in gamma_k as the packed (r1−r0) × χ_c slab
+ *                   (gamma_k needs only that capacity on ranks > 0) and is consumed as by
+ *                   tn_theta_exec_slab. Γk1, λk, λl, λr and U — replicated by design — are
+ *                   ncclBroadcast into the same full-size buffers on every rank.
+ *                 TN_BCAST_FULL  — the whole Γk is broadcast as well (every rank full-size, caller order).
  *   gather_mode   TN_GATHER_NONE: theta_out holds the local slabs (tn_plan_local_sector_shape).
  *                 TN_GATHER_ROOT: on rank 0 theta_out holds the FULL Θ(c) (R_c×C_c) and every
  *                 rank's slab is sent to it with grouped ncclSend/ncclRecv; on other ranks
@@ -261,8 +309,10 @@ TN_API tn_status tn_plan_slab_rows(const tn_plan* plan, int c, int rank, int64_t
  *                 TN_GATHER_SECTOR_OWNER: Θ(c) goes to rank tn_plan_sector_owner(c)
  *                 (sectors spread over ranks by element count — the hand-off to per-sector SVD); on the
  *                 owner theta_out[c] holds the FULL Θ(c), elsewhere the local slab.
- * Other arguments as tn_theta_exec. Errors: as tn_theta_exec, plus TN_ERR_NCCL,
- * TN_ERR_CONSISTENCY. */
+ *                 The transfers are exactly tn_plan_gather_schedule(plan, gather_mode).
+ * Other arguments as tn_theta_exec. Errors: as tn_theta_exec, plus TN_ERR_NCCL (including an asynchronous
+ * communicator error), TN_ERR_CONSISTENCY, TN_ERR_DOMAIN (unknown mode), TN_ERR_UNSUPPORTED (TN_BCAST_SLABS
+ * with the paper-literal ablation engine). */
 TN_API tn_status tn_theta_exec_sharded(const tn_plan* plan, tn_stream stream, tn_comm* comm,
                                 double* gamma_k, double* lambda_k, double* gamma_k1,
                                 double* lambda_l, double* lambda_r, double* U,

@@ -16,11 +16,13 @@ import numpy as np
 import torch
 
 from ._lib import (lib, check, TnError, STATUS, TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT, TN_GATHER_NONE,
-                   TN_GATHER_ROOT, TN_GATHER_SECTOR_OWNER, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH)
+                   TN_GATHER_ROOT, TN_GATHER_SECTOR_OWNER, TN_MAX_N, TN_MAX_MIX, TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI, LIB_PATH,
+                   TN_BCAST_NONE, TN_BCAST_SLABS, TN_BCAST_FULL, Transfer)
 
 __all__ = ["TN_CONTRACT_F64_DMMA", "TN_CONTRACT_INT8_OZAKI", "Plan", "Plan2", "Comm", "svd_truncate", "build_bs_unitary", "theta_exec", "theta_exec_sharded", "alloc_theta",
            "shard_rows_host", "release_cached_memory", "TnError", "lib", "LIB_PATH", "TN_GATHER_NONE", "TN_GATHER_ROOT",
-           "TN_GATHER_SECTOR_OWNER", "sector_owners_host",
+           "TN_GATHER_SECTOR_OWNER", "sector_owners_host", "TN_BCAST_NONE", "TN_BCAST_SLABS", "TN_BCAST_FULL",
+           "gather_schedule_host", "pack_row_slab", "theta_exec_slab",
            "theta_exec_to_owners", "ipc_handle"]
 
 
@@ -135,6 +137,16 @@ class Plan:
         check(lib.tn_plan_slab_rows(self.handle, int(c), int(rank), C.byref(b), C.byref(n)), "tn_plan_slab_rows")
         return b.value, n.value
 
+    def gather_schedule(self, gather_mode: int):
+        """tn_plan_gather_schedule: the transfer list tn_theta_exec_sharded executes, as a list of dicts
+        (sector, src, dst, row_begin, rows, cols)."""
+        n = C.c_int64()
+        check(lib.tn_plan_gather_schedule(self.handle, int(gather_mode), 0, None, C.byref(n)), "tn_plan_gather_schedule")
+        arr = (Transfer * max(1, n.value))()
+        check(lib.tn_plan_gather_schedule(self.handle, int(gather_mode), n.value, arr, C.byref(n)),
+              "tn_plan_gather_schedule")
+        return [{f: getattr(arr[i], f) for f, _ in Transfer._fields_} for i in range(n.value)]
+
     def exec_launches(self) -> int:
         """tn_plan_exec_launches: kernel launches of one tn_theta_exec with the current engine."""
         n = C.c_int64()
@@ -225,9 +237,12 @@ def _theta_ptrs(outs):
 
 def _check_inputs(plan, gk, lk, gk1, ll, lr, U):
     chi_l, chi_c, chi_r = plan.chi
-    for t, shp, dt in ((gk, (chi_l, chi_c), torch.complex128), (gk1, (chi_c, chi_r), torch.complex128),
+    for t, shp, dt in ((gk, (chi_l, chi_c) if gk is not None else None, torch.complex128),
+                       (gk1, (chi_c, chi_r), torch.complex128),
                        (lk, (chi_c,), torch.float64), (ll, (chi_l,), torch.float64),
                        (lr, (chi_r,), torch.float64)):
+        if shp is None:  # validated by the caller (a packed Γk slab)
+            continue
         if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dt or tuple(t.shape) != shp:
             raise ValueError(f"expected CUDA {dt} tensor of shape {shp}")
     if not isinstance(U, torch.Tensor) or not U.is_cuda or U.dtype != torch.complex128 or U.numel() < plan.u_size():
@@ -243,6 +258,38 @@ def theta_exec(plan: Plan, gk, lk, gk1, ll, lr, U, out=None, stream=None):
     check(lib.tn_theta_exec(plan.handle, _stream_ptr(stream), _ptr(gk), _ptr(lk), _ptr(gk1), _ptr(ll), _ptr(lr),
                             _ptr(U), ptrs), "tn_theta_exec")
     return out
+
+
+def pack_row_slab(plan: Plan, gk, rank: int, out=None, stream=None):
+    """tn_pack_row_slab: rank `rank`'s rows of Γk packed in sorted order, a CUDA tensor [(r1−r0), χ_c]."""
+    r0, r1 = plan.shard_rows(rank)
+    if out is None:
+        out = torch.empty((r1 - r0, plan.chi[1]), dtype=torch.complex128, device=gk.device)
+    if out.numel() < (r1 - r0) * plan.chi[1] or out.dtype != torch.complex128 or not out.is_cuda:
+        raise ValueError("slab buffer too small or not CUDA complex128")
+    _check_inputs_gk(plan, gk)
+    check(lib.tn_pack_row_slab(plan.handle, _stream_ptr(stream), _ptr(gk), int(rank), _ptr(out)), "tn_pack_row_slab")
+    return out
+
+
+def theta_exec_slab(plan: Plan, gk_slab, lk, gk1, ll, lr, U, out=None, stream=None):
+    """tn_theta_exec_slab: tn_theta_exec for the plan's rank with Γk given as its packed row slab."""
+    r0, r1 = plan.shard_rows(plan.rank)
+    if not (isinstance(gk_slab, torch.Tensor) and gk_slab.is_cuda and gk_slab.dtype == torch.complex128
+            and gk_slab.is_contiguous() and gk_slab.numel() >= (r1 - r0) * plan.chi[1]):
+        raise ValueError("gk_slab must be a contiguous CUDA complex128 tensor of ≥ (r1−r0)·χ_c entries")
+    _check_inputs(plan, None, lk, gk1, ll, lr, U)
+    if out is None:
+        out = alloc_theta(plan)
+    check(lib.tn_theta_exec_slab(plan.handle, _stream_ptr(stream), _ptr(gk_slab), _ptr(lk), _ptr(gk1), _ptr(ll),
+                                 _ptr(lr), _ptr(U), _theta_ptrs(out)), "tn_theta_exec_slab")
+    return out
+
+
+def _check_inputs_gk(plan, gk):
+    if not isinstance(gk, torch.Tensor) or not gk.is_cuda or gk.dtype != torch.complex128 or \
+            tuple(gk.shape) != (plan.chi[0], plan.chi[1]) or not gk.is_contiguous():
+        raise ValueError(f"expected contiguous CUDA complex128 Γk of shape {(plan.chi[0], plan.chi[1])}")
 
 
 def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None):
@@ -287,16 +334,31 @@ class Comm:
     def handle(self):
         return self._h
 
+    def async_error(self) -> None:
+        """tn_comm_async_error: raises TnError (TN_ERR_NCCL) if the communicator holds an asynchronous error."""
+        check(lib.tn_comm_async_error(self._h), "tn_comm_async_error")
+
     def destroy(self):
         if self._h is not None:
             lib.tn_comm_destroy(self._h)
             self._h = None
 
 
-def theta_exec_sharded(plan: Plan, comm: Comm, gk, lk, gk1, ll, lr, U, out=None, bcast_operands=False,
+def theta_exec_sharded(plan: Plan, comm: Comm, gk, lk, gk1, ll, lr, U, out=None, bcast_operands=TN_BCAST_NONE,
                        gather_mode=TN_GATHER_NONE, stream=None):
-    """tn_theta_exec_sharded: this rank's rows (+ optional NCCL operand broadcast / gather to rank 0)."""
-    _check_inputs(plan, gk, lk, gk1, ll, lr, U)
+    """tn_theta_exec_sharded: this rank's rows (+ optional operand distribution from rank 0 and the NCCL gather
+    to rank 0 / the sector owners). bcast_operands: TN_BCAST_NONE / TN_BCAST_SLABS (Γk row slabs; on ranks > 0
+    `gk` receives the packed slab and may be any CUDA complex128 tensor with ≥ (r1−r0)·χ_c elements) /
+    TN_BCAST_FULL; True means TN_BCAST_SLABS."""
+    bc = int(bcast_operands) if not isinstance(bcast_operands, bool) else (TN_BCAST_SLABS if bcast_operands else TN_BCAST_NONE)
+    if bc == TN_BCAST_SLABS and plan.rank > 0:
+        r0, r1 = plan.shard_rows(plan.rank)
+        if not (isinstance(gk, torch.Tensor) and gk.is_cuda and gk.dtype == torch.complex128 and gk.is_contiguous()
+                and gk.numel() >= (r1 - r0) * plan.chi[1]):
+            raise ValueError("TN_BCAST_SLABS: gk must be a contiguous CUDA complex128 tensor of ≥ (r1−r0)·χ_c entries")
+        _check_inputs(plan, None, lk, gk1, ll, lr, U)
+    else:
+        _check_inputs(plan, gk, lk, gk1, ll, lr, U)
     if out is None:
         out = alloc_theta(plan, full=(gather_mode == TN_GATHER_ROOT and plan.rank == 0))
         if gather_mode == TN_GATHER_SECTOR_OWNER:
@@ -305,7 +367,7 @@ def theta_exec_sharded(plan: Plan, comm: Comm, gk, lk, gk1, ll, lr, U, out=None,
                     out[c] = torch.empty(plan.sector_shape(c), dtype=torch.complex128, device=out[c].device)
     ptrs = _theta_ptrs(out)
     check(lib.tn_theta_exec_sharded(plan.handle, _stream_ptr(stream), comm.handle, _ptr(gk), _ptr(lk), _ptr(gk1),
-                                    _ptr(ll), _ptr(lr), _ptr(U), ptrs, int(bool(bcast_operands)), int(gather_mode)),
+                                    _ptr(ll), _ptr(lr), _ptr(U), ptrs, bc, int(gather_mode)),
           "tn_theta_exec_sharded")
     return out
 
@@ -337,6 +399,24 @@ def sector_owners_host(sizes, world_size: int) -> np.ndarray:
     check(lib.tn_sector_owners_host(int(sz.shape[0]), sz.ctypes.data_as(C.POINTER(C.c_int64)), int(world_size),
                                     out.ctypes.data_as(C.POINTER(C.c_int32))), "tn_sector_owners_host")
     return out
+
+
+def gather_schedule_host(d: int, N: int, off_l, off_r, bounds, gather_mode: int):
+    """tn_gather_schedule_host: the gather transfer list from host offsets and shard bounds (no plan, no GPU)."""
+    ol = np.ascontiguousarray(np.asarray(off_l, dtype=np.int32))
+    orr = np.ascontiguousarray(np.asarray(off_r, dtype=np.int32))
+    b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    if ol.shape != (N + 2,) or orr.shape != (N + 2,):
+        raise ValueError("offsets must have N+2 entries")
+    world = b.shape[0] - 1
+    i32p, i64p = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
+    args = (int(d), int(N), ol.ctypes.data_as(i32p), orr.ctypes.data_as(i32p), int(world), b.ctypes.data_as(i64p),
+            int(gather_mode))
+    n = C.c_int64()
+    check(lib.tn_gather_schedule_host(*args, 0, None, C.byref(n)), "tn_gather_schedule_host")
+    arr = (Transfer * max(1, n.value))()
+    check(lib.tn_gather_schedule_host(*args, n.value, arr, C.byref(n)), "tn_gather_schedule_host")
+    return [{f: getattr(arr[i], f) for f, _ in Transfer._fields_} for i in range(n.value)]
 
 
 def ipc_handle(t: torch.Tensor):

@@ -18,6 +18,14 @@ STATUS = {0: "TN_OK", 1: "TN_ERR_DOMAIN", 2: "TN_ERR_DIMENSION", 3: "TN_ERR_CONS
           5: "TN_ERR_OOM", 6: "TN_ERR_NCCL", 7: "TN_ERR_UNSUPPORTED"}
 TN_BOND_LEFT, TN_BOND_CENTER, TN_BOND_RIGHT = 0, 1, 2
 TN_GATHER_NONE, TN_GATHER_ROOT, TN_GATHER_SECTOR_OWNER = 0, 1, 2
+TN_BCAST_NONE, TN_BCAST_SLABS, TN_BCAST_FULL = 0, 1, 2
+
+
+class Transfer(C.Structure):
+    """tn_transfer: rank `src`'s slab of `sector` (rows × cols) lands at row `row_begin` of the full Θ on `dst`."""
+    _fields_ = [("sector", C.c_int64), ("src", C.c_int64), ("dst", C.c_int64), ("row_begin", C.c_int64),
+                ("rows", C.c_int64), ("cols", C.c_int64)]
+
 TN_CONTRACT_F64_DMMA, TN_CONTRACT_INT8_OZAKI = 0, 1
 TN_MAX_N, TN_MAX_MIX = 100, 64
 
@@ -41,6 +49,11 @@ SIGNATURES = {
     "tn_plan_u_size": [_p, _i64p],
     "tn_plan_exec_launches": [_p, _i64p],
     "tn_plan_slab_rows": [_p, C.c_int, C.c_int, _i64p, _i64p],
+    "tn_plan_gather_schedule": [_p, C.c_int, C.c_int64, _p, _i64p],
+    "tn_gather_schedule_host": [C.c_int, C.c_int, _i32p, _i32p, C.c_int, _i64p, C.c_int, C.c_int64, _p, _i64p],
+    "tn_comm_async_error": [_p],
+    "tn_pack_row_slab": [_p, _p, _p, C.c_int, _p],
+    "tn_theta_exec_slab": [_p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
     "tn_plan_workspace_bytes": [_p, _i64p],
     "tn_plan_kernel_times": [_p, _p],
     "tn_plan_set_contraction": [_p, C.c_int, C.c_int],

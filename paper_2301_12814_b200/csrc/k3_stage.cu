@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k3_stage_b(const GroupDesc* __restrict__ 
 }
 
 cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
-                         cudaStream_t s) {
+                         cudaStream_t s, const int32_t* rowperm) {
   const int ng = (int)p->groups.size();
   if (ng == 0) return cudaSuccess;
   int64_t amax = 0, bmax = 0;
@@ -95,7 +95,7 @@ cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, 
                                                               p->chi[2], p->d_bpanel);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaEventRecord(aux->join[0], aux->st[0])) != cudaSuccess) return e;
-  k3_stage_a<<<dim3(blocks(amax), ng), 256, 0, s>>>(p->d_groups, p->d_rowperm, p->d_perm[1], gk, p->chi[1],
+  k3_stage_a<<<dim3(blocks(amax), ng), 256, 0, s>>>(p->d_groups, rowperm, p->d_perm[1], gk, p->chi[1],
                                                      lk, p->d_apanel);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return cudaStreamWaitEvent(s, aux->join[0], 0);

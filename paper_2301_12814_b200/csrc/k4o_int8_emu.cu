@@ -538,7 +538,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
 
 // ---- launchers ----------------------------------------------------------------------------------
 template <int S>
-static cudaError_t stage_s(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1, cudaStream_t s) {
+static cudaError_t stage_s(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1, cudaStream_t s,
+                           const int32_t* rowperm) {
   const int ng = (int)p->oz_groups.size();
   int maxr = 0, maxc = 0, maxa = 0, maxb = 0;
   for (const auto& g : p->oz_groups) {
@@ -561,22 +562,23 @@ static cudaError_t stage_s(const tn_plan* p, const double2* gk, const double* lk
                                                 p->d_ob);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaEventRecord(aux->join[0], sb)) != cudaSuccess) return e;
-  if (maxr > 0) k3o_row_exp<<<dim3((maxr + 7) / 8, ng), 256, 0, s>>>(p->d_oz_groups, p->d_rowperm, p->d_perm[1], gk,
+  if (maxr > 0) k3o_row_exp<<<dim3((maxr + 7) / 8, ng), 256, 0, s>>>(p->d_oz_groups, rowperm, p->d_perm[1], gk,
                                                                      p->chi[1], lk, p->d_oea);
-  k3o_rows<S><<<dim3(maxa, ng), OZ_BM, 0, s>>>(p->d_oz_groups, p->d_rowperm, p->d_perm[1], gk, p->chi[1], lk, p->d_oea,
+  k3o_rows<S><<<dim3(maxa, ng), OZ_BM, 0, s>>>(p->d_oz_groups, rowperm, p->d_perm[1], gk, p->chi[1], lk, p->d_oea,
                                                p->d_oa);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return cudaStreamWaitEvent(s, aux->join[0], 0);
 }
 
-cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1, cudaStream_t s) {
+cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1, cudaStream_t s,
+                            const int32_t* rowperm) {
   if (p->oz_groups.empty()) return cudaSuccess;
   switch (p->oz_slices) {
-    case 4: return stage_s<4>(p, gk, lk, gk1, s);
-    case 5: return stage_s<5>(p, gk, lk, gk1, s);
-    case 6: return stage_s<6>(p, gk, lk, gk1, s);
-    case 7: return stage_s<7>(p, gk, lk, gk1, s);
-    case 8: return stage_s<8>(p, gk, lk, gk1, s);
+    case 4: return stage_s<4>(p, gk, lk, gk1, s, rowperm);
+    case 5: return stage_s<5>(p, gk, lk, gk1, s, rowperm);
+    case 6: return stage_s<6>(p, gk, lk, gk1, s, rowperm);
+    case 7: return stage_s<7>(p, gk, lk, gk1, s, rowperm);
+    case 8: return stage_s<8>(p, gk, lk, gk1, s, rowperm);
   }
   return cudaErrorInvalidValue;
 }

@@ -91,16 +91,34 @@ static void shard_bounds(const Counts& k, int world, std::vector<int64_t>& bound
   while (r < world) bounds[r++] = row;
 }
 
+// Sector owners for TN_GATHER_SECTOR_OWNER (SURVEY.md §8(e)): longest-processing-time assignment by
+// element count R_c·C_c (largest first onto the least-loaded rank, ties to the lower rank/sector).
+void sector_owners(const std::vector<int64_t>& sizes, int world, std::vector<int32_t>& owner) {
+  const int n = (int)sizes.size();
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sizes[a] > sizes[b]; });
+  std::vector<int64_t> load(world, 0);
+  owner.assign(n, 0);
+  for (int c : order) {
+    int best = 0;
+    for (int r = 1; r < world; ++r)
+      if (load[r] < load[best]) best = r;
+    owner[c] = best;
+    load[best] += sizes[c];
+  }
+}
+
 static void free_plan(tn_plan* p) {
   if (!p) return;
-  const bool used = p->rec_exec;
   // a captured exec may be replayed on any stream: wait for every replay before the blocks are reused
   if (p->captured) cudaDeviceSynchronize();
-  pool_release(p->blk_oz, p->last_stream, used);
-  pool_release(p->blk_lit, p->last_stream, used);
-  pool_release(p->blk_p, p->last_stream, used);
-  pool_release(p->blk_work, p->last_stream, used);
-  pool_release(p->blk_tab, p->last_stream, used);
+  // fence: the last exec stream (it waited for the plan stream's K1 and table uploads), or — for a plan that
+  // never executed — the plan stream itself (a host-charge plan never waited for its own K1 / uploads)
+  cudaStream_t fence = p->rec_exec ? p->last_stream : p->plan_stream;
+  const bool used = p->rec_exec || p->plan_stream != nullptr;
+  for (void* blk : {p->blk_oz, p->blk_lit, p->blk_p, p->blk_slab, p->blk_pack, p->blk_work, p->blk_tab})
+    pool_release(blk, fence, used);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
   if (p->ev_ready) cudaEventDestroy(p->ev_ready);
@@ -186,24 +204,6 @@ tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_
   return TN_OK;
 }
 
-// Sector owners for TN_GATHER_SECTOR_OWNER (SURVEY.md §8(e)): longest-processing-time assignment by
-// element count R_c·C_c (largest first onto the least-loaded rank, ties to the lower rank/sector).
-static void sector_owners(const std::vector<int64_t>& sizes, int world, std::vector<int32_t>& owner) {
-  const int n = (int)sizes.size();
-  std::vector<int> order(n);
-  for (int i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sizes[a] > sizes[b]; });
-  std::vector<int64_t> load(world, 0);
-  owner.assign(n, 0);
-  for (int c : order) {
-    int best = 0;
-    for (int r = 1; r < world; ++r)
-      if (load[r] < load[best]) best = r;
-    owner[c] = best;
-    load[best] += sizes[c];
-  }
-}
-
 tn_status tn_sector_owners_host(int n_sectors, const int64_t* sizes, int world_size, int32_t* owners) {
   if (n_sectors < 0 || world_size < 1) return fail(TN_ERR_DOMAIN, "tn_sector_owners_host: bad n/world");
   if ((n_sectors && (!sizes || !owners))) return fail(TN_ERR_DIMENSION, "tn_sector_owners_host: NULL");
@@ -274,6 +274,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
   Carver ct;
   size_t o_perm[3], o_qs[3], o_off[3], o_err, o_q[3] = {0, 0, 0}, o_q2[3] = {0, 0, 0};
   bool host_q[3], host_q2[3] = {false, false, false};
+  bool all_host = true;
   int32_t* d_err = nullptr;
   const int nmax_u = std::min(N, 2 * d - 2);
   size_t o_bin = 0;
@@ -295,9 +296,11 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     o_off[b] = ct.take<int32_t>(p->nq + 1);
     host_q[b] = !is_device_ptr(qs_in[b]);
     if (host_q[b]) o_q[b] = ct.take<int32_t>(p->chi[b]);
+    all_host = all_host && host_q[b];
     if (q2) {
       host_q2[b] = !is_device_ptr(q2[b]);
       if (host_q2[b]) o_q2[b] = ct.take<int32_t>(p->chi[b]);
+      all_host = all_host && host_q2[b];
     }
   }
   o_err = ct.take<int32_t>(4);
@@ -343,6 +346,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     }
     d_err = reinterpret_cast<int32_t*>(base + o_err);
     p->d_rowperm = p->d_perm[0];  // single-charge groups index sorted positions directly
+    p->n_rowlist = p->chi[0];
     p->d_colperm = p->d_perm[2];
     sa.err = d_err;
     p->d_binom = reinterpret_cast<double2*>(base + o_bin);
@@ -355,8 +359,27 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     TN_TRY(cudaEventRecord(p->ev[1], p->plan_stream), "event");
     p->rec_k1 = true;
   }
-  {
-    // one D2H of off[3] + err: the tables are contiguous with padding, copy each
+  if (all_host) {
+    // host charges: the offset tables are counted here (the same stable counting-sort definition K1 applies
+    // on the device for perm), so the plan never waits for the GPU — the tables below go up asynchronously
+    // and the next gate's planning overlaps this gate's kernels
+    for (int b = 0; b < 3; ++b) {
+      std::vector<int32_t>& o = p->off[b];
+      o.assign(p->nq + 1, 0);
+      const int32_t* a = qs_in[b];
+      const int32_t* a2 = q2 ? q2[b] : nullptr;
+      for (int64_t i = 0; i < p->chi[b]; ++i) {
+        const int32_t x = a[i];
+        if (x < 0 || x > N || (a2 && (a2[i] < 0 || a2[i] > N))) {
+          st = fail(TN_ERR_DOMAIN, "tn_theta_plan: a bond charge lies outside [0, N]");
+          goto done;
+        }
+        ++o[(a2 ? x * (N + 1) + a2[i] : x) + 1];
+      }
+      for (int k = 0; k < p->nq; ++k) o[k + 1] += o[k];
+    }
+  } else {
+    // device charges: one D2H of off[3] + err after K1 (the call's only host synchronisation)
     int32_t herr[4] = {0, 0, 0, 0};
     for (int b = 0; b < 3; ++b) p->off[b].resize(p->nq + 1);
     for (int b = 0; b < 3; ++b)
@@ -568,8 +591,11 @@ tn_status tn_plan_local_sector_shape(const tn_plan* p, int c, int64_t* R, int64_
 tn_status tn_plan_perm(const tn_plan* p, int bond, int32_t* host_out) {
   if (!p || !host_out) return fail(TN_ERR_DIMENSION, "tn_plan_perm: NULL");
   if (bond < 0 || bond > 2) return fail(TN_ERR_DIMENSION, "tn_plan_perm: bond id");
-  return cuda_check(cudaMemcpy(host_out, p->d_perm[bond], p->chi[bond] * sizeof(int32_t), cudaMemcpyDeviceToHost),
-                    "tn_plan_perm D2H");
+  // K1 ran on the plan's own stream (and a host-charge plan never waited for it): copy on that stream
+  tn_status st = cuda_check(cudaMemcpyAsync(host_out, p->d_perm[bond], p->chi[bond] * sizeof(int32_t),
+                                            cudaMemcpyDeviceToHost, p->plan_stream), "tn_plan_perm D2H");
+  if (st != TN_OK) return st;
+  return cuda_check(cudaStreamSynchronize(p->plan_stream), "tn_plan_perm sync");
 }
 
 tn_status tn_plan_offsets(const tn_plan* p, int bond, int32_t* host_out) {
@@ -794,9 +820,13 @@ static tn_status wait_tables(const tn_plan* p, cudaStream_t s) {
   return cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
 }
 
-tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
-                        const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
-                        double* const* theta_out) {
+}  // extern "C"
+
+namespace tn {
+// tn_theta_exec with an explicit A-row gather list (tn_theta_exec_sharded's slab scatter passes its own)
+tn_status exec_impl(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
+                    const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
+                    double* const* theta_out, const int32_t* rowperm) {
   if (!p) return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL plan");
   if (!gamma_k || !lambda_k || !gamma_k1 || !lambda_l || !lambda_r || !U || !theta_out)
     return fail(TN_ERR_DIMENSION, "tn_theta_exec: NULL input pointer");
@@ -823,9 +853,9 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
   }
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
   st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
-                                        reinterpret_cast<const double2*>(gamma_k1), s)
+                                        reinterpret_cast<const double2*>(gamma_k1), s, rowperm)
                       : launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
-                                     reinterpret_cast<const double2*>(gamma_k1), s),
+                                     reinterpret_cast<const double2*>(gamma_k1), s, rowperm),
                   "K3 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;
@@ -843,6 +873,16 @@ tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_
     if (st != TN_OK) return st;
   }
   return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+}
+}  // namespace tn
+
+extern "C" {
+
+tn_status tn_theta_exec(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
+                        const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
+                        double* const* theta_out) {
+  return exec_impl(p, stream, gamma_k, lambda_k, gamma_k1, lambda_l, lambda_r, U, theta_out,
+                   p ? p->d_rowperm : nullptr);
 }
 
 tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
@@ -887,9 +927,9 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
   if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
   st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
-                                        reinterpret_cast<const double2*>(gamma_k1), s)
+                                        reinterpret_cast<const double2*>(gamma_k1), s, p->d_rowperm)
                       : launch_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
-                                     reinterpret_cast<const double2*>(gamma_k1), s),
+                                     reinterpret_cast<const double2*>(gamma_k1), s, p->d_rowperm),
                   "K3 launch");
   if (st != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[5], s), "event")) != TN_OK) return st;

@@ -133,6 +133,13 @@ struct tn_plan {
   // plans (group rows are contiguous sorted positions), per-group gathered lists for pair plans
   const int32_t* d_rowperm = nullptr;
   const int32_t* d_colperm = nullptr;
+  const int32_t* d_rowpos = nullptr;           // pair plans: sorted left position of every d_rowperm entry (single: identity)
+  int64_t n_rowlist = 0;                       // entries of d_rowperm (single-charge: χ_l)
+  // tn_theta_exec_sharded's Γk slab scatter (TN_BCAST_SLABS): d_rowperm re-expressed as rows of this rank's
+  // packed slab (sorted position − r0), and on rank 0 the staging copy of Γk in sorted row order
+  void* blk_slab = nullptr;
+  int32_t* d_slab_rowlist = nullptr;
+  void* blk_pack = nullptr;
   // pair plans: two-pass U⊗U* mix (tn_pair.cu)
   tn::MixTile2* d_mix2 = nullptr;
   int32_t* d_rowoff = nullptr;                 // [sector][left key]: local row of the segment in the sector (−1: absent)
@@ -196,6 +203,14 @@ void set_error(const std::string& s);
 tn_status fail(tn_status st, const std::string& s);
 tn_status cuda_check(cudaError_t e, const char* what);
 
+// TN_GATHER_SECTOR_OWNER owners: LPT over element counts (tn_api.cu); rows of Θ(c) before a sorted left
+// position (tn_comm.cu)
+void sector_owners(const std::vector<int64_t>& sizes, int world, std::vector<int32_t>& owner);
+int64_t sector_rows_before(const tn_plan* p, int c, int64_t pos);
+tn_status exec_impl(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
+                    const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
+                    double* const* theta_out, const int32_t* rowperm);
+
 // ---- kernel launchers (stream-ordered) ----
 struct SortArgs {           // K1: one CTA per bond (0 = left, 1 = center, 2 = right)
   const int32_t* q[3];
@@ -211,11 +226,13 @@ void* pool_alloc(size_t bytes, cudaError_t* err);
 void pool_release(void* ptr, cudaStream_t last_stream, bool used);
 cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const double2* binom, double2* U,
                               cudaStream_t s);
+// rowperm: the A-row gather list (p->d_rowperm; tn_theta_exec_sharded passes a slab list when Γk arrived as
+// this rank's packed row slab)
 cudaError_t launch_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
-                         cudaStream_t s);
+                         cudaStream_t s, const int32_t* rowperm);
 cudaError_t launch_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
 cudaError_t launch_oz_stage(const tn_plan* p, const double2* gk, const double* lk, const double2* gk1,
-                            cudaStream_t s);
+                            cudaStream_t s, const int32_t* rowperm);
 cudaError_t launch_oz_contract(const tn_plan* p, const SectorParams& sp, cudaStream_t s);
 // Per-thread auxiliary streams for launches that touch disjoint data (K3 a/b, K3O's two exponent→slice
 // chains, K5's register classes): fork from s, run, join back into s. One set per (device, caller stream),

@@ -288,6 +288,8 @@ tn_status build_pair_tables(tn_plan* p) {
   p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
   p->d_rowperm = d_rg;
   p->d_colperm = d_cg;
+  p->d_rowpos = d_rpos;
+  p->n_rowlist = (int64_t)rpos.size();
   p->ws_bytes += (int64_t)cw.off;
   auto up = [&](void* dst, const void* src, size_t bytes, const char* what) -> tn_status {
     if (!bytes) return TN_OK;

@@ -41,12 +41,30 @@ def test_int8_emulation_parity(tn, cfg, variant):
     assert worst < 1e-11
 
 
-@pytest.mark.parametrize("slices", [6, 8])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", ["plain", "flat"])
+def test_int8_emulation_parity_s6(tn, cfg, variant):
+    # the slice count bench.py's alt_engine line uses (S = 6, R20): the same ≤ 1e-10 bar
+    kw = dict(flat=variant == "flat")
+    case = _case(cfg, **kw)
+    ref, *_ = _oracle(cfg, **kw)
+    plan, _, got = gpu_theta(case, contraction=("int8", 6))
+    assert plan.contraction() == ("int8", 6)
+    assert_sectors_close(got, ref, TOL, f"int8 S=6 config{cfg}-{variant}")
+
+
+@pytest.mark.parametrize("slices", [5, 8])
 def test_int8_emulation_slices(tn, slices):
+    # S = 8 meets the bar with margin; S = 5 is the documented failure (≈ 1e-9, R20) — it must be
+    # worse than 1e-10 somewhere yet still close (a wrong slice layout would be O(1))
     case = _case(2)
     ref, *_ = _oracle(2)
     _, _, got = gpu_theta(case, contraction=("int8", slices))
-    assert_sectors_close(got, ref, TOL if slices >= 7 else 1e-9, f"int8 S={slices}")
+    if slices >= 6:
+        assert_sectors_close(got, ref, TOL, f"int8 S={slices}")
+    else:
+        worst = max(rel_err(g, r) for g, r in zip(got, ref))
+        assert 1e-12 < worst < 1e-6, worst
 
 
 def test_int8_vs_dmma_agree(tn):

@@ -77,6 +77,31 @@ def test_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
             assert np.allclose(B @ B.conj().T, np.eye(B.shape[0]), atol=1e-12)
 
 
+def test_svd_truncate_parity_config3(tn):
+    # the configuration whose SVD-step time is quoted (bench.py --svd): config 3, χ_max = 4096,
+    # default algorithm; oracle SVD (numpy LAPACK) of the ORACLE's Θ, so nothing on the reference side comes
+    # from the GPU
+    case = synth.make_config(3)
+    got, res = _run(tn, case, 4096)
+    ref_secs, *_ = oracle_theta(case)
+    ref = osvd.truncate_update(case.N, case.d, case.q_l, case.q_r, ref_secs, case.lam_l, case.lam_r, 4096)
+    assert res["chi"] == ref["chi"] == 4096
+    assert np.array_equal(res["q_new"], ref["q_new"])
+    smax = max(float(s.max()) for s in ref["svals"] if s.size)
+    assert np.max(np.abs(res["lam_new"] - ref["lam_new"])) <= 1e-12 * smax
+    tot = sum(np.linalg.norm(x) ** 2 for x in ref_secs)
+    assert abs(res["discarded"] - ref["discarded"]) <= 1e-12 * tot
+    for c in range(case.N + 1):
+        if ref_secs[c].size == 0:
+            continue
+        rg, A, B = _recon(case, res, c)
+        rr, *_ = _recon(case, ref, c)
+        assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), c
+        if A.shape[1]:
+            assert np.abs(A.conj().T @ A - np.eye(A.shape[1])).max() <= 1e-12
+            assert np.abs(B @ B.conj().T - np.eye(B.shape[0])).max() <= 1e-12
+
+
 @pytest.mark.parametrize("algo", ALGOS + ["gram-tested"])
 @pytest.mark.parametrize("chi", [40, 250, 100000])
 def test_svd_wide_spectrum(tn, chi, algo, monkeypatch):
