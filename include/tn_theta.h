@@ -245,6 +245,20 @@ TN_API tn_status tn_svd_truncate(const tn_plan* plan, tn_stream stream, double* 
                                  double cutoff, int32_t* q_new, double* lambda_new, double* gamma_k_new,
                                  double* gamma_k1_new, int64_t* chi_out, double* discarded);
 
+/* tn_svd_truncate_bform — the same step for an MPS kept in right-canonical ("B") form, B^{[k]} = Γ^{[k]}λ^{[k+1]}
+ * (Hastings, J. Math. Phys. 50, 095207 (2009); R22). The caller builds Θ(c) = λ^{[k−1]} B^{[k]} B^{[k+1]}
+ * (gated) with tn_theta_exec(gamma_k = B^{[k]}, lambda_k = 1, gamma_k1 = B^{[k+1]}, lambda_l = λ^{[k−1]},
+ * lambda_r = 1); ranking, q_new and lambda_new are as tn_svd_truncate's, and the new factors need no division by a
+ * singular value or a small λ:
+ *   b_k_new  [χ_l × χ_new] (ld *chi_out): B^{[k]}_new[α, a]  = (Θ(c)·V_c)[α, s] / λ^{[k−1]}[α]  (undoes Θ's own row
+ *            scaling, exact to rounding per element; x/0 := 0)
+ *   b_k1_new [χ_new × χ_r]:              B^{[k+1]}_new[a, β] = V_c†[s, β]
+ * Arguments, synchronisation and errors as tn_svd_truncate (lambda_r is not needed). */
+TN_API tn_status tn_svd_truncate_bform(const tn_plan* plan, tn_stream stream, double* const* theta,
+                                       const double* lambda_l, int64_t chi_max, double cutoff, int32_t* q_new,
+                                       double* lambda_new, double* b_k_new, double* b_k1_new, int64_t* chi_out,
+                                       double* discarded);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Multi-GPU (one process per GPU): row-sharded exec + NCCL.                 */
 /* ------------------------------------------------------------------------------------------ */

@@ -18,14 +18,36 @@ from .svd import truncate_update
 from .theta import theta_sectors
 
 
+def _form(state):
+    return state.get("form", "vidal")
+
+
+def _inner(state, k):
+    """The λ's Θ of Eq. S5 puts between / right of the two sites: Vidal form uses the stored λ^{[k+1]}, λ^{[k+2]};
+    the right-canonical form (gam holds B^{[k]} = Γ^{[k]}λ^{[k+1]}, oracle/svd.py) has them inside its B's."""
+    lam = state["lam"]
+    if _form(state) == "b":
+        return np.ones(len(lam[k + 1])), np.ones(len(lam[k + 2]))
+    return lam[k + 1], lam[k + 2]
+
+
+def to_bform(state):
+    """Vidal → right-canonical form: B^{[k]} = Γ^{[k]} λ^{[k+1]} (a product, no division)."""
+    out = {key: ([x.copy() for x in v] if isinstance(v, list) else v) for key, v in state.items()}
+    out["gam"] = [g * state["lam"][k + 1][None, :] for k, g in enumerate(state["gam"])]
+    out["form"] = "b"
+    return out
+
+
 def apply_gate(state, k, theta, phi, chi_max, cutoff=1e-14):
     """In-place TEBD update of sites (k, k+1). `state` = dict(N, d, q: [M+1 int arrays], gam: [M complex],
-    lam: [M+1 real]). Returns the discarded weight."""
+    lam: [M+1 real], optional form: "vidal" (default) | "b" (gam holds B^{[k]}, the update of oracle/svd.py's
+    right-canonical form)). Returns the discarded weight."""
     N, d = state["N"], state["d"]
     q, gam, lam = state["q"], state["gam"], state["lam"]
-    secs, *_ = theta_sectors(N, d, q[k], q[k + 1], q[k + 2], gam[k], lam[k + 1], gam[k + 1], lam[k], lam[k + 2],
-                             theta, phi)
-    res = truncate_update(N, d, q[k], q[k + 2], secs, lam[k], lam[k + 2], chi_max, cutoff)
+    lk, lr = _inner(state, k)
+    secs, *_ = theta_sectors(N, d, q[k], q[k + 1], q[k + 2], gam[k], lk, gam[k + 1], lam[k], lr, theta, phi)
+    res = truncate_update(N, d, q[k], q[k + 2], secs, lam[k], lr, chi_max, cutoff, _form(state))
     q[k + 1] = res["q_new"]
     lam[k + 1] = res["lam_new"]
     gam[k] = res["gamma_k_new"]
@@ -51,7 +73,7 @@ def dense_state(state):
     # vec[α_k, i_0..i_{k−1}]
     vec = np.asarray(lam[0], dtype=np.complex128).copy()
     for k in range(M):
-        G = gam[k] * lam[k + 1][None, :]
+        G = gam[k] if _form(state) == "b" else gam[k] * lam[k + 1][None, :]
         new = np.zeros((len(q[k + 1]),) + (d,) * (k + 1), dtype=np.complex128)
         for a in range(len(q[k])):
             for b in range(len(q[k + 1])):
@@ -97,7 +119,7 @@ def random_mps(M, N, d, chi, seed):
 
 def copy_state(s):
     return dict(N=s["N"], d=s["d"], q=[x.copy() for x in s["q"]], gam=[x.copy() for x in s["gam"]],
-                lam=[x.copy() for x in s["lam"]])
+                lam=[x.copy() for x in s["lam"]], form=_form(s))
 
 
 # ---------------------------------------------------------------------------------------------------------
@@ -113,9 +135,11 @@ def apply_gate2(state, k, theta, phi, chi_max, cutoff=1e-14):
     from .theta2 import theta2_sectors
     N, d = state["N"], state["d"]
     q1, q2, gam, lam = state["q1"], state["q2"], state["gam"], state["lam"]
-    secs, *_ = theta2_sectors(N, d, q1[k], q2[k], q1[k + 1], q2[k + 1], q1[k + 2], q2[k + 2], gam[k], lam[k + 1],
-                              gam[k + 1], lam[k], lam[k + 2], theta, phi)
-    res = truncate_update2(N, d, q1[k], q2[k], q1[k + 2], q2[k + 2], secs, lam[k], lam[k + 2], chi_max, cutoff)
+    lk, lr = _inner(state, k)
+    secs, *_ = theta2_sectors(N, d, q1[k], q2[k], q1[k + 1], q2[k + 1], q1[k + 2], q2[k + 2], gam[k], lk,
+                              gam[k + 1], lam[k], lr, theta, phi)
+    res = truncate_update2(N, d, q1[k], q2[k], q1[k + 2], q2[k + 2], secs, lam[k], lr, chi_max, cutoff,
+                           _form(state))
     q1[k + 1], q2[k + 1] = res["q1_new"].astype(np.int32), res["q2_new"].astype(np.int32)
     lam[k + 1] = res["lam_new"]
     gam[k] = res["gamma_k_new"]
@@ -134,7 +158,8 @@ def vectorize_mps(state):
     pq = lambda q: (np.repeat(q, len(q)).astype(np.int32), np.tile(q, len(q)).astype(np.int32))
     q1, q2 = zip(*(pq(q) for q in state["q"]))
     return dict(N=state["N"], d=state["d"], q1=list(q1), q2=list(q2),
-                gam=[np.kron(g, np.conj(g)) for g in state["gam"]], lam=[np.kron(l, l) for l in state["lam"]])
+                gam=[np.kron(g, np.conj(g)) for g in state["gam"]], lam=[np.kron(l, l) for l in state["lam"]],
+                form=_form(state))
 
 
 def dense_state2(state):
@@ -145,7 +170,7 @@ def dense_state2(state):
     M = len(gam)
     vec = np.asarray(lam[0], dtype=np.complex128).copy()
     for k in range(M):
-        G = gam[k] * lam[k + 1][None, :]
+        G = gam[k] if _form(state) == "b" else gam[k] * lam[k + 1][None, :]
         new = np.zeros((len(q1[k + 1]),) + (d * d,) * (k + 1), dtype=np.complex128)
         for a in range(len(q1[k])):
             for b in range(len(q1[k + 1])):
@@ -187,4 +212,4 @@ def random_mpo(M, N, d, chi, seed):
 
 def copy_state2(s):
     return dict(N=s["N"], d=s["d"], q1=[x.copy() for x in s["q1"]], q2=[x.copy() for x in s["q2"]],
-                gam=[x.copy() for x in s["gam"]], lam=[x.copy() for x in s["lam"]])
+                gam=[x.copy() for x in s["gam"]], lam=[x.copy() for x in s["lam"]], form=_form(s))

@@ -13,6 +13,14 @@ ascending, then by value descending (a prefix of each sector's spectrum);
   Γ^{[k]}_new[α, a]   = U_c[α, s] / λ^{[k−1]}[α]     (α in Θ(c)'s rows; 0 elsewhere)
   Γ^{[k+1]}_new[a, β] = V_c†[s, β] / λ^{[k+1]}[β]    (β in Θ(c)'s columns; 0 elsewhere)
 with a ↔ (c, s), and x/0 := 0. Rows/columns are returned in the CALLER's bond order.
+
+Right-canonical ("B") form (Hastings, J. Math. Phys. 50, 095207 (2009); R22): an MPS stored as
+B^{[k]} = Γ^{[k]} λ^{[k+1]} and λ's gives Θ(c) = λ^{[k−1]} B^{[k]} B^{[k+1]} (gated; tn_theta_exec with λk = λr = 1),
+and the update needs no division by a singular value or a small λ:
+  B^{[k]}_new[α, a]   = (Θ(c) V_c)[α, s] / λ^{[k−1]}[α]   (= Θ̃(c)·V_c, Θ̃ = Θ without its left λ; x/0 := 0)
+  B^{[k+1]}_new[a, β] = V_c†[s, β]
+(the division by λ^{[k−1]} undoes the row scaling Θ carries — each element to rounding — instead of dividing the
+singular vectors U_c, whose absolute rounding errors the Vidal form amplifies by 1/λ).
 """
 from __future__ import annotations
 
@@ -50,11 +58,12 @@ def global_top_chi(svals, chi_max: int, cutoff: float = 1e-14):
     return kept, disc
 
 
-def truncate_update_rows(sectors, rows, cols, chi_l, chi_r, lam_l, lam_r, chi_max, cutoff=1e-14):
+def truncate_update_rows(sectors, rows, cols, chi_l, chi_r, lam_l, lam_r, chi_max, cutoff=1e-14, form="vidal"):
     """The whole step on host for sectors given with their row / column bond lists: `rows[c]`, `cols[c]`
     are the CALLER indices of Θ(c)'s rows / columns (sector c = its position in `sectors`, which is the
     charge order of the ranking). Returns dict(chi, q_new (sector index per new bond), lam_new,
-    gamma_k_new [χ_l × chi], gamma_k1_new [chi × χ_r], kept, discarded, svals)."""
+    gamma_k_new [χ_l × chi], gamma_k1_new [chi × χ_r], kept, discarded, svals). form="b": the right-canonical
+    update of the module docstring (gamma_k_new = B^{[k]}_new, gamma_k1_new = B^{[k+1]}_new; lam_r unused)."""
     svd = sector_svds(sectors)
     kept, disc = global_top_chi([s for _, s, _ in svd], chi_max, cutoff)
     chi = sum(kept)
@@ -72,8 +81,12 @@ def truncate_update_rows(sectors, rows, cols, chi_l, chi_r, lam_l, lam_r, chi_ma
         lr = np.asarray(lam_r)[cols[c]]
         inv_l = np.divide(1.0, ll, out=np.zeros_like(ll), where=ll != 0)
         inv_r = np.divide(1.0, lr, out=np.zeros_like(lr), where=lr != 0)
-        gk[rows[c], a:a + k] = U[:, :k] * inv_l[:, None]
-        gk1[a:a + k][:, cols[c]] = Vh[:k, :] * inv_r[None, :]
+        if form == "b":
+            gk[rows[c], a:a + k] = (sectors[c] @ Vh[:k, :].conj().T) * inv_l[:, None]
+            gk1[a:a + k][:, cols[c]] = Vh[:k, :]
+        else:
+            gk[rows[c], a:a + k] = U[:, :k] * inv_l[:, None]
+            gk1[a:a + k][:, cols[c]] = Vh[:k, :] * inv_r[None, :]
         q_new[a:a + k] = c
         lam_new[a:a + k] = s[:k]
         a += k
@@ -81,7 +94,7 @@ def truncate_update_rows(sectors, rows, cols, chi_l, chi_r, lam_l, lam_r, chi_ma
                 discarded=disc, svals=[s for _, s, _ in svd])
 
 
-def truncate_update(N, d, q_l, q_r, sectors, lam_l, lam_r, chi_max, cutoff=1e-14):
+def truncate_update(N, d, q_l, q_r, sectors, lam_l, lam_r, chi_max, cutoff=1e-14, form="vidal"):
     """Single-charge plans: Θ(c) rows are the sorted left bonds with c_l − c ∈ [0, d−1], columns the sorted
     right bonds with c − c_r ∈ [0, d−1] (oracle.theta.sector_ranges)."""
     perm_l, off_l = sort_bonds(q_l, N)
@@ -91,10 +104,10 @@ def truncate_update(N, d, q_l, q_r, sectors, lam_l, lam_r, chi_max, cutoff=1e-14
         (r0, r1), (k0, k1) = sector_ranges(off_l, off_r, N, d, c)
         rows.append(perm_l[r0:r1])
         cols.append(perm_r[k0:k1])
-    return truncate_update_rows(sectors, rows, cols, len(q_l), len(q_r), lam_l, lam_r, chi_max, cutoff)
+    return truncate_update_rows(sectors, rows, cols, len(q_l), len(q_r), lam_l, lam_r, chi_max, cutoff, form)
 
 
-def truncate_update2(N, d, q1_l, q2_l, q1_r, q2_r, sectors2, lam_l, lam_r, chi_max, cutoff=1e-14):
+def truncate_update2(N, d, q1_l, q2_l, q1_r, q2_r, sectors2, lam_l, lam_r, chi_max, cutoff=1e-14, form="vidal"):
     """MPO (pair-charge) plans: sector (c1, c2) has index c1·(N+1) + c2 — the ranking's
     charge order is the lexicographic pair order — and its rows / columns are the admissible
     sorted bonds of oracle.theta2 (l − c ∈ [0, d−1]², c − r ∈ [0, d−1]²). `sectors2[(c1, c2)]` as returned by
@@ -107,6 +120,6 @@ def truncate_update2(N, d, q1_l, q2_l, q1_r, q2_r, sectors2, lam_l, lam_r, chi_m
             secs.append(sectors2[(c1, c2)])
             rows.append(pl[pair_sector_rows(np.asarray(q1_l)[pl], np.asarray(q2_l)[pl], d, c1, c2)])
             cols.append(pr[pair_sector_cols(np.asarray(q1_r)[pr], np.asarray(q2_r)[pr], d, c1, c2)])
-    res = truncate_update_rows(secs, rows, cols, len(q1_l), len(q1_r), lam_l, lam_r, chi_max, cutoff)
+    res = truncate_update_rows(secs, rows, cols, len(q1_l), len(q1_r), lam_l, lam_r, chi_max, cutoff, form)
     res["q1_new"], res["q2_new"] = np.divmod(res["q_new"], N + 1)
     return res

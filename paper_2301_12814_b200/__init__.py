@@ -292,10 +292,11 @@ def _check_inputs_gk(plan, gk):
         raise ValueError(f"expected contiguous CUDA complex128 Γk of shape {(plan.chi[0], plan.chi[1])}")
 
 
-def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None):
+def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14, stream=None, form: str = "vidal"):
     """tn_svd_truncate: per-sector SVD + global top-χ + new canonical factors (single-charge or MPO pair
     plans). `theta` (the list from theta_exec) is only read. Returns dict(chi, q_new, lam_new, gamma_k_new [χ_l × chi], gamma_k1_new
-    [chi × χ_r], discarded) as contiguous CUDA tensors (views of chi_max-capacity buffers)."""
+    [chi × χ_r], discarded) as contiguous CUDA tensors (views of chi_max-capacity buffers).
+    form="b": tn_svd_truncate_bform — right-canonical factors B^{[k]}_new, B^{[k+1]}_new (`lr` unused)."""
     chi_l, _, chi_r = plan.chi
     dev = ll.device
     q_new = torch.zeros(chi_max, dtype=torch.int32, device=dev)
@@ -303,9 +304,14 @@ def svd_truncate(plan: Plan, theta, ll, lr, chi_max: int, cutoff: float = 1e-14,
     gk = torch.empty((chi_l, chi_max), dtype=torch.complex128, device=dev)
     gk1 = torch.empty((chi_max, chi_r), dtype=torch.complex128, device=dev)
     chi_out, disc = C.c_int64(), C.c_double()
-    check(lib.tn_svd_truncate(plan.handle, _stream_ptr(stream), _theta_ptrs(theta), _ptr(ll), _ptr(lr), int(chi_max),
-                              float(cutoff), _ptr(q_new), _ptr(lam_new), _ptr(gk), _ptr(gk1), C.byref(chi_out),
-                              C.byref(disc)), "tn_svd_truncate")
+    if form == "b":
+        check(lib.tn_svd_truncate_bform(plan.handle, _stream_ptr(stream), _theta_ptrs(theta), _ptr(ll), int(chi_max),
+                                        float(cutoff), _ptr(q_new), _ptr(lam_new), _ptr(gk), _ptr(gk1),
+                                        C.byref(chi_out), C.byref(disc)), "tn_svd_truncate_bform")
+    else:
+        check(lib.tn_svd_truncate(plan.handle, _stream_ptr(stream), _theta_ptrs(theta), _ptr(ll), _ptr(lr),
+                                  int(chi_max), float(cutoff), _ptr(q_new), _ptr(lam_new), _ptr(gk), _ptr(gk1),
+                                  C.byref(chi_out), C.byref(disc)), "tn_svd_truncate")
     k = chi_out.value
     res = dict(chi=k, q_new=q_new[:k], lam_new=lam_new[:k], gamma_k_new=gk.view(-1)[:chi_l * k].view(chi_l, k),
                gamma_k1_new=gk1[:k], discarded=disc.value)

@@ -63,6 +63,8 @@ SIGNATURES = {
     "tn_theta_exec": [_p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
     "tn_svd_truncate": [_p, _p, C.POINTER(_p), _p, _p, C.c_int64, C.c_double, _p, _p, _p, _p, _i64p,
                         C.POINTER(C.c_double)],
+    "tn_svd_truncate_bform": [_p, _p, C.POINTER(_p), _p, C.c_int64, C.c_double, _p, _p, _p, _p, _i64p,
+                              C.POINTER(C.c_double)],
     "tn_theta_exec_remote": [_p, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
     "tn_ipc_get_handle": [_p, _p, _i64p],
     "tn_ipc_open": [_p, C.POINTER(_p)],

@@ -22,11 +22,14 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs arg
   int32_t* __restrict__ qs = args.qs[bond];
   int32_t* __restrict__ off = args.off[bond];
   int32_t* __restrict__ err = args.err + bond;
-  __shared__ int32_t hist[MAXC + 1];
-  __shared__ int32_t base[MAXC + 1];
-  __shared__ int32_t wcnt[SORT_WARPS][MAXC];
+  const int nq = q2 ? (N + 1) * (N + 1) : N + 1;   // number of (pair) charge keys ≤ MAX_SEC
+  // dynamic shared memory sized by the key count: hist[nq+1], base[nq+1], wcnt[SORT_WARPS][nq]
+  extern __shared__ int32_t k1_smem[];
+  int32_t* hist = k1_smem;
+  int32_t* base = hist + nq + 1;
+  int32_t* wcnt_flat = base + nq + 1;
+  auto wcnt = [&](int w, int v) -> int32_t& { return wcnt_flat[w * nq + v]; };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nq = q2 ? (N + 1) * (N + 1) : N + 1;   // number of (pair) charge keys ≤ MAXC
   for (int i = tid; i <= nq; i += SORT_THREADS) hist[i] = 0;
   __syncthreads();
   int bad = 0;
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs arg
   __syncthreads();
   // Chunked stable scatter: a chunk of SORT_THREADS consecutive bonds at a time, in order.
   for (int64_t c0 = 0; c0 < chi; c0 += SORT_THREADS) {
-    for (int i = tid; i < SORT_WARPS * nq; i += SORT_THREADS) (&wcnt[0][0])[(i / nq) * MAXC + i % nq] = 0;
+    for (int i = tid; i < SORT_WARPS * nq; i += SORT_THREADS) wcnt_flat[i] = 0;
     __syncthreads();
     const int64_t i = c0 + tid;
     const bool valid = i < chi;
@@ -70,18 +73,18 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs arg
     unsigned peers = __match_any_sync(0xffffffffu, v);
     peers &= active;
     const int rank_in_warp = __popc(peers & ((1u << lane) - 1u));
-    if (valid && rank_in_warp == 0) wcnt[warp][v] = __popc(peers);
+    if (valid && rank_in_warp == 0) wcnt(warp, v) = __popc(peers);
     __syncthreads();
     if (valid) {
       int pos = base[v] + rank_in_warp;
-      for (int w = 0; w < warp; ++w) pos += wcnt[w][v];
+      for (int w = 0; w < warp; ++w) pos += wcnt(w, v);
       perm[pos] = (int32_t)i;
       qs[pos] = v;
     }
     __syncthreads();
     for (int v2 = tid; v2 < nq; v2 += SORT_THREADS) {
       int s = 0;
-      for (int w = 0; w < SORT_WARPS; ++w) s += wcnt[w][v2];
+      for (int w = 0; w < SORT_WARPS; ++w) s += wcnt(w, v2);
       base[v2] += s;
     }
     __syncthreads();
@@ -89,7 +92,9 @@ __global__ void __launch_bounds__(SORT_THREADS) k1_sort_bonds(const SortArgs arg
 }
 
 cudaError_t launch_sort_bonds(const SortArgs& a, int N, cudaStream_t s) {
-  k1_sort_bonds<<<3, SORT_THREADS, 0, s>>>(a, N);
+  const int nq = a.q2[0] ? (N + 1) * (N + 1) : N + 1;
+  const size_t smem = (size_t)(2 * (nq + 1) + SORT_WARPS * nq) * sizeof(int32_t);   // ≤ 41 KB at MAX_SEC keys
+  k1_sort_bonds<<<3, SORT_THREADS, smem, s>>>(a, N);
   return cudaGetLastError();
 }
 

@@ -21,6 +21,48 @@
 
 namespace tn {
 
+// One ring stage of a warp's 32×16 outputs: MV of its four 8-row m-subtiles and NV of its two 8-column
+// n-subtiles hold valid rows / columns (the rest is tile padding: its DMMAs are skipped — at a shard's or a
+// group's ragged edge up to 56 of 64 rows are padding, and the DMMA pipe is what bounds K4).
+// One 8×8×4 complex step: the Gauss sums first, then all T1/T2 products (which do not need them), then the T3
+// products — every DMMA is issued well after the DADD that feeds it.
+template <int MV, int NV, int KSTEPS>
+__device__ __forceinline__ void k4_stage(double (&acc)[4][2][6], const double2* __restrict__ As,
+                                         const double2* __restrict__ Bs, int nks) {
+  auto kstep = [&](int ks) {
+    double2 a[MV], b[NV];
+#pragma unroll
+    for (int mi = 0; mi < MV; ++mi) a[mi] = As[ks * 256 + mi * 32];
+#pragma unroll
+    for (int ni = 0; ni < NV; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
+    double asum[MV], bsum[NV];
+#pragma unroll
+    for (int ni = 0; ni < NV; ++ni) bsum[ni] = b[ni].x + b[ni].y;
+#pragma unroll
+    for (int mi = 0; mi < MV; ++mi) asum[mi] = a[mi].x + a[mi].y;
+#pragma unroll
+    for (int mi = 0; mi < MV; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NV; ++ni) {
+        double* c = acc[mi][ni];
+        dmma(c[0], c[1], a[mi].x, b[ni].x);  // T1 += Ar·Br
+        dmma(c[2], c[3], a[mi].y, b[ni].y);  // T2 += Ai·Bi
+      }
+#pragma unroll
+    for (int mi = 0; mi < MV; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NV; ++ni) dmma(acc[mi][ni][4], acc[mi][ni][5], asum[mi], bsum[ni]);  // T3
+  };
+  if (nks == KSTEPS) {  // full stage: no guards, so the fragment loads of step ks+1 can overlap step ks
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) kstep(ks);
+  } else {
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks)
+      if (ks < nks) kstep(ks);
+  }
+}
+
 template <int STAGES, int CPS>  // CPS: BK-chunks per ring stage (one bulk copy per operand per stage)
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k4_contract(const GroupDesc* __restrict__ groups, const TileDesc* __restrict__ tiles, int ntiles,
@@ -103,44 +145,27 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < 6; ++q) acc[mi][ni][q] = 0.0;
 
+    // valid 8-row / 8-column subtiles of this warp's 32×16 outputs (full tiles: 4 and 2)
+    const int rows_w = g.R - (td.mt * BM + wm * 32), cols_w = g.C - (td.nt * BN + wn * 16);
+    const int mv = rows_w <= 0 ? 0 : min(4, (rows_w + 7) >> 3);
+    const int nv = cols_w <= 0 ? 0 : min(2, (cols_w + 7) >> 3);
+    const int shape = (mv == 0 || nv == 0) ? 0 : mv * 2 + nv - 2;   // 1..8; 8 = full
     for (int kc = 0; kc * SBK < g.K4; ++kc) {
       mbar_wait(&full[stage], phase);
       const int nks = min(SBK, g.K4 - kc * SBK) >> 2;
       const double2* As = sA + stage * SCH + wm * 128 + lane;
       const double2* Bs = sB + stage * SCH + wn * 64 + lane;
-      // one 8×8×4 complex step: the Gauss sums first, then all T1/T2 products (which do not need them), then
-      // the T3 products — every DMMA is issued well after the DADD that feeds it
-      auto kstep = [&](int ks) {
-        double2 a[4], b[2];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks * 256 + mi * 32];
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[ks * 256 + ni * 32];
-        double asum[4], bsum[2];
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) bsum[ni] = b[ni].x + b[ni].y;
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) asum[mi] = a[mi].x + a[mi].y;
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 2; ++ni) {
-            double* c = acc[mi][ni];
-            dmma(c[0], c[1], a[mi].x, b[ni].x);  // T1 += Ar·Br
-            dmma(c[2], c[3], a[mi].y, b[ni].y);  // T2 += Ai·Bi
-          }
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][4], acc[mi][ni][5], asum[mi], bsum[ni]);  // T3
-      };
-      if (nks == 4 * CPS) {  // full stage: no guards, so the fragment loads of step ks+1 can overlap step ks
-#pragma unroll
-        for (int ks = 0; ks < 4 * CPS; ++ks) kstep(ks);
-      } else {
-#pragma unroll
-        for (int ks = 0; ks < 4 * CPS; ++ks)
-          if (ks < nks) kstep(ks);
+      constexpr int KS = 4 * CPS;
+      switch (shape) {
+        case 8: k4_stage<4, 2, KS>(acc, As, Bs, nks); break;
+        case 7: k4_stage<4, 1, KS>(acc, As, Bs, nks); break;
+        case 6: k4_stage<3, 2, KS>(acc, As, Bs, nks); break;
+        case 5: k4_stage<3, 1, KS>(acc, As, Bs, nks); break;
+        case 4: k4_stage<2, 2, KS>(acc, As, Bs, nks); break;
+        case 3: k4_stage<2, 1, KS>(acc, As, Bs, nks); break;
+        case 2: k4_stage<1, 2, KS>(acc, As, Bs, nks); break;
+        case 1: k4_stage<1, 1, KS>(acc, As, Bs, nks); break;
+        default: break;  // no valid output in this warp's quarter of the tile
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -151,8 +176,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     }
 
     // epilogue: P tile → Θ(c_c) slab (row-major, ld = C_{c_c}); lane owns rows gq, cols 2tq, 2tq+1
-    double2* out = sp.out[g.cc];
-    const int ld = sp.ld[g.cc];
+    double2* out = sp.sec[g.cc].out;
+    const int ld = sp.sec[g.cc].ld;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
       const int row = td.mt * BM + wm * 32 + mi * 8 + gq;

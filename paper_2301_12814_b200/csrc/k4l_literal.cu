@@ -223,8 +223,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
         ++sg;
       }
     }
-    double2* out = sp.out[c];
-    const int ld = sp.ld[c];
+    double2* out = sp.sec[c].out;
+    const int ld = sp.sec[c].ld;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
       const int row = td.mt * BM + wm * 32 + mi * 8 + gq;

@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)  // 10 warps: ≤ 3 per SM sub-
         ebase = (ebase + S) & (OZ_SLOTS - 1);
         const double srow = oz_pow2(er - (S <= 6 ? 7 * (S + 1) : 0));
         // the Re pass stores the real halves, the Im pass the imaginary halves of the same 16-byte elements
-        double* orow = reinterpret_cast<double*>(sp.out[g.cc] + (int64_t)row * sp.ld[g.cc]) + pass;
+        double* orow = reinterpret_cast<double*>(sp.sec[g.cc].out + (int64_t)row * sp.sec[g.cc].ld) + pass;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int col = col0 + j;

@@ -149,13 +149,14 @@ __device__ __forceinline__ void mix_stage(const MixTile& mt, const SectorParams&
   ust = us_stride(UP);
   for (int u = tid; u < L; u += nthr) {
     const int cc = lo + u;
-    const int64_t off = ((int64_t)mt.pl0 - sp.lrow0[cc]) * sp.ld[cc] + ((int64_t)mt.pr0 - sp.col0[cc]);
-    const double2* base = sp.out[cc] + off;
-    const bool ne = (sp.cc_mask[cc >> 5] >> (cc & 31)) & 1u;
+    const SecEntry e = sp.sec[cc];
+    const int64_t off = ((int64_t)mt.pl0 - e.lrow0) * e.ld + ((int64_t)mt.pr0 - e.col0);
+    const double2* base = e.out + off;
+    const bool ne = e.nonempty;
     // P is read in place from Θ(c_c), or from a local workspace when Θ goes elsewhere (tn_theta_exec_remote)
-    const double2* lbase = sp.src[cc] ? sp.src[cc] + off : base;
-    ld_sec[u] = SecRef{ne ? lbase : nullptr, (int64_t)sp.ld[cc]};
-    st_sec[u] = SecRef{base, (int64_t)sp.ld[cc]};
+    const double2* lbase = e.src ? e.src + off : base;
+    ld_sec[u] = SecRef{ne ? lbase : nullptr, (int64_t)e.ld};
+    st_sec[u] = SecRef{base, (int64_t)e.ld};
   }
   // Us[t][u] = U_n[i = c_l − (lo+t)][j = c_l − (lo+u)], zero-padded to TP × UP
   const double2* Ub = U + sp.ustart[n];

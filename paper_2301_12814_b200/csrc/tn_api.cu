@@ -40,53 +40,78 @@ struct Counts {
   std::vector<int64_t> nl, nc, nr;
 };
 
-// Useful flops of one left row of charge c_l, 8 per complex MAC: contraction part (*fc) and
-// U-mix part (*fm); returns their sum.
-static double row_cost(const Counts& k, int c_l, double* fc = nullptr, double* fm = nullptr) {
+// Per-row work of a left row of charge q (prefix sums, O((N+1)·d) for all q):
+//   fc[q] = 8 Σ_{c_c ∈ [q−d+1, q], n_c > 0} n_c(c_c) · cols(c_c)        (its K4 contraction flops, 8 per CMAC)
+//   fm[q] = 8 Σ_{c_r} n_r(c_r) · #c · #non-empty c_c                     (its U-mix flops)
+//   el[q] = Σ_{c ∈ [q−d+1, q]} C_c                                        (its Θ elements: K5 moves 32 B each)
+struct RowCosts {
+  std::vector<double> fc, fm, el;
+};
+static void row_costs(const Counts& k, RowCosts& rc) {
   const int d = k.d, N = k.N;
-  double f = 0.0;
-  for (int cc = std::max(0, c_l - d + 1); cc <= c_l; ++cc) {      // j_k = c_l − c_c ∈ [0, d−1]
-    if (k.nc[cc] == 0) continue;
-    int64_t cols = 0;                                             // columns of group c_c
-    for (int cr = std::max(0, cc - d + 1); cr <= cc; ++cr) cols += k.nr[cr];
-    f += 8.0 * (double)k.nc[cc] * (double)cols;
+  std::vector<int64_t> pr(N + 2, 0), pc(N + 2, 0), pz(N + 2, 0);
+  for (int q = 0; q <= N; ++q) {
+    pr[q + 1] = pr[q] + k.nr[q];
+    pc[q + 1] = pc[q] + k.nc[q];
+    pz[q + 1] = pz[q] + (k.nc[q] > 0);
   }
-  if (fc) *fc = f;
-  const double f_con = f;
-  for (int cr = std::max(0, c_l - 2 * d + 2); cr <= std::min(N, c_l); ++cr) {
-    int nvc = 0, nvcc = 0;
-    for (int c = cr; c <= c_l; ++c)
-      if (c_l - c <= d - 1 && c - cr <= d - 1) {
-        ++nvc;
-        if (k.nc[c] > 0) ++nvcc;
-      }
-    f += 8.0 * (double)k.nr[cr] * nvc * nvcc;
+  auto cols = [&](int c) { return (double)(pr[c + 1] - pr[std::max(0, c - d + 1)]); };  // C_c
+  rc.fc.assign(N + 1, 0.0);
+  rc.fm.assign(N + 1, 0.0);
+  rc.el.assign(N + 1, 0.0);
+  for (int q = 0; q <= N; ++q) {
+    for (int cc = std::max(0, q - d + 1); cc <= q; ++cc) {
+      rc.el[q] += cols(cc);
+      if (k.nc[cc]) rc.fc[q] += 8.0 * (double)k.nc[cc] * cols(cc);
+    }
+    for (int cr = std::max(0, q - 2 * d + 2); cr <= q; ++cr) {
+      const int lo = std::max(cr, q - d + 1), hi = std::min(q, cr + d - 1);
+      if (hi < lo || !k.nr[cr]) continue;
+      rc.fm[q] += 8.0 * (double)k.nr[cr] * (double)(hi - lo + 1) * (double)(pz[hi + 1] - pz[lo]);
+    }
   }
-  if (fm) *fm = f - f_con;
-  return f;
 }
 
-static void shard_bounds(const Counts& k, int world, std::vector<int64_t>& bounds) {
+// Shard bounds balance the estimated DEVICE TIME per row rather than raw flops: K4 turns
+// contraction flops into time at ~41 TFLOP/s (useful, 3M form), K5 moves 32 B per Θ element at ~3.7 TB/s, so a
+// Θ element weighs KAPPA ≈ 32·41/3.7 ≈ 355 flop-equivalents; the mix flops themselves ride on the memory-bound K5.
+constexpr double KAPPA_EL = 355.0;
+static void shard_bounds(const Counts& k, const RowCosts& rc, int world, std::vector<int64_t>& bounds) {
   std::vector<double> cost(k.N + 1);
   double total = 0.0;
   int64_t chi_l = 0;
   for (int q = 0; q <= k.N; ++q) {
-    cost[q] = row_cost(k, q);
+    cost[q] = rc.fc[q] + KAPPA_EL * rc.el[q];
     total += cost[q] * (double)k.nl[q];
     chi_l += k.nl[q];
   }
   bounds.assign(world + 1, 0);
   bounds[world] = chi_l;
-  // bounds[r] = first sorted row whose prefix cost reaches r/world of the total (row granularity)
+  // bounds[r] = first sorted row whose prefix cost (over the rows before it) reaches r/world of the total; the rows
+  // of one charge q all cost cost[q], so each boundary inside a segment is found in O(1)
   double prefix = 0.0;
   int64_t row = 0;
   int r = 1;
   for (int q = 0; q <= k.N && r < world; ++q) {
-    for (int64_t i = 0; i < k.nl[q] && r < world; ++i) {
-      while (r < world && prefix >= total * (double)r / world) bounds[r++] = row;
-      prefix += cost[q];
-      ++row;
+    const int64_t n = k.nl[q];
+    if (!n) continue;
+    while (r < world) {
+      const double target = total * (double)r / world;
+      int64_t i;
+      if (prefix >= target) {
+        i = 0;
+      } else if (cost[q] > 0.0) {
+        i = (int64_t)std::ceil((target - prefix) / cost[q]);
+        while (i > 0 && prefix + (double)(i - 1) * cost[q] >= target) --i;   // guard the rounding of ceil
+        while (i < n && prefix + (double)i * cost[q] < target) ++i;
+      } else {
+        i = n;
+      }
+      if (i >= n) break;               // reached in a later segment
+      bounds[r++] = row + i;
     }
+    prefix += cost[q] * (double)n;
+    row += n;
   }
   while (r < world) bounds[r++] = row;
 }
@@ -113,16 +138,19 @@ static void free_plan(tn_plan* p) {
   if (!p) return;
   // a captured exec may be replayed on any stream: wait for every replay before the blocks are reused
   if (p->captured) cudaDeviceSynchronize();
-  // fence: the last exec stream (it waited for the plan stream's K1 and table uploads), or — for a plan that
-  // never executed — the plan stream itself (a host-charge plan never waited for its own K1 / uploads)
-  cudaStream_t fence = p->rec_exec ? p->last_stream : p->plan_stream;
-  const bool used = p->rec_exec || p->plan_stream != nullptr;
+  // the blocks become reusable once the last library work that touched them is done (ev_fence, recorded after
+  // the plan's own uploads and after every later exec / U build / SVD); the pool takes the event over
+  Fence* f = fence_adopt(p->ev_fence);
+  p->ev_fence = nullptr;
   for (void* blk : {p->blk_oz, p->blk_lit, p->blk_p, p->blk_slab, p->blk_pack, p->blk_work, p->blk_tab})
-    pool_release(blk, fence, used);
-  for (auto& e : p->ev)
-    if (e) cudaEventDestroy(e);
-  if (p->ev_ready) cudaEventDestroy(p->ev_ready);
-  if (p->plan_stream) cudaStreamDestroy(p->plan_stream);
+    pool_release_fenced(blk, f);
+  fence_release(f);
+  PlanShell sh;
+  sh.dev = p->dev;
+  sh.stream = p->plan_stream;
+  for (int i = 0; i < 8; ++i) sh.ev[i] = p->ev[i];
+  sh.ev_ready = p->ev_ready;
+  shell_release(sh);   // stream + timing events go back to the shell pool
   delete p;
 }
 
@@ -137,6 +165,18 @@ struct Carver {
   }
 };
 
+static int sm_count_of(int dev) {
+  static int cached[64] = {};
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    n = 148;
+  }
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
+}
+
 static bool is_device_ptr(const void* ptr) {
   cudaPointerAttributes a;
   cudaError_t e = cudaPointerGetAttributes(&a, ptr);
@@ -147,23 +187,49 @@ static bool is_device_ptr(const void* ptr) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-static SectorParams make_sector_params(const tn_plan* p, double* const* theta_out) {
-  SectorParams sp;
-  std::memset(&sp, 0, sizeof(sp));
-  sp.d = p->d;
-  sp.N = p->N;
-  for (int c = 0; c < p->nsec; ++c) {
-    sp.out[c] = reinterpret_cast<double2*>(theta_out[c]);
-    sp.lrow0[c] = p->lrow0[c];
-    sp.col0[c] = p->col0[c];
-    sp.ld[c] = (int32_t)p->C[c];
+__global__ void k_set_sectors(const SectorPtrs ptrs, SecEntry* __restrict__ tab) {
+  for (int c = threadIdx.x; c < ptrs.n; c += blockDim.x) {
+    tab[c].out = ptrs.out[c];
+    tab[c].src = ptrs.src[c];
   }
-  for (size_t n = 0; n < p->ustart.size(); ++n) sp.ustart[n] = p->ustart[n];
-  // The mix reads P_{c_c} iff seg_c(c_c) is non-empty: exactly then K4 ran group c_c for every
-  // local row that can need it (a row of Θ(c_c) in this shard).
-  for (int cc = 0; cc < p->nq; ++cc)  // pair plans: one bit per centre KEY
-    if (p->off[1][cc + 1] > p->off[1][cc]) sp.cc_mask[cc >> 5] |= 1u << (cc & 31);
-  return sp;
+}
+
+tn_status make_sector_params(const tn_plan* p, double* const* out, const double* const* src, int which, cudaStream_t s,
+                             SectorParams* sp) {
+  SectorPtrs ptrs;
+  ptrs.n = p->nsec;
+  for (int c = 0; c < p->nsec; ++c) {
+    ptrs.out[c] = reinterpret_cast<double2*>(out[c]);
+    ptrs.src[c] = src ? reinterpret_cast<const double2*>(src[c]) : nullptr;
+  }
+  k_set_sectors<<<1, 256, 0, s>>>(ptrs, p->d_sec[which]);
+  tn_status st = cuda_check(cudaGetLastError(), "sector table");
+  sp->sec = p->d_sec[which];
+  sp->ustart = p->d_ustart;
+  sp->d = p->d;
+  sp->N = p->N;
+  return st;
+}
+
+// static part of the sector tables + the packed-U offsets, uploaded once per plan (both tables)
+static tn_status upload_sector_tables(tn_plan* p) {
+  p->h_sec.assign(p->nsec, SecEntry{});
+  for (int c = 0; c < p->nsec; ++c) {
+    SecEntry& e = p->h_sec[c];
+    e.lrow0 = p->lrow0[c];
+    e.col0 = p->col0[c];
+    e.ld = (int32_t)p->C[c];
+    // the mix reads P_{c_c} iff seg_c(c_c) is non-empty: exactly then K4 ran group c_c for every local row that
+    // can need it (a row of Θ(c_c) in this shard); pair plans: one entry per centre KEY
+    e.nonempty = p->off[1][c + 1] > p->off[1][c];
+  }
+  for (int w = 0; w < 2; ++w) {
+    tn_status st = cuda_check(cudaMemcpyAsync(p->d_sec[w], p->h_sec.data(), p->nsec * sizeof(SecEntry),
+                                              cudaMemcpyHostToDevice, p->plan_stream), "H2D sector table");
+    if (st != TN_OK) return st;
+  }
+  return cuda_check(cudaMemcpyAsync(p->d_ustart, p->ustart.data(), p->ustart.size() * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, p->plan_stream), "H2D U offsets");
 }
 
 }  // namespace tn
@@ -199,7 +265,9 @@ tn_status tn_shard_rows_host(int d, int N, const int64_t* n_l, const int64_t* n_
   for (int q = 0; q <= N; ++q)
     if (k.nl[q] < 0 || k.nc[q] < 0 || k.nr[q] < 0) return fail(TN_ERR_DOMAIN, "tn_shard_rows_host: negative count");
   std::vector<int64_t> b;
-  shard_bounds(k, world_size, b);
+  RowCosts rc;
+  row_costs(k, rc);
+  shard_bounds(k, rc, world_size, b);
   std::copy(b.begin(), b.end(), bounds);
   return TN_OK;
 }
@@ -249,8 +317,8 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
   if (std::min(N + 1, d) > TN_MAX_MIX) return fail(TN_ERR_UNSUPPORTED, "tn_theta_plan: min(N+1, d) > TN_MAX_MIX");
   if (q2) {
     if (!q2[0] || !q2[1] || !q2[2]) return fail(TN_ERR_DIMENSION, "tn_theta2_plan: NULL charge array");
-    if ((N + 1) * (N + 1) > MAXC)
-      return fail(TN_ERR_UNSUPPORTED, "tn_theta2_plan: (N+1)^2 charge pairs exceed this build's sector limit (N <= 9)");
+    if ((N + 1) * (N + 1) > MAX_SEC)
+      return fail(TN_ERR_UNSUPPORTED, "tn_theta2_plan: (N+1)^2 charge pairs exceed this build's sector limit (N <= 31)");
   }
 
   tn_plan* p = new (std::nothrow) tn_plan();
@@ -277,7 +345,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
   bool all_host = true;
   int32_t* d_err = nullptr;
   const int nmax_u = std::min(N, 2 * d - 2);
-  size_t o_bin = 0;
+  size_t o_bin = 0, o_sec[2] = {0, 0}, o_ust = 0;
   std::vector<double2> hbin((size_t)(nmax_u + 1) * (nmax_u + 1), double2{0.0, 0.0});
 #define TN_TRY(expr, what)                      \
   do {                                          \
@@ -285,10 +353,16 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     if (st != TN_OK) goto done;                 \
   } while (0)
   TN_TRY(cudaGetDevice(&dev), "cudaGetDevice");
-  TN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  TN_TRY(cudaStreamCreateWithFlags(&p->plan_stream, cudaStreamNonBlocking), "plan stream");
-  for (auto& e : p->ev) TN_TRY(cudaEventCreate(&e), "event create");
-  TN_TRY(cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming), "event create");
+  p->dev = dev;
+  p->sm_count = sm_count_of(dev);
+  {
+    PlanShell sh;
+    TN_TRY(shell_acquire(&sh), "plan stream");
+    p->plan_stream = sh.stream;
+    for (int i = 0; i < 8; ++i) p->ev[i] = sh.ev[i];
+    p->ev_ready = sh.ev_ready;
+  }
+  TN_TRY(cudaEventCreateWithFlags(&p->ev_fence, cudaEventDisableTiming), "event create");
   // ---- one pool block for the bond tables (+ staging of host charges) ----
   for (int b = 0; b < 3; ++b) {
     o_perm[b] = ct.take<int32_t>(p->chi[b]);
@@ -305,6 +379,9 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
   }
   o_err = ct.take<int32_t>(4);
   o_bin = ct.take<double2>((int64_t)(nmax_u + 1) * (nmax_u + 1));
+  o_sec[0] = ct.take<SecEntry>(p->nq);
+  o_sec[1] = ct.take<SecEntry>(p->nq);
+  o_ust = ct.take<int32_t>(nmax_u + 1);
   for (int n = 0; n <= nmax_u; ++n) {  // exact C(n,k) as a double-double pair (n ≤ TN_MAX_N)
     unsigned __int128 c = 1;
     for (int k = 0; k <= n; ++k) {
@@ -350,6 +427,9 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->d_colperm = p->d_perm[2];
     sa.err = d_err;
     p->d_binom = reinterpret_cast<double2*>(base + o_bin);
+    p->d_sec[0] = reinterpret_cast<SecEntry*>(base + o_sec[0]);
+    p->d_sec[1] = reinterpret_cast<SecEntry*>(base + o_sec[1]);
+    p->d_ustart = reinterpret_cast<int32_t*>(base + o_ust);
     TN_TRY(cudaMemcpyAsync(p->d_binom, hbin.data(), hbin.size() * sizeof(double2), cudaMemcpyHostToDevice,
                            p->plan_stream), "H2D binomials");
     // ---- K1: sort each bond by charge (one launch, one CTA per bond) ----
@@ -368,13 +448,25 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       o.assign(p->nq + 1, 0);
       const int32_t* a = qs_in[b];
       const int32_t* a2 = q2 ? q2[b] : nullptr;
-      for (int64_t i = 0; i < p->chi[b]; ++i) {
-        const int32_t x = a[i];
-        if (x < 0 || x > N || (a2 && (a2[i] < 0 || a2[i] > N))) {
-          st = fail(TN_ERR_DOMAIN, "tn_theta_plan: a bond charge lies outside [0, N]");
-          goto done;
+      bool bad = false;
+      int32_t* hist = o.data() + 1;
+      if (!a2) {
+        for (int64_t i = 0; i < p->chi[b]; ++i) {
+          const uint32_t x = (uint32_t)a[i];
+          bad |= x > (uint32_t)N;
+          hist[x > (uint32_t)N ? 0 : x]++;
         }
-        ++o[(a2 ? x * (N + 1) + a2[i] : x) + 1];
+      } else {
+        for (int64_t i = 0; i < p->chi[b]; ++i) {
+          const uint32_t x = (uint32_t)a[i], y = (uint32_t)a2[i];
+          const bool oob = x > (uint32_t)N || y > (uint32_t)N;
+          bad |= oob;
+          hist[oob ? 0 : x * (N + 1) + y]++;
+        }
+      }
+      if (bad) {
+        st = fail(TN_ERR_DOMAIN, "tn_theta_plan: a bond charge lies outside [0, N]");
+        goto done;
       }
       for (int k = 0; k < p->nq; ++k) o[k + 1] += o[k];
     }
@@ -402,8 +494,10 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       sector_owners(sizes, world_size, p->owner);
     }
     p->ws_bytes += (int64_t)ct.off;
-    TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     u_layout(p);
+    if ((st = upload_sector_tables(p)) != TN_OK) goto done;
+    TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
+    TN_TRY(plan_touch(p, p->plan_stream), "plan fence");
   } else {
     // ---- sectors (R2) ----
     const auto& ol = p->off[0];
@@ -415,7 +509,9 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       k.nc[q] = oc[q + 1] - oc[q];
       k.nr[q] = orr[q + 1] - orr[q];
     }
-    shard_bounds(k, world_size, p->bounds);
+    RowCosts rc;
+    row_costs(k, rc);
+    shard_bounds(k, rc, world_size, p->bounds);
     p->r0 = p->bounds[rank];
     p->r1 = p->bounds[rank + 1];
     {  // this rank's share of the useful work (rows [r0, r1))
@@ -423,10 +519,8 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       for (int q = 0; q <= N; ++q) {
         const int64_t a = std::max<int64_t>(ol[q], p->r0), b = std::min<int64_t>(ol[q + 1], p->r1);
         if (b <= a) continue;
-        double fc = 0.0, fm = 0.0;
-        row_cost(k, q, &fc, &fm);
-        lc += fc * (double)(b - a);
-        lm += fm * (double)(b - a);
+        lc += rc.fc[q] * (double)(b - a);
+        lm += rc.fm[q] * (double)(b - a);
       }
       p->f_contract_local = (int64_t)llround(lc);
       p->f_mix_local = (int64_t)llround(lm);
@@ -458,21 +552,25 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       sector_owners(sizes, world_size, p->owner);
     }
     // ---- useful flops of the whole problem ----
-    for (int cl = 0; cl <= N; ++cl)
-      for (int cr = 0; cr <= N; ++cr) {
-        const int n = cl - cr;
-        if (n < 0 || n > 2 * d - 2) continue;
-        int64_t nvc = 0, nvcc = 0;
-        for (int c = cr; c <= cl; ++c)
-          if (cl - c <= d - 1 && c - cr <= d - 1) {
-            ++nvc;
-            if (k.nc[c] > 0) {
-              ++nvcc;
-              p->f_contract += 8 * k.nl[cl] * k.nc[c] * k.nr[cr];
-            }
-          }
-        p->f_mix += 8 * k.nl[cl] * k.nr[cr] * nvc * nvcc;
+    // for a (c_l, c_r) block the valid c (= c_c) form the range [max(c_r, c_l−d+1), min(c_l, c_r+d−1)]: prefix
+    // sums over n_c and over [n_c > 0] give Σ n_c and #non-empty c_c in O(1) per block
+    {
+      std::vector<int64_t> pc(N + 2, 0), pz(N + 2, 0);
+      for (int q = 0; q <= N; ++q) {
+        pc[q + 1] = pc[q] + k.nc[q];
+        pz[q + 1] = pz[q] + (k.nc[q] > 0);
       }
+      for (int cl = 0; cl <= N; ++cl) {
+        if (!k.nl[cl]) continue;
+        for (int cr = std::max(0, cl - 2 * d + 2); cr <= cl; ++cr) {
+          const int lo = std::max(cr, cl - d + 1), hi = std::min(cl, cr + d - 1);
+          if (hi < lo || !k.nr[cr]) continue;
+          const int64_t nvc = hi - lo + 1, nvcc = pz[hi + 1] - pz[lo];
+          p->f_contract += 8 * k.nl[cl] * k.nr[cr] * (pc[hi + 1] - pc[lo]);
+          p->f_mix += 8 * k.nl[cl] * k.nr[cr] * nvc * nvcc;
+        }
+      }
+    }
     // ---- groups: one per center charge with a non-empty segment and local rows ----
     int64_t a_off = 0, b_off = 0;
     for (int cc = 0; cc <= N; ++cc) {
@@ -540,8 +638,10 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       p->ws_bytes = (int64_t)cw.off;
     }
     p->ws_bytes += (int64_t)ct.off;
-    TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     u_layout(p);
+    if ((st = upload_sector_tables(p)) != TN_OK) goto done;
+    TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
+    TN_TRY(plan_touch(p, p->plan_stream), "plan fence");
   }
 done:
 #undef TN_TRY
@@ -732,6 +832,7 @@ tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
                                   p->plan_stream), "H2D oz tiles");
   if (st != TN_OK) return st;
   st = cuda_check(cudaEventRecord(p->ev_ready, p->plan_stream), "oz tables ready");
+  if (st == TN_OK) st = cuda_check(plan_touch(p, p->plan_stream), "plan fence");
   if (st != TN_OK) return st;
   p->ws_bytes += (int64_t)cw.off;
   p->oz_slices = slices;
@@ -785,27 +886,13 @@ tn_status tn_plan_kernel_times(const tn_plan* p, float* ms) {
   return TN_OK;
 }
 
-tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_stream stream, double* U_out) {
-  if (!p || !U_out) return fail(TN_ERR_DIMENSION, "tn_build_bs_unitary: NULL");
-  if (!std::isfinite(theta) || !std::isfinite(phi)) return fail(TN_ERR_DOMAIN, "tn_build_bs_unitary: non-finite angle");
-  cudaError_t e = cudaPeekAtLastError();
-  if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_build_bs_unitary");
-  cudaStream_t s = (cudaStream_t)stream;
-  tn_status st = cuda_check(cudaEventRecord(p->ev[2], s), "event");
-  if (st != TN_OK) return st;
-  st = cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->d_binom, reinterpret_cast<double2*>(U_out), s),
-                  "K2 launch");
-  if (st != TN_OK) return st;
-  st = cuda_check(cudaEventRecord(p->ev[3], s), "event");
-  p->rec_k2 = st == TN_OK;
-  return st;
-}
-
 // The exec stream waits for the plan's asynchronous table upload. Under CUDA graph capture that event lies
 // outside the capture (waiting on it would invalidate the capture), and a replay may run on any stream, so
 // the host waits for the upload instead and marks the plan captured: its blocks then go back to the pool
 // only after a device-wide synchronisation (free_plan), because a replay's stream is unknown to the plan.
-static tn_status wait_tables(const tn_plan* p, cudaStream_t s) {
+}  // extern "C"
+namespace tn {
+tn_status wait_tables(const tn_plan* p, cudaStream_t s) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) cs = cudaStreamCaptureStatusNone;
   if (cs != cudaStreamCaptureStatusNone) {
@@ -818,6 +905,28 @@ static tn_status wait_tables(const tn_plan* p, cudaStream_t s) {
     return cuda_check(e, "plan tables (captured exec)");
   }
   return cuda_check(cudaStreamWaitEvent(s, p->ev_ready, 0), "wait for plan tables");
+}
+}  // namespace tn
+extern "C" {
+
+tn_status tn_build_bs_unitary(const tn_plan* p, double theta, double phi, tn_stream stream, double* U_out) {
+  if (!p || !U_out) return fail(TN_ERR_DIMENSION, "tn_build_bs_unitary: NULL");
+  if (!std::isfinite(theta) || !std::isfinite(phi)) return fail(TN_ERR_DOMAIN, "tn_build_bs_unitary: non-finite angle");
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_build_bs_unitary");
+  cudaStream_t s = (cudaStream_t)stream;
+  // K2 reads the plan's binomial table, uploaded asynchronously on the plan stream
+  tn_status st = wait_tables(p, s);
+  if (st != TN_OK) return st;
+  st = cuda_check(cudaEventRecord(p->ev[2], s), "event");
+  if (st != TN_OK) return st;
+  st = cuda_check(launch_bs_unitary(p->d, p->N, theta, phi, p->d_binom, reinterpret_cast<double2*>(U_out), s),
+                  "K2 launch");
+  if (st != TN_OK) return st;
+  st = cuda_check(cudaEventRecord(p->ev[3], s), "event");
+  p->rec_k2 = st == TN_OK;
+  if (st == TN_OK) st = cuda_check(plan_touch(p, s), "plan fence");
+  return st;
 }
 
 }  // extern "C"
@@ -836,11 +945,12 @@ tn_status exec_impl(const tn_plan* p, tn_stream stream, const double* gamma_k, c
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return cuda_check(e, "sticky CUDA error before tn_theta_exec");
   cudaStream_t s = (cudaStream_t)stream;
-  const SectorParams sp = make_sector_params(p, theta_out);
   p->last_stream = s;
   p->rec_exec = true;  // the workspace is in use from here on (pool release fence)
   tn_status st = wait_tables(p, s);
   if (st != TN_OK) return st;
+  SectorParams sp;
+  if ((st = make_sector_params(p, theta_out, nullptr, 0, s, &sp)) != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
   if (p->contraction == TN_CONTRACT_PAPER_LITERAL) {  // ablation: K3L → K4L, no K5
     st = cuda_check(launch_literal(p, sp, reinterpret_cast<const double2*>(gamma_k), lambda_k,
@@ -849,7 +959,8 @@ tn_status exec_impl(const tn_plan* p, tn_stream stream, const double* gamma_k, c
                     "literal launch");
     if (st != TN_OK) return st;
     if ((st = cuda_check(cudaEventRecord(p->ev[6], s), "event")) != TN_OK) return st;
-    return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+    if ((st = cuda_check(cudaEventRecord(p->ev[7], s), "event")) != TN_OK) return st;
+    return cuda_check(plan_touch(p, s), "plan fence");
   }
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
   st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
@@ -872,7 +983,8 @@ tn_status exec_impl(const tn_plan* p, tn_stream stream, const double* gamma_k, c
     st = cuda_check(launch_mix(p, sp, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
     if (st != TN_OK) return st;
   }
-  return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+  if ((st = cuda_check(cudaEventRecord(p->ev[7], s), "event")) != TN_OK) return st;
+  return cuda_check(plan_touch(p, s), "plan fence");
 }
 }  // namespace tn
 
@@ -917,13 +1029,14 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
       if (p->lR[c] * p->C[c] > 0) pw[c] = reinterpret_cast<double*>(static_cast<double2*>(p->blk_p) + off[c]);
   }
   cudaStream_t s = (cudaStream_t)stream;
-  const SectorParams sp4 = make_sector_params(p, pw.data());   // K4 writes P into the local workspace
-  SectorParams sp5 = make_sector_params(p, theta_dst);         // K5 reads it there, writes Θ to theta_dst
-  for (int c = 0; c < p->nsec; ++c) sp5.src[c] = reinterpret_cast<const double2*>(pw[c]);
   p->last_stream = s;
   p->rec_exec = true;
   tn_status st = wait_tables(p, s);
   if (st != TN_OK) return st;
+  SectorParams sp4, sp5;
+  // K4 writes P into the local workspace (table 0); K5 reads it there and writes Θ to theta_dst (table 1)
+  if ((st = make_sector_params(p, pw.data(), nullptr, 0, s, &sp4)) != TN_OK) return st;
+  if ((st = make_sector_params(p, theta_dst, pw.data(), 1, s, &sp5)) != TN_OK) return st;
   if ((st = cuda_check(cudaEventRecord(p->ev[4], s), "event")) != TN_OK) return st;
   const bool emu = p->contraction == TN_CONTRACT_INT8_OZAKI;
   st = cuda_check(emu ? launch_oz_stage(p, reinterpret_cast<const double2*>(gamma_k), lambda_k,
@@ -942,7 +1055,8 @@ tn_status tn_theta_exec_remote(tn_plan* p, tn_stream stream, const double* gamma
   else
     st = cuda_check(launch_mix(p, sp5, lambda_l, lambda_r, reinterpret_cast<const double2*>(U), s), "K5 launch");
   if (st != TN_OK) return st;
-  return cuda_check(cudaEventRecord(p->ev[7], s), "event");
+  if ((st = cuda_check(cudaEventRecord(p->ev[7], s), "event")) != TN_OK) return st;
+  return cuda_check(plan_touch(p, s), "plan fence");
 }
 
 // ---- CUDA IPC helpers: export a device buffer to another process, open a peer's buffer ----

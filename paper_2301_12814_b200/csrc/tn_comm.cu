@@ -283,7 +283,8 @@ static tn_status pack_rows(const tn_plan* p, cudaStream_t s, const double* gamma
   const unsigned grid = (unsigned)std::min<int64_t>((rows * chi_c + 255) / 256, (int64_t)p->sm_count * 16);
   k6_pack_rows<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(gamma_k), p->d_perm[0], p0, rows, chi_c,
                                     reinterpret_cast<double2*>(out));
-  return cuda_check(cudaGetLastError(), "K6 pack rows");
+  if ((st = cuda_check(cudaGetLastError(), "K6 pack rows")) != TN_OK) return st;
+  return cuda_check(plan_touch(p, s), "plan fence");
 }
 
 tn_status tn_pack_row_slab(const tn_plan* p, tn_stream stream, const double* gamma_k, int rank, double* slab_out) {

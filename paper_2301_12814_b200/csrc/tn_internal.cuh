@@ -91,16 +91,28 @@ struct OzTile {
   int32_t g, mt, nt, pad;
 };
 
-// Per-sector tables passed BY VALUE as a kernel parameter (no device copy needed).
+// Per-sector table in device memory (DESIGN.md §4 "Runtime pieces"): the static part (slab origin, ld, whether
+// the centre segment of that key is non-empty) is uploaded with the plan; the caller's output pointers (and
+// the P source of tn_theta_exec_remote) are written by k_set_sectors at the start of every exec, so the table
+// size is not limited by the kernel-parameter space and an exec stays capturable into a CUDA graph.
+constexpr int MAX_SEC = 1024;   // sectors / charge keys of one plan: N+1 ≤ 101; pair plans (N+1)² ≤ 1024 (N ≤ 31)
+struct SecEntry {
+  double2* out;             // this rank's slab of Θ(c) (row-major, ld = C_c)
+  const double2* src;       // K5 reads P_{c_c} from here when set (tn_theta_exec_remote), else from out
+  int64_t lrow0;            // sorted left position of slab row 0
+  int64_t col0;             // sorted right position of column 0
+  int32_t ld;               // C_c
+  int32_t nonempty;         // seg_c(c) is non-empty (K4 ran group c: P_c exists), c read as a centre key
+};
 struct SectorParams {
-  double2* out[MAXC];       // this rank's slab of Θ(c) (row-major, ld = C_c)
-  const double2* src[MAXC]; // K5 reads P_{c_c} from here when set (tn_theta_exec_remote), else from out
-  int64_t lrow0[MAXC];      // sorted left position of slab row 0
-  int64_t col0[MAXC];       // sorted right position of column 0
-  int32_t ld[MAXC];         // C_c
-  int32_t ustart[MAXC];     // packed-U block offsets
+  SecEntry* sec;            // device table, one entry per sector / key
+  const int32_t* ustart;    // device packed-U block offsets
   int32_t d, N;
-  uint32_t cc_mask[4];      // bit c_c set iff seg_c(c_c) is non-empty (a group exists)
+};
+struct SectorPtrs {         // k_set_sectors' by-value argument (≤ 16 KB of the 32 KB kernel-parameter space)
+  double2* out[MAX_SEC];
+  const double2* src[MAX_SEC];
+  int32_t n;
 };
 
 }  // namespace tn
@@ -116,6 +128,9 @@ struct tn_plan {
   int32_t* d_qs[3] = {nullptr, nullptr, nullptr};    // device sorted charges
   int32_t* d_off[3] = {nullptr, nullptr, nullptr};   // device offset tables (N+2)
   double2* d_binom = nullptr;                  // (nmax+1)² exact binomials as double-double (K2)
+  tn::SecEntry* d_sec[2] = {nullptr, nullptr}; // sector tables: [0] exec / remote K4, [1] remote K5 (tn_theta_exec_remote)
+  int32_t* d_ustart = nullptr;                 // packed-U block offsets (device)
+  std::vector<tn::SecEntry> h_sec;             // static part of the sector table (host source of the upload)
   std::vector<int64_t> bounds;                 // world+1 shard bounds (sorted left positions)
   std::vector<int32_t> owner;                  // TN_GATHER_SECTOR_OWNER: receiving rank of every sector
   int64_t r0 = 0, r1 = 0;                      // this rank's window
@@ -171,6 +186,10 @@ struct tn_plan {
   mutable bool rec_k1 = false, rec_k2 = false, rec_exec = false;
   mutable cudaStream_t last_stream = nullptr;  // stream of the last exec (pool release fence)
   mutable bool captured = false;               // an exec was captured into a CUDA graph (free_plan syncs the device)
+  mutable cudaEvent_t ev_fence = nullptr;      // end of the last library work touching the plan's memory (pool fence)
+  mutable cudaStream_t touch_stream = nullptr; // stream ev_fence was last recorded on
+  mutable bool touch_stream_set = false;
+  int dev = 0;
   // contraction mode (TN_CONTRACT_*) and the INT8-emulation layout (built by tn_plan_set_contraction)
   int contraction = TN_CONTRACT_F64_DMMA;
   int oz_slices = 0;
@@ -199,6 +218,21 @@ struct tn_plan {
 
 namespace tn {
 
+inline cudaError_t plan_touch(const tn_plan* p, cudaStream_t s) {
+  if (!p->ev_fence) return cudaSuccess;
+  // one event covers every stream that touched the plan: a new stream first joins the previous fence
+  if (p->touch_stream_set && p->touch_stream != s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+      cudaError_t e = cudaStreamWaitEvent(s, p->ev_fence, 0);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  p->touch_stream = s;
+  p->touch_stream_set = true;
+  return cudaEventRecord(p->ev_fence, s);
+}
+
 void set_error(const std::string& s);
 tn_status fail(tn_status st, const std::string& s);
 tn_status cuda_check(cudaError_t e, const char* what);
@@ -207,6 +241,11 @@ tn_status cuda_check(cudaError_t e, const char* what);
 // position (tn_comm.cu)
 void sector_owners(const std::vector<int64_t>& sizes, int world, std::vector<int32_t>& owner);
 int64_t sector_rows_before(const tn_plan* p, int c, int64_t pos);
+// fill table `which` with the caller's output pointers (and P sources) on stream s; returns the kernel view
+tn_status make_sector_params(const tn_plan* p, double* const* out, const double* const* src, int which,
+                             cudaStream_t s, SectorParams* sp);
+// make s wait for the plan's asynchronous table upload (host wait under graph capture)
+tn_status wait_tables(const tn_plan* p, cudaStream_t s);
 tn_status exec_impl(const tn_plan* p, tn_stream stream, const double* gamma_k, const double* lambda_k,
                     const double* gamma_k1, const double* lambda_l, const double* lambda_r, const double* U,
                     double* const* theta_out, const int32_t* rowperm);
@@ -224,6 +263,28 @@ struct SortArgs {           // K1: one CTA per bond (0 = left, 1 = center, 2 = r
 cudaError_t launch_sort_bonds(const SortArgs& a, int N, cudaStream_t s);
 void* pool_alloc(size_t bytes, cudaError_t* err);
 void pool_release(void* ptr, cudaStream_t last_stream, bool used);
+// Shared fences: a destroyed plan hands its last-use event (recorded right after the last library work that
+// touched its memory) to all of its blocks, so a block is reusable as soon as THAT work is done — not only once
+// everything queued up to the destroy call has drained.
+struct Fence {
+  cudaEvent_t ev;
+  int refs;
+};
+Fence* fence_adopt(cudaEvent_t ev);               // takes ownership of ev
+void pool_release_fenced(void* ptr, Fence* f);    // the block shares f (nullptr: reusable at once)
+void fence_release(Fence* f);                     // drop a fence no block adopted
+// Plan shells: the plan's own stream and timing events are recycled between plans (stream creation costs
+// tens of µs per gate otherwise).
+struct PlanShell {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_ready = nullptr;
+};
+cudaError_t shell_acquire(PlanShell* out);
+void shell_release(const PlanShell& sh);
+// record the plan's pool fence at the current tail of s (after library work that touched the plan's memory)
+inline cudaError_t plan_touch(const tn_plan* p, cudaStream_t s);
 cudaError_t launch_bs_unitary(int d, int N, double theta, double phi, const double2* binom, double2* U,
                               cudaStream_t s);
 // rowperm: the A-row gather list (p->d_rowperm; tn_theta_exec_sharded passes a slab list when Γk arrived as

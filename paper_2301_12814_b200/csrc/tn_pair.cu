@@ -333,13 +333,14 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
   for (int u = threadIdx.x; u < L; u += K5P_THREADS) {
     // pass 1: sectors (lo+u, fixed), sources P valid only for a non-empty centre pair; pass 2: (fixed, lo+u)
     const int s = pass2 ? t.fixed * nk + t.lo + u : (t.lo + u) * nk + t.fixed;
-    const int64_t off = (int64_t)(rowoff[s * nq + t.lkey] + t.band) * sp.ld[s] + coloff[s * nq + t.rkey];
-    const double2* base = sp.out[s] + off;
-    const bool valid = pass2 || ((sp.cc_mask[s >> 5] >> (s & 31)) & 1u);
+    const SecEntry e = sp.sec[s];
+    const int64_t off = (int64_t)(rowoff[s * nq + t.lkey] + t.band) * e.ld + coloff[s * nq + t.rkey];
+    const double2* base = e.out + off;
+    const bool valid = pass2 || e.nonempty;
     // the source is Θ(s) itself, or a local workspace when Θ goes elsewhere (tn_theta_exec_remote, pass 2)
-    const double2* lbase = sp.src[s] ? sp.src[s] + off : base;
-    ld_sec[u] = SecRef{valid ? lbase : nullptr, (int64_t)sp.ld[s]};
-    st_sec[u] = SecRef{base, (int64_t)sp.ld[s]};
+    const double2* lbase = e.src ? e.src + off : base;
+    ld_sec[u] = SecRef{valid ? lbase : nullptr, (int64_t)e.ld};
+    st_sec[u] = SecRef{base, (int64_t)e.ld};
   }
   // Us[t][u] = U_n[i = cl − (lo+t)][j = cl − (lo+u)]  (conjugated for the bra species), padded to TP × UP
   const int TP = (L + 7) & ~7, UP = (L + 3) & ~3;

@@ -15,8 +15,11 @@ struct Block {
   size_t bytes = 0;
   int dev = 0;
   cudaEvent_t ev = nullptr;  // completion of the last work that used the block (nullptr: none)
+  Fence* fence = nullptr;    // or a shared fence (a destroyed plan's last-use event, pool_release_fenced)
   bool in_use = false;
+  uint64_t stamp = 0;        // release order (backpressure waits on the earliest)
 };
+uint64_t g_stamp = 0;
 
 std::mutex g_mu;
 std::vector<Block> g_blocks;
@@ -26,10 +29,22 @@ size_t round_bytes(size_t b) {
   return (b + g - 1) / g * g;
 }
 
+void drop_fence(Block& b) {
+  if (b.fence && --b.fence->refs == 0) {
+    cudaEventDestroy(b.fence->ev);
+    delete b.fence;
+  }
+  b.fence = nullptr;
+}
+
 bool ready(Block& b) {
-  if (!b.ev) return true;
-  cudaError_t e = cudaEventQuery(b.ev);
-  if (e == cudaSuccess) return true;
+  cudaEvent_t ev = b.fence ? b.fence->ev : b.ev;
+  if (!ev) return true;
+  cudaError_t e = cudaEventQuery(ev);
+  if (e == cudaSuccess) {
+    drop_fence(b);
+    return true;
+  }
   if (e != cudaErrorNotReady) cudaGetLastError();
   return false;
 }
@@ -39,6 +54,8 @@ size_t free_idle_locked(bool wait) {
   for (size_t i = 0; i < g_blocks.size();) {
     Block& b = g_blocks[i];
     if (!b.in_use && (wait || ready(b))) {
+      if (b.fence) cudaEventSynchronize(b.fence->ev);
+      drop_fence(b);
       if (b.ev) {
         cudaEventSynchronize(b.ev);
         cudaEventDestroy(b.ev);
@@ -78,6 +95,25 @@ void* pool_alloc(size_t bytes, cudaError_t* err) {
     g_blocks[best].in_use = true;
     return g_blocks[best].ptr;
   }
+  // Backpressure: a fitting block whose last use is still in flight is waited for rather than allocating
+  // another one — a host that plans gates faster than the GPU runs them would otherwise grow the pool without
+  // bound (and pay a cudaMalloc per gate); the earliest-released candidate completes first.
+  int wait = -1;
+  for (int i = 0; i < (int)g_blocks.size(); ++i) {
+    Block& b = g_blocks[i];
+    if (b.in_use || b.dev != dev || b.bytes < bytes || b.bytes > 2 * bytes + (size_t(2) << 20)) continue;
+    if (wait < 0 || b.stamp < g_blocks[wait].stamp) wait = i;
+  }
+  if (wait >= 0) {
+    Block& b = g_blocks[wait];
+    cudaEvent_t ev = b.fence ? b.fence->ev : b.ev;
+    if (ev && cudaEventSynchronize(ev) == cudaSuccess) {
+      drop_fence(b);
+      b.in_use = true;
+      return b.ptr;
+    }
+    cudaGetLastError();
+  }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e == cudaErrorMemoryAllocation) {
@@ -98,12 +134,47 @@ void* pool_alloc(size_t bytes, cudaError_t* err) {
   return p;
 }
 
+Fence* fence_adopt(cudaEvent_t ev) {
+  if (!ev) return nullptr;
+  Fence* f = new (std::nothrow) Fence{ev, 0};
+  if (!f) {  // cannot track it: make the event's work complete the slow way
+    cudaEventSynchronize(ev);
+    cudaEventDestroy(ev);
+  }
+  return f;
+}
+
+void pool_release_fenced(void* ptr, Fence* f) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (Block& b : g_blocks) {
+    if (b.ptr != ptr) continue;
+    b.in_use = false;
+    b.stamp = ++g_stamp;
+    drop_fence(b);
+    if (f) {
+      b.fence = f;
+      ++f->refs;
+    }
+    return;
+  }
+}
+
+void fence_release(Fence* f) {  // a fence no block adopted
+  if (f && f->refs == 0) {
+    cudaEventDestroy(f->ev);
+    delete f;
+  }
+}
+
 void pool_release(void* ptr, cudaStream_t last_stream, bool used) {
   if (!ptr) return;
   std::lock_guard<std::mutex> lk(g_mu);
   for (Block& b : g_blocks) {
     if (b.ptr != ptr) continue;
     b.in_use = false;
+    b.stamp = ++g_stamp;
+    drop_fence(b);
     if (used) {
       if (!b.ev) cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
       if (b.ev && cudaEventRecord(b.ev, last_stream) != cudaSuccess) {
@@ -113,6 +184,41 @@ void pool_release(void* ptr, cudaStream_t last_stream, bool used) {
     }
     return;
   }
+}
+
+namespace {
+std::mutex g_shell_mu;
+std::vector<PlanShell> g_shells;
+}  // namespace
+
+cudaError_t shell_acquire(PlanShell* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(g_shell_mu);
+    for (size_t i = 0; i < g_shells.size(); ++i)
+      if (g_shells[i].dev == dev) {
+        *out = g_shells[i];
+        g_shells[i] = g_shells.back();
+        g_shells.pop_back();
+        return cudaSuccess;
+      }
+  }
+  PlanShell sh;
+  sh.dev = dev;
+  if ((e = cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  for (auto& ev : sh.ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&sh.ev_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
+  *out = sh;
+  return cudaSuccess;
+}
+
+void shell_release(const PlanShell& sh) {
+  if (!sh.stream) return;
+  std::lock_guard<std::mutex> lk(g_shell_mu);
+  g_shells.push_back(sh);
 }
 
 }  // namespace tn

@@ -220,6 +220,38 @@ __global__ void k_svd_factors(const SvdParams sp, const int32_t* __restrict__ of
   }
 }
 
+struct BformPtrs {          // per sector: T = (Θ(c)·V_c)ᵀ, kept-count × R column-major (ld = kept count)
+  const double2* t[SVD_MAXSEC];
+};
+
+// right-canonical factors (R22): B^{[k]}_new[α, a0+s] = T[s, r] / λl[α] (x/0 := 0), B^{[k+1]}_new[a0+s, β]
+// = V_Θ†[s, col] = U_x[col, s]
+__global__ void k_svd_bform(const SvdParams sp, const BformPtrs bp, const int32_t* __restrict__ off_new,
+                            const int32_t* __restrict__ perm_l, const int32_t* __restrict__ perm_r,
+                            const double* __restrict__ lam_l, int64_t ld_k, int64_t chi_r, double2* __restrict__ bk_new,
+                            double2* __restrict__ bk1_new) {
+  const int c = blockIdx.y;
+  const SvdSector S = sp.sec[c];
+  const int32_t a0 = off_new[c], kc = off_new[c + 1] - a0;
+  if (kc == 0) return;
+  const int64_t na = (int64_t)S.R * kc, nb = (int64_t)kc * S.C;
+  const double2* T = bp.t[c];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < na) {
+      const int r = (int)(i / kc), s = (int)(i - (int64_t)r * kc);
+      const int32_t al = perm_l[S.rpos ? (int64_t)S.rpos[r] : S.row0 + r];
+      const double l = lam_l[al];
+      const double2 v = T[s + (int64_t)r * kc];
+      bk_new[(int64_t)al * ld_k + a0 + s] = l != 0.0 ? make_double2(v.x / l, v.y / l) : make_double2(0.0, 0.0);
+    } else {
+      const int64_t j = i - na;
+      const int s = (int)(j / S.C), col = (int)(j - (int64_t)s * S.C);
+      const int32_t be = perm_r[S.cpos ? (int64_t)S.cpos[col] : S.col0 + col];
+      bk1_new[(int64_t)(a0 + s) * chi_r + be] = S.ux[col + (int64_t)s * S.C];
+    }
+  }
+}
+
 // Run job(lane, c, host_workspace) for every sector of `wave` on the SVD lanes (largest cost first onto the
 // least-loaded lane; one host thread per lane, each lane's stream joined back into `s`).
 template <class Cost, class Job>
@@ -602,16 +634,19 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
 
 using namespace tn;
 
-extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double* const* theta, const double* lambda_l,
-                                     const double* lambda_r, int64_t chi_max, double cutoff, int32_t* q_new,
-                                     double* lambda_new, double* gamma_k_new, double* gamma_k1_new, int64_t* chi_out,
-                                     double* discarded) {
+// form 0: Vidal factors (tn_svd_truncate); form 1: right-canonical factors (tn_svd_truncate_bform)
+static tn_status svd_truncate_impl(const tn_plan* p, tn_stream stream, double* const* theta, const double* lambda_l,
+                                   const double* lambda_r, int64_t chi_max, double cutoff, int32_t* q_new,
+                                   double* lambda_new, double* gamma_k_new, double* gamma_k1_new, int64_t* chi_out,
+                                   double* discarded, int form) {
   if (chi_max < 1 || !(cutoff >= 0.0)) return fail(TN_ERR_DOMAIN, "tn_svd_truncate: chi_max < 1 or cutoff < 0");
-  if (!p || !theta || !lambda_l || !lambda_r || !q_new || !lambda_new || !gamma_k_new || !gamma_k1_new || !chi_out ||
-      !discarded)
+  if (!p || !theta || !lambda_l || (!lambda_r && form == 0) || !q_new || !lambda_new || !gamma_k_new ||
+      !gamma_k1_new || !chi_out || !discarded)
     return fail(TN_ERR_DIMENSION, "tn_svd_truncate: NULL argument");
   if (p->world != 1) return fail(TN_ERR_UNSUPPORTED, "tn_svd_truncate: needs a single-GPU plan (full sectors)");
+  if (p->nsec > SVD_MAXSEC) return fail(TN_ERR_UNSUPPORTED, "tn_svd_truncate: more sectors than this build's SVD step handles");
   cudaStream_t s = (cudaStream_t)stream;
+  if (tn_status w = wait_tables(p, s); w != TN_OK) return w;   // the factors read the plan's perm tables
   SvdCtx& X = ctx();
   std::lock_guard<std::mutex> lock(X.mu);
   if (!X.h[0]) {
@@ -894,15 +929,72 @@ extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double*
     if ((st = cuda_check(cudaMemsetAsync(gamma_k1_new, 0, (size_t)chi_new * p->chi[2] * 16, s), "memset Γk1_new")) !=
         TN_OK)
       return st;
-    k_svd_factors<<<dim3(std::max(1, 2 * p->sm_count / std::max(1, ns) + 1), ns), 256, 0, s>>>(
-        sp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, lambda_r, chi_new, p->chi[2],
-        reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
-    if ((st = cuda_check(cudaGetLastError(), "SVD factors")) != TN_OK) return st;
+    if (form == 0) {
+      k_svd_factors<<<dim3(std::max(1, 2 * p->sm_count / std::max(1, ns) + 1), ns), 256, 0, s>>>(
+          sp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, lambda_r, chi_new, p->chi[2],
+          reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
+      if ((st = cuda_check(cudaGetLastError(), "SVD factors")) != TN_OK) return st;
+    } else {
+      // right-canonical form (R22): B^{[k]}_new = Θ(c)·V_c / λl (one ZGEMM per sector, T = U_xᴴ·Z with
+      // Z = Θ(c)ᵀ column-major, then a scatter that undoes Θ's row scaling), B^{[k+1]}_new = V_c† = U_xᵀ
+      std::vector<int32_t> hoff(ns + 1, 0);
+      if ((st = cuda_check(cudaMemcpyAsync(hoff.data(), d_off, (ns + 1) * 4, cudaMemcpyDeviceToHost, s), "D2H offsets")) !=
+          TN_OK)
+        return st;
+      if ((st = cuda_check(cudaStreamSynchronize(s), "offsets sync")) != TN_OK) return st;
+      std::vector<size_t> o_t(ns, 0);
+      size_t tb = 0;
+      for (int c = 0; c < ns; ++c) {
+        o_t[c] = tb;
+        tb += ((size_t)sp.sec[c].R * (hoff[c + 1] - hoff[c]) * 16 + 255) & ~(size_t)255;
+      }
+      char* Tb = nullptr;
+      if ((st = grow(X.gbuf[2], X.gcap[2], std::max<size_t>(tb, 256), &Tb)) != TN_OK) return st;
+      cublasSetStream(X.hb[0], s);
+      const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+      BformPtrs bp{};
+      for (int c = 0; c < ns; ++c) {
+        const int kc = hoff[c + 1] - hoff[c];
+        bp.t[c] = reinterpret_cast<const double2*>(Tb + o_t[c]);
+        if (kc == 0) continue;
+        const SvdSector& S = sp.sec[c];
+        const cublasStatus_t b = cublasZgemm(
+            X.hb[0], CUBLAS_OP_C, CUBLAS_OP_N, kc, S.R, S.C, &one, reinterpret_cast<const cuDoubleComplex*>(S.ux), S.C,
+            reinterpret_cast<const cuDoubleComplex*>(theta[c]), S.C, &zero, reinterpret_cast<cuDoubleComplex*>(Tb + o_t[c]),
+            kc);
+        if (b != CUBLAS_STATUS_SUCCESS) {
+          cublasSetStream(X.hb[0], X.st[0]);
+          return fail(TN_ERR_CUDA, "tn_svd_truncate_bform: ZGEMM Θ·V failed in sector " + std::to_string(c));
+        }
+      }
+      cublasSetStream(X.hb[0], X.st[0]);
+      k_svd_bform<<<dim3(std::max(1, 2 * p->sm_count / std::max(1, ns) + 1), ns), 256, 0, s>>>(
+          sp, bp, d_off, p->d_perm[0], p->d_perm[2], lambda_l, chi_new, p->chi[2],
+          reinterpret_cast<double2*>(gamma_k_new), reinterpret_cast<double2*>(gamma_k1_new));
+      if ((st = cuda_check(cudaGetLastError(), "SVD factors (B form)")) != TN_OK) return st;
+    }
     // k_svd_factors reads the process-wide scratch (X.buf, gbuf): drain it before another call (on any stream
     // or thread) may overwrite that scratch — negligible next to the SVD itself
     if ((st = cuda_check(cudaStreamSynchronize(s), "SVD factors sync")) != TN_OK) return st;
   }
+  if ((st = cuda_check(plan_touch(p, s), "plan fence")) != TN_OK) return st;
   *chi_out = res[0];
   std::memcpy(discarded, &res[1], 8);
   return TN_OK;
+}
+
+extern "C" tn_status tn_svd_truncate(const tn_plan* p, tn_stream stream, double* const* theta, const double* lambda_l,
+                                     const double* lambda_r, int64_t chi_max, double cutoff, int32_t* q_new,
+                                     double* lambda_new, double* gamma_k_new, double* gamma_k1_new, int64_t* chi_out,
+                                     double* discarded) {
+  return svd_truncate_impl(p, stream, theta, lambda_l, lambda_r, chi_max, cutoff, q_new, lambda_new, gamma_k_new,
+                           gamma_k1_new, chi_out, discarded, 0);
+}
+
+extern "C" tn_status tn_svd_truncate_bform(const tn_plan* p, tn_stream stream, double* const* theta,
+                                           const double* lambda_l, int64_t chi_max, double cutoff, int32_t* q_new,
+                                           double* lambda_new, double* b_k_new, double* b_k1_new, int64_t* chi_out,
+                                           double* discarded) {
+  return svd_truncate_impl(p, stream, theta, lambda_l, nullptr, chi_max, cutoff, q_new, lambda_new, b_k_new, b_k1_new,
+                           chi_out, discarded, 1);
 }

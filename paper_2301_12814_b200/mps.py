@@ -1,12 +1,14 @@
 """Brick-wall layers of beam-splitter gates on a device-resident U(1) MPS.
 
 Host orchestration only (argument marshalling): every gate is tn_theta_plan (K1) → tn_build_bs_unitary
-(K2) → tn_theta_exec (K3–K5) → tn_svd_truncate (per-sector SVD + global top-χ + Vidal update), all in
-libtn_theta.so. The MPS is the Vidal form of PAPER.md:45 with the U(1) constraint of PAPER.md:49-51:
-site k carries Γ^{[k]} [χ_k × χ_{k+1}] (complex128, rows/columns in the bonds' stored order), bond k
-carries λ (float64) and its charges (int32, photons to the right); bond 0 is one bond of charge N,
-bond M one bond of charge 0. A gate on sites (k, k+1) uses bonds k, k+1, k+2 as the left, centre and
-right bonds of Eq. S5 and replaces Γ^{[k]}, λ^{[k+1]}, q^{[k+1]}, Γ^{[k+1]} (oracle: oracle/layer.py).
+(K2) → tn_theta_exec (K3–K5) → tn_svd_truncate_bform (per-sector SVD + global top-χ + right-canonical update),
+all in libtn_theta.so. The MPS is the canonical form of PAPER.md:45 with the U(1) constraint of
+PAPER.md:49-51, kept in right-canonical ("B") form: site k carries B^{[k]} = Γ^{[k]}λ^{[k+1]} [χ_k × χ_{k+1}]
+(complex128, rows/columns in the bonds' stored order), bond k carries λ (float64) and its charges (int32,
+photons to the right); bond 0 is one bond of charge N, bond M one bond of charge 0. A gate on sites (k, k+1)
+builds Θ(c) = λ^{[k]} B^{[k]} B^{[k+1]} (gated; Eq. S5 with the inner λ's inside the B's) and replaces B^{[k]},
+λ^{[k+1]}, q^{[k+1]}, B^{[k+1]} without dividing by any singular value or small λ (Hastings' update, DESIGN.md
+R22; oracle: oracle/layer.py with form "b"). Vidal states (Γ, λ) are converted on construction (B = Γλ).
 
 Layer parallelism ("beam splitter updates within a layer are parallel"; PAPER.md:96-103
 first-level parallelism): with a torch.distributed process group, every rank holds a replica of the MPS,
@@ -107,27 +109,39 @@ class _Chain:
                 bc(torch.view_as_real(t))
 
 
+def _to_b(gam, lam, form):
+    """Site tensors in right-canonical form: B^{[k]} = Γ^{[k]}λ^{[k+1]} for a Vidal input (a product, no division)."""
+    if form == "b":
+        return gam
+    return [(g * l[None, :]).contiguous() for g, l in zip(gam, lam[1:])]
+
+
 class MPS(_Chain):
-    def __init__(self, N: int, d: int, q, gam, lam, device="cuda"):
+    def __init__(self, N: int, d: int, q, gam, lam, device="cuda", form: str = "vidal"):
+        """`gam`: Vidal Γ^{[k]} (form "vidal", converted) or right-canonical B^{[k]} (form "b")."""
         dev = torch.device(device)
         as_t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
             dev, dt).contiguous()
         self.N, self.d = int(N), int(d)
         self.device = dev
         self.q = [as_t(x, torch.int32) for x in q]
-        self.gam = [as_t(x, torch.complex128) for x in gam]
         self.lam = [as_t(x, torch.float64) for x in lam]
+        self.gam = _to_b([as_t(x, torch.complex128) for x in gam], self.lam, form)   # B^{[k]}
         self.M = len(self.gam)
         if len(self.q) != self.M + 1 or len(self.lam) != self.M + 1:
             raise ValueError("an MPS of M sites needs M+1 bonds of charges and λ")
 
     @classmethod
     def from_state(cls, st: dict, device="cuda"):
-        return cls(st["N"], st["d"], st["q"], st["gam"], st["lam"], device)
+        return cls(st["N"], st["d"], st["q"], st["gam"], st["lam"], device, st.get("form", "vidal"))
 
     def to_state(self) -> dict:
+        """Host copy in right-canonical form (oracle/layer.py state dict with form "b")."""
         return dict(N=self.N, d=self.d, q=[x.cpu().numpy() for x in self.q], gam=[x.cpu().numpy() for x in self.gam],
-                    lam=[x.cpu().numpy() for x in self.lam])
+                    lam=[x.cpu().numpy() for x in self.lam], form="b")
+
+    def _ones(self, n: int):
+        return torch.ones(n, dtype=torch.float64, device=self.device)
 
     def apply_gate(self, k: int, theta: float, phi: float, chi_max: int, cutoff: float = 1e-14, contraction=None):
         """One TEBD update of sites (k, k+1); returns the discarded weight Σ dropped s²."""
@@ -137,8 +151,10 @@ class MPS(_Chain):
         if contraction is not None:
             plan.set_contraction(*contraction)
         U = build_bs_unitary(plan, theta, phi)
-        out = theta_exec(plan, self.gam[k], self.lam[k + 1], self.gam[k + 1], self.lam[k], self.lam[k + 2], U)
-        res = svd_truncate(plan, out, self.lam[k], self.lam[k + 2], chi_max, cutoff)
+        # Θ = λ^{[k]} B^{[k]} B^{[k+1]} (gated): the inner λ's are inside the B's
+        out = theta_exec(plan, self.gam[k], self._ones(plan.chi[1]), self.gam[k + 1], self.lam[k],
+                         self._ones(plan.chi[2]), U)
+        res = svd_truncate(plan, out, self.lam[k], None, chi_max, cutoff, form="b")
         self.q[k + 1] = res["q_new"]
         self.lam[k + 1] = res["lam_new"]
         self.gam[k] = res["gamma_k_new"]
@@ -157,26 +173,29 @@ class MPO(_Chain):
     on sites (k, k+1) is tn_theta2_plan → U → tn_theta_exec (Θ(c1, c2), two-pass U⊗U* mix) →
     tn_svd_truncate on the pair plan (oracle: oracle/layer.py apply_gate2)."""
 
-    def __init__(self, N: int, d: int, q1, q2, gam, lam, device="cuda"):
+    def __init__(self, N: int, d: int, q1, q2, gam, lam, device="cuda", form: str = "vidal"):
         dev = torch.device(device)
         as_t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
             dev, dt).contiguous()
         self.N, self.d, self.device = int(N), int(d), dev
         self.q1 = [as_t(x, torch.int32) for x in q1]
         self.q2 = [as_t(x, torch.int32) for x in q2]
-        self.gam = [as_t(x, torch.complex128) for x in gam]
         self.lam = [as_t(x, torch.float64) for x in lam]
+        self.gam = _to_b([as_t(x, torch.complex128) for x in gam], self.lam, form)   # B^{[k]}
         self.M = len(self.gam)
         if not (len(self.q1) == len(self.q2) == len(self.lam) == self.M + 1):
             raise ValueError("an MPO of M sites needs M+1 bonds of charge pairs and λ")
 
     @classmethod
     def from_state(cls, st: dict, device="cuda"):
-        return cls(st["N"], st["d"], st["q1"], st["q2"], st["gam"], st["lam"], device)
+        return cls(st["N"], st["d"], st["q1"], st["q2"], st["gam"], st["lam"], device, st.get("form", "vidal"))
 
     def to_state(self) -> dict:
         c = lambda xs: [x.cpu().numpy() for x in xs]
-        return dict(N=self.N, d=self.d, q1=c(self.q1), q2=c(self.q2), gam=c(self.gam), lam=c(self.lam))
+        return dict(N=self.N, d=self.d, q1=c(self.q1), q2=c(self.q2), gam=c(self.gam), lam=c(self.lam), form="b")
+
+    def _ones(self, n: int):
+        return torch.ones(n, dtype=torch.float64, device=self.device)
 
     def apply_gate(self, k: int, theta: float, phi: float, chi_max: int, cutoff: float = 1e-14, contraction=None):
         """One TEBD update of sites (k, k+1) with U⊗U*; returns the discarded weight."""
@@ -187,8 +206,9 @@ class MPO(_Chain):
         if contraction is not None:
             plan.set_contraction(*contraction)
         U = build_bs_unitary(plan, theta, phi)
-        out = theta_exec(plan, self.gam[k], self.lam[k + 1], self.gam[k + 1], self.lam[k], self.lam[k + 2], U)
-        res = svd_truncate(plan, out, self.lam[k], self.lam[k + 2], chi_max, cutoff)
+        out = theta_exec(plan, self.gam[k], self._ones(plan.chi[1]), self.gam[k + 1], self.lam[k],
+                         self._ones(plan.chi[2]), U)
+        res = svd_truncate(plan, out, self.lam[k], None, chi_max, cutoff, form="b")
         self.q1[k + 1] = res["q1_new"].to(torch.int32).contiguous()
         self.q2[k + 1] = res["q2_new"].to(torch.int32).contiguous()
         self.lam[k + 1] = res["lam_new"]

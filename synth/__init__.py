@@ -213,6 +213,10 @@ PAIR_CONFIGS = {
     1: dict(N=4, d=5, chi=256, charges="uniform", lam="random", seed=101),
     2: dict(N=5, d=6, chi=1024, charges="gauss", lam="geometric", seed=102),
     3: dict(N=5, d=6, chi=4096, charges="gauss", lam="geometric", seed=103),
+    # the paper's larger MPO charge ranges: d = 14 (Fig. S2(b)) and d = 18 (its largest run,
+    # PAPER.md:408), with N = d − 1 so every occupation 0..d−1 is reachable; (N+1)² = 196 / 324 pair keys
+    4: dict(N=13, d=14, chi=4096, charges="gauss", lam="geometric", seed=104),
+    5: dict(N=17, d=18, chi=4096, charges="gauss", lam="geometric", seed=105),
 }
 
 

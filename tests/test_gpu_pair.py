@@ -115,6 +115,43 @@ def test_pair_config3_sampled(tn):
             assert abs(g[a, b] - v) <= 1e-10 * max(scale, abs(v)), (key, a, b)
 
 
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_pair_paper_charge_ranges_sampled(tn, cfg):
+    # PAIR_CONFIGS 4/5: d = 14 and d = 18, N = 13 / 17 — 196 / 324 pair keys, beyond
+    # round 1's by-value sector tables (N ≤ 9). Pair-key tables bit-exact; every sector shape as the oracle's row /
+    # column rule; 40 sectors sampled element-wise against the literal pair sum (≤ 1e-10 of the sector's RMS).
+    c = _pair(cfg)
+    nk = c.N + 1
+    plan, got = gpu_theta2(tn, c)
+    perms = tuple(oracle.sort_pair_bonds(*q) for q in ((c.q1_l, c.q2_l), (c.q1_c, c.q2_c), (c.q1_r, c.q2_r)))
+    for b, (q1, q2) in enumerate(((c.q1_l, c.q2_l), (c.q1_c, c.q2_c), (c.q1_r, c.q2_r))):
+        assert np.array_equal(plan.perm(b), perms[b])
+        key = q1.astype(np.int64) * nk + q2
+        ref = np.concatenate([[0], np.cumsum(np.bincount(key, minlength=nk * nk))]).astype(np.int32)
+        assert np.array_equal(plan.offsets(b), ref)
+    ub = [oracle.bs_unitary_block(n, c.theta, c.phi, c.d) for n in range(min(c.N, 2 * c.d - 2) + 1)]
+    rng = np.random.default_rng(50 + cfg)
+    keys = [k for k, g in got.items() if g.size > 0]
+    assert len(keys) > 100
+    for i in rng.permutation(len(keys))[:40]:
+        key = keys[int(i)]
+        g = got[key]
+        rows = oracle.pair_sector_rows(c.q1_l[perms[0]], c.q2_l[perms[0]], c.d, *key)
+        cols = oracle.pair_sector_cols(c.q1_r[perms[2]], c.q2_r[perms[2]], c.d, *key)
+        assert g.shape == (len(rows), len(cols))
+        scale = np.linalg.norm(g) / np.sqrt(g.size)
+        for _ in range(3):
+            a, b = int(rng.integers(g.shape[0])), int(rng.integers(g.shape[1]))
+            v = oracle.theta2_element(c.N, c.d, *key, a, b, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r,
+                                      c.gamma_k, c.lam_k, c.gamma_k1, c.lam_l, c.lam_r, ub, perms)
+            assert abs(g[a, b] - v) <= 1e-10 * max(scale, abs(v)), (key, a, b)
+    # U⊗U* is unitary on every pair block: Σ‖Θ‖² with the gate equals Σ‖Θ‖² with the identity (d = N+1)
+    s_u = sum(np.linalg.norm(g) ** 2 for g in got.values())
+    _, got_i = gpu_theta2(tn, c, plan=plan, theta=0.0)
+    s_i = sum(np.linalg.norm(g) ** 2 for g in got_i.values())
+    assert abs(s_u - s_i) <= 1e-11 * s_i
+
+
 def test_pair_vectorized_pure_state_matches_single_path(tn):
     # Θ2(c1,c2)[(α,α'),(β,β')] = Θ(c1)[α,β]·conj(Θ(c2)[α',β']) — both sides on the GPU, at χ = 24 → 576 pairs
     base = synth.make_case(4, 5, 24, 24, 24, seed=21, charges="uniform", lam="random")
@@ -154,7 +191,7 @@ def test_pair_edge_cases(tn, name, N, d, chi):
 
 def test_pair_errors(tn):
     with pytest.raises(tn.TnError, match="UNSUPPORTED"):
-        tn.Plan2(11, 10, [0], [0], [0], [0], [0], [0])        # (N+1)^2 sectors beyond this build
+        tn.Plan2(33, 32, [0], [0], [0], [0], [0], [0])        # (N+1)^2 = 1089 sectors beyond this build (≤ 1024)
     with pytest.raises(tn.TnError, match="DOMAIN"):
         tn.Plan2(4, 3, [0, 4], [0, 0], [0], [0], [0], [0])    # charge outside [0, N]
     with pytest.raises(tn.TnError, match="DOMAIN"):

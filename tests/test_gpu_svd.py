@@ -229,3 +229,42 @@ def test_pair_svd_edge_cases(tn, name, N, d, chi, chi_max):
                 rg, _, _ = _recon2(c, res, c1, c2, res["q_new"])
                 rr, *_ = _recon2(c, ref, c1, c2, ref["q_new"])
                 assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), (name, c1, c2)
+
+
+# ------------------------------------------------------------------ right-canonical (B) form, R22
+def _recon_b(case, res, c):
+    """λl·B^{[k]}_new·B^{[k+1]}_new restricted to Θ(c)'s rows / columns and charge c's new bonds = the truncated Θ(c)."""
+    perm_l, off_l = oracle.sort_bonds(case.q_l, case.N)
+    perm_r, off_r = oracle.sort_bonds(case.q_r, case.N)
+    (r0, r1), (k0, k1) = oracle.sector_ranges(off_l, off_r, case.N, case.d, c)
+    rows, cols = perm_l[r0:r1], perm_r[k0:k1]
+    a = np.nonzero(res["q_new"] == c)[0]
+    A = case.lam_l[rows][:, None] * res["gamma_k_new"][np.ix_(rows, a)]
+    B = res["gamma_k1_new"][np.ix_(a, cols)]
+    return A @ B, B
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("cfg,chi", [(0, 5), (1, 64), (1, 100000), (2, 300), ("steep", 250)])
+def test_svd_truncate_bform_parity(tn, cfg, chi, algo, monkeypatch):
+    monkeypatch.setenv("TN_SVD_ALGO", algo)
+    case = (synth.make_case(6, 7, 300, 280, 320, seed=44, charges="uniform", lam="steep") if cfg == "steep"
+            else synth.make_config(cfg))
+    plan, U, got = gpu_theta(case)
+    t = [torch.from_numpy(np.ascontiguousarray(g)).cuda() for g in got]
+    res = tn.svd_truncate(plan, t, torch.from_numpy(case.lam_l).cuda(), None, chi, form="b")
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
+    ref_secs, *_ = oracle_theta(case)
+    ref = osvd.truncate_update(case.N, case.d, case.q_l, case.q_r, ref_secs, case.lam_l, case.lam_r, chi, form="b")
+    assert res["chi"] == ref["chi"] and np.array_equal(res["q_new"], ref["q_new"])
+    smax = max(float(s.max()) for s in ref["svals"] if s.size)
+    assert np.max(np.abs(res["lam_new"] - ref["lam_new"]), initial=0.0) <= 1e-12 * smax
+    for c in range(case.N + 1):
+        if ref_secs[c].size == 0:
+            continue
+        rg, Bg = _recon_b(case, res, c)
+        rr, _ = _recon_b(case, ref, c)
+        assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), c
+        if Bg.shape[0]:
+            assert np.abs(Bg @ Bg.conj().T - np.eye(Bg.shape[0])).max() <= 1e-12   # V_c† rows orthonormal

@@ -28,7 +28,7 @@ def _free_port():
 def _oracle_gate(mps, k, theta, phi, chi_max, cutoff):
     import oracle.layer as L
     st = dict(N=mps.N, d=mps.d, q=[x.numpy() for x in mps.q], gam=[x.numpy() for x in mps.gam],
-              lam=[x.numpy() for x in mps.lam])
+              lam=[x.numpy() for x in mps.lam], form="b")
     disc = L.apply_gate(st, k, theta, phi, chi_max, cutoff)
     for b in (k + 1,):
         mps.q[b] = torch.from_numpy(np.ascontiguousarray(st["q"][b]).astype(np.int32))
@@ -41,7 +41,7 @@ def _oracle_gate(mps, k, theta, phi, chi_max, cutoff):
 def _oracle_gate2(mpo, k, theta, phi, chi_max, cutoff):
     import oracle.layer as L
     st = dict(N=mpo.N, d=mpo.d, q1=[x.numpy() for x in mpo.q1], q2=[x.numpy() for x in mpo.q2],
-              gam=[x.numpy() for x in mpo.gam], lam=[x.numpy() for x in mpo.lam])
+              gam=[x.numpy() for x in mpo.gam], lam=[x.numpy() for x in mpo.lam], form="b")
     disc = L.apply_gate2(st, k, theta, phi, chi_max, cutoff)
     mpo.q1[k + 1] = torch.from_numpy(np.ascontiguousarray(st["q1"][k + 1]).astype(np.int32))
     mpo.q2[k + 1] = torch.from_numpy(np.ascontiguousarray(st["q2"][k + 1]).astype(np.int32))
@@ -60,7 +60,7 @@ def _worker_mpo(rank, world, port, M, N, d, chi, chi_max, seed, q):
         import oracle.layer as L
         from paper_2301_12814_b200.mps import MPO
         st = L.random_mpo(M, N, d, chi, seed)
-        ref = L.copy_state2(st)
+        ref = L.copy_state2(L.to_bform(st))   # the MPO class keeps right-canonical tensors
         class OracleMPO(MPO):  # test subclass: the GPU gate replaced by the oracle's
             def apply_gate(self, k, theta, phi, chi_max, cutoff=1e-14, contraction=None):
                 return _oracle_gate2(self, k, theta, phi, chi_max, cutoff)
@@ -96,7 +96,7 @@ def _worker(rank, world, port, M, N, d, chi, chi_max, seed, q):
         import oracle.layer as L
         from paper_2301_12814_b200.mps import MPS
         st = L.random_mps(M, N, d, chi, seed)
-        ref = L.copy_state(st)
+        ref = L.copy_state(L.to_bform(st))    # the MPS class keeps right-canonical tensors
         class OracleMPS(MPS):  # test subclass: the GPU gate replaced by the oracle's
             def apply_gate(self, k, theta, phi, chi_max, cutoff=1e-14, contraction=None):
                 return _oracle_gate(self, k, theta, phi, chi_max, cutoff)

@@ -46,19 +46,18 @@ def test_status_strings_and_version():
 
 
 def _cost_rows(d, N, nl, nc, nr):
-    """Independent re-statement of the per-row useful work to check the balance."""
+    """Independent re-statement of the per-row device-time model the shard split balances: the
+    row's K4 contraction flops (SURVEY.md §8(d), 8 per complex MAC) plus 355 flop-equivalents per Θ element it
+    owns (K5 moves 32 B per element at ~3.7 TB/s while K4 runs at ~41 TFLOP/s)."""
+    C = [sum(nr[max(0, c - d + 1):c + 1]) for c in range(N + 1)]
     cost = np.zeros(N + 1)
     for cl in range(N + 1):
         f = 0.0
         for cc in range(max(0, cl - d + 1), cl + 1):
             if nc[cc]:
-                f += 8.0 * nc[cc] * sum(nr[max(0, cc - d + 1):cc + 1])
-        for cr in range(N + 1):
-            if not (0 <= cl - cr <= 2 * d - 2):
-                continue
-            cs = [c for c in range(N + 1) if 0 <= cl - c <= d - 1 and 0 <= c - cr <= d - 1]
-            f += 8.0 * nr[cr] * len(cs) * sum(1 for c in cs if nc[c])
-        cost[cl] = f
+                f += 8.0 * nc[cc] * C[cc]
+        el = sum(C[c] for c in range(max(0, cl - d + 1), cl + 1))
+        cost[cl] = f + 355.0 * el
     return cost
 
 

@@ -157,3 +157,27 @@ def test_pair_no_truncation_reconstructs_theta2():
             rec = (A * res["lam_new"][a][None, :]) @ B
             assert np.linalg.norm(rec - th) <= 1e-12 * max(np.linalg.norm(th), 1e-300), (c1, c2)
     assert res["discarded"] <= 1e-24
+
+
+@pytest.mark.parametrize("chi", [40, 10 ** 6])
+def test_bform_update_reconstructs_like_vidal(chi):
+    # the right-canonical update (R22) is the same truncation as the Vidal one: identical ranking and
+    # λ, λl·B^{[k]}·B^{[k+1]} = λl·Γ^{[k]}·diag(λ)·Γ^{[k+1]}·λr on every sector, B^{[k+1]} rows orthonormal per charge
+    import synth
+    case = synth.make_config(1)
+    secs, *_ = oracle.theta_sectors(case.N, case.d, case.q_l, case.q_c, case.q_r, case.gamma_k, case.lam_k,
+                                    case.gamma_k1, case.lam_l, case.lam_r, case.theta, case.phi)
+    v = osvd.truncate_update(case.N, case.d, case.q_l, case.q_r, secs, case.lam_l, case.lam_r, chi)
+    b = osvd.truncate_update(case.N, case.d, case.q_l, case.q_r, secs, case.lam_l, case.lam_r, chi, form="b")
+    assert v["chi"] == b["chi"] and np.array_equal(v["q_new"], b["q_new"])
+    assert np.array_equal(v["lam_new"], b["lam_new"]) and v["discarded"] == b["discarded"]
+    ll, lr = case.lam_l, case.lam_r
+    for c in range(case.N + 1):
+        a = np.nonzero(b["q_new"] == c)[0]
+        if a.size == 0:
+            continue
+        rv = (ll[:, None] * v["gamma_k_new"][:, a] * v["lam_new"][a][None, :]) @ (v["gamma_k1_new"][a] * lr[None, :])
+        rb = (ll[:, None] * b["gamma_k_new"][:, a]) @ b["gamma_k1_new"][a]
+        assert np.linalg.norm(rb - rv) <= 1e-12 * np.linalg.norm(rv)
+        B1 = b["gamma_k1_new"][a]
+        assert np.abs(B1 @ B1.conj().T - np.eye(a.size)).max() <= 1e-12
