@@ -721,7 +721,8 @@ def run_pair(args, rank, world, local_rank):
     c = synth.make_pair_config(args.pair)
     h = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     gk, gk1, lk, ll, lr = h(c.gamma_k), h(c.gamma_k1), h(c.lam_k), h(c.lam_l), h(c.lam_r)
-    qs = [h(q) for q in (c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)]
+    # pair charges stay on the host (plan metadata): the plan counts them there, no per-gate host sync
+    qs = [np.ascontiguousarray(q) for q in (c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)]
     int8 = args.contraction == "int8"
 
     def mk():
@@ -825,7 +826,7 @@ def run_sweep(args, rank, world, local_rank):
         _, _, ql, qc, qr = synth.make_charges(4, g)
         gen = torch.Generator(device=dev)
         gen.manual_seed(4_000_000 + g)
-        qd = [torch.from_numpy(q).to(dev) for q in (ql, qc, qr)]
+        qd = [torch.from_numpy(q).to(dev) for q in (ql, qc, qr)]   # device copies draw the δ masks below
 
         def gamma(a, b):
             m = ((a[:, None] - b[None, :]) >= 0) & ((a[:, None] - b[None, :]) <= d - 1)
@@ -834,7 +835,7 @@ def run_sweep(args, rank, world, local_rank):
             return (torch.complex(x, y) / math.sqrt(2)) * m
 
         rng = np.random.default_rng([4, g, 7])
-        gates.append(dict(q=qd, gk=gamma(qd[0], qd[1]), gk1=gamma(qd[1], qd[2]),
+        gates.append(dict(q=[np.ascontiguousarray(q) for q in (ql, qc, qr)], gk=gamma(qd[0], qd[1]), gk1=gamma(qd[1], qd[2]),
                           theta=float(rng.uniform(0, math.pi / 2)), phi=float(rng.uniform(0, 2 * math.pi))))
     # Θ buffers: per sector the largest slab over this rank's gates, reused by every gate
     plans = [tn.Plan(d, N, *gt["q"]) for gt in gates]

@@ -39,46 +39,58 @@ __device__ __forceinline__ void load_group(double2 (&a)[KSM], const SecRef* __re
 // L2ONLY: P was written by other SMs during the same kernel → bypass L1 (ld.global.cg)
 // PF: groups further ahead (beyond the one held in registers) whose P lines are prefetched into L2
 // (PF = 2 measured slower at configs 3 and 4: 0.82 vs 0.78 ms, 6.57 vs 6.05 ms)
-template <int NT, int NW, bool L2ONLY = false, int PF = 0>  // NT = ⌈L/8⌉ output tiles of 8 sectors; NW warps per tile
-__device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* __restrict__ sec,
-                                              const SecRef* __restrict__ st_sec, const double2* __restrict__ Us,
+// MULTI: the tile spans `nsub` sub-tiles of mt.ne 8-groups each, sub-tile i using sector tables sec + i·sstride
+// and st_sec + i·sstride (K5P: several values of the other charge species in one CTA)
+template <int NT, int NW, bool L2ONLY = false, int PF = 0, bool MULTI = false>  // NT = ⌈L/8⌉ output tiles of 8 sectors; NW warps per tile
+__device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* __restrict__ sec0,
+                                              const SecRef* __restrict__ st_sec0, const double2* __restrict__ Us,
                                               const double* __restrict__ UsS,
                                               int ust, int L, const int32_t* __restrict__ perm_l,
                                               const int32_t* __restrict__ perm_r, const double* __restrict__ ll,
-                                              const double* __restrict__ lr, int warp, int lane) {
+                                              const double* __restrict__ lr, int warp, int lane, int nsub = 1,
+                                              int sstride = 0) {
   constexpr int KSM = 2 * NT;
   const int g = lane >> 2, q = lane & 3;
   const int KS = (L + 3) >> 2;
+  const int ntot = MULTI ? mt.ne * nsub : mt.ne;
   int k = warp;
-  if (k >= mt.ne) return;
-  auto coords = [&](int kk, int64_t& row, int& col) {
+  if (k >= ntot) return;
+  auto coords = [&](int kk, int64_t& row, int& col, int& sub) {
+    if (MULTI) {
+      sub = kk / mt.ne;
+      kk -= sub * mt.ne;
+    } else {
+      sub = 0;
+    }
     const int grp = mt.e0 + kk;
     row = grp / mt.ngr;
     col = (int)(grp - row * mt.ngr) * 8 + g;
   };
   int64_t row;
-  int col;
-  coords(k, row, col);
+  int col, sub;
+  coords(k, row, col, sub);
   bool valid = col < mt.nr;
+  const SecRef* sec = sec0 + (MULTI ? sub * sstride : 0);
+  const SecRef* st_sec = st_sec0 + (MULTI ? sub * sstride : 0);
   double2 a[KSM];
   load_group<KSM, L2ONLY>(a, sec, L, row, col, valid, q);
   while (true) {
     // prefetch the next group of this warp before computing the current one
     const int kn = k + NW;
-    const bool has_next = kn < mt.ne;
+    const bool has_next = kn < ntot;
     int64_t rown = 0;
-    int coln = 0;
+    int coln = 0, subn = 0;
     bool validn = false;
     double2 an[KSM];
     if (has_next) {
-      coords(kn, rown, coln);
+      coords(kn, rown, coln, subn);
       validn = coln < mt.nr;
-      load_group<KSM, L2ONLY>(an, sec, L, rown, coln, validn, q);
+      load_group<KSM, L2ONLY>(an, MULTI ? sec0 + subn * sstride : sec, L, rown, coln, validn, q);
     }
-    if (PF > 0 && k + (PF + 1) * NW < mt.ne) {  // L2 prefetch PF groups further ahead (no registers held)
+    if (PF > 0 && k + (PF + 1) * NW < ntot) {  // L2 prefetch PF groups further ahead (no registers held)
       int64_t rp;
-      int cp;
-      coords(k + (PF + 1) * NW, rp, cp);
+      int cp, sp_;
+      coords(k + (PF + 1) * NW, rp, cp, sp_);
       if (cp < mt.nr)
 #pragma unroll
         for (int ks = 0; ks < KSM; ++ks) {
@@ -129,6 +141,10 @@ __device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* _
     row = rown;
     col = coln;
     valid = validn;
+    if (MULTI) {
+      sec = sec0 + subn * sstride;
+      st_sec = st_sec0 + subn * sstride;
+    }
 #pragma unroll
     for (int ks = 0; ks < KSM; ++ks) a[ks] = an[ks];
   }

@@ -54,7 +54,7 @@ struct MixTile2 {           // K5P work unit (pair plans): one species' U mix ov
   int32_t pl0, pr0;         // sorted positions of the tile's first row / the block's first column
   int32_t lkey, rkey;       // pair keys of the left / right segment
   int32_t fixed, band;      // the other species' output value; the tile's first row within segment l
-  int32_t flags, pad;       // bit 0: pass 2 (species 2: conj(U), sectors (fixed, lo+u), outer λ's)
+  int32_t flags, nfix;      // bit 0: pass 2 (species 2: conj(U), sectors (fixed, lo+u), outer λ's); values fixed..+nfix−1
 };
 
 struct MixTile {            // K5 work unit: ≤ 128 "8-groups" (8 consecutive columns of one row) of one (c_l, c_r) block
@@ -160,6 +160,8 @@ struct tn_plan {
   int32_t* d_rowoff = nullptr;                 // [sector][left key]: local row of the segment in the sector (−1: absent)
   int32_t* d_coloff = nullptr;                 // [sector][right key]: local column of the segment
   int64_t nmix2[2] = {0, 0};                   // tiles of pass 1 (species 1) and pass 2 (species 2)
+  int nfix_max = 1;                            // most values of the other species one K5P tile covers
+  int64_t nmix2_multi[2] = {0, 0};             // of each pass's tiles, the trailing ones covering > 1 value
   std::vector<tn::MixTile2> h_mix2;
   std::vector<int32_t> h_rowoff, h_coloff;
   std::vector<int32_t> h_rowperm_pos, h_colperm_pos;

@@ -41,7 +41,27 @@ tn_status build_pair_tables(tn_plan* p) {
   const auto& oc = p->off[1];
   const auto& orr = p->off[2];
   auto cnt = [](const std::vector<int32_t>& o, int k) { return (int64_t)o[k + 1] - o[k]; };
-  auto ok = [d](int a, int b) { return a - b >= 0 && a - b <= d - 1; };
+  // For a (left pair l, right pair r) block the admissible centre pairs are the rectangle I1 × I2, Ik = [max(rk,
+  // lk−d+1), min(lk, rk+d−1)] (both species' δ's): their count L1·L2 and Σ n_c over it come from a 2-D prefix
+  // sum over the centre-pair counts, O(1) per block instead of a scan over all (N+1)² centre pairs.
+  std::vector<int64_t> P2((size_t)(nk + 1) * (nk + 1), 0);   // P2[(a)(nk+1) + b] = Σ_{m1<a, m2<b} n_c(m1, m2)
+  for (int a = 0; a < nk; ++a)
+    for (int b = 0; b < nk; ++b)
+      P2[(size_t)(a + 1) * (nk + 1) + b + 1] = P2[(size_t)a * (nk + 1) + b + 1] + P2[(size_t)(a + 1) * (nk + 1) + b] -
+                                               P2[(size_t)a * (nk + 1) + b] + cnt(oc, a * nk + b);
+  struct Blk {
+    int64_t L1, L2, mc;
+  };
+  auto blk = [&](int l, int r) {
+    const int l1 = l / nk, l2 = l % nk, r1 = r / nk, r2 = r % nk;
+    const int a0 = std::max(r1, l1 - d + 1), a1 = std::min(l1, r1 + d - 1);
+    const int b0 = std::max(r2, l2 - d + 1), b1 = std::min(l2, r2 + d - 1);
+    Blk x{std::max(0, a1 - a0 + 1), std::max(0, b1 - b0 + 1), 0};
+    if (x.L1 && x.L2)
+      x.mc = P2[(size_t)(a1 + 1) * (nk + 1) + b1 + 1] - P2[(size_t)a0 * (nk + 1) + b1 + 1] -
+             P2[(size_t)(a1 + 1) * (nk + 1) + b0] + P2[(size_t)a0 * (nk + 1) + b0];
+    return x;
+  };
   // ---- sector layouts: local row / column offset of every pair segment inside every sector ----
   std::vector<int32_t>& rowoff = p->h_rowoff;
   std::vector<int32_t>& coloff = p->h_coloff;
@@ -58,17 +78,12 @@ tn_status build_pair_tables(tn_plan* p) {
     std::vector<double> cost(nq, 0.0);
     for (int l = 0; l < nq; ++l) {
       if (!cnt(ol, l)) continue;
-      const int l1 = l / nk, l2 = l % nk;
       for (int r = 0; r < nq; ++r) {
         const int64_t nr = cnt(orr, r);
         if (!nr) continue;
-        const int r1 = r / nk, r2 = r % nk;
-        double L1 = 0, L2 = 0, mc = 0;
-        for (int x = 0; x <= N; ++x) L1 += ok(l1, x) && ok(x, r1);
-        for (int y = 0; y <= N; ++y) L2 += ok(l2, y) && ok(y, r2);
-        for (int m = 0; m < nq; ++m)
-          if (cnt(oc, m) && ok(l1, m / nk) && ok(m / nk, r1) && ok(l2, m % nk) && ok(m % nk, r2)) mc += (double)cnt(oc, m);
-        cost[l] += (double)nr * (mc + L1 * L1 * L2 + L1 * L2 * L2);
+        const Blk b = blk(l, r);
+        const double L1 = (double)b.L1, L2 = (double)b.L2;
+        cost[l] += (double)nr * ((double)b.mc + L1 * L1 * L2 + L1 * L2 * L2);
       }
     }
     double total = 0.0;
@@ -127,38 +142,20 @@ tn_status build_pair_tables(tn_plan* p) {
     }
   // ---- useful work (oracle.flop_counts2 definitions) ----
   p->f_contract = p->f_mix = 0;
-  for (int l = 0; l < nq; ++l) {
-    const int64_t nl = cnt(ol, l);
-    if (!nl) continue;
-    for (int r = 0; r < nq; ++r) {
-      const int64_t nr = cnt(orr, r);
-      if (!nr) continue;
-      const int l1 = l / nk, l2 = l % nk, r1 = r / nk, r2 = r % nk;
-      int64_t L1 = 0, L2 = 0;
-      for (int x = 0; x <= N; ++x) L1 += ok(l1, x) && ok(x, r1);
-      for (int y = 0; y <= N; ++y) L2 += ok(l2, y) && ok(y, r2);
-      for (int m = 0; m < nq; ++m)
-        if (cnt(oc, m) && ok(l1, m / nk) && ok(m / nk, r1) && ok(l2, m % nk) && ok(m % nk, r2))
-          p->f_contract += 8 * nl * cnt(oc, m) * nr;
-      if (L1 && L2) p->f_mix += 8 * nl * nr * (L1 * L1 * L2 + L1 * L2 * L2);
-    }
-  }
   p->f_contract_local = p->f_mix_local = 0;
   for (int l = 0; l < nq; ++l) {
-    const int64_t nl = in_shard(l).second;
+    const int64_t nl = cnt(ol, l), nll = in_shard(l).second;
     if (!nl) continue;
-    const int l1 = l / nk, l2 = l % nk;
     for (int r = 0; r < nq; ++r) {
       const int64_t nr = cnt(orr, r);
       if (!nr) continue;
-      const int r1 = r / nk, r2 = r % nk;
-      int64_t L1 = 0, L2 = 0;
-      for (int x = 0; x <= N; ++x) L1 += ok(l1, x) && ok(x, r1);
-      for (int y = 0; y <= N; ++y) L2 += ok(l2, y) && ok(y, r2);
-      for (int m = 0; m < nq; ++m)
-        if (cnt(oc, m) && ok(l1, m / nk) && ok(m / nk, r1) && ok(l2, m % nk) && ok(m % nk, r2))
-          p->f_contract_local += 8 * nl * cnt(oc, m) * nr;
-      if (L1 && L2) p->f_mix_local += 8 * nl * nr * (L1 * L1 * L2 + L1 * L2 * L2);
+      const Blk b = blk(l, r);
+      if (!b.L1 || !b.L2) continue;
+      const int64_t fmix = b.L1 * b.L1 * b.L2 + b.L1 * b.L2 * b.L2;
+      p->f_contract += 8 * nl * b.mc * nr;
+      p->f_mix += 8 * nl * nr * fmix;
+      p->f_contract_local += 8 * nll * b.mc * nr;
+      p->f_mix_local += 8 * nll * nr * fmix;
     }
   }
   // ---- groups: one per non-empty centre pair; rows / cols = those of Θ(m), gathered by position ----
@@ -213,6 +210,7 @@ tn_status build_pair_tables(tn_plan* p) {
   // ---- two-pass mix tiles: rows of one left pair segment (≈ 128 8-groups) × one right pair segment ----
   std::vector<MixTile2>& mix = p->h_mix2;
   mix.clear();
+  p->nfix_max = 1;
   int max_l = 1;
   for (int pass = 0; pass < 2; ++pass) {
     for (int l = 0; l < nq; ++l) {
@@ -231,7 +229,11 @@ tn_status build_pair_tables(tn_plan* p) {
         const int64_t ngr = (nr + 7) / 8;
         const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
         const int fixed_lo = pass == 0 ? lo2 : lo1, fixed_hi = pass == 0 ? hi2 : hi1;
-        for (int f = fixed_lo; f <= fixed_hi; ++f)
+        // several values of the other species per tile when one value's band is small (≈ 128 8-groups a tile)
+        const int64_t per_val = std::min<int64_t>(rows_per, nl) * ngr;
+        const int nfix = (int)std::max<int64_t>(1, std::min<int64_t>(fixed_hi - fixed_lo + 1,
+                                                                      MIX_GROUPS_PER_TILE / std::max<int64_t>(1, per_val)));
+        for (int f = fixed_lo; f <= fixed_hi; f += nfix)
           for (int64_t band = 0; band < nl; band += rows_per) {
             const int64_t rows = std::min<int64_t>(rows_per, nl - band);
             MixTile2 t{};
@@ -248,11 +250,20 @@ tn_status build_pair_tables(tn_plan* p) {
             t.lkey = l;
             t.rkey = r;
             t.fixed = f;
+            t.nfix = std::min(nfix, fixed_hi - f + 1);
+            p->nfix_max = std::max(p->nfix_max, t.nfix);
             t.band = (int32_t)band;
             t.flags = pass;
             mix.push_back(t);
           }
       }
+    }
+    // within the pass: single-value tiles first, then the multi-value ones (launched with the MULTI kernel, whose
+    // extra index arithmetic the common single-value tiles do not pay)
+    {
+      const size_t b0 = pass ? (size_t)p->nmix2[0] : 0;
+      auto mid = std::stable_partition(mix.begin() + b0, mix.end(), [](const MixTile2& t) { return t.nfix == 1; });
+      p->nmix2_multi[pass] = (int64_t)(mix.end() - mid);
     }
     p->nmix2[pass] = (int64_t)mix.size() - (pass ? p->nmix2[0] : 0);
   }
@@ -316,31 +327,36 @@ tn_status build_pair_tables(tn_plan* p) {
 // ---- K5P: one species' mix of one pair tile (same warp loop as K5, sector list from the plan) ----
 constexpr int K5P_THREADS = 128;
 
-template <int NTMAX>
+template <int NTMAX, bool MULTI>
 __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
     k5p_mix(const SectorParams sp, const MixTile2* __restrict__ tiles, const int32_t* __restrict__ rowoff,
             const int32_t* __restrict__ coloff, int nq, const int32_t* __restrict__ perm_l,
             const int32_t* __restrict__ perm_r, const double* __restrict__ ll, const double* __restrict__ lr,
-            const double2* __restrict__ U, int us_elems) {
+            const double2* __restrict__ U, int us_elems, int nfix_max) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const MixTile2 t = tiles[blockIdx.x];
+  // nfix_max sector tables (one per value of the other species the tile covers), each 8·NTMAX entries
+  constexpr int SSTR = 8 * NTMAX;
   SecRef* ld_sec = reinterpret_cast<SecRef*>(smem_raw);
-  SecRef* st_sec = ld_sec + 8 * NTMAX;
-  double2* Us = reinterpret_cast<double2*>(st_sec + 8 * NTMAX);
+  SecRef* st_sec = ld_sec + SSTR * nfix_max;
+  double2* Us = reinterpret_cast<double2*>(st_sec + SSTR * nfix_max);
   double* UsS = reinterpret_cast<double*>(Us + us_elems);
   const int L = t.L, d = sp.d, nk = sp.N + 1;
   const bool pass2 = t.flags & 1;
-  for (int u = threadIdx.x; u < L; u += K5P_THREADS) {
-    // pass 1: sectors (lo+u, fixed), sources P valid only for a non-empty centre pair; pass 2: (fixed, lo+u)
-    const int s = pass2 ? t.fixed * nk + t.lo + u : (t.lo + u) * nk + t.fixed;
+  // the sector tables of the tile's nfix values f of the other species: pass 1 sectors (lo+u, f), sources valid
+  // only for a non-empty centre pair; pass 2 sectors (f, lo+u)
+  const int nfix = MULTI ? t.nfix : 1;
+  for (int x = threadIdx.x; x < L * nfix; x += K5P_THREADS) {
+    const int fi = x / L, u = x - fi * L, f = t.fixed + fi;
+    const int s = pass2 ? f * nk + t.lo + u : (t.lo + u) * nk + f;
     const SecEntry e = sp.sec[s];
     const int64_t off = (int64_t)(rowoff[s * nq + t.lkey] + t.band) * e.ld + coloff[s * nq + t.rkey];
     const double2* base = e.out + off;
     const bool valid = pass2 || e.nonempty;
     // the source is Θ(s) itself, or a local workspace when Θ goes elsewhere (tn_theta_exec_remote, pass 2)
     const double2* lbase = e.src ? e.src + off : base;
-    ld_sec[u] = SecRef{valid ? lbase : nullptr, (int64_t)e.ld};
-    st_sec[u] = SecRef{base, (int64_t)e.ld};
+    ld_sec[fi * SSTR + u] = SecRef{valid ? lbase : nullptr, (int64_t)e.ld};
+    st_sec[fi * SSTR + u] = SecRef{base, (int64_t)e.ld};
   }
   // Us[t][u] = U_n[i = cl − (lo+t)][j = cl − (lo+u)]  (conjugated for the bra species), padded to TP × UP
   const int TP = (L + 7) & ~7, UP = (L + 3) & ~3;
@@ -369,12 +385,13 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
   mt.pr0 = t.pr0;
   const bool sc = pass2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the tile's nfix values form one 8-group index space (several small pair segments per CTA)
   switch (TP >> 3) {
 #define TN_MIX_CASE(m)                                                                                       \
   case m:                                                                                                    \
     if constexpr (m <= NTMAX)                                                                                \
-      mix_tile_warp<m, K5P_THREADS / 32>(mt, ld_sec, st_sec, Us, UsS, ust, L, perm_l, perm_r, sc ? ll : nullptr, \
-                                         lr, warp, lane);                                                    \
+      mix_tile_warp<m, K5P_THREADS / 32, false, 0, MULTI>(mt, ld_sec, st_sec, Us, UsS, ust, L, perm_l, perm_r, \
+                                                          sc ? ll : nullptr, lr, warp, lane, nfix, SSTR);    \
     break;
     TN_MIX_CASE(1) TN_MIX_CASE(2) TN_MIX_CASE(3) TN_MIX_CASE(4)
     TN_MIX_CASE(5) TN_MIX_CASE(6) TN_MIX_CASE(7) TN_MIX_CASE(8)
@@ -391,30 +408,36 @@ cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp1, const dou
   const int NT = (L + 7) >> 3;
   const int smax = mix_us_elems(L);
   for (int pass = 0; pass < 2; ++pass) {
-    const int64_t n = p->nmix2[pass];
+    const int64_t n = p->nmix2[pass], nm = p->nmix2_multi[pass], n1 = n - nm;
     if (n == 0) continue;
     const MixTile2* tiles = p->d_mix2 + (pass ? p->nmix2[0] : 0);
     const SectorParams& sp = pass ? sp2 : sp1;
-#define TN_P_LAUNCH(M)                                                                                        \
+#define TN_P_LAUNCH(M, MULTI, CNT, TILES, NFIX)                                                               \
   do {                                                                                                        \
-    const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * sizeof(SecRef);    \
+    const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * (size_t)(NFIX) * sizeof(SecRef); \
     if (smem > 48 * 1024) {                                                                                   \
-      cudaError_t e = cudaFuncSetAttribute(k5p_mix<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cudaError_t e = cudaFuncSetAttribute(k5p_mix<M, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                                         \
     }                                                                                                         \
-    k5p_mix<M><<<(unsigned)n, K5P_THREADS, smem, s>>>(sp, tiles, p->d_rowoff, p->d_coloff, p->nq, p->d_perm[0],   \
-                                                       p->d_perm[2], ll, lr, U, smax);                       \
+    k5p_mix<M, MULTI><<<(unsigned)(CNT), K5P_THREADS, smem, s>>>(sp, TILES, p->d_rowoff, p->d_coloff, p->nq,     \
+                                                                  p->d_perm[0], p->d_perm[2], ll, lr, U, smax, NFIX); \
+  } while (0)
+#define TN_P_BOTH(M)                                                                                          \
+  do {                                                                                                        \
+    if (n1 > 0) TN_P_LAUNCH(M, false, n1, tiles, 1);                                                         \
+    if (nm > 0) TN_P_LAUNCH(M, true, nm, tiles + n1, p->nfix_max);                                           \
   } while (0)
     if (NT <= 1)
-      TN_P_LAUNCH(1);
+      TN_P_BOTH(1);
     else if (NT <= 2)
-      TN_P_LAUNCH(2);
+      TN_P_BOTH(2);
     else if (NT <= 4)
-      TN_P_LAUNCH(4);
+      TN_P_BOTH(4);
     else if (NT <= 6)
-      TN_P_LAUNCH(6);
+      TN_P_BOTH(6);
     else
-      TN_P_LAUNCH(8);
+      TN_P_BOTH(8);
+#undef TN_P_BOTH
 #undef TN_P_LAUNCH
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
