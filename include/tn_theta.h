@@ -152,8 +152,9 @@ TN_API tn_status tn_plan_workspace_bytes(const tn_plan* plan, int64_t* bytes);
  * events. Entries for calls not yet made are −1. */
 TN_API tn_status tn_plan_kernel_times(const tn_plan* plan, float* ms5);
 /* Number of kernel launches one tn_theta_exec on this plan makes with its current contraction engine
- * (K3/K3O/K3L staging, K4/K4O/K4L, and one K5 launch per non-empty register class of the mix; the
- * plan's K1 and tn_build_bs_unitary's K2 are one launch each on top). HOST output. Errors: DIMENSION. */
+ * (the sector-table update k_set_sectors, K3/K3O/K3L staging, K4/K4O/K4L, and one K5 launch per non-empty
+ * register class of the mix — pair plans: per K5P pass, single- and multi-value tiles; the plan's K1 and
+ * tn_build_bs_unitary's K2 are one launch each on top). HOST output. Errors: DIMENSION. */
 TN_API tn_status tn_plan_exec_launches(const tn_plan* plan, int64_t* n_launches);
 
 /* Contraction engine of tn_theta_exec (default TN_CONTRACT_F64_DMMA):

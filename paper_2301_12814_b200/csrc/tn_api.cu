@@ -864,6 +864,7 @@ tn_status tn_plan_exec_launches(const tn_plan* p, int64_t* n_launches) {
       n += (c0 > 0) + (c1 > 0) + (c2 > 0) + (c3 > 0);                        // K5, one launch per L class
     }
   }
+  if (n > 0) ++n;   // k_set_sectors: the exec's output pointers into the plan's sector table
   *n_launches = n;
   return TN_OK;
 }

@@ -452,19 +452,20 @@ def test_theta_parity_config4_flat_per_block_sampled(tn):
 
 
 def test_exec_launch_count(tn):
-    # tn_plan_exec_launches (bench.py's gpu_launches): K3 a/b + K4 + one K5 launch per non-empty L class;
-    # config 3 has blocks in the L ≤ 8, ≤ 16 and ≤ 32 classes (the ncu launch list of bench.py shows the
-    # same 8 launches per step with K1 and K2: profiles/r01_launches_final.csv)
+    # tn_plan_exec_launches (bench.py's gpu_launches): k_set_sectors + K3 a/b + K4 + one K5 launch per non-empty
+    # L class; config 3 has blocks in the L ≤ 8, ≤ 16 and ≤ 32 classes (the ncu launch list of bench.py shows the
+    # same 9 launches per step with K1 and K2: profiles/r02_launches.csv)
     N, d, ql, qc, qr = synth.make_charges(3)
     plan = tn.Plan(d, N, ql, qc, qr)
-    assert plan.exec_launches() == 6
+    assert plan.exec_launches() == 7
     plan.set_contraction("int8", 6)
-    assert plan.exec_launches() == 8                 # K3O ×4, K4O, K5 ×3
+    assert plan.exec_launches() == 9                 # set, K3O ×4, K4O, K5 ×3
     plan.set_contraction("literal")
-    assert plan.exec_launches() == 3                 # K3L a/b, K4L (no mix)
+    assert plan.exec_launches() == 4                 # set, K3L a/b, K4L (no mix)
     c = synth.make_pair_config(1)
     p2 = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
-    assert p2.exec_launches() == 5                   # K3 a/b, K4, K5P ×2
+    # set, K3 a/b, K4, and per K5P pass one launch for single-value and one for multi-value tiles
+    assert p2.exec_launches() == 8
 
 
 def test_exec_captured_in_cuda_graph(tn):
