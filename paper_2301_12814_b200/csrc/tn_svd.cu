@@ -23,6 +23,7 @@
 #include <cusolverDn.h>
 
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -329,6 +330,10 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   auto cost = [&](int c) { return (double)g[c].ng * g[c].ng * ((double)g[c].mt + 3.0 * g[c].ng); };
   // phase-A scratch for every candidate sector
   std::vector<size_t> oG(ns, 0), oW(ns, 0), oWs(ns, 0), wsA(ns, 0), hsA(ns, 0);
+  // eigenpairs computed per sector (ascending, the top of the spectrum): n_g with Xsyevd, or only those ≥ vlo[c]
+  // with the ranged Xsyevdx (wave 2: the values that can still reach the top χ, DESIGN.md §4 "SVD step")
+  std::vector<int64_t> nw(ns, 0);
+  std::vector<double> vlo(ns, -1.0);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -343,6 +348,17 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
                                     nullptr, n, CUDA_R_64F, nullptr, CUDA_C_64F, &wsA[c], &hsA[c]) !=
         CUSOLVER_STATUS_SUCCESS)
       return fail(TN_ERR_CUDA, "cusolverDnXsyevd_bufferSize failed");
+    {
+      double vl = 0.0, vu = 1.0;
+      int64_t m = 0;
+      size_t wx = 0, hx = 0;
+      if (cusolverDnXsyevdx_bufferSize(X.h[0], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_V,
+                                       CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F, nullptr, n, &vl, &vu, 0, 0, &m, CUDA_R_64F,
+                                       nullptr, CUDA_C_64F, &wx, &hx) != CUSOLVER_STATUS_SUCCESS)
+        return fail(TN_ERR_CUDA, "cusolverDnXsyevdx_bufferSize failed");
+      wsA[c] = std::max(wsA[c], wx);
+      hsA[c] = std::max(hsA[c], hx);
+    }
     oG[c] = take((size_t)n * n * 16);
     oW[c] = take((size_t)n * 8);
     oWs[c] = take(wsA[c]);
@@ -367,11 +383,22 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   auto eig = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
     const Geo& q = g[c];
     hbuf.resize(std::max<size_t>(hsA[c], 1));
-    const cusolverStatus_t r =
-        cusolverDnXsyevd(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, q.ng, CUDA_C_64F,
-                         A + oG[c], q.ng, CUDA_R_64F, A + oW[c], CUDA_C_64F, A + oWs[c], wsA[c], hbuf.data(), hsA[c],
-                         infoA + c);
-    return r == CUSOLVER_STATUS_SUCCESS ? std::string() : "cuSOLVER Xsyevd failed in sector " + std::to_string(c);
+    cusolverStatus_t r;
+    if (vlo[c] > 0.0) {
+      // only the eigenvalues ≥ vlo (they land in the first m columns / entries, ascending)
+      double vl = vlo[c], vu = std::numeric_limits<double>::max();
+      int64_t m = 0;
+      r = cusolverDnXsyevdx(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_V, CUBLAS_FILL_MODE_LOWER,
+                            q.ng, CUDA_C_64F, A + oG[c], q.ng, &vl, &vu, 0, 0, &m, CUDA_R_64F, A + oW[c], CUDA_C_64F,
+                            A + oWs[c], wsA[c], hbuf.data(), hsA[c], infoA + c);
+      nw[c] = m;
+    } else {
+      r = cusolverDnXsyevd(X.h[l], X.xparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, q.ng, CUDA_C_64F,
+                           A + oG[c], q.ng, CUDA_R_64F, A + oW[c], CUDA_C_64F, A + oWs[c], wsA[c], hbuf.data(), hsA[c],
+                           infoA + c);
+      nw[c] = q.ng;
+    }
+    return r == CUSOLVER_STATUS_SUCCESS ? std::string() : "cuSOLVER eigensolver failed in sector " + std::to_string(c);
   };
   auto jobA = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
     std::string e = gram(l, c);
@@ -381,7 +408,8 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   auto fetch = [&](const std::vector<int>& secs) -> tn_status {
     std::vector<int> info(ns, 0);
     for (int c : secs) {
-      w[c].resize(g[c].ng);
+      w[c].resize(nw[c]);
+      if (nw[c] == 0) continue;
       tn_status r = cuda_check(cudaMemcpyAsync(w[c].data(), A + oW[c], w[c].size() * 8, cudaMemcpyDeviceToHost, s), "D2H w");
       if (r != TN_OK) return r;
     }
@@ -393,7 +421,7 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
     return TN_OK;
   };
   const double eps = std::ldexp(1.0, -53);
-  auto delta = [&](int c) { return 16.0 * g[c].ng * eps * std::max(w[c].back(), 0.0); };
+  auto delta = [&](int c) { return w[c].empty() ? 0.0 : 16.0 * g[c].ng * eps * std::max(w[c].back(), 0.0); };
   // approximate χ-th largest s² over `secs` (−1 if fewer than χ values) and the largest error bound
   auto kth = [&](const std::vector<int>& secs, double& dmax) {
     std::vector<double> v;
@@ -417,6 +445,16 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   // sectors at least this large get the trace-power test (TN_SVD_TEST_MIN_NG lets tests reach it at small sizes)
   const int test_min_ng = getenv("TN_SVD_TEST_MIN_NG") ? atoi(getenv("TN_SVD_TEST_MIN_NG")) : 256;
   std::vector<int> wave2, done(wave1), tested;
+  // wave-2 sectors need only the eigenvalues that can still reach the exact top χ: T_final ≥ T1 (more sectors only
+  // raise the χ-th value), and a sector's eigenvalue error is ≤ Δ_c ≤ 16·n_g·ε·‖Θ(c)‖²_F (its trace bounds λ_max)
+  // Phase C keeps w ≥ max(τ, cutoff² − Δ_c) with τ = T2 − 2·max Δ ≥ T1 − 2D, D bounding every Δ; so vl = T1 − 2D
+  // can never cut a value phase C would keep.
+  if (T1 > 0.0) {
+    double D = d1;
+    for (int c : rest) D = std::max(D, 16.0 * g[c].ng * eps * n2[c]);
+    const double vl = T1 - 2.0 * D;
+    for (int c : rest) vlo[c] = vl > 0.0 ? vl : -1.0;
+  }
   for (int c : rest) {
     if (T1 > 0.0 && n2[c] < T1 - d1) {
       disc_skipped += n2[c];
@@ -497,7 +535,7 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   for (int c : done) {
     const double lo = std::max(tau, cutoff * cutoff - delta(c));
     int k = 0;
-    for (int i = g[c].ng - 1; i >= 0 && w[c][i] >= lo; --i) ++k;
+    for (int i = (int)nw[c] - 1; i >= 0 && w[c][i] >= lo; --i) ++k;
     kp[c] = k;
     if (k == 0) {
       disc_skipped += n2[c];
@@ -524,7 +562,7 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
     const Geo& q = g[c];
     const int k = kp[c];
     const auto* Z = reinterpret_cast<const cuDoubleComplex*>(theta[c]);
-    const auto* E = reinterpret_cast<const cuDoubleComplex*>(A + oG[c]) + (size_t)(q.ng - k) * q.ng;
+    const auto* E = reinterpret_cast<const cuDoubleComplex*>(A + oG[c]) + (size_t)(nw[c] - k) * q.ng;
     auto* T = reinterpret_cast<cuDoubleComplex*>(Cb + oT[c]);
     auto* Wm = reinterpret_cast<cuDoubleComplex*>(Cb + oWm[c]);
     cublasStatus_t b =
