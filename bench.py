@@ -42,6 +42,10 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="tn", choices=["tn", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--streams", type=int, default=1,
+                    help="independent gates in flight (each on its own stream with its own U and Θ buffers); 1 = serial")
+    ap.add_argument("--projection-streams", type=int, default=3,
+                    help="gates in flight for the multi-GPU projection (its wall(1) is re-measured with the same count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt-engine", action="store_true", help="skip timing the INT8 emulation engine")
     ap.add_argument("--cpu-sectors", default="0,6,12,18,24,30")
@@ -251,21 +255,32 @@ def run_tn(args, rank, world, local_rank):
             if K and R and Cc:
                 int8_ops += 2 * (-(-R // 128) * 128) * (-(-Cc // 64) * 64) * (-(-K // 32) * 32) * 4 * (
                     args.slices * (args.slices + 1) // 2)
+    # `--streams` independent gates in flight (a brick-wall layer's gates are independent): gate i runs
+    # plan + U + exec on stream i mod S with its own U and Θ buffers, so one gate's staging / tails overlap another's
+    nslot = max(1, args.streams)
     outs = tn.alloc_theta(probe, device=dev)
-    U = torch.empty(probe.u_size(), dtype=torch.complex128, device=dev)
+    slot_outs = [outs] + [tn.alloc_theta(probe, device=dev) for _ in range(nslot - 1)]
+    slot_U = [torch.empty(probe.u_size(), dtype=torch.complex128, device=dev) for _ in range(nslot)]
+    U = slot_U[0]
     del probe
     stream = torch.cuda.current_stream(dev)
+    slot_streams = [stream] if nslot == 1 else [torch.cuda.Stream(dev) for _ in range(nslot)]
 
     plan_host_ms = []
+    step_i = [0]
 
     def step(keep):
-        t_p = time.perf_counter()
-        plan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)          # K1 + decomposition
-        plan_host_ms.append((time.perf_counter() - t_p) * 1e3)
-        if int8:
-            plan.set_contraction("int8", args.slices)                      # slice layout (K3O/K4O)
-        tn.build_bs_unitary(plan, case.theta, case.phi, out=U)            # K2
-        tn.theta_exec(plan, gk, lk, gk1, ll, lr, U, out=outs)            # K3 → K4 → K5
+        i = step_i[0] % nslot
+        step_i[0] += 1
+        st = slot_streams[i]
+        with torch.cuda.stream(st):
+            t_p = time.perf_counter()
+            plan = tn.Plan(case.d, case.N, ql, qc, qr, world, rank)          # K1 + decomposition
+            plan_host_ms.append((time.perf_counter() - t_p) * 1e3)
+            if int8:
+                plan.set_contraction("int8", args.slices)                      # slice layout (K3O/K4O)
+            tn.build_bs_unitary(plan, case.theta, case.phi, out=slot_U[i], stream=st)          # K2
+            tn.theta_exec(plan, gk, lk, gk1, ll, lr, slot_U[i], out=slot_outs[i], stream=st)  # K3 → K4 → K5
         keep.append(plan)
 
     def barrier():
@@ -292,10 +307,14 @@ def run_tn(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
+        for st in slot_streams:
+            st.wait_stream(stream)
         for i in range(args.steps):
             step(keep)
-            if len(keep) > 2:
+            if len(keep) > 1 + 2 * nslot:
                 harvest(keep.pop(0))
+        for st in slot_streams:
+            stream.wait_stream(st)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -453,8 +472,18 @@ def run_tn(args, rank, world, local_rank):
 
     projection = None
     if world == 1 and args.emulate_ranks > 1 and not int8:
+        # the projection runs every rank's step with `--projection-streams` gates in flight and divides a world-1
+        # step measured the same way (like with like); the headline line above keeps `--streams`
+        ps = max(1, args.projection_streams)
+        pstreams = [torch.cuda.Stream(dev) for _ in range(ps)] if ps > 1 else [stream]
+        pU = [torch.empty_like(U) for _ in range(ps)]
+        wall1 = emulate_ranks(tn, case, 1, args.steps, args.warmup, dev, stream, hq, (gk, lk, gk1, ll, lr), pU, 0.0,
+                              pstreams)["max_ms"] if ps != nslot else ms_step
         projection = emulate_ranks(tn, case, args.emulate_ranks, args.steps, args.warmup, dev, stream, hq,
-                                   (gk, lk, gk1, ll, lr), U, ms_step)
+                                   (gk, lk, gk1, ll, lr), pU, wall1, pstreams)
+        projection["gates_in_flight"] = ps
+        projection["wall1_def"] = (f"world-1 step with the same {ps} gate(s) in flight, same process "
+                                   f"(the headline ms_per_step above uses {nslot})")
 
     if rank != 0:
         return
@@ -510,6 +539,7 @@ def run_tn(args, rank, world, local_rank):
         "gates_per_s": round(1000.0 / ms_step, 3),
         "pct_fp64_tc_peak": round(100.0 * value / (FP64_TC_PEAK_TFLOPS * 1e3 * world), 2),
         "config": dict(workload_config(case, args.config), parallelism=f"rows{world}" if world > 1 else "single",
+                       gates_in_flight=nslot,
                        contraction="dmma (FP64 tensor cores)" if not int8 else
                        f"int8 tcgen05 Ozaki emulation, {args.slices} slices (≤1e-11 rel. error vs oracle)",
                        f_contract=flops["f_contract"], f_mix=flops["f_mix"], f_exec_rank0=flops["f_exec"],
@@ -530,28 +560,34 @@ def run_tn(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
-def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, U, wall1_ms):
+def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, slot_U, wall1_ms, slot_streams):
     """A PROJECTION of the world-R row-sharded step (compute only, operands
     pre-replicated, Θ left sharded), measured on this one GPU: every rank's own step — tn_theta_plan(R, r) with
     host charges + U + tn_theta_exec of its flop-balanced row shard — runs back to back `steps` times in turn,
-    timed with CUDA events exactly like the N=1 line; a rank on its own B200 would see this device time (same
-    SM count and HBM), while the host-side plan time per rank is what could keep it from staying GPU-bound.
-    projected_speedup = wall(1) / max_r wall(r)."""
+    timed with CUDA events exactly like the N=1 line (same gates in flight); a rank on its own B200 would see this
+    device time (same SM count and HBM), while the host-side plan time per rank is what could keep it from staying
+    GPU-bound. projected_speedup = wall(1) / max_r wall(r)."""
     import torch
     gk, lk, gk1, ll, lr = ops
+    nslot = len(slot_streams)
     per, host, kern = [], [], []
     for r in range(R):
         probe = tn.Plan(case.d, case.N, *hq, R, r)
-        outs = tn.alloc_theta(probe, device=dev)
+        outs = [tn.alloc_theta(probe, device=dev) for _ in range(nslot)]
         probe.destroy()
         hms = []
+        cnt = [0]
 
         def step(keep):
-            t0 = time.perf_counter()
-            p = tn.Plan(case.d, case.N, *hq, R, r)
-            hms.append((time.perf_counter() - t0) * 1e3)
-            tn.build_bs_unitary(p, case.theta, case.phi, out=U)
-            tn.theta_exec(p, gk, lk, gk1, ll, lr, U, out=outs)
+            i = cnt[0] % nslot
+            cnt[0] += 1
+            st = slot_streams[i]
+            with torch.cuda.stream(st):
+                t0 = time.perf_counter()
+                p = tn.Plan(case.d, case.N, *hq, R, r)
+                hms.append((time.perf_counter() - t0) * 1e3)
+                tn.build_bs_unitary(p, case.theta, case.phi, out=slot_U[i], stream=st)
+                tn.theta_exec(p, gk, lk, gk1, ll, lr, slot_U[i], out=outs[i], stream=st)
             keep.append(p)
         keep = []
         for _ in range(warmup):
@@ -564,12 +600,16 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, U, wall1_ms)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kt = []
         e0.record(stream)
+        for st in slot_streams:
+            st.wait_stream(stream)
         for _ in range(steps):
             step(keep)
-            if len(keep) > 2:
+            if len(keep) > 1 + 2 * nslot:
                 old = keep.pop(0)
                 kt.append(old.kernel_times())
                 old.destroy()
+        for st in slot_streams:
+            stream.wait_stream(st)
         e1.record(stream)
         torch.cuda.synchronize()
         for p in keep:
@@ -583,7 +623,8 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, U, wall1_ms)
     return {"kind": "projection (not a multi-GPU measurement): each rank's step timed alone on this GPU",
             "ranks": R, "per_rank_ms": [round(x, 4) for x in per], "max_ms": round(mx, 4),
             "imbalance_max_over_mean": round(mx / mean, 4), "wall1_ms": round(wall1_ms, 4),
-            "projected_speedup": round(wall1_ms / mx, 3), "plan_host_ms_per_rank": [round(x, 4) for x in host],
+            "projected_speedup": round(wall1_ms / mx, 3) if wall1_ms > 0 else None,
+            "plan_host_ms_per_rank": [round(x, 4) for x in host],
             "kernels_ms_rank0": kern[0], "kernels_ms_slowest": kern[per.index(mx)],
             "excludes": "operand distribution and Θ gathers (comm_variants_ms at N>1 measures those)"}
 

@@ -74,42 +74,50 @@ __global__ void __launch_bounds__(MIX_THREADS, (NTMAX == 1 ? 8 : NTMAX == 2 ? K5
 // the same rows across consecutive c_r blocks, i.e. the sector rows are swept contiguously
 // (tools/probe_mix_bw.cu: 5.2–5.4 TB/s row-major vs 2.8–3.5 TB/s block-major for a pure copy).
 void build_mix_tiles(tn_plan* p, std::vector<MixTile>& out) {
-  out.clear();
-  std::vector<MixTile> mid, big, huge;  // L ≤ 8 → out, ≤ 16 → mid, ≤ 32 → big, > 32: one launch per register class
+  // classes: L ≤ 8, ≤ 16, ≤ 32, > 32 (one launch per register class), each in band-major order. Two passes — count,
+  // then write every tile straight into its class's range — keep this host loop (on the per-gate plan's path)
+  // free of reallocations and concatenation copies.
   const auto& ol = p->off[0];
   const auto& orr = p->off[2];
   constexpr int BAND = 4;  // 2 / 8 / 16 measured: 0.714 / 0.763 / 0.779 ms at config 3, 4.34 / 4.31 / 4.28 at config 4
-  for (int cl = 0; cl <= p->N; ++cl) {
-    const int64_t a0 = std::max<int64_t>(ol[cl], p->r0), a1 = std::min<int64_t>(ol[cl + 1], p->r1);
-    for (int64_t band = a0, rows = 0; band < a1; band += rows) {
-      rows = std::min<int64_t>(BAND, a1 - band);
-      for (int cr = std::max(0, cl - 2 * p->d + 2); cr <= cl; ++cr) {
-        const int64_t nr = orr[cr + 1] - orr[cr];
-        if (nr == 0) continue;
-        const int64_t ngr = (nr + 7) / 8;
-        const int64_t G = rows * ngr;
-        for (int64_t e0 = 0; e0 < G; e0 += MIX_GROUPS_PER_TILE) {
-          MixTile t;
-          t.cl = cl;
-          t.cr = cr;
-          t.e0 = (int32_t)e0;
-          t.ne = (int32_t)std::min<int64_t>(MIX_GROUPS_PER_TILE, G - e0);
-          t.nr = (int32_t)nr;
-          t.ngr = (int32_t)ngr;
-          t.pl0 = (int32_t)band;
-          t.pr0 = (int32_t)orr[cr];
-          const int L = std::min(cl, cr + p->d - 1) - std::max(cr, cl - p->d + 1) + 1;
-          (L <= 8 ? out : L <= 16 ? mid : L <= 32 ? big : huge).push_back(t);
+  const int d = p->d;
+  auto cls = [d](int cl, int cr) {
+    const int L = std::min(cl, cr + d - 1) - std::max(cr, cl - d + 1) + 1;
+    return L <= 8 ? 0 : L <= 16 ? 1 : L <= 32 ? 2 : 3;
+  };
+  auto walk = [&](auto&& emit) {
+    for (int cl = 0; cl <= p->N; ++cl) {
+      const int64_t a0 = std::max<int64_t>(ol[cl], p->r0), a1 = std::min<int64_t>(ol[cl + 1], p->r1);
+      for (int64_t band = a0, rows = 0; band < a1; band += rows) {
+        rows = std::min<int64_t>(BAND, a1 - band);
+        for (int cr = std::max(0, cl - 2 * d + 2); cr <= cl; ++cr) {
+          const int64_t nr = orr[cr + 1] - orr[cr];
+          if (nr == 0) continue;
+          const int64_t ngr = (nr + 7) / 8, G = rows * ngr;
+          for (int64_t e0 = 0; e0 < G; e0 += MIX_GROUPS_PER_TILE) emit(cl, cr, band, nr, ngr, G, e0);
         }
       }
     }
-  }
-  p->nmix_cls[0] = (int64_t)out.size();
-  p->nmix_cls[1] = (int64_t)mid.size();
-  p->nmix_cls[2] = (int64_t)big.size();
-  out.insert(out.end(), mid.begin(), mid.end());
-  out.insert(out.end(), big.begin(), big.end());
-  out.insert(out.end(), huge.begin(), huge.end());
+  };
+  int64_t cnt[4] = {0, 0, 0, 0};
+  walk([&](int cl, int cr, int64_t, int64_t, int64_t, int64_t, int64_t) { ++cnt[cls(cl, cr)]; });
+  int64_t at[4] = {0, cnt[0], cnt[0] + cnt[1], cnt[0] + cnt[1] + cnt[2]};
+  out.resize((size_t)(at[3] + cnt[3]));
+  MixTile* o = out.data();
+  walk([&](int cl, int cr, int64_t band, int64_t nr, int64_t ngr, int64_t G, int64_t e0) {
+    MixTile& t = o[at[cls(cl, cr)]++];
+    t.cl = cl;
+    t.cr = cr;
+    t.e0 = (int32_t)e0;
+    t.ne = (int32_t)std::min<int64_t>(MIX_GROUPS_PER_TILE, G - e0);
+    t.nr = (int32_t)nr;
+    t.ngr = (int32_t)ngr;
+    t.pl0 = (int32_t)band;
+    t.pr0 = (int32_t)orr[cr];
+  });
+  p->nmix_cls[0] = cnt[0];
+  p->nmix_cls[1] = cnt[1];
+  p->nmix_cls[2] = cnt[2];
 }
 
 cudaError_t launch_mix(const tn_plan* p, const SectorParams& sp, const double* ll, const double* lr,

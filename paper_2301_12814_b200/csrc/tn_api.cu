@@ -601,10 +601,16 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p->groups[x].K4 > p->groups[y].K4; });
     std::vector<TileDesc>& tiles = p->h_tiles;
-    for (int gi : order) {
-      const auto& g = p->groups[gi];
-      for (int mt = 0; mt < g.nmt; ++mt)
-        for (int nt = 0; nt < g.nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
+    {
+      int64_t nt_all = 0;
+      for (const auto& g : p->groups) nt_all += (int64_t)g.nmt * g.nnt;
+      tiles.resize((size_t)nt_all);
+      TileDesc* t = tiles.data();
+      for (int gi : order) {
+        const auto& g = p->groups[gi];
+        for (int mt = 0; mt < g.nmt; ++mt)
+          for (int nt = 0; nt < g.nnt; ++nt) *t++ = TileDesc{gi, mt, nt, 0};
+      }
     }
     p->ntiles = (int64_t)tiles.size();
     std::vector<MixTile>& mix = p->h_mix;
