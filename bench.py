@@ -287,10 +287,12 @@ def run_tn(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    # warm-up
+    # warm-up; then the pool is sized for every plan the timed loop keeps alive (tn_plan_reserve), so that no
+    # step pays a cudaMalloc on its enqueue path
     keep = []
     for _ in range(args.warmup):
         step(keep)
+    keep[-1].reserve(3 * nslot + 3)
     torch.cuda.synchronize()
     keep.clear()
 
@@ -444,7 +446,9 @@ def run_tn(args, rank, world, local_rank):
         return plan
 
     for g in range(NSLOT):
-        e2e_step(g).destroy()
+        p_ = e2e_step(g)
+        p_.reserve(2 * NSLOT + 2)
+        p_.destroy()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -570,7 +574,7 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, slot_U, wall
     import torch
     gk, lk, gk1, ll, lr = ops
     nslot = len(slot_streams)
-    per, host, kern = [], [], []
+    per, host, kern, slow = [], [], [], []
     for r in range(R):
         probe = tn.Plan(case.d, case.N, *hq, R, r)
         outs = [tn.alloc_theta(probe, device=dev) for _ in range(nslot)]
@@ -585,13 +589,18 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, slot_U, wall
             with torch.cuda.stream(st):
                 t0 = time.perf_counter()
                 p = tn.Plan(case.d, case.N, *hq, R, r)
-                hms.append((time.perf_counter() - t0) * 1e3)
+                t1 = time.perf_counter()
+                hms.append((t1 - t0) * 1e3)
                 tn.build_bs_unitary(p, case.theta, case.phi, out=slot_U[i], stream=st)
+                t2 = time.perf_counter()
                 tn.theta_exec(p, gk, lk, gk1, ll, lr, slot_U[i], out=outs[i], stream=st)
+                t3 = time.perf_counter()
             keep.append(p)
+            return t0, t1, t2, t3
         keep = []
         for _ in range(warmup):
             step(keep)
+        keep[-1].reserve(3 * nslot + 3)
         torch.cuda.synchronize()
         for p in keep:
             p.destroy()
@@ -602,12 +611,16 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, slot_U, wall
         e0.record(stream)
         for st in slot_streams:
             st.wait_stream(stream)
-        for _ in range(steps):
-            step(keep)
+        for k in range(steps):
+            t = step(keep)
             if len(keep) > 1 + 2 * nslot:
                 old = keep.pop(0)
                 kt.append(old.kernel_times())
+                t = t + (time.perf_counter(),)
                 old.destroy()
+                t = t + (time.perf_counter(),)
+            if t[-1] - t[0] > 2e-3:   # diagnostics: which host call held the enqueue (backpressure waits are < 2 ms)
+                slow.append([r, k] + [round((b - a) * 1e3, 3) for a, b in zip(t, t[1:])])
         for st in slot_streams:
             stream.wait_stream(st)
         e1.record(stream)
@@ -626,7 +639,10 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, slot_U, wall
             "projected_speedup": round(wall1_ms / mx, 3) if wall1_ms > 0 else None,
             "plan_host_ms_per_rank": [round(x, 4) for x in host],
             "kernels_ms_rank0": kern[0], "kernels_ms_slowest": kern[per.index(mx)],
-            "excludes": "operand distribution and Θ gathers (comm_variants_ms at N>1 measures those)"}
+            "excludes": "operand distribution and Θ gathers (comm_variants_ms at N>1 measures those)",
+            "slow_host_steps": slow[:16],
+            "slow_host_steps_def": "[rank, step, plan ms, U ms, exec ms, kernel_times ms, destroy ms] of steps whose "
+                                   "host enqueue took > 2 ms"}
 
 
 # --------------------------------------------------------------------------------------------- brick-wall layer
@@ -794,6 +810,7 @@ def run_pair(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         step()
+    keep[-1].reserve(5)
     torch.cuda.synchronize()
     kt.clear()
     if world > 1:

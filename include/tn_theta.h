@@ -368,6 +368,16 @@ TN_API tn_status tn_sector_owners_host(int n_sectors, const int64_t* sizes, int 
  * freed; *cached (may be NULL) receives the bytes still held by live plans. */
 TN_API tn_status tn_release_cached_memory(int64_t* freed, int64_t* cached);
 
+/* Pipelined gates: makes the pool hold at least `count` blocks (in use or idle) of each size `plan`
+ * holds (tables, workspace and any exec_sharded / INT8 / literal workspace created so far), allocating
+ * the missing ones now. A caller that keeps up to `count` plans of this shape alive at once (gates in
+ * flight on several streams, plans kept for kernel_times) then never reaches cudaMalloc on the
+ * enqueue path: a cudaMalloc of a workspace-sized block costs the host milliseconds, during which
+ * the GPU drains its queue. New blocks are sized with ≤ 6.25% slack so that plans of slightly
+ * different shape share them. count ≤ 0 is a no-op. Errors: TN_ERR_CUDA (out of memory; the blocks
+ * allocated before the failure stay in the pool). */
+TN_API tn_status tn_plan_reserve(const tn_plan* plan, int32_t count);
+
 TN_API const char* tn_status_string(tn_status s);
 TN_API const char* tn_last_error(void);       /* thread-local detail of the last failure ("" if none) */
 TN_API int tn_version(void);                  /* (major << 16) | minor */

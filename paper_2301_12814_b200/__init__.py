@@ -153,6 +153,11 @@ class Plan:
         check(lib.tn_plan_exec_launches(self.handle, C.byref(n)), "tn_plan_exec_launches")
         return n.value
 
+    def reserve(self, count: int) -> None:
+        """tn_plan_reserve: pool blocks for `count` live plans of this shape (no cudaMalloc on the enqueue path
+        of pipelined gates)."""
+        check(lib.tn_plan_reserve(self.handle, int(count)), "tn_plan_reserve")
+
     def u_size(self) -> int:
         n = C.c_int64()
         check(lib.tn_plan_u_size(self.handle, C.byref(n)), "tn_plan_u_size")

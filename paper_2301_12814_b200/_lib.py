@@ -48,6 +48,7 @@ SIGNATURES = {
     "tn_plan_flops": [_p, _i64p, _i64p, _i64p, _i64p, _i64p],
     "tn_plan_u_size": [_p, _i64p],
     "tn_plan_exec_launches": [_p, _i64p],
+    "tn_plan_reserve": [_p, C.c_int32],
     "tn_plan_slab_rows": [_p, C.c_int, C.c_int, _i64p, _i64p],
     "tn_plan_gather_schedule": [_p, C.c_int, C.c_int64, _p, _i64p],
     "tn_gather_schedule_host": [C.c_int, C.c_int, _i32p, _i32p, C.c_int, _i64p, C.c_int, C.c_int64, _p, _i64p],

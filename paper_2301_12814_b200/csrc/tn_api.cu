@@ -853,6 +853,18 @@ tn_status tn_plan_get_contraction(const tn_plan* p, int* mode, int* slices) {
   return TN_OK;
 }
 
+tn_status tn_plan_reserve(const tn_plan* p, int32_t count) {
+  if (!p) return fail(TN_ERR_DIMENSION, "tn_plan_reserve: NULL plan");
+  for (const void* blk : {p->blk_tab, p->blk_work, p->blk_p, p->blk_slab, p->blk_pack, p->blk_oz, p->blk_lit}) {
+    const cudaError_t e = pool_reserve_like(blk, count);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cuda_check(e, "tn_plan_reserve");
+    }
+  }
+  return TN_OK;
+}
+
 tn_status tn_plan_exec_launches(const tn_plan* p, int64_t* n_launches) {
   if (!p || !n_launches) return fail(TN_ERR_DIMENSION, "tn_plan_exec_launches: NULL");
   int64_t n = 0;

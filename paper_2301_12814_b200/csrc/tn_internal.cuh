@@ -265,6 +265,7 @@ struct SortArgs {           // K1: one CTA per bond (0 = left, 1 = center, 2 = r
 cudaError_t launch_sort_bonds(const SortArgs& a, int N, cudaStream_t s);
 void* pool_alloc(size_t bytes, cudaError_t* err);
 void pool_release(void* ptr, cudaStream_t last_stream, bool used);
+cudaError_t pool_reserve_like(const void* ptr, int count);  // ≥ count blocks fitting ptr's request
 // Shared fences: a destroyed plan hands its last-use event (recorded right after the last library work that
 // touched its memory) to all of its blocks, so a block is reusable as soon as THAT work is done — not only once
 // everything queued up to the destroy call has drained.

@@ -18,6 +18,7 @@ struct Block {
   Fence* fence = nullptr;    // or a shared fence (a destroyed plan's last-use event, pool_release_fenced)
   bool in_use = false;
   uint64_t stamp = 0;        // release order (backpressure waits on the earliest)
+  size_t req = 0;            // bytes last requested for it (tn_plan_reserve reserves blocks that fit this)
 };
 uint64_t g_stamp = 0;
 
@@ -27,6 +28,20 @@ std::vector<Block> g_blocks;
 size_t round_bytes(size_t b) {
   const size_t g = b >= (size_t(1) << 24) ? (size_t(2) << 20) : 4096;
   return (b + g - 1) / g * g;
+}
+
+// size of a NEW block: large requests round up to 1/16 of their power-of-two octave (≤ 6.25% slack) so that
+// plans of slightly different shape (the ranks of a row sharding, successive gates of a sweep) share blocks
+size_t grow_bytes(size_t b) {
+  if (b < (size_t(1) << 24)) return b;
+  size_t o = size_t(1) << 24;
+  while (o * 2 <= b) o *= 2;
+  const size_t g = o / 16;
+  return (b + g - 1) / g * g;
+}
+
+bool fits(const Block& b, size_t bytes, int dev) {
+  return b.dev == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + (size_t(2) << 20);
 }
 
 void drop_fence(Block& b) {
@@ -87,12 +102,13 @@ void* pool_alloc(size_t bytes, cudaError_t* err) {
   int best = -1;
   for (int i = 0; i < (int)g_blocks.size(); ++i) {
     Block& b = g_blocks[i];
-    if (b.in_use || b.dev != dev || b.bytes < bytes || b.bytes > 2 * bytes + (size_t(2) << 20)) continue;
+    if (b.in_use || !fits(b, bytes, dev)) continue;
     if (!ready(b)) continue;
     if (best < 0 || b.bytes < g_blocks[best].bytes) best = i;
   }
   if (best >= 0) {
     g_blocks[best].in_use = true;
+    g_blocks[best].req = bytes;
     return g_blocks[best].ptr;
   }
   // Backpressure: a fitting block whose last use is still in flight is waited for rather than allocating
@@ -101,7 +117,7 @@ void* pool_alloc(size_t bytes, cudaError_t* err) {
   int wait = -1;
   for (int i = 0; i < (int)g_blocks.size(); ++i) {
     Block& b = g_blocks[i];
-    if (b.in_use || b.dev != dev || b.bytes < bytes || b.bytes > 2 * bytes + (size_t(2) << 20)) continue;
+    if (b.in_use || !fits(b, bytes, dev)) continue;
     if (wait < 0 || b.stamp < g_blocks[wait].stamp) wait = i;
   }
   if (wait >= 0) {
@@ -110,16 +126,19 @@ void* pool_alloc(size_t bytes, cudaError_t* err) {
     if (ev && cudaEventSynchronize(ev) == cudaSuccess) {
       drop_fence(b);
       b.in_use = true;
+      b.req = bytes;
       return b.ptr;
     }
     cudaGetLastError();
   }
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes);
+  size_t nb = grow_bytes(bytes);
+  cudaError_t e = cudaMalloc(&p, nb);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     free_idle_locked(true);
-    e = cudaMalloc(&p, bytes);
+    nb = bytes;
+    e = cudaMalloc(&p, nb);
   }
   if (e != cudaSuccess) {
     *err = e;
@@ -127,11 +146,44 @@ void* pool_alloc(size_t bytes, cudaError_t* err) {
   }
   Block b;
   b.ptr = p;
-  b.bytes = bytes;
+  b.bytes = nb;
   b.dev = dev;
   b.in_use = true;
+  b.req = bytes;
   g_blocks.push_back(b);
   return p;
+}
+
+// tn_plan_reserve: at least `count` blocks (in use or idle) that a request like the one that produced `ptr`
+// would accept; the missing ones are allocated now, idle
+cudaError_t pool_reserve_like(const void* ptr, int count) {
+  if (!ptr || count <= 0) return cudaSuccess;
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t req = 0;
+  int dev = 0;
+  for (const Block& b : g_blocks)
+    if (b.ptr == ptr) {
+      req = b.req;
+      dev = b.dev;
+    }
+  if (req == 0) return cudaSuccess;
+  int have = 0;
+  for (const Block& b : g_blocks) have += fits(b, req, dev) ? 1 : 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaError_t e = cudaSuccess;
+  for (; have < count; ++have) {
+    Block b;
+    b.bytes = grow_bytes(req);
+    if ((e = cudaMalloc(&b.ptr, b.bytes)) != cudaSuccess) break;
+    b.dev = dev;
+    b.req = req;
+    b.stamp = ++g_stamp;
+    g_blocks.push_back(b);
+  }
+  if (cur != dev) cudaSetDevice(cur);
+  return e;
 }
 
 Fence* fence_adopt(cudaEvent_t ev) {

@@ -122,3 +122,30 @@ def test_host_and_device_charges_same_plan(tn):
         assert pd.sector_shape(c) == ph.sector_shape(c)
     with pytest.raises(tn.TnError, match="DOMAIN"):      # host charges are validated on the host
         tn.Plan(case.d, case.N, np.full(5, case.N + 1, np.int32), case.q_c, case.q_r)
+
+
+def test_reserve_covers_pipelined_plans(tn):
+    # tn_plan_reserve(6): five more plans of the same shape kept alive take the reserved blocks (no new
+    # cudaMalloc), so with all six alive the pool holds no idle block; their gates are exact
+    case = synth.make_config(2)
+    t = to_dev(case)
+    hq = [np.ascontiguousarray(q) for q in (case.q_l, case.q_c, case.q_r)]
+    torch.cuda.synchronize()
+    tn.release_cached_memory()
+    plans = [tn.Plan(case.d, case.N, *hq)]
+    plans[0].reserve(6)
+    for _ in range(5):
+        plans.append(tn.Plan(case.d, case.N, *hq))
+    outs = []
+    for p in plans:
+        U = tn.build_bs_unitary(p, case.theta, case.phi)
+        outs.append(tn.theta_exec(p, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U))
+    torch.cuda.synchronize()
+    freed, held = tn.release_cached_memory()
+    assert freed == 0, freed                  # every reserved block is in use by one of the six plans
+    assert held >= 6 * plans[0].workspace_bytes() * 0.9
+    for o in outs[::5]:
+        for g, r in zip(o, _alone(2)):
+            assert np.array_equal(g.cpu().numpy(), r)
+    with pytest.raises(tn.TnError, match="NULL"):
+        tn.check(tn.lib.tn_plan_reserve(None, 2), "tn_plan_reserve")

@@ -82,3 +82,10 @@ def test_shard_rows_host_errors():
         tn.shard_rows_host(1, 3, [1] * 4, [1] * 4, [1] * 4, 2)
     with pytest.raises(tn.TnError, match="DOMAIN"):
         tn.shard_rows_host(4, 3, [1] * 4, [1] * 4, [1] * 4, 0)
+
+
+def test_null_plan_is_rejected_without_touching_cuda():
+    import paper_2301_12814_b200 as tn
+    for name, args in (("tn_plan_reserve", (None, 2)), ("tn_plan_exec_launches", (None, None))):
+        with pytest.raises(tn.TnError, match="NULL"):
+            tn.check(getattr(tn.lib, name)(*args), name)
