@@ -7,6 +7,7 @@
 #include <numeric>
 
 #include <cstdlib>
+#include <chrono>
 
 #include <dlfcn.h>
 
@@ -150,6 +151,12 @@ static void free_plan(tn_plan* p) {
   sh.stream = p->plan_stream;
   for (int i = 0; i < 8; ++i) sh.ev[i] = p->ev[i];
   sh.ev_ready = p->ev_ready;
+  sh.ha = p->ha;
+  if (sh.ha && sh.ha->pending && cudaEventRecord(sh.ha->ev, p->plan_stream) != cudaSuccess) {
+    cudaGetLastError();
+    cudaStreamSynchronize(p->plan_stream);  // cannot fence the staged uploads: wait for them
+    sh.ha->pending = false;
+  }
   shell_release(sh);   // stream + timing events go back to the shell pool
   delete p;
 }
@@ -224,12 +231,10 @@ static tn_status upload_sector_tables(tn_plan* p) {
     e.nonempty = p->off[1][c + 1] > p->off[1][c];
   }
   for (int w = 0; w < 2; ++w) {
-    tn_status st = cuda_check(cudaMemcpyAsync(p->d_sec[w], p->h_sec.data(), p->nsec * sizeof(SecEntry),
-                                              cudaMemcpyHostToDevice, p->plan_stream), "H2D sector table");
+    tn_status st = cuda_check(plan_h2d(p, p->d_sec[w], p->h_sec.data(), p->nsec * sizeof(SecEntry)), "H2D sector table");
     if (st != TN_OK) return st;
   }
-  return cuda_check(cudaMemcpyAsync(p->d_ustart, p->ustart.data(), p->ustart.size() * sizeof(int32_t),
-                                    cudaMemcpyHostToDevice, p->plan_stream), "H2D U offsets");
+  return cuda_check(plan_h2d(p, p->d_ustart, p->ustart.data(), p->ustart.size() * sizeof(int32_t)), "H2D U offsets");
 }
 
 }  // namespace tn
@@ -302,6 +307,17 @@ static void u_layout(tn_plan* p) {
   p->u_size = tot;
 }
 
+// TN_PLAN_PROFILE=1: host µs per phase of tn_theta_plan on stderr (tools/plan_profile.py)
+static bool plan_prof() {
+  static const bool on = getenv("TN_PLAN_PROFILE") != nullptr;
+  return on;
+}
+static double plan_now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#define TN_PT(i) \
+  if (plan_prof()) pt[i] = plan_now_us()
+
 static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t chi_r, const int32_t* q_l,
                            const int32_t* q_c, const int32_t* q_r, const int32_t* const* q2, int world_size, int rank,
                            tn_plan** out) {
@@ -323,6 +339,8 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
 
   tn_plan* p = new (std::nothrow) tn_plan();
   if (!p) return fail(TN_ERR_OOM, "tn_theta_plan: host allocation");
+  double pt[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  TN_PT(0);
   p->d = d;
   p->N = N;
   p->world = world_size;
@@ -361,8 +379,10 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->plan_stream = sh.stream;
     for (int i = 0; i < 8; ++i) p->ev[i] = sh.ev[i];
     p->ev_ready = sh.ev_ready;
+    p->ha = sh.ha;
   }
   TN_TRY(cudaEventCreateWithFlags(&p->ev_fence, cudaEventDisableTiming), "event create");
+  TN_PT(1);
   // ---- one pool block for the bond tables (+ staging of host charges) ----
   for (int b = 0; b < 3; ++b) {
     o_perm[b] = ct.take<int32_t>(p->chi[b]);
@@ -392,7 +412,9 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       hbin[(size_t)n * (nmax_u + 1) + k] = double2{hi, lo};
     }
   }
+  TN_PT(2);
   p->blk_tab = pool_alloc(ct.off, &aerr);
+  TN_PT(3);
   TN_TRY(aerr, "pool alloc (bond tables)");
   {
     char* base = static_cast<char*>(p->blk_tab);
@@ -404,7 +426,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       const int32_t* src = qs_in[b];
       if (host_q[b]) {
         d_q[b] = reinterpret_cast<int32_t*>(base + o_q[b]);
-        TN_TRY(cudaMemcpyAsync(d_q[b], src, p->chi[b] * sizeof(int32_t), cudaMemcpyHostToDevice, p->plan_stream),
+        TN_TRY(plan_h2d(p, d_q[b], src, p->chi[b] * sizeof(int32_t)),
                "H2D charges");
         src = d_q[b];
       }
@@ -412,7 +434,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       sa.q2[b] = q2 ? q2[b] : nullptr;
       if (q2 && host_q2[b]) {
         int32_t* dq2 = reinterpret_cast<int32_t*>(base + o_q2[b]);
-        TN_TRY(cudaMemcpyAsync(dq2, q2[b], p->chi[b] * sizeof(int32_t), cudaMemcpyHostToDevice, p->plan_stream),
+        TN_TRY(plan_h2d(p, dq2, q2[b], p->chi[b] * sizeof(int32_t)),
                "H2D charges (second species)");
         sa.q2[b] = dq2;
       }
@@ -430,12 +452,12 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->d_sec[0] = reinterpret_cast<SecEntry*>(base + o_sec[0]);
     p->d_sec[1] = reinterpret_cast<SecEntry*>(base + o_sec[1]);
     p->d_ustart = reinterpret_cast<int32_t*>(base + o_ust);
-    TN_TRY(cudaMemcpyAsync(p->d_binom, hbin.data(), hbin.size() * sizeof(double2), cudaMemcpyHostToDevice,
-                           p->plan_stream), "H2D binomials");
+    TN_TRY(plan_h2d(p, p->d_binom, hbin.data(), hbin.size() * sizeof(double2)), "H2D binomials");
     // ---- K1: sort each bond by charge (one launch, one CTA per bond) ----
     TN_TRY(cudaMemsetAsync(d_err, 0, 4 * sizeof(int32_t), p->plan_stream), "memset err");
     TN_TRY(cudaEventRecord(p->ev[0], p->plan_stream), "event");
     TN_TRY(launch_sort_bonds(sa, N, p->plan_stream), "K1 launch");
+    TN_PT(4);
     TN_TRY(cudaEventRecord(p->ev[1], p->plan_stream), "event");
     p->rec_k1 = true;
   }
@@ -484,6 +506,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       goto done;
     }
   }
+  TN_PT(5);
   if (p->pair) {
     // ---- MPO pair plan: sectors, groups, two-pass mix (tn_pair.cu) ----
     st = build_pair_tables(p);
@@ -596,6 +619,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     }
     p->a_elems = a_off;
     p->b_elems = b_off;
+    TN_PT(6);
     // ---- tile list, heavy-first (longest K first) ----
     std::vector<int> order(p->groups.size());
     std::iota(order.begin(), order.end(), 0);
@@ -615,6 +639,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->ntiles = (int64_t)tiles.size();
     std::vector<MixTile>& mix = p->h_mix;
     build_mix_tiles(p, mix);
+    TN_PT(7);
     p->nmix = (int64_t)mix.size();
     if (!p->groups.empty() || !mix.empty()) {
       Carver cw;
@@ -624,6 +649,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       const size_t o_a = cw.take<double2>(p->a_elems);
       const size_t o_b = cw.take<double2>(p->b_elems);
       p->blk_work = pool_alloc(cw.off, &aerr);
+      TN_PT(8);
       TN_TRY(aerr, "pool alloc (workspace)");
       char* base = static_cast<char*>(p->blk_work);
       p->d_groups = reinterpret_cast<GroupDesc*>(base + o_g);
@@ -632,14 +658,11 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       p->d_apanel = reinterpret_cast<double2*>(base + o_a);
       p->d_bpanel = reinterpret_cast<double2*>(base + o_b);
       if (!p->groups.empty()) {
-        TN_TRY(cudaMemcpyAsync(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc),
-                               cudaMemcpyHostToDevice, p->plan_stream), "H2D groups");
-        TN_TRY(cudaMemcpyAsync(p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice,
-                               p->plan_stream), "H2D tiles");
+        TN_TRY(plan_h2d(p, p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc)), "H2D groups");
+        TN_TRY(plan_h2d(p, p->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc)), "H2D tiles");
       }
       if (!mix.empty())
-        TN_TRY(cudaMemcpyAsync(p->d_mix, mix.data(), mix.size() * sizeof(MixTile), cudaMemcpyHostToDevice,
-                               p->plan_stream), "H2D mix tiles");
+        TN_TRY(plan_h2d(p, p->d_mix, mix.data(), mix.size() * sizeof(MixTile)), "H2D mix tiles");
       // no host sync: tn_theta_exec's stream waits for ev_ready (the host vectors stay alive in the plan)
       p->ws_bytes = (int64_t)cw.off;
     }
@@ -648,6 +671,13 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     if ((st = upload_sector_tables(p)) != TN_OK) goto done;
     TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     TN_TRY(plan_touch(p, p->plan_stream), "plan fence");
+    TN_PT(9);
+    if (plan_prof())
+      fprintf(stderr, "[plan] world %d rank %d us: shell %.1f sizing %.1f tab_alloc %.1f h2d+K1 %.1f count %.1f "
+              "sectors+groups %.1f tiles+mix %.1f ws_alloc %.1f uploads %.1f total %.1f (tiles %lld mix %lld)\n",
+              world_size, rank, pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4],
+              pt[6] - pt[5], pt[7] - pt[6], pt[8] - pt[7], pt[9] - pt[8], pt[9] - pt[0], (long long)p->ntiles,
+              (long long)p->nmix);
   }
 done:
 #undef TN_TRY

@@ -304,7 +304,7 @@ tn_status build_pair_tables(tn_plan* p) {
   p->ws_bytes += (int64_t)cw.off;
   auto up = [&](void* dst, const void* src, size_t bytes, const char* what) -> tn_status {
     if (!bytes) return TN_OK;
-    return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->plan_stream), what);
+    return cuda_check(plan_h2d(p, dst, src, bytes), what);
   };
   tn_status st;
   if ((st = up(p->d_groups, p->groups.data(), p->groups.size() * sizeof(GroupDesc), "H2D groups")) != TN_OK) return st;

@@ -3,6 +3,7 @@
 // the plan's device memory is recycled instead of cudaMalloc/cudaFree per gate (cudaFree also
 // synchronises the device). Reuse is stream-safe: a released block carries an event recorded on the
 // stream of the last exec that used it, and is only handed out again once that event has completed.
+#include <cstring>
 #include <mutex>
 
 #include "tn_internal.cuh"
@@ -243,6 +244,29 @@ std::mutex g_shell_mu;
 std::vector<PlanShell> g_shells;
 }  // namespace
 
+static cudaError_t arena_prepare(HostArena* ha) {
+  if (ha->pending) {  // the previous plan's staged uploads must have left the arena
+    cudaError_t e = cudaEventSynchronize(ha->ev);
+    if (e != cudaSuccess) return e;
+    ha->pending = false;
+  }
+  ha->off = 0;
+  if (ha->want > ha->cap) {
+    if (ha->ptr) cudaFreeHost(ha->ptr);
+    ha->ptr = nullptr;
+    ha->cap = 0;
+    const size_t want = ha->want + ha->want / 4;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&ha->ptr), want, cudaHostAllocDefault) == cudaSuccess) {
+      ha->cap = want;
+    } else {
+      cudaGetLastError();  // stays pageable
+      ha->ptr = nullptr;
+    }
+    ha->want = ha->cap;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t shell_acquire(PlanShell* out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -254,7 +278,7 @@ cudaError_t shell_acquire(PlanShell* out) {
         *out = g_shells[i];
         g_shells[i] = g_shells.back();
         g_shells.pop_back();
-        return cudaSuccess;
+        return arena_prepare(out->ha);
       }
   }
   PlanShell sh;
@@ -263,9 +287,31 @@ cudaError_t shell_acquire(PlanShell* out) {
   for (auto& ev : sh.ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return e;
   if ((e = cudaEventCreateWithFlags(&sh.ev_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
+  sh.ha = new (std::nothrow) HostArena();
+  if (!sh.ha) return cudaErrorMemoryAllocation;
+  if ((e = cudaEventCreateWithFlags(&sh.ha->ev, cudaEventDisableTiming)) != cudaSuccess) return e;
   *out = sh;
-  return cudaSuccess;
+  return arena_prepare(sh.ha);
 }
+
+cudaError_t plan_h2d(tn_plan* p, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  HostArena* ha = p->ha;
+  const void* from = src;
+  if (ha) {
+    const size_t need = (ha->off + bytes + 255) & ~size_t(255);
+    if (ha->ptr && need <= ha->cap) {
+      std::memcpy(ha->ptr + ha->off, src, bytes);
+      from = ha->ptr + ha->off;
+      ha->off = need;
+      ha->pending = true;
+    } else if (need > ha->want) {
+      ha->want = need;  // this plan's tables go up pageable; the shell's next plan gets a larger arena
+    }
+  }
+  return cudaMemcpyAsync(dst, from, bytes, cudaMemcpyHostToDevice, p->plan_stream);
+}
+
 
 void shell_release(const PlanShell& sh) {
   if (!sh.stream) return;
