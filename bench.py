@@ -481,13 +481,19 @@ def run_tn(args, rank, world, local_rank):
         ps = max(1, args.projection_streams)
         pstreams = [torch.cuda.Stream(dev) for _ in range(ps)] if ps > 1 else [stream]
         pU = [torch.empty_like(U) for _ in range(ps)]
-        wall1 = emulate_ranks(tn, case, 1, args.steps, args.warmup, dev, stream, hq, (gk, lk, gk1, ll, lr), pU, 0.0,
-                              pstreams)["max_ms"] if ps != nslot else ms_step
+        wall1_same = emulate_ranks(tn, case, 1, args.steps, args.warmup, dev, stream, hq, (gk, lk, gk1, ll, lr), pU,
+                                   0.0, pstreams)["max_ms"] if ps != nslot else ms_step
+        # the speedup divides the BEST world-1 step of this run (with three gates in flight one GPU is slower
+        # than with one: L2 contention), so the projection never gains from a slowed baseline
+        wall1 = min(wall1_same, ms_step)
         projection = emulate_ranks(tn, case, args.emulate_ranks, args.steps, args.warmup, dev, stream, hq,
                                    (gk, lk, gk1, ll, lr), pU, wall1, pstreams)
         projection["gates_in_flight"] = ps
-        projection["wall1_def"] = (f"world-1 step with the same {ps} gate(s) in flight, same process "
-                                   f"(the headline ms_per_step above uses {nslot})")
+        projection["wall1_same_streams_ms"] = round(wall1_same, 4)
+        projection["projected_speedup_same_streams"] = round(wall1_same / projection["max_ms"], 3)
+        projection["wall1_def"] = (f"the best world-1 step of this run: min(headline ms_per_step with {nslot} gate(s) "
+                                   f"in flight, the world-1 step with the ranks' {ps} gates in flight = "
+                                   f"wall1_same_streams_ms)")
 
     if rank != 0:
         return
@@ -633,16 +639,66 @@ def emulate_ranks(tn, case, R, steps, warmup, dev, stream, hq, ops, slot_U, wall
         kern.append({k: round(statistics.mean(x[k] for x in kt), 4) for k in ("k3_stage", "k4_contract", "k5_mix")})
         del outs
     mx, mean = max(per), statistics.mean(per)
+    comm = comm_model(tn, case, hq, R, per, wall1_ms) if R > 1 else None
     return {"kind": "projection (not a multi-GPU measurement): each rank's step timed alone on this GPU",
+            "comm_model": comm,
             "ranks": R, "per_rank_ms": [round(x, 4) for x in per], "max_ms": round(mx, 4),
             "imbalance_max_over_mean": round(mx / mean, 4), "wall1_ms": round(wall1_ms, 4),
             "projected_speedup": round(wall1_ms / mx, 3) if wall1_ms > 0 else None,
             "plan_host_ms_per_rank": [round(x, 4) for x in host],
             "kernels_ms_rank0": kern[0], "kernels_ms_slowest": kern[per.index(mx)],
-            "excludes": "operand distribution and Θ gathers (comm_variants_ms at N>1 measures those)",
+            "excludes": "operand distribution and Θ gathers (modelled in comm_model; comm_variants_ms at N>1 "
+                        "measures them)",
             "slow_host_steps": slow[:16],
             "slow_host_steps_def": "[rank, step, plan ms, U ms, exec ms, kernel_times ms, destroy ms] of steps whose "
                                    "host enqueue took > 2 ms"}
+
+
+NVLINK_GBS = 900.0   # NVLink 5 per GPU per direction, nominal (B200_PROFILING.md); NCCL reaches less
+
+
+def comm_model(tn, case, hq, R, per_ms, wall1_ms):
+    """A MODEL (bytes from the library's own schedules, time at the nominal NVLink rate) of the exchange steps the
+    compute projection leaves out: the Γk row-slab scatter from rank 0 (TN_BCAST_SLABS) and the Θ gather to the
+    sector owners (TN_GATHER_SECTOR_OWNER, tn_plan_gather_schedule). Per rank, t = max(bytes sent, bytes
+    received) / NVLINK_GBS; "serial" adds it to the rank's compute, "overlapped" takes the max of the two (gates
+    in flight: gate g's exchange under gate g+1's kernels, which touch other buffers)."""
+    import numpy as np
+    N = case.N
+    cnt = [np.bincount(np.asarray(q), minlength=N + 1).astype(np.int64) for q in hq]
+    off = [np.concatenate([[0], np.cumsum(c)]).astype(np.int32) for c in cnt]
+    bounds = tn.shard_rows_host(case.d, N, cnt[0], cnt[1], cnt[2], R)        # the plan's own row shards
+    sched = tn.gather_schedule_host(case.d, N, off[0], off[2], bounds, tn.TN_GATHER_SECTOR_OWNER)
+    chi_c = int(len(hq[1]))
+    rows = [(int(bounds[r]), int(bounds[r + 1])) for r in range(R)]
+    sent, recv = [0] * R, [0] * R
+    for r in range(1, R):                       # Γk slabs: rank 0 → r
+        b = (rows[r][1] - rows[r][0]) * chi_c * 16
+        sent[0] += b
+        recv[r] += b
+    gsent, grecv = [0] * R, [0] * R
+    for t in sched:                             # Θ slabs: src → owner
+        if t["src"] == t["dst"]:
+            continue
+        b = t["rows"] * t["cols"] * 16
+        gsent[t["src"]] += b
+        grecv[t["dst"]] += b
+    ms = lambda b: b / (NVLINK_GBS * 1e9) * 1e3
+    t_slab = [ms(max(a, b)) for a, b in zip(sent, recv)]
+    t_gath = [ms(max(a, b)) for a, b in zip(gsent, grecv)]
+    out = {"kind": "model: library schedules' bytes at the nominal NVLink 5 rate (not measured)",
+           "nvlink_gbs": NVLINK_GBS,
+           "slab_scatter_mb_rank0_sent": round(sent[0] / 1e6, 1),
+           "gather_owner_mb_max_sent": round(max(gsent) / 1e6, 1),
+           "gather_owner_mb_max_recv": round(max(grecv) / 1e6, 1),
+           "t_slab_ms": [round(x, 4) for x in t_slab], "t_gather_ms": [round(x, 4) for x in t_gath]}
+    if wall1_ms > 0:
+        for name, extra in (("slabs", t_slab), ("slabs_and_owner_gather", [a + b for a, b in zip(t_slab, t_gath)])):
+            serial = max(c + e for c, e in zip(per_ms, extra))
+            over = max(max(c, e) for c, e in zip(per_ms, extra))
+            out[f"projected_speedup_{name}_serial"] = round(wall1_ms / serial, 3)
+            out[f"projected_speedup_{name}_overlapped"] = round(wall1_ms / over, 3)
+    return out
 
 
 # --------------------------------------------------------------------------------------------- brick-wall layer
