@@ -253,6 +253,120 @@ __global__ void k_svd_bform(const SvdParams sp, const BformPtrs bp, const int32_
   }
 }
 
+// ---- Ritz refinement (phase C of the Gram path, DESIGN.md §4 "SVD step") ----
+// Y = Z·E_k' has nearly orthogonal columns (E_k' are eigenvectors of ZᴴZ): with M = YᴴY, the scaled coupling
+// ρ_ij = |M_ij| / √(M_ii M_jj) is ~ ε·w_max / w at worst (the eigenvectors' backward error). Instead of a full SVD
+// of Y, each pass rotates every column pair (i, j) by the exact 2×2 Jacobi rotation of [[M_ii, M_ij], [M_ji,
+// M_jj]], all pairs at once (V = I + the rotations' off-diagonal entries): first order in ρ, so a pass squares ρ
+// and the second pass finds it at rounding level. The scaled convergence test is the one-sided Jacobi criterion
+// (Demmel–Veselić), so the column norms of the rotated Y are the Ritz values to relative rounding accuracy.
+
+// V[i + j·k] for column-major M (k × k); atomically records max ρ over the off-diagonal pairs (bit pattern of a
+// non-negative double orders like an unsigned integer)
+__global__ void k_ritz_rot(const double2* __restrict__ M, int k, double2* __restrict__ V,
+                           unsigned long long* __restrict__ rho_max) {
+  double rho = 0.0;
+  const int64_t kk = (int64_t)k * k;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < kk; x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x % k), j = (int)(x / k);
+    if (i == j) {
+      V[x] = make_double2(1.0, 0.0);
+      if (!(M[x].x > 0.0)) rho = INFINITY;   // a zero column has no direction to refine: library SVD
+      continue;
+    }
+    const double a = M[i + (int64_t)i * k].x, d = M[j + (int64_t)j * k].x;
+    const double2 b = M[x];                      // M_ij = y_iᴴ y_j
+    const double ab = hypot(b.x, b.y);
+    double2 v = make_double2(0.0, 0.0);
+    if (ab > 0.0) {
+      const double den = sqrt(fmax(a, 0.0)) * sqrt(fmax(d, 0.0));
+      rho = fmax(rho, den > 0.0 ? ab / den : INFINITY);
+      // v_j's i-th component: s·b/|b| with t = tan θ the smaller root of the 2×2 problem (|θ| ≤ π/4);
+      // to first order b / (M_jj − M_ii)
+      const double zeta = (d - a) / (2.0 * ab);
+      const double az = fabs(zeta);
+      const double r = az > 1.0 ? az * sqrt(1.0 + 1.0 / (az * az)) : sqrt(1.0 + az * az);
+      const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (az + r);
+      const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+      v = make_double2(s * b.x / ab, s * b.y / ab);
+    }
+    V[x] = v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) rho = fmax(rho, __shfl_xor_sync(0xffffffffu, rho, o));
+  if ((threadIdx.x & 31) == 0 && rho > 0.0) {
+    unsigned long long bits = (unsigned long long)__double_as_longlong(rho);
+    atomicMax(rho_max, bits);
+  }
+}
+
+__global__ void k_eye(double2* __restrict__ W, int k, double alpha, double beta) {  // W ← α·I + β·W
+  const int64_t kk = (int64_t)k * k;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < kk; x += (int64_t)gridDim.x * blockDim.x) {
+    const double2 w = beta != 0.0 ? W[x] : make_double2(0.0, 0.0);
+    const double e = (x % k) == (x / k) ? alpha : 0.0;
+    W[x] = make_double2(e + beta * w.x, beta * w.y);
+  }
+}
+
+// s²_j = ‖Y[:, j]‖² (one block per column; Y column-major, ld m)
+__global__ void k_colnorm2(const double2* __restrict__ Y, int64_t m, double* __restrict__ s2) {
+  const int j = blockIdx.x;
+  const double2* y = Y + (int64_t)j * m;
+  double acc = 0.0;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) acc += y[r].x * y[r].x + y[r].y * y[r].y;
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    s2[j] = t;
+  }
+}
+
+// descending order of s² (ties: lower column first): src[rank] = column
+__global__ void k_ritz_rank(const double* __restrict__ s2, int k, int32_t* __restrict__ src) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const double v = s2[i];
+  int r = 0;
+  for (int j = 0; j < k; ++j) {
+    const double u = s2[j];
+    r += (u > v) || (u == v && j < i);
+  }
+  src[r] = i;
+}
+
+// P[:, r] = Y[:, src[r]] / s, Wout[:, r] = W[:, src[r]], S[r] = s = √s²[src[r]]
+__global__ void k_ritz_permute(const double2* __restrict__ Y, const double2* __restrict__ W,
+                               const double* __restrict__ s2, const int32_t* __restrict__ src, int64_t m, int k,
+                               double2* __restrict__ P, double2* __restrict__ Wout, double* __restrict__ S) {
+  const int64_t ny = m * k, nw = (int64_t)k * k;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < ny + nw + k;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (x < ny) {
+      const int r = (int)(x / m);
+      const int64_t row = x - (int64_t)r * m;
+      const int j = src[r];
+      const double s = sqrt(s2[j]);
+      const double inv = s > 0.0 ? 1.0 / s : 0.0;
+      const double2 y = Y[row + (int64_t)j * m];
+      P[x] = make_double2(y.x * inv, y.y * inv);
+    } else if (x < ny + nw) {
+      const int64_t z = x - ny;
+      const int r = (int)(z / k);
+      const int64_t row = z - (int64_t)r * k;
+      Wout[z] = W[row + (int64_t)src[r] * k];
+    } else {
+      const int r = (int)(x - ny - nw);
+      S[r] = sqrt(s2[src[r]]);
+    }
+  }
+}
+
 // Run job(lane, c, host_workspace) for every sector of `wave` on the SVD lanes (largest cost first onto the
 // least-loaded lane; one host thread per lane, each lane's stream joined back into `s`).
 template <class Cost, class Job>
@@ -309,8 +423,10 @@ tn_status run_lanes(SvdCtx& X, cudaStream_t s, std::vector<int> wave, Cost cost,
 //     with w ≥ T² − 2Δ (Δ = the largest error bound 16·n_g·ε·w_max over sectors) and w ≥ cutoff² − Δ_c, so
 //     every value that can make the exact top χ (or pass the cutoff) is inside E_k'. The norm bound of the
 //     library path skips whole sectors the same way (‖Θ(c)‖²_F < T² − Δ).
-//  C. Rayleigh–Ritz: Y = Z·E_k' (tall) or Zᴴ·E_k' (max(R,C) × k', ZGEMM), exact SVD Y = P S Wᴴ (one-sided Jacobi),
-//     then Z ≈ P S (E_k' W)ᴴ (tall) or (E_k' W) S Pᴴ. Ritz values are accurate to second order in the
+//  C. Rayleigh–Ritz: Y = Z·E_k' (tall) or Zᴴ·E_k' (max(R,C) × k', ZGEMM), exact SVD Y = P S Wᴴ — by the Ritz
+//     refinement (simultaneous 2×2 Jacobi rotations of Y's nearly orthogonal columns until the scaled coupling is at
+//     rounding level, k_ritz_rot; falls back to a library SVD of Y when it does not converge, e.g. kept values
+//     below the Gram matrix's resolution) — then Z ≈ P S (E_k' W)ᴴ (tall) or (E_k' W) S Pᴴ. Ritz values are accurate to second order in the
 //     subspace error, i.e. to ~ε relative, and both factors are orthonormal to ~ε. The weight outside the
 //     computed values, ‖Θ(c)‖²_F − Σ S², joins the discarded weight. Θ(c) is read, not destroyed.
 tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& sp, const std::vector<double>& n2,
@@ -531,6 +647,7 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
   // phase C: k' per sector and its scratch
   std::vector<int> kp(ns, 0), waveC;
   std::vector<size_t> oT(ns), oP(ns), oWm(ns), oS(ns), oEW(ns), oWc(ns), wsC(ns), hsC(ns);
+  std::vector<size_t> oM(ns), oV(ns), oW2(ns), oS2(ns), oSrc(ns), oRho(ns);   // Ritz refinement scratch
   off = 0;
   for (int c : done) {
     const double lo = std::max(tau, cutoff * cutoff - delta(c));
@@ -554,10 +671,104 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
     oS[c] = take((size_t)k * 8);
     oEW[c] = take((size_t)q.ng * k * 16);
     oWc[c] = take(wsC[c]);
+    oM[c] = take((size_t)k * k * 16);
+    oV[c] = take((size_t)k * k * 16);
+    oW2[c] = take((size_t)k * k * 16);
+    oS2[c] = take((size_t)k * 8);
+    oSrc[c] = take((size_t)k * 4);
+    oRho[c] = take(8);
   }
   char* Cb = nullptr;
   if ((st = grow(X.gbuf[1], X.gcap[1], std::max<size_t>(off, 256), &Cb)) != TN_OK) return st;
-  std::atomic<int> n_jacobi{0};
+  std::atomic<int> n_jacobi{0}, n_refined{0}, n_refine_fallback{0}, n_passes{0};
+  // Ritz refinement (k_ritz_rot above): 0 = done (P, Wm, S written), 1 = did not converge (caller falls back to a
+  // library SVD of a recomputed Y), -1 = a CUDA / cuBLAS error
+  auto refine = [&](int l, int c, int mt, int k, double2* T, std::string& err) -> int {
+    cublasHandle_t hb = X.hb[l];
+    cudaStream_t st = X.st[l];
+    double2* Ya = T;
+    double2* Yb = reinterpret_cast<double2*>(Cb + oP[c]);
+    double2* Wa = reinterpret_cast<double2*>(Cb + oWm[c]);
+    double2* Wb = reinterpret_cast<double2*>(Cb + oW2[c]);
+    double2* M = reinterpret_cast<double2*>(Cb + oM[c]);
+    double2* V = reinterpret_cast<double2*>(Cb + oV[c]);
+    auto* rho_d = reinterpret_cast<unsigned long long*>(Cb + oRho[c]);
+    auto cz = [](double2* p) { return reinterpret_cast<cuDoubleComplex*>(p); };
+    const unsigned gk = (unsigned)std::min<int64_t>(1024, ((int64_t)k * k + 255) / 256);
+    auto gemm = [&](cublasOperation_t ta, int mm, int nn, int kk, const double2* A_, int lda, const double2* B_, int ldb,
+                    double2* C_, int ldc) {
+      return cublasZgemm(hb, ta, CUBLAS_OP_N, mm, nn, kk, &one, reinterpret_cast<const cuDoubleComplex*>(A_), lda,
+                         reinterpret_cast<const cuDoubleComplex*>(B_), ldb, &zero, cz(C_), ldc) == CUBLAS_STATUS_SUCCESS;
+    };
+    // ρ_max of Y's column pairs (M = YᴴY, V = the simultaneous rotation); the one host sync per pass
+    auto measure = [&](double& rho) -> bool {
+      if (!gemm(CUBLAS_OP_C, k, k, mt, Ya, mt, Ya, mt, M, k)) return false;
+      if (cudaMemsetAsync(rho_d, 0, 8, st) != cudaSuccess) return false;
+      k_ritz_rot<<<gk, 256, 0, st>>>(M, k, V, rho_d);
+      unsigned long long bits = 0;
+      if (cudaMemcpyAsync(&bits, rho_d, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return false;
+      if (cudaStreamSynchronize(st) != cudaSuccess) return false;
+      rho = __builtin_bit_cast(double, bits);
+      return true;
+    };
+    // converged when every column pair is orthogonal to rounding of the dot products that measure it
+    const double tol = 16.0 * std::sqrt((double)mt) * std::ldexp(1.0, -53);
+    k_eye<<<gk, 256, 0, st>>>(Wa, k, 1.0, 0.0);
+    bool conv = false, applied = false;
+    double rho = 0.0;
+    const bool prof_r = prof;
+    for (int pass = 0; pass < 8; ++pass) {
+      if (!measure(rho)) return err = "Ritz refinement (measure) failed in sector " + std::to_string(c), -1;
+      ++n_passes;
+      if (prof_r) fprintf(stderr, "[svd] refine sector %d %dx%d pass %d rho %.3e\n", c, mt, k, pass, rho);
+      if (rho <= tol) {
+        conv = true;
+        break;
+      }
+      if (!(rho < 0.5)) break;  // far from orthogonal (clusters, noise-level columns): leave it to the library SVD
+      if (!gemm(CUBLAS_OP_N, mt, k, k, Ya, mt, V, k, Yb, mt) || !gemm(CUBLAS_OP_N, k, k, k, Wa, k, V, k, Wb, k))
+        return err = "Ritz refinement (rotate) failed in sector " + std::to_string(c), -1;
+      std::swap(Ya, Yb);
+      std::swap(Wa, Wb);
+      applied = true;
+    }
+    if (!conv) return 1;
+    if (applied) {
+      // one Newton–Schulz step makes the accumulated rotation unitary to rounding: C = (3I − WᴴW)/2,
+      // W ← W·C, Y ← Y·C; then the pairs are measured once more
+      if (!gemm(CUBLAS_OP_C, k, k, k, Wa, k, Wa, k, M, k)) return err = "Ritz refinement (NS) failed", -1;
+      k_eye<<<gk, 256, 0, st>>>(M, k, 1.5, -0.5);
+      if (!gemm(CUBLAS_OP_N, mt, k, k, Ya, mt, M, k, Yb, mt) || !gemm(CUBLAS_OP_N, k, k, k, Wa, k, M, k, Wb, k))
+        return err = "Ritz refinement (NS) failed", -1;
+      std::swap(Ya, Yb);
+      std::swap(Wa, Wb);
+      if (!measure(rho)) return err = "Ritz refinement (check) failed in sector " + std::to_string(c), -1;
+      if (rho > tol) return 1;
+    }
+    // outputs P (Cb + oP), Wm (Cb + oWm), S: stage the current Y / W out of the output buffers first
+    double2* Pout = reinterpret_cast<double2*>(Cb + oP[c]);
+    double2* Wout = reinterpret_cast<double2*>(Cb + oWm[c]);
+    if (Ya == Pout) {
+      if (cudaMemcpyAsync(T, Ya, (size_t)mt * k * 16, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return err = "Ritz refinement copy failed", -1;
+      Ya = T;
+    }
+    if (Wa == Wout) {
+      if (cudaMemcpyAsync(Wb, Wa, (size_t)k * k * 16, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return err = "Ritz refinement copy failed", -1;
+      Wa = Wb;
+    }
+    auto* s2 = reinterpret_cast<double*>(Cb + oS2[c]);
+    auto* src = reinterpret_cast<int32_t*>(Cb + oSrc[c]);
+    k_colnorm2<<<k, 256, 0, st>>>(Ya, mt, s2);
+    k_ritz_rank<<<(k + 255) / 256, 256, 0, st>>>(s2, k, src);
+    const int64_t tot = (int64_t)mt * k + (int64_t)k * k + k;
+    k_ritz_permute<<<(unsigned)std::min<int64_t>(4096, (tot + 255) / 256), 256, 0, st>>>(
+        Ya, Wa, s2, src, mt, k, Pout, Wout, reinterpret_cast<double*>(Cb + oS[c]));
+    if (cudaGetLastError() != cudaSuccess) return err = "Ritz refinement kernels failed", -1;
+    ++n_refined;
+    return 0;
+  };
   auto jobC = [&](int l, int c, std::vector<char>& hbuf) -> std::string {
     const Geo& q = g[c];
     const int k = kp[c];
@@ -569,13 +780,29 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
         q.tall ? cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.C, k, q.R, &one, Z, q.C, E, q.R, &zero, T, q.C)
                : cublasZgemm(X.hb[l], CUBLAS_OP_C, CUBLAS_OP_N, q.R, k, q.C, &one, Z, q.C, E, q.C, &zero, T, q.R);
     if (b != CUBLAS_STATUS_SUCCESS) return "cuBLAS Ritz projection failed in sector " + std::to_string(c);
-    // one-sided Jacobi by default: Y = Z·E_k' already has nearly orthogonal columns (E_k' are eigenvectors of
-    // ZᴴZ), so it converges in a few sweeps and is accurate to rounding (config 3: Ritz 89 vs 110 ms with the
-    // polar-decomposition Xgesvdp, which TN_RITZ_POLAR=1 selects, guarded by its backward-error report)
-    static const bool force_polar = getenv("TN_RITZ_POLAR") != nullptr;
+    // default: the Ritz refinement above (GEMMs + own kernels; Y's columns are already nearly orthogonal);
+    // TN_RITZ_SVD=1 (or a refinement that does not converge) takes a library SVD of Y instead: one-sided Jacobi
+    // for narrow Y (config 3: 89 ms for the Ritz phase vs 110 ms with the polar-decomposition Xgesvdp, which
+    // TN_RITZ_POLAR=1 selects, guarded by its backward-error report)
+    const bool force_polar = getenv("TN_RITZ_POLAR") != nullptr;
+    const bool library_ritz = force_polar || getenv("TN_RITZ_SVD") != nullptr;
+    bool refine_failed = false;
+    if (!library_ritz) {
+      std::string err;
+      const int r = refine(l, c, q.mt, k, reinterpret_cast<double2*>(T), err);
+      if (r < 0) return err;
+      if (r == 0) {
+        b = cublasZgemm(X.hb[l], CUBLAS_OP_N, CUBLAS_OP_N, q.ng, k, k, &one, E, q.ng, Wm, k, &zero,
+                        reinterpret_cast<cuDoubleComplex*>(Cb + oEW[c]), q.ng);
+        return b == CUBLAS_STATUS_SUCCESS ? std::string() : "cuBLAS Ritz rotation failed in sector " + std::to_string(c);
+      }
+      ++n_refine_fallback;
+      refine_failed = true;
+    }
     // Jacobi for narrow Y; for wide ones (k' > 512: wide spectra where the Gram bound keeps most values, e.g.
     // MPO gates) the GEMM-rich polar decomposition is faster (MPO pair-config-3 layer: 4.9 → 5.9 gates/s)
     const bool ritz_jacobi = !force_polar && k <= 512;
+    (void)refine_failed;
     double herr = 0.0;
     if (!ritz_jacobi) {
       hbuf.resize(std::max<size_t>(hsC[c], 1));
@@ -624,7 +851,9 @@ tn_status svd_gram(SvdCtx& X, cudaStream_t s, double* const* theta, SvdParams& s
     return b == CUBLAS_STATUS_SUCCESS ? std::string() : "cuBLAS Ritz rotation failed in sector " + std::to_string(c);
   };
   if ((st = run_lanes(X, s, waveC, cost, jobC)) != TN_OK) return st;
-  if (prof && n_jacobi.load()) fprintf(stderr, "[svd_gram] Jacobi fallback in %d Ritz SVDs\n", n_jacobi.load());
+  if (prof)
+    fprintf(stderr, "[svd_gram] Ritz: %d refined (%d passes), %d refinement fallbacks, %d Jacobi SVDs\n",
+            n_refined.load(), n_passes.load(), n_refine_fallback.load(), n_jacobi.load());
   std::vector<int> info(ns, 0);
   std::vector<std::vector<double>> sv(ns);
   for (int c : waveC) {

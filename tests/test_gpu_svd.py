@@ -48,13 +48,16 @@ def _recon(case, res, c):
 ALGOS = ["gram", "gesvdp", "gesvdj"]   # TN_SVD_ALGO: Gram eigensolver + Rayleigh–Ritz (default), library SVDs
 
 
-@pytest.mark.parametrize("algo", ALGOS + ["gram-tested"])
+@pytest.mark.parametrize("algo", ALGOS + ["gram-tested", "gram-libritz"])
 @pytest.mark.parametrize("cfg,chi", [(0, 5), (1, 64), (1, 100000), (2, 1024), (2, 300)])
 def test_svd_truncate_parity(tn, cfg, chi, algo, monkeypatch):
-    # "gram-tested": the trace-power sector test (normally only for n_g ≥ 256) applied to every candidate
+    # "gram-tested": the trace-power sector test (normally only for n_g ≥ 256) applied to every candidate;
+    # "gram-libritz": the Ritz step by a library SVD of Y instead of the default Ritz refinement
     monkeypatch.setenv("TN_SVD_ALGO", algo.split("-")[0])
     if algo == "gram-tested":
         monkeypatch.setenv("TN_SVD_TEST_MIN_NG", "1")
+    if algo == "gram-libritz":
+        monkeypatch.setenv("TN_RITZ_SVD", "1")
     case = synth.make_config(cfg)
     got, res = _run(tn, case, chi)
     ref_secs, *_ = oracle_theta(case)
@@ -102,7 +105,7 @@ def test_svd_truncate_parity_config3(tn):
             assert np.abs(B @ B.conj().T - np.eye(B.shape[0])).max() <= 1e-12
 
 
-@pytest.mark.parametrize("algo", ALGOS + ["gram-tested"])
+@pytest.mark.parametrize("algo", ALGOS + ["gram-tested", "gram-libritz"])
 @pytest.mark.parametrize("chi", [40, 250, 100000])
 def test_svd_wide_spectrum(tn, chi, algo, monkeypatch):
     # λ = 0.97^i on every bond: Θ's singular values span many decades, the regime where an eigen-
@@ -110,6 +113,8 @@ def test_svd_wide_spectrum(tn, chi, algo, monkeypatch):
     monkeypatch.setenv("TN_SVD_ALGO", algo.split("-")[0])
     if algo == "gram-tested":
         monkeypatch.setenv("TN_SVD_TEST_MIN_NG", "1")
+    if algo == "gram-libritz":
+        monkeypatch.setenv("TN_RITZ_SVD", "1")
     case = synth.make_case(6, 7, 300, 280, 320, seed=44, charges="uniform", lam="steep")
     got, res = _run(tn, case, chi)
     ref_secs, *_ = oracle_theta(case)
@@ -268,3 +273,16 @@ def test_svd_truncate_bform_parity(tn, cfg, chi, algo, monkeypatch):
         assert np.linalg.norm(rg - rr) <= 1e-10 * max(np.linalg.norm(rr), 1e-300), c
         if Bg.shape[0]:
             assert np.abs(Bg @ Bg.conj().T - np.eye(Bg.shape[0])).max() <= 1e-12   # V_c† rows orthonormal
+
+
+def test_ritz_refinement_is_the_default_path(tn, capfd, monkeypatch):
+    # config 2 at χ_max 300 and 1024: every Ritz step converges in the refinement (no library SVD), and
+    # TN_SVD_PROFILE reports it; the result is the one the parity tests above check
+    monkeypatch.setenv("TN_SVD_PROFILE", "1")
+    case = synth.make_config(2)
+    for chi in (300, 1024):
+        _run(tn, case, chi)
+        err = capfd.readouterr().err
+        line = [x for x in err.splitlines() if "[svd_gram] Ritz:" in x][-1]
+        refined, fallbacks = int(line.split()[2]), int(line.split("),")[1].split()[0])
+        assert refined > 0 and fallbacks == 0, line
