@@ -287,7 +287,7 @@ tn_status build_literal(tn_plan* p) {
       for (int nt = 0; nt < secs[i].nnt; ++nt) tiles.push_back(TileDesc{(int32_t)i, mt, nt, 0});
   std::stable_sort(tiles.begin(), tiles.end(), [&](const TileDesc& x, const TileDesc& y) { return secs[x.g].K4 > secs[y.g].K4; });
   if (p->blk_lit) {
-    cudaStreamSynchronize(p->last_stream);
+    if (cudaEventSynchronize(p->ev_fence) != cudaSuccess) cudaGetLastError();   // last use (any stream)
     pool_release(p->blk_lit, nullptr, false);
     p->blk_lit = nullptr;
   }

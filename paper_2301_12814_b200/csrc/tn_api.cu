@@ -26,10 +26,11 @@ tn_status fail(tn_status st, const std::string& s) {
 
 tn_status cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return TN_OK;
-  if (e == cudaErrorMemoryAllocation) {
-    cudaGetLastError();
-    return fail(TN_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
-  }
+  // the failure is reported through the returned status: take it out of the runtime's per-thread last-error
+  // slot, or the next launch check of ANY later call would report it again as its own (a sticky error keeps
+  // failing every later call regardless)
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) return fail(TN_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
   return fail(TN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
@@ -370,6 +371,9 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     st = cuda_check((expr), what);              \
     if (st != TN_OK) goto done;                 \
   } while (0)
+  // a non-sticky error left in this thread's last-error slot by an earlier, already reported failure must not be
+  // reported again by the launch checks below as if this plan's K1 had failed; a sticky one fails them anyway
+  cudaGetLastError();
   TN_TRY(cudaGetDevice(&dev), "cudaGetDevice");
   p->dev = dev;
   p->sm_count = sm_count_of(dev);
@@ -799,7 +803,8 @@ tn_status tn_plan_set_contraction(tn_plan* p, int mode, int slices) {
       return fail(TN_ERR_UNSUPPORTED, "tn_plan_set_contraction: a centre charge segment exceeds 2048 bonds (INT8 emulation)");
   // (re)build the slice layout: same groups (center charges) as the DMMA path
   if (p->blk_oz) {
-    cudaStreamSynchronize(p->last_stream);
+    // the previous layout's last use is fenced by ev_fence (the exec stream itself may no longer exist)
+    if (cudaEventSynchronize(p->ev_fence) != cudaSuccess) cudaGetLastError();
     pool_release(p->blk_oz, nullptr, false);
     p->blk_oz = nullptr;
   }

@@ -149,3 +149,16 @@ def test_reserve_covers_pipelined_plans(tn):
             assert np.array_equal(g.cpu().numpy(), r)
     with pytest.raises(tn.TnError, match="NULL"):
         tn.check(tn.lib.tn_plan_reserve(None, 2), "tn_plan_reserve")
+
+
+def test_failed_call_does_not_poison_the_next(tn):
+    # a CUDA-level failure (opening a garbage IPC handle) is reported by its own status and cleared from the
+    # runtime's last-error slot: the next plan / exec must not report it again as its own
+    import ctypes as C
+    junk = (C.c_char * 64).from_buffer_copy(bytes(range(64)))
+    ptr = C.c_void_p()
+    with pytest.raises(tn.TnError, match="CUDA"):
+        tn.check(tn.lib.tn_ipc_open(junk, C.byref(ptr)), "tn_ipc_open")
+    out = gpu_theta(synth.make_config(1))[2]
+    for g, r in zip(out, _alone(1)):
+        assert np.array_equal(g, r)
