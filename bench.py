@@ -669,6 +669,7 @@ def comm_model(tn, case, hq, R, per_ms, wall1_ms):
     off = [np.concatenate([[0], np.cumsum(c)]).astype(np.int32) for c in cnt]
     bounds = tn.shard_rows_host(case.d, N, cnt[0], cnt[1], cnt[2], R)        # the plan's own row shards
     sched = tn.gather_schedule_host(case.d, N, off[0], off[2], bounds, tn.TN_GATHER_SECTOR_OWNER)
+    sched_root = tn.gather_schedule_host(case.d, N, off[0], off[2], bounds, tn.TN_GATHER_ROOT)
     chi_c = int(len(hq[1]))
     rows = [(int(bounds[r]), int(bounds[r + 1])) for r in range(R)]
     sent, recv = [0] * R, [0] * R
@@ -683,17 +684,32 @@ def comm_model(tn, case, hq, R, per_ms, wall1_ms):
         b = t["rows"] * t["cols"] * 16
         gsent[t["src"]] += b
         grecv[t["dst"]] += b
+    rsent, rrecv = [0] * R, [0] * R
+    for t in sched_root:                        # Θ slabs: every rank → rank 0
+        if t["src"] == t["dst"]:
+            continue
+        b = t["rows"] * t["cols"] * 16
+        rsent[t["src"]] += b
+        rrecv[t["dst"]] += b
     ms = lambda b: b / (NVLINK_GBS * 1e9) * 1e3
     t_slab = [ms(max(a, b)) for a, b in zip(sent, recv)]
     t_gath = [ms(max(a, b)) for a, b in zip(gsent, grecv)]
+    t_root = [ms(max(a, b)) for a, b in zip(rsent, rrecv)]
+    # full Γk broadcast (TN_BCAST_FULL): every rank receives all of Γk (a pipelined broadcast costs ≈ one copy)
+    t_full = [ms(len(hq[0]) * chi_c * 16) if R > 1 else 0.0] * R
     out = {"kind": "model: library schedules' bytes at the nominal NVLink 5 rate (not measured)",
            "nvlink_gbs": NVLINK_GBS,
            "slab_scatter_mb_rank0_sent": round(sent[0] / 1e6, 1),
            "gather_owner_mb_max_sent": round(max(gsent) / 1e6, 1),
            "gather_owner_mb_max_recv": round(max(grecv) / 1e6, 1),
-           "t_slab_ms": [round(x, 4) for x in t_slab], "t_gather_ms": [round(x, 4) for x in t_gath]}
+           "gather_root_mb_recv": round(rrecv[0] / 1e6, 1),
+           "t_slab_ms": [round(x, 4) for x in t_slab], "t_gather_ms": [round(x, 4) for x in t_gath],
+           "t_root_gather_ms": round(max(t_root), 4), "t_full_bcast_ms": round(t_full[0], 4)}
     if wall1_ms > 0:
-        for name, extra in (("slabs", t_slab), ("slabs_and_owner_gather", [a + b for a, b in zip(t_slab, t_gath)])):
+        # SURVEY.md §8(e) reporting items 2–4: + operand distribution, + sector-owner gather, + root gather
+        for name, extra in (("slabs", t_slab), ("full_bcast", t_full),
+                            ("slabs_and_owner_gather", [a + b for a, b in zip(t_slab, t_gath)]),
+                            ("slabs_and_root_gather", [a + b for a, b in zip(t_slab, t_root)])):
             serial = max(c + e for c, e in zip(per_ms, extra))
             over = max(max(c, e) for c, e in zip(per_ms, extra))
             out[f"projected_speedup_{name}_serial"] = round(wall1_ms / serial, 3)

@@ -33,6 +33,10 @@ def test_comm_model_bytes(cfg, R):
     assert 0 < m["gather_owner_mb_max_sent"] * 1e6 <= theta_bytes
     # time model: bytes / nominal NVLink rate, and the speedups are ordered serial ≤ overlapped ≤ compute-only
     assert m["t_slab_ms"][0] == pytest.approx(m["slab_scatter_mb_rank0_sent"] * 1e6 / 900e9 * 1e3, rel=2e-3, abs=1e-4)
-    for name in ("slabs", "slabs_and_owner_gather"):
+    # the root gather pulls every other rank's slabs into rank 0: more than any owner
+    # receives, at most all of Θ, and never faster than the owner gather
+    assert m["gather_owner_mb_max_recv"] <= m["gather_root_mb_recv"] <= theta_bytes / 1e6 + 0.1
+    assert m["projected_speedup_slabs_and_root_gather_serial"] <= m["projected_speedup_slabs_and_owner_gather_serial"]
+    for name in ("slabs", "full_bcast", "slabs_and_owner_gather", "slabs_and_root_gather"):
         s, o = m[f"projected_speedup_{name}_serial"], m[f"projected_speedup_{name}_overlapped"]
         assert s <= o <= 4.0 / max(per) + 1e-9
