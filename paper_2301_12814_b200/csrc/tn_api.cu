@@ -152,12 +152,7 @@ static void free_plan(tn_plan* p) {
   sh.stream = p->plan_stream;
   for (int i = 0; i < 8; ++i) sh.ev[i] = p->ev[i];
   sh.ev_ready = p->ev_ready;
-  sh.ha = p->ha;
-  if (sh.ha && sh.ha->pending && cudaEventRecord(sh.ha->ev, p->plan_stream) != cudaSuccess) {
-    cudaGetLastError();
-    cudaStreamSynchronize(p->plan_stream);  // cannot fence the staged uploads: wait for them
-    sh.ha->pending = false;
-  }
+  plan_h2d_seal(p);   // a plan that failed mid-build may still hold unsealed ranges of the upload ring
   shell_release(sh);   // stream + timing events go back to the shell pool
   delete p;
 }
@@ -383,7 +378,6 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->plan_stream = sh.stream;
     for (int i = 0; i < 8; ++i) p->ev[i] = sh.ev[i];
     p->ev_ready = sh.ev_ready;
-    p->ha = sh.ha;
   }
   TN_TRY(cudaEventCreateWithFlags(&p->ev_fence, cudaEventDisableTiming), "event create");
   TN_PT(1);
@@ -523,6 +517,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->ws_bytes += (int64_t)ct.off;
     u_layout(p);
     if ((st = upload_sector_tables(p)) != TN_OK) goto done;
+    plan_h2d_seal(p);
     TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     TN_TRY(plan_touch(p, p->plan_stream), "plan fence");
   } else {
@@ -673,6 +668,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->ws_bytes += (int64_t)ct.off;
     u_layout(p);
     if ((st = upload_sector_tables(p)) != TN_OK) goto done;
+    plan_h2d_seal(p);
     TN_TRY(cudaEventRecord(p->ev_ready, p->plan_stream), "plan tables ready");
     TN_TRY(plan_touch(p, p->plan_stream), "plan fence");
     TN_PT(9);

@@ -115,7 +115,6 @@ struct SectorPtrs {         // k_set_sectors' by-value argument (≤ 16 KB of th
   int32_t n;
 };
 
-struct HostArena;
 }  // namespace tn
 
 struct tn_plan {
@@ -177,7 +176,7 @@ struct tn_plan {
   int max_mix = 0;                             // min(N+1, d): longest U-mix vector
   int sm_count = 148;
   cudaStream_t plan_stream = nullptr;
-  tn::HostArena* ha = nullptr;                 // the shell's pinned staging arena (plan_h2d)
+  int n_staged = 0;                            // ranges of the pinned upload ring not yet sealed (plan_h2d)
   void* blk_tab = nullptr;                     // pool block: perm / qs / off tables
   void* blk_work = nullptr;                    // pool block: group + tile tables, A/B panels
   // per-kernel timing events: [0,1] K1, [2,3] K2, [4] K3 start, [5] K4 start, [6] K5 start, [7] end
@@ -280,27 +279,18 @@ void pool_release_fenced(void* ptr, Fence* f);    // the block shares f (nullptr
 void fence_release(Fence* f);                     // drop a fence no block adopted
 // Plan shells: the plan's own stream and timing events are recycled between plans (stream creation costs
 // tens of µs per gate otherwise).
-// Pinned host staging for a plan's table uploads (one per shell): the tables go up with cudaMemcpyAsync from
-// pinned memory instead of pageable vectors, which costs the host a driver-side staging copy per call
-// (measured 14–65 µs per phase of tn_theta_plan). Bump-allocated per plan; `ev` is recorded on the plan
-// stream when the plan is destroyed, and the shell's next plan waits for it before reusing the arena. Too small → pageable fallback, and the
-// arena grows to `want` when the shell is next acquired.
-struct HostArena {
-  char* ptr = nullptr;
-  size_t cap = 0, off = 0, want = size_t(1) << 20;
-  cudaEvent_t ev = nullptr;
-  bool pending = false;
-};
 struct PlanShell {
   int dev = -1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_ready = nullptr;
-  HostArena* ha = nullptr;
 };
-// async H2D of a plan table on the plan stream, staged through the shell's pinned arena when it fits (the
-// arena's event is recorded on the plan stream when the plan is destroyed)
+// Async H2D of a plan table on the plan stream, staged through the process-wide pinned ring (tn_pool.cu) when it
+// fits: a pageable source costs the host a driver-side staging copy per call (measured 14–65 µs per phase of
+// tn_theta_plan). plan_h2d_seal records the event that releases the plan's staged ranges (called after the
+// plan's last upload, and again — harmlessly — when the plan is destroyed).
 cudaError_t plan_h2d(tn_plan* p, void* dst, const void* src, size_t bytes);
+void plan_h2d_seal(tn_plan* p);
 cudaError_t shell_acquire(PlanShell* out);
 void shell_release(const PlanShell& sh);
 // record the plan's pool fence at the current tail of s (after library work that touched the plan's memory)
