@@ -360,6 +360,7 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
   int32_t* d_err = nullptr;
   const int nmax_u = std::min(N, 2 * d - 2);
   size_t o_bin = 0, o_sec[2] = {0, 0}, o_ust = 0;
+  size_t up_bytes = 0;   // the leading, host-provided part of the table block (one upload)
   std::vector<double2> hbin((size_t)(nmax_u + 1) * (nmax_u + 1), double2{0.0, 0.0});
 #define TN_TRY(expr, what)                      \
   do {                                          \
@@ -382,21 +383,28 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
   TN_TRY(cudaEventCreateWithFlags(&p->ev_fence, cudaEventDisableTiming), "event create");
   TN_PT(1);
   // ---- one pool block for the bond tables (+ staging of host charges) ----
+  // layout: the host-provided part first — error flags (uploaded as zeros), binomials, host charges — so it goes
+  // up as ONE staged copy; then the device-built tables
   for (int b = 0; b < 3; ++b) {
-    o_perm[b] = ct.take<int32_t>(p->chi[b]);
-    o_qs[b] = ct.take<int32_t>(p->chi[b]);
-    o_off[b] = ct.take<int32_t>(p->nq + 1);
     host_q[b] = !is_device_ptr(qs_in[b]);
-    if (host_q[b]) o_q[b] = ct.take<int32_t>(p->chi[b]);
     all_host = all_host && host_q[b];
     if (q2) {
       host_q2[b] = !is_device_ptr(q2[b]);
-      if (host_q2[b]) o_q2[b] = ct.take<int32_t>(p->chi[b]);
       all_host = all_host && host_q2[b];
     }
   }
   o_err = ct.take<int32_t>(4);
   o_bin = ct.take<double2>((int64_t)(nmax_u + 1) * (nmax_u + 1));
+  for (int b = 0; b < 3; ++b) {
+    if (host_q[b]) o_q[b] = ct.take<int32_t>(p->chi[b]);
+    if (q2 && host_q2[b]) o_q2[b] = ct.take<int32_t>(p->chi[b]);
+  }
+  up_bytes = ct.off;
+  for (int b = 0; b < 3; ++b) {
+    o_perm[b] = ct.take<int32_t>(p->chi[b]);
+    o_qs[b] = ct.take<int32_t>(p->chi[b]);
+    o_off[b] = ct.take<int32_t>(p->nq + 1);
+  }
   o_sec[0] = ct.take<SecEntry>(p->nq);
   o_sec[1] = ct.take<SecEntry>(p->nq);
   o_ust = ct.take<int32_t>(nmax_u + 1);
@@ -424,18 +432,11 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       const int32_t* src = qs_in[b];
       if (host_q[b]) {
         d_q[b] = reinterpret_cast<int32_t*>(base + o_q[b]);
-        TN_TRY(plan_h2d(p, d_q[b], src, p->chi[b] * sizeof(int32_t)),
-               "H2D charges");
         src = d_q[b];
       }
       sa.q[b] = src;
       sa.q2[b] = q2 ? q2[b] : nullptr;
-      if (q2 && host_q2[b]) {
-        int32_t* dq2 = reinterpret_cast<int32_t*>(base + o_q2[b]);
-        TN_TRY(plan_h2d(p, dq2, q2[b], p->chi[b] * sizeof(int32_t)),
-               "H2D charges (second species)");
-        sa.q2[b] = dq2;
-      }
+      if (q2 && host_q2[b]) sa.q2[b] = reinterpret_cast<int32_t*>(base + o_q2[b]);
       sa.chi[b] = p->chi[b];
       sa.perm[b] = p->d_perm[b];
       sa.qs[b] = p->d_qs[b];
@@ -450,9 +451,18 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
     p->d_sec[0] = reinterpret_cast<SecEntry*>(base + o_sec[0]);
     p->d_sec[1] = reinterpret_cast<SecEntry*>(base + o_sec[1]);
     p->d_ustart = reinterpret_cast<int32_t*>(base + o_ust);
-    TN_TRY(plan_h2d(p, p->d_binom, hbin.data(), hbin.size() * sizeof(double2)), "H2D binomials");
+    {  // error flags (zero), binomials and host charges: one staged upload of the block's leading region
+      static const int32_t zeros[4] = {0, 0, 0, 0};
+      std::vector<H2DPart> parts;
+      parts.push_back(H2DPart{o_err, zeros, sizeof(zeros)});
+      parts.push_back(H2DPart{o_bin, hbin.data(), hbin.size() * sizeof(double2)});
+      for (int b = 0; b < 3; ++b) {
+        if (host_q[b]) parts.push_back(H2DPart{o_q[b], qs_in[b], (size_t)p->chi[b] * sizeof(int32_t)});
+        if (q2 && host_q2[b]) parts.push_back(H2DPart{o_q2[b], q2[b], (size_t)p->chi[b] * sizeof(int32_t)});
+      }
+      TN_TRY(plan_h2d_parts(p, base, parts.data(), (int)parts.size(), up_bytes), "H2D charges / binomials");
+    }
     // ---- K1: sort each bond by charge (one launch, one CTA per bond) ----
-    TN_TRY(cudaMemsetAsync(d_err, 0, 4 * sizeof(int32_t), p->plan_stream), "memset err");
     TN_TRY(cudaEventRecord(p->ev[0], p->plan_stream), "event");
     TN_TRY(launch_sort_bonds(sa, N, p->plan_stream), "K1 launch");
     TN_PT(4);
@@ -471,11 +481,25 @@ static tn_status plan_impl(int d, int N, int64_t chi_l, int64_t chi_c, int64_t c
       bool bad = false;
       int32_t* hist = o.data() + 1;
       if (!a2) {
-        for (int64_t i = 0; i < p->chi[b]; ++i) {
+        // four interleaved histograms: charge-sorted input hits one bin many times in a row, and a single
+        // histogram serialises those increments on store-to-load forwarding
+        std::vector<int32_t> h4(4 * (size_t)p->nq, 0);
+        const int64_t n = p->chi[b];
+        int64_t i = 0;
+        for (; i + 4 <= n; i += 4) {
+          uint32_t x[4];
+          for (int u = 0; u < 4; ++u) {
+            x[u] = (uint32_t)a[i + u];
+            bad |= x[u] > (uint32_t)N;
+          }
+          for (int u = 0; u < 4; ++u) h4[u * (size_t)p->nq + (x[u] > (uint32_t)N ? 0 : x[u])]++;
+        }
+        for (; i < n; ++i) {
           const uint32_t x = (uint32_t)a[i];
           bad |= x > (uint32_t)N;
-          hist[x > (uint32_t)N ? 0 : x]++;
+          h4[x > (uint32_t)N ? 0 : x]++;
         }
+        for (int k = 0; k < p->nq; ++k) hist[k] = h4[k] + h4[p->nq + k] + h4[2 * p->nq + k] + h4[3 * p->nq + k];
       } else {
         for (int64_t i = 0; i < p->chi[b]; ++i) {
           const uint32_t x = (uint32_t)a[i], y = (uint32_t)a2[i];

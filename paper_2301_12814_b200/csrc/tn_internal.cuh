@@ -290,6 +290,14 @@ struct PlanShell {
 // tn_theta_plan). plan_h2d_seal records the event that releases the plan's staged ranges (called after the
 // plan's last upload, and again — harmlessly — when the plan is destroyed).
 cudaError_t plan_h2d(tn_plan* p, void* dst, const void* src, size_t bytes);
+// several host arrays into one device region [dst_base, dst_base + total): one staged copy (gaps undefined), or
+// one pageable copy per part when the ring cannot take it
+struct H2DPart {
+  size_t off;
+  const void* src;
+  size_t bytes;
+};
+cudaError_t plan_h2d_parts(tn_plan* p, char* dst_base, const H2DPart* parts, int n, size_t total);
 void plan_h2d_seal(tn_plan* p);
 cudaError_t shell_acquire(PlanShell* out);
 void shell_release(const PlanShell& sh);

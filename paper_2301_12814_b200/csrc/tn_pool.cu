@@ -378,6 +378,30 @@ cudaError_t plan_h2d(tn_plan* p, void* dst, const void* src, size_t bytes) {
   return cudaMemcpyAsync(dst, from, bytes, cudaMemcpyHostToDevice, p->plan_stream);
 }
 
+cudaError_t plan_h2d_parts(tn_plan* p, char* dst_base, const H2DPart* parts, int n, size_t total) {
+  static const bool pageable = getenv("TN_PAGEABLE_UPLOADS") != nullptr;
+  if (!pageable && total > 0) {
+    char* slot = nullptr;
+    {
+      PinnedRing& r = ring();
+      std::lock_guard<std::mutex> lk(r.mu);
+      slot = ring_alloc(r, total, p);
+      if (slot) {
+        for (int i = 0; i < n; ++i) std::memcpy(slot + parts[i].off, parts[i].src, parts[i].bytes);
+        ++p->n_staged;
+      }
+    }
+    if (slot) return cudaMemcpyAsync(dst_base, slot, total, cudaMemcpyHostToDevice, p->plan_stream);
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!parts[i].bytes) continue;
+    const cudaError_t e = cudaMemcpyAsync(dst_base + parts[i].off, parts[i].src, parts[i].bytes,
+                                          cudaMemcpyHostToDevice, p->plan_stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 void plan_h2d_seal(tn_plan* p) {
   if (p->n_staged == 0) return;
   PinnedRing& r = ring();
