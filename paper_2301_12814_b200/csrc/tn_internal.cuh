@@ -162,6 +162,8 @@ struct tn_plan {
   int64_t nmix2[2] = {0, 0};                   // tiles of pass 1 (species 1) and pass 2 (species 2)
   int nfix_max = 1;                            // most values of the other species one K5P tile covers
   int64_t nmix2_multi[2] = {0, 0};             // of each pass's tiles, the trailing ones covering > 1 value
+  // tiles per (pass, single/multi-value, register class L ≤ 8 / ≤ 16 / ≤ 32 / larger), in that order in d_mix2
+  int64_t nmix2_grp[2][2][4] = {};
   std::vector<tn::MixTile2> h_mix2;
   std::vector<int32_t> h_rowoff, h_coloff;
   std::vector<int32_t> h_rowperm_pos, h_colperm_pos;

@@ -13,6 +13,12 @@
 // are the sorted left positions with l − c ∈ [0, d−1]² — a union of whole pair segments, in sorted order —
 // and its columns likewise. P_m has exactly Θ(m)'s shape, so K4 writes it straight into Θ(m) as before;
 // the group's rows/columns are gathered through per-group position lists (d_rowperm / d_colperm).
+#include <chrono>
+#include <numeric>
+#include <type_traits>
+#include <cstdio>
+#include <cstdlib>
+
 #include "k5_mix.cuh"
 
 namespace tn {
@@ -36,6 +42,15 @@ struct Carve {  // bump allocator over one pool block (256-byte aligned pieces)
 }  // namespace
 
 tn_status build_pair_tables(tn_plan* p) {
+  // TN_PLAN_PROFILE=1: host µs per phase on stderr
+  static const bool prof = getenv("TN_PLAN_PROFILE") != nullptr;
+  double pt[10] = {};
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+#define PP(i) \
+  if (prof) pt[i] = now_us()
+  PP(0);
   const int N = p->N, d = p->d, nk = N + 1, nq = p->nq;
   const auto& ol = p->off[0];
   const auto& oc = p->off[1];
@@ -62,6 +77,18 @@ tn_status build_pair_tables(tn_plan* p) {
              P2[(size_t)(a1 + 1) * (nk + 1) + b0] + P2[(size_t)a0 * (nk + 1) + b0];
     return x;
   };
+  // the non-empty left / right pair keys with their charges: the O(keys²) loops below visit only these (no
+  // divisions by N+1 in them)
+  struct Key {
+    int k, k1, k2;
+    int64_t n;
+  };
+  std::vector<Key> lkeys, rkeys;
+  for (int k = 0; k < nq; ++k) {
+    if (cnt(ol, k)) lkeys.push_back(Key{k, k / nk, k % nk, cnt(ol, k)});
+    if (cnt(orr, k)) rkeys.push_back(Key{k, k / nk, k % nk, cnt(orr, k)});
+  }
+  PP(1);
   // ---- sector layouts: local row / column offset of every pair segment inside every sector ----
   std::vector<int32_t>& rowoff = p->h_rowoff;
   std::vector<int32_t>& coloff = p->h_coloff;
@@ -73,18 +100,27 @@ tn_status build_pair_tables(tn_plan* p) {
   p->col0.assign(nq, 0);
   p->lR.assign(nq, 0);
   p->lrow0.assign(nq, 0);
+  PP(2);
   // ---- flop-balanced row shards over sorted left positions (per-pair row cost: contraction + mix) ----
+  // per left key: Σ_r n_r·(centre count) and Σ_r n_r·(mix MACs) — the row cost, and (× rows) the flop counts below
+  std::vector<int64_t> lmc(nq, 0), lmx(nq, 0);
   {
     std::vector<double> cost(nq, 0.0);
-    for (int l = 0; l < nq; ++l) {
-      if (!cnt(ol, l)) continue;
-      for (int r = 0; r < nq; ++r) {
-        const int64_t nr = cnt(orr, r);
-        if (!nr) continue;
-        const Blk b = blk(l, r);
-        const double L1 = (double)b.L1, L2 = (double)b.L2;
-        cost[l] += (double)nr * ((double)b.mc + L1 * L1 * L2 + L1 * L2 * L2);
+    for (const Key& L : lkeys) {
+      int64_t smc = 0, smx = 0;
+      for (const Key& R : rkeys) {
+        const int a0 = std::max(R.k1, L.k1 - d + 1), a1 = std::min(L.k1, R.k1 + d - 1);
+        const int b0 = std::max(R.k2, L.k2 - d + 1), b1 = std::min(L.k2, R.k2 + d - 1);
+        if (a1 < a0 || b1 < b0) continue;
+        const int64_t L1 = a1 - a0 + 1, L2 = b1 - b0 + 1;
+        const int64_t mc = P2[(size_t)(a1 + 1) * (nk + 1) + b1 + 1] - P2[(size_t)a0 * (nk + 1) + b1 + 1] -
+                           P2[(size_t)(a1 + 1) * (nk + 1) + b0] + P2[(size_t)a0 * (nk + 1) + b0];
+        smc += R.n * mc;
+        smx += R.n * (L1 * L1 * L2 + L1 * L2 * L2);
       }
+      lmc[L.k] = smc;
+      lmx[L.k] = smx;
+      cost[L.k] = (double)smc + (double)smx;
     }
     double total = 0.0;
     for (int l = 0; l < nq; ++l) total += cost[l] * (double)cnt(ol, l);
@@ -140,24 +176,18 @@ tn_status build_pair_tables(tn_plan* p) {
       p->lrow0[s] = rl ? a_s : 0;  // pair plans: slab start as a row index of Θ(s) (row0 = 0)
       p->C[s] = c;
     }
-  // ---- useful work (oracle.flop_counts2 definitions) ----
+  PP(3);
+  // ---- useful work (oracle.flop_counts2 definitions), from the per-left-key sums above ----
   p->f_contract = p->f_mix = 0;
   p->f_contract_local = p->f_mix_local = 0;
-  for (int l = 0; l < nq; ++l) {
-    const int64_t nl = cnt(ol, l), nll = in_shard(l).second;
-    if (!nl) continue;
-    for (int r = 0; r < nq; ++r) {
-      const int64_t nr = cnt(orr, r);
-      if (!nr) continue;
-      const Blk b = blk(l, r);
-      if (!b.L1 || !b.L2) continue;
-      const int64_t fmix = b.L1 * b.L1 * b.L2 + b.L1 * b.L2 * b.L2;
-      p->f_contract += 8 * nl * b.mc * nr;
-      p->f_mix += 8 * nl * nr * fmix;
-      p->f_contract_local += 8 * nll * b.mc * nr;
-      p->f_mix_local += 8 * nll * nr * fmix;
-    }
+  for (const Key& L : lkeys) {
+    const int64_t nll = in_shard(L.k).second;
+    p->f_contract += 8 * L.n * lmc[L.k];
+    p->f_mix += 8 * L.n * lmx[L.k];
+    p->f_contract_local += 8 * nll * lmc[L.k];
+    p->f_mix_local += 8 * nll * lmx[L.k];
   }
+  PP(4);
   // ---- groups: one per non-empty centre pair; rows / cols = those of Θ(m), gathered by position ----
   std::vector<int32_t>& rpos = p->h_rowperm_pos;
   std::vector<int32_t>& cpos = p->h_colperm_pos;
@@ -173,15 +203,27 @@ tn_status build_pair_tables(tn_plan* p) {
     GroupDesc g{};
     g.cc = m;
     g.row0 = (int64_t)rpos.size();
-    for (int l1 = m1; l1 <= std::min(N, m1 + d - 1); ++l1)
-      for (int l2 = m2; l2 <= std::min(N, m2 + d - 1); ++l2)
-        for (int32_t q = (int32_t)in_shard(l1 * nk + l2).first,
-                     qe = (int32_t)(in_shard(l1 * nk + l2).first + in_shard(l1 * nk + l2).second); q < qe; ++q)
-          rpos.push_back(q);
+    rpos.resize(rpos.size() + (size_t)p->lR[m]);   // whole runs of consecutive positions: fill, no push_back
+    {
+      int32_t* w = rpos.data() + g.row0;
+      for (int l1 = m1; l1 <= std::min(N, m1 + d - 1); ++l1)
+        for (int l2 = m2; l2 <= std::min(N, m2 + d - 1); ++l2) {
+          const auto sh = in_shard(l1 * nk + l2);
+          std::iota(w, w + sh.second, (int32_t)sh.first);
+          w += sh.second;
+        }
+    }
     g.col0 = (int64_t)cpos.size();
-    for (int r1 = std::max(0, m1 - d + 1); r1 <= m1; ++r1)
-      for (int r2 = std::max(0, m2 - d + 1); r2 <= m2; ++r2)
-        for (int32_t q = orr[r1 * nk + r2]; q < orr[r1 * nk + r2 + 1]; ++q) cpos.push_back(q);
+    cpos.resize(cpos.size() + (size_t)p->C[m]);
+    {
+      int32_t* w = cpos.data() + g.col0;
+      for (int r1 = std::max(0, m1 - d + 1); r1 <= m1; ++r1)
+        for (int r2 = std::max(0, m2 - d + 1); r2 <= m2; ++r2) {
+          const int rk = r1 * nk + r2;
+          std::iota(w, w + cnt(orr, rk), orr[rk]);
+          w += cnt(orr, rk);
+        }
+    }
     g.k0 = oc[m];
     g.R = (int32_t)p->lR[m];
     g.C = (int32_t)p->C[m];
@@ -207,25 +249,34 @@ tn_status build_pair_tables(tn_plan* p) {
     for (int mt = 0; mt < p->groups[gi].nmt; ++mt)
       for (int nt = 0; nt < p->groups[gi].nnt; ++nt) tiles.push_back(TileDesc{gi, mt, nt, 0});
   p->ntiles = (int64_t)tiles.size();
+  PP(5);
   // ---- two-pass mix tiles: rows of one left pair segment (≈ 128 8-groups) × one right pair segment ----
+  // Within a pass: single-value tiles first, then the multi-value ones (launched with the MULTI kernel, whose
+  // extra index arithmetic the common single-value tiles do not pay); inside each, by register class of L (one
+  // launch per class: a kernel sized for the largest L of the plan held every tile at its register count — the
+  // K5 register classes of the single-charge path). Two walks — count per bucket, then write each
+  // tile straight into its bucket — keep this loop (≈ 10⁵ tiles at pair config 5, on the per-gate plan's path)
+  // free of reallocation, sorting and copies.
   std::vector<MixTile2>& mix = p->h_mix2;
   mix.clear();
   p->nfix_max = 1;
   int max_l = 1;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int l = 0; l < nq; ++l) {
-      const int64_t nl = in_shard(l).second, lfirst = in_shard(l).first;
+  auto cls = [](int L) { return L <= 8 ? 0 : L <= 16 ? 1 : L <= 32 ? 2 : 3; };
+  // count == true: whole (left key, right key) blocks are counted in O(1) (every tile of a block has the same L; only
+  // the last value group of a block can cover fewer values), emit(bucket, n, ·) adds n tiles
+  auto walk = [&](int pass, bool count, auto&& emit) {
+    for (const Key& Lk : lkeys) {
+      const auto sh = in_shard(Lk.k);
+      const int64_t nl = sh.second, lfirst = sh.first;
       if (!nl) continue;
-      const int l1 = l / nk, l2 = l % nk;
-      for (int r = 0; r < nq; ++r) {
-        const int64_t nr = cnt(orr, r);
-        if (!nr) continue;
-        const int r1 = r / nk, r2 = r % nk;
+      const int l1 = Lk.k1, l2 = Lk.k2;
+      for (const Key& Rk : rkeys) {
+        const int64_t nr = Rk.n;
+        const int r1 = Rk.k1, r2 = Rk.k2;
         const int lo1 = std::max(r1, l1 - d + 1), hi1 = std::min(l1, r1 + d - 1);
         const int lo2 = std::max(r2, l2 - d + 1), hi2 = std::min(l2, r2 + d - 1);
         if (hi1 < lo1 || hi2 < lo2) continue;
         const int L = pass == 0 ? hi1 - lo1 + 1 : hi2 - lo2 + 1;
-        max_l = std::max(max_l, L);
         const int64_t ngr = (nr + 7) / 8;
         const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
         const int fixed_lo = pass == 0 ? lo2 : lo1, fixed_hi = pass == 0 ? hi2 : hi1;
@@ -233,42 +284,64 @@ tn_status build_pair_tables(tn_plan* p) {
         const int64_t per_val = std::min<int64_t>(rows_per, nl) * ngr;
         const int nfix = (int)std::max<int64_t>(1, std::min<int64_t>(fixed_hi - fixed_lo + 1,
                                                                       MIX_GROUPS_PER_TILE / std::max<int64_t>(1, per_val)));
+        max_l = std::max(max_l, L);
+        p->nfix_max = std::max(p->nfix_max, nfix);
+        if (count) {
+          const int span = fixed_hi - fixed_lo + 1, ngrp = (span + nfix - 1) / nfix, nf_last = span - (ngrp - 1) * nfix;
+          const int64_t bands = (nl + rows_per - 1) / rows_per;
+          emit((nfix == 1 ? 0 : 4) + cls(L), (int64_t)(ngrp - 1) * bands, nullptr);
+          emit((nf_last == 1 ? 0 : 4) + cls(L), bands, nullptr);
+          continue;
+        }
         for (int f = fixed_lo; f <= fixed_hi; f += nfix)
           for (int64_t band = 0; band < nl; band += rows_per) {
-            const int64_t rows = std::min<int64_t>(rows_per, nl - band);
-            MixTile2 t{};
-            t.cl = pass == 0 ? l1 : l2;
-            t.n = pass == 0 ? l1 - r1 : l2 - r2;
-            t.lo = pass == 0 ? lo1 : lo2;
-            t.L = L;
-            t.e0 = 0;
-            t.ne = (int32_t)(rows * ngr);
-            t.nr = (int32_t)nr;
-            t.ngr = (int32_t)ngr;
-            t.pl0 = (int32_t)(lfirst + band);
-            t.pr0 = orr[r];
-            t.lkey = l;
-            t.rkey = r;
-            t.fixed = f;
-            t.nfix = std::min(nfix, fixed_hi - f + 1);
-            p->nfix_max = std::max(p->nfix_max, t.nfix);
-            t.band = (int32_t)band;
-            t.flags = pass;
-            mix.push_back(t);
+            const int nf = std::min(nfix, fixed_hi - f + 1);
+            const int bucket = (nf == 1 ? 0 : 4) + cls(L);
+            emit(bucket, 1, [&](MixTile2& t) {
+              const int64_t rows = std::min<int64_t>(rows_per, nl - band);
+              t = MixTile2{};
+              t.cl = pass == 0 ? l1 : l2;
+              t.n = pass == 0 ? l1 - r1 : l2 - r2;
+              t.lo = pass == 0 ? lo1 : lo2;
+              t.L = L;
+              t.e0 = 0;
+              t.ne = (int32_t)(rows * ngr);
+              t.nr = (int32_t)nr;
+              t.ngr = (int32_t)ngr;
+              t.pl0 = (int32_t)(lfirst + band);
+              t.pr0 = orr[Rk.k];
+              t.lkey = Lk.k;
+              t.rkey = Rk.k;
+              t.fixed = f;
+              t.nfix = nf;
+              t.band = (int32_t)band;
+              t.flags = pass;
+            });
           }
       }
     }
-    // within the pass: single-value tiles first, then the multi-value ones (launched with the MULTI kernel, whose
-    // extra index arithmetic the common single-value tiles do not pay)
-    {
-      const size_t b0 = pass ? (size_t)p->nmix2[0] : 0;
-      auto mid = std::stable_partition(mix.begin() + b0, mix.end(), [](const MixTile2& t) { return t.nfix == 1; });
-      p->nmix2_multi[pass] = (int64_t)(mix.end() - mid);
+  };
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t cntb[8] = {};
+    walk(pass, true, [&](int bucket, int64_t n, auto&&) { cntb[bucket] += n; });
+    int64_t tot = 0, at[8];
+    for (int g = 0; g < 8; ++g) {
+      at[g] = tot;
+      tot += cntb[g];
     }
-    p->nmix2[pass] = (int64_t)mix.size() - (pass ? p->nmix2[0] : 0);
+    const size_t b0 = mix.size();
+    mix.resize(b0 + (size_t)tot);
+    MixTile2* o = mix.data() + b0;
+    walk(pass, false, [&](int bucket, int64_t, auto&& fill) {
+      if constexpr (!std::is_same_v<std::decay_t<decltype(fill)>, std::nullptr_t>) fill(o[at[bucket]++]);
+    });
+    for (int g = 0; g < 8; ++g) p->nmix2_grp[pass][g >> 2][g & 3] = cntb[g];
+    p->nmix2_multi[pass] = cntb[4] + cntb[5] + cntb[6] + cntb[7];
+    p->nmix2[pass] = tot;
   }
   p->max_mix = max_l;
   p->nmix = 0;
+  PP(6);
   // ---- device tables ----
   Carve cw;
   const size_t o_g = cw.take<GroupDesc>((int64_t)p->groups.size());
@@ -321,6 +394,12 @@ tn_status build_pair_tables(tn_plan* p) {
   if (!cpos.empty())
     k_gather_idx<<<(unsigned)std::min<int64_t>(1024, ((int64_t)cpos.size() + 255) / 256), 256, 0, p->plan_stream>>>(
         d_cg, p->d_perm[2], d_cpos, (int64_t)cpos.size());
+  PP(7);
+  if (prof)
+    fprintf(stderr, "[plan2] us: P2 %.1f layouts %.1f shards %.1f flops %.1f groups+tiles %.1f mix %.1f (%zu tiles) "
+            "tables+uploads %.1f\n", pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4],
+            pt[6] - pt[5], p->h_mix2.size(), pt[7] - pt[6]);
+#undef PP
   return cuda_check(cudaGetLastError(), "pair gather launch");
 }
 
@@ -328,7 +407,7 @@ tn_status build_pair_tables(tn_plan* p) {
 constexpr int K5P_THREADS = 128;
 
 template <int NTMAX, bool MULTI>
-__global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
+__global__ void __launch_bounds__(K5P_THREADS, (NTMAX == 1 ? 8 : NTMAX == 2 ? 7 : NTMAX <= 4 ? 4 : 2))
     k5p_mix(const SectorParams sp, const MixTile2* __restrict__ tiles, const int32_t* __restrict__ rowoff,
             const int32_t* __restrict__ coloff, int nq, const int32_t* __restrict__ perm_l,
             const int32_t* __restrict__ perm_r, const double* __restrict__ ll, const double* __restrict__ lr,
@@ -404,43 +483,50 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX <= 4 ? 4 : 2))
 cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp1, const double* ll, const double* lr,
                             const double2* U, cudaStream_t s, const SectorParams* sp2_in) {
   const SectorParams& sp2 = sp2_in ? *sp2_in : sp1;   // pass 2 may read one set of buffers and write another
-  const int L = p->max_mix;
-  const int NT = (L + 7) >> 3;
-  const int smax = mix_us_elems(L);
+  const int Lmax = p->max_mix;
+  const int Lc[4] = {std::min(Lmax, 8), std::min(Lmax, 16), std::min(Lmax, 32), Lmax};
   for (int pass = 0; pass < 2; ++pass) {
-    const int64_t n = p->nmix2[pass], nm = p->nmix2_multi[pass], n1 = n - nm;
-    if (n == 0) continue;
+    if (p->nmix2[pass] == 0) continue;
     const MixTile2* tiles = p->d_mix2 + (pass ? p->nmix2[0] : 0);
     const SectorParams& sp = pass ? sp2 : sp1;
-#define TN_P_LAUNCH(M, MULTI, CNT, TILES, NFIX)                                                               \
+    for (int multi = 0; multi < 2; ++multi)
+      for (int c = 0; c < 4; ++c) {
+        const int64_t cnt = p->nmix2_grp[pass][multi][c];
+        if (cnt == 0) {
+          continue;
+        }
+        const int L = Lc[c], NT = (L + 7) >> 3, smax = mix_us_elems(L), nfix = multi ? p->nfix_max : 1;
+#define TN_P_LAUNCH(M, MULTI)                                                                                 \
   do {                                                                                                        \
-    const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * (size_t)(NFIX) * sizeof(SecRef); \
+    const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * (size_t)nfix * sizeof(SecRef); \
     if (smem > 48 * 1024) {                                                                                   \
       cudaError_t e = cudaFuncSetAttribute(k5p_mix<M, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                                         \
     }                                                                                                         \
-    k5p_mix<M, MULTI><<<(unsigned)(CNT), K5P_THREADS, smem, s>>>(sp, TILES, p->d_rowoff, p->d_coloff, p->nq,     \
-                                                                  p->d_perm[0], p->d_perm[2], ll, lr, U, smax, NFIX); \
+    k5p_mix<M, MULTI><<<(unsigned)cnt, K5P_THREADS, smem, s>>>(sp, tiles, p->d_rowoff, p->d_coloff, p->nq,       \
+                                                               p->d_perm[0], p->d_perm[2], ll, lr, U, smax, nfix); \
   } while (0)
-#define TN_P_BOTH(M)                                                                                          \
-  do {                                                                                                        \
-    if (n1 > 0) TN_P_LAUNCH(M, false, n1, tiles, 1);                                                         \
-    if (nm > 0) TN_P_LAUNCH(M, true, nm, tiles + n1, p->nfix_max);                                           \
+#define TN_P_CLASS(M)                    \
+  do {                                   \
+    if (multi) TN_P_LAUNCH(M, true);     \
+    else TN_P_LAUNCH(M, false);          \
   } while (0)
-    if (NT <= 1)
-      TN_P_BOTH(1);
-    else if (NT <= 2)
-      TN_P_BOTH(2);
-    else if (NT <= 4)
-      TN_P_BOTH(4);
-    else if (NT <= 6)
-      TN_P_BOTH(6);
-    else
-      TN_P_BOTH(8);
-#undef TN_P_BOTH
+        if (NT <= 1)
+          TN_P_CLASS(1);
+        else if (NT <= 2)
+          TN_P_CLASS(2);
+        else if (NT <= 4)
+          TN_P_CLASS(4);
+        else if (NT <= 6)
+          TN_P_CLASS(6);
+        else
+          TN_P_CLASS(8);
+#undef TN_P_CLASS
 #undef TN_P_LAUNCH
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+        tiles += cnt;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
   }
   return cudaSuccess;
 }
