@@ -933,6 +933,7 @@ tn_status tn_plan_exec_launches(const tn_plan* p, int64_t* n_launches) {
       for (int ps = 0; ps < 2; ++ps)                                          // K5P, two passes × (single / multi-value tiles) × register class
         for (int m = 0; m < 2; ++m)
           for (int c = 0; c < 4; ++c) n += p->nmix2_grp[ps][m][c] > 0;                // one launch per class
+      n += p->nmix_fused > 0;                                                          // K5F (short-vector blocks)
     } else {
       const int64_t c0 = p->nmix_cls[0], c1 = p->nmix_cls[1], c2 = p->nmix_cls[2], c3 = p->nmix - c0 - c1 - c2;
       n += (c0 > 0) + (c1 > 0) + (c2 > 0) + (c3 > 0);                        // K5, one launch per L class

@@ -164,6 +164,7 @@ struct tn_plan {
   int64_t nmix2_multi[2] = {0, 0};             // of each pass's tiles, the trailing ones covering > 1 value
   // tiles per (pass, single/multi-value, register class L ≤ 8 / ≤ 16 / ≤ 32 / larger), in that order in d_mix2
   int64_t nmix2_grp[2][2][4] = {};
+  int64_t nmix_fused = 0;                      // K5F tiles (blocks with L1, L2 ≤ 8: both species in one pass), first in d_mix2
   std::vector<tn::MixTile2> h_mix2;
   std::vector<int32_t> h_rowoff, h_coloff;
   std::vector<int32_t> h_rowperm_pos, h_colperm_pos;

@@ -264,6 +264,10 @@ tn_status build_pair_tables(tn_plan* p) {
   auto cls = [](int L) { return L <= 8 ? 0 : L <= 16 ? 1 : L <= 32 ? 2 : 3; };
   // count == true: whole (left key, right key) blocks are counted in O(1) (every tile of a block has the same L; only
   // the last value group of a block can cover fewer values), emit(bucket, n, ·) adds n tiles
+  static const bool two_pass = getenv("TN_PAIR_TWO_PASS") != nullptr;
+  constexpr int FUSE_MAXL = 8;
+  const bool fuse = !two_pass;
+  auto fused_block = [&](int L1, int L2) { return fuse && L1 <= FUSE_MAXL && L2 <= FUSE_MAXL; };
   auto walk = [&](int pass, bool count, auto&& emit) {
     for (const Key& Lk : lkeys) {
       const auto sh = in_shard(Lk.k);
@@ -276,6 +280,7 @@ tn_status build_pair_tables(tn_plan* p) {
         const int lo1 = std::max(r1, l1 - d + 1), hi1 = std::min(l1, r1 + d - 1);
         const int lo2 = std::max(r2, l2 - d + 1), hi2 = std::min(l2, r2 + d - 1);
         if (hi1 < lo1 || hi2 < lo2) continue;
+        if (fused_block(hi1 - lo1 + 1, hi2 - lo2 + 1)) continue;   // K5F mixes this block
         const int L = pass == 0 ? hi1 - lo1 + 1 : hi2 - lo2 + 1;
         const int64_t ngr = (nr + 7) / 8;
         const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
@@ -321,6 +326,66 @@ tn_status build_pair_tables(tn_plan* p) {
       }
     }
   };
+  // Blocks whose both species' vectors are short (L1, L2 ≤ 8) are mixed by K5F in one pass (Θ read and written once);
+  // longer ones keep the two passes, which run on the tensor pipe (measured: K5F with L up to 18 held one CTA per
+  // SM at 130–200 registers and lost to the two passes: pair config 5 4.68 vs 3.18 ms; at L ≤ 8 it wins, pair
+  // config 3 0.51 vs 0.80 ms). TN_PAIR_TWO_PASS=1 sends every block through the two passes.
+  p->nmix_fused = 0;
+  {
+    // K5F tiles: one per (left key, right key) block and band of ≈ 128 8-groups; both species mixed in one pass.
+    // MixTile2 fields: (cl, n, lo, L) of species 1; fixed = lo2, nfix = L2 of species 2; bucket = class of max(L1, L2)
+    auto walkf = [&](bool count, auto&& emit) {
+      for (const Key& Lk : lkeys) {
+        const auto sh = in_shard(Lk.k);
+        const int64_t nl = sh.second, lfirst = sh.first;
+        if (!nl) continue;
+        for (const Key& Rk : rkeys) {
+          const int lo1 = std::max(Rk.k1, Lk.k1 - d + 1), hi1 = std::min(Lk.k1, Rk.k1 + d - 1);
+          const int lo2 = std::max(Rk.k2, Lk.k2 - d + 1), hi2 = std::min(Lk.k2, Rk.k2 + d - 1);
+          if (hi1 < lo1 || hi2 < lo2) continue;
+          const int L1 = hi1 - lo1 + 1, L2 = hi2 - lo2 + 1, c = 0;
+          if (!fused_block(L1, L2)) continue;
+          max_l = std::max(max_l, std::max(L1, L2));
+          const int64_t ngr = (Rk.n + 7) / 8;
+          const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
+          if (count) {
+            emit(c, (nl + rows_per - 1) / rows_per, nullptr);
+            continue;
+          }
+          for (int64_t band = 0; band < nl; band += rows_per)
+            emit(c, 1, [&](MixTile2& t) {
+              const int64_t rows = std::min<int64_t>(rows_per, nl - band);
+              t = MixTile2{};
+              t.cl = Lk.k1;
+              t.n = Lk.k1 - Rk.k1;
+              t.lo = lo1;
+              t.L = L1;
+              t.e0 = 0;
+              t.ne = (int32_t)(rows * ngr);
+              t.nr = (int32_t)Rk.n;
+              t.ngr = (int32_t)ngr;
+              t.pl0 = (int32_t)(lfirst + band);
+              t.pr0 = orr[Rk.k];
+              t.lkey = Lk.k;
+              t.rkey = Rk.k;
+              t.fixed = lo2;
+              t.nfix = L2;
+              t.band = (int32_t)band;
+              t.flags = 2;
+            });
+        }
+      }
+    };
+    int64_t tot = 0;
+    walkf(true, [&](int, int64_t n, auto&&) { tot += n; });
+    mix.resize((size_t)tot);
+    MixTile2* o = mix.data();
+    int64_t at = 0;
+    walkf(false, [&](int, int64_t, auto&& fill) {
+      if constexpr (!std::is_same_v<std::decay_t<decltype(fill)>, std::nullptr_t>) fill(o[at++]);
+    });
+    p->nmix_fused = tot;
+  }
   for (int pass = 0; pass < 2; ++pass) {
     int64_t cntb[8] = {};
     walk(pass, true, [&](int bucket, int64_t n, auto&&) { cntb[bucket] += n; });
@@ -480,14 +545,166 @@ __global__ void __launch_bounds__(K5P_THREADS, (NTMAX == 1 ? 8 : NTMAX == 2 ? 7 
   }
 }
 
+// ---- K5F: both species' mix of one pair tile in ONE pass (DESIGN.md §4 "Pair plans") ----
+// For every element (α, β) of the tile's (l, r) block the L1 × L2 values X[i][j] = P(lo1+i, lo2+j)[α, β] become
+// Θ(lo1+t, lo2+u)[α, β] = λlλr Σ_{i,j} U_{n1}[l1−lo1−t][l1−lo1−i] · conj(U_{n2}[l2−lo2−u][l2−lo2−j]) · X[i][j], i.e.
+// Y = U1·X·U2ᴴ: the CTA stages a chunk of E elements' X blocks in shared memory (coalesced 128-byte runs per
+// sector), applies U1 down the columns (one thread per (j, e), L1 values in registers) and U2* along the rows (one
+// thread per (t, e)), and stores Y straight from registers. Θ is read once and written once — the two-pass K5P
+// moved it twice (pass 1 and pass 2 each read and wrote every element).
+constexpr int K5F_THREADS = 256;
+constexpr int K5F_X_BYTES = 64 * 1024;   // X chunk budget (E = 8·G elements per chunk, G 8-groups; two CTAs per SM)
+
+template <int LMAX>
+__global__ void __launch_bounds__(K5F_THREADS, 2)
+    k5f_mix(const SectorParams sp_ld, const SectorParams sp_st, const MixTile2* __restrict__ tiles,
+            const int32_t* __restrict__ rowoff, const int32_t* __restrict__ coloff, int nq,
+            const int32_t* __restrict__ perm_l, const int32_t* __restrict__ perm_r, const double* __restrict__ ll,
+            const double* __restrict__ lr, const double2* __restrict__ U) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  double2* U1s = reinterpret_cast<double2*>(smem_raw);                 // [LMAX][LMAX]
+  double2* U2s = U1s + LMAX * LMAX;                                    // conj, [u][j]
+  uint8_t* tab = reinterpret_cast<uint8_t*>(U2s + LMAX * LMAX);
+  const double2** ldp = reinterpret_cast<const double2**>(tab);                          // [L1·L2] load base (nullptr: P = 0)
+  double2** stp = reinterpret_cast<double2**>(tab + LMAX * LMAX * sizeof(void*));         // [L1·L2] store base
+  int64_t* ldv = reinterpret_cast<int64_t*>(tab + 2 * LMAX * LMAX * sizeof(void*));      // [L1·L2] load row stride
+  int64_t* stv = ldv + LMAX * LMAX;                                              // [L1·L2] store row stride
+  double2* X = reinterpret_cast<double2*>(stv + LMAX * LMAX);                    // [L1·L2][E]
+  const MixTile2 t = tiles[blockIdx.x];
+  const int nk = sp_ld.N + 1, d = sp_ld.d;
+  const int L1 = t.L, lo1 = t.lo, L2 = t.nfix, lo2 = t.fixed;
+  const int l1 = t.cl, n1 = t.n, l2 = t.lkey % nk, n2 = l2 - t.rkey % nk;
+  const int LL = L1 * L2;
+  const int tid = threadIdx.x;
+  for (int x = tid; x < LL; x += K5F_THREADS) {
+    const int i = x / L2, j = x - i * L2;
+    const int s = (lo1 + i) * nk + lo2 + j;
+    const SecEntry el = sp_ld.sec[s], es = sp_st.sec[s];
+    const int64_t off = (int64_t)(rowoff[s * nq + t.lkey] + t.band) * el.ld + coloff[s * nq + t.rkey];
+    ldp[x] = el.nonempty ? (el.src ? el.src : el.out) + off : nullptr;
+    stp[x] = es.out + ((int64_t)(rowoff[s * nq + t.lkey] + t.band) * es.ld + coloff[s * nq + t.rkey]);
+    ldv[x] = el.ld;
+    stv[x] = es.ld;
+  }
+  {
+    const int nlo1 = max(0, n1 - d + 1), sn1 = min(n1, d - 1) - nlo1 + 1;
+    const int nlo2 = max(0, n2 - d + 1), sn2 = min(n2, d - 1) - nlo2 + 1;
+    const double2* Ub1 = U + sp_ld.ustart[n1];
+    const double2* Ub2 = U + sp_ld.ustart[n2];
+    for (int x = tid; x < L1 * L1; x += K5F_THREADS) {
+      const int a = x / L1, b = x - a * L1;
+      U1s[a * LMAX + b] = __ldg(Ub1 + (l1 - lo1 - a - nlo1) * sn1 + (l1 - lo1 - b - nlo1));
+    }
+    for (int x = tid; x < L2 * L2; x += K5F_THREADS) {
+      const int a = x / L2, b = x - a * L2;
+      const double2 v = __ldg(Ub2 + (l2 - lo2 - a - nlo2) * sn2 + (l2 - lo2 - b - nlo2));
+      U2s[a * LMAX + b] = make_double2(v.x, -v.y);   // the bra species carries conj(U)
+    }
+  }
+  __syncthreads();
+  const int G = max(1, K5F_X_BYTES / (LL * 8 * (int)sizeof(double2)));   // 8-groups per chunk
+  for (int k0 = 0; k0 < t.ne; k0 += G) {
+    const int ng = min(G, t.ne - k0), E = 8 * ng;
+    // stage X[ij][e]: consecutive threads → consecutive columns of one sector row (128-byte runs); 8 loads in
+    // flight per thread before any is stored (one at a time left every warp waiting out a full HBM latency per load)
+    constexpr int MLP = 8;
+    for (int x0 = tid; x0 < LL * E; x0 += K5F_THREADS * MLP) {
+      double2 v[MLP];
+#pragma unroll
+      for (int q = 0; q < MLP; ++q) {
+        const int x = x0 + q * K5F_THREADS;
+        v[q] = make_double2(0.0, 0.0);
+        if (x < LL * E) {
+          const int ij = x / E, e = x - ij * E;
+          const int grp = t.e0 + k0 + (e >> 3);
+          const int row = grp / t.ngr, col = (grp - row * t.ngr) * 8 + (e & 7);
+          const double2* b = ldp[ij];
+          if (b && col < t.nr) v[q] = __ldcs(b + (int64_t)row * ldv[ij] + col);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < MLP; ++q) {
+        const int x = x0 + q * K5F_THREADS;
+        if (x < LL * E) X[x] = v[q];
+      }
+    }
+    __syncthreads();
+    // U1 down every column (j, e): X[:, j, e] ← U1 · X[:, j, e] — the column's L1 inputs and all L1 outputs in
+    // registers, input-major, so the L1 output accumulations are independent (no dependent FMA chains)
+    for (int y = tid; y < L2 * E; y += K5F_THREADS) {
+      const int j = y / E, e = y - j * E;
+      double2 acc[LMAX];
+#pragma unroll
+      for (int a = 0; a < LMAX; ++a) acc[a] = make_double2(0.0, 0.0);
+      for (int i = 0; i < L1; ++i) {
+        const double2 v = X[(i * L2 + j) * E + e];
+#pragma unroll
+        for (int a = 0; a < LMAX; ++a)
+          if (a < L1) {
+            const double2 u = U1s[a * LMAX + i];
+            acc[a].x = fma(u.x, v.x, fma(-u.y, v.y, acc[a].x));
+            acc[a].y = fma(u.x, v.y, fma(u.y, v.x, acc[a].y));
+          }
+      }
+#pragma unroll
+      for (int a = 0; a < LMAX; ++a)
+        if (a < L1) X[(a * L2 + j) * E + e] = acc[a];
+    }
+    __syncthreads();
+    // U2* along every row (a, e), λlλr, store: Θ(lo1+a, lo2+u)[row, col]
+    for (int y = tid; y < L1 * E; y += K5F_THREADS) {
+      const int a = y / E, e = y - a * E;
+      const int grp = t.e0 + k0 + (e >> 3);
+      const int row = grp / t.ngr, col = (grp - row * t.ngr) * 8 + (e & 7);
+      if (col >= t.nr) continue;
+      double2 acc[LMAX];
+#pragma unroll
+      for (int u = 0; u < LMAX; ++u) acc[u] = make_double2(0.0, 0.0);
+      for (int j = 0; j < L2; ++j) {
+        const double2 v = X[(a * L2 + j) * E + e];
+#pragma unroll
+        for (int u = 0; u < LMAX; ++u)
+          if (u < L2) {
+            const double2 w = U2s[u * LMAX + j];
+            acc[u].x = fma(w.x, v.x, fma(-w.y, v.y, acc[u].x));
+            acc[u].y = fma(w.x, v.y, fma(w.y, v.x, acc[u].y));
+          }
+      }
+      const double scale = ll ? ll[perm_l[t.pl0 + row]] * lr[perm_r[t.pr0 + col]] : 1.0;
+#pragma unroll
+      for (int u = 0; u < LMAX; ++u)
+        if (u < L2) {
+          const int ij = a * L2 + u;
+          __stcs(stp[ij] + (int64_t)row * stv[ij] + col, make_double2(acc[u].x * scale, acc[u].y * scale));
+        }
+    }
+    __syncthreads();
+  }
+}
+
+static cudaError_t launch_pair_mix_fused(const tn_plan* p, const SectorParams& sp_ld, const SectorParams& sp_st,
+                                         const double* ll, const double* lr, const double2* U, cudaStream_t s) {
+  if (p->nmix_fused == 0) return cudaSuccess;
+  constexpr int LM = 8;
+  const size_t smem = (size_t)2 * LM * LM * sizeof(double2) + (size_t)LM * LM * (2 * sizeof(void*) + 16) + K5F_X_BYTES;
+  cudaError_t e = cudaFuncSetAttribute(k5f_mix<LM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k5f_mix<LM><<<(unsigned)p->nmix_fused, K5F_THREADS, smem, s>>>(sp_ld, sp_st, p->d_mix2, p->d_rowoff, p->d_coloff,
+                                                                 p->nq, p->d_perm[0], p->d_perm[2], ll, lr, U);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp1, const double* ll, const double* lr,
                             const double2* U, cudaStream_t s, const SectorParams* sp2_in) {
   const SectorParams& sp2 = sp2_in ? *sp2_in : sp1;   // pass 2 may read one set of buffers and write another
+  // K5F blocks (both species at once) read P from sp1's buffers and write Θ through sp2's (the same tables for a
+  // plain exec; tn_theta_exec_remote: local workspace → the owners' buffers)
+  if (cudaError_t e = launch_pair_mix_fused(p, sp1, sp2, ll, lr, U, s); e != cudaSuccess) return e;
   const int Lmax = p->max_mix;
   const int Lc[4] = {std::min(Lmax, 8), std::min(Lmax, 16), std::min(Lmax, 32), Lmax};
   for (int pass = 0; pass < 2; ++pass) {
     if (p->nmix2[pass] == 0) continue;
-    const MixTile2* tiles = p->d_mix2 + (pass ? p->nmix2[0] : 0);
+    const MixTile2* tiles = p->d_mix2 + p->nmix_fused + (pass ? p->nmix2[0] : 0);
     const SectorParams& sp = pass ? sp2 : sp1;
     for (int multi = 0; multi < 2; ++multi)
       for (int c = 0; c < 4; ++c) {

@@ -464,8 +464,9 @@ def test_exec_launch_count(tn):
     assert plan.exec_launches() == 4                 # set, K3L a/b, K4L (no mix)
     c = synth.make_pair_config(1)
     p2 = tn.Plan2(c.d, c.N, c.q1_l, c.q2_l, c.q1_c, c.q2_c, c.q1_r, c.q2_r)
-    # set, K3 a/b, K4, and per K5P pass one launch for single-value and one for multi-value tiles
-    assert p2.exec_launches() == 8
+    # set, K3 a/b, K4 and one K5F launch: at d = 5 every (l, r) block has L1, L2 ≤ 8, so both species are mixed in
+    # one pass (no two-pass K5P launches)
+    assert p2.exec_launches() == 5
 
 
 def test_exec_captured_in_cuda_graph(tn):
