@@ -262,147 +262,135 @@ tn_status build_pair_tables(tn_plan* p) {
   p->nfix_max = 1;
   int max_l = 1;
   auto cls = [](int L) { return L <= 8 ? 0 : L <= 16 ? 1 : L <= 32 ? 2 : 3; };
-  // count == true: whole (left key, right key) blocks are counted in O(1) (every tile of a block has the same L; only
-  // the last value group of a block can cover fewer values), emit(bucket, n, ·) adds n tiles
-  static const bool two_pass = getenv("TN_PAIR_TWO_PASS") != nullptr;
-  constexpr int FUSE_MAXL = 8;
-  const bool fuse = !two_pass;
-  auto fused_block = [&](int L1, int L2) { return fuse && L1 <= FUSE_MAXL && L2 <= FUSE_MAXL; };
-  auto walk = [&](int pass, bool count, auto&& emit) {
-    for (const Key& Lk : lkeys) {
-      const auto sh = in_shard(Lk.k);
-      const int64_t nl = sh.second, lfirst = sh.first;
-      if (!nl) continue;
-      const int l1 = Lk.k1, l2 = Lk.k2;
-      for (const Key& Rk : rkeys) {
-        const int64_t nr = Rk.n;
-        const int r1 = Rk.k1, r2 = Rk.k2;
-        const int lo1 = std::max(r1, l1 - d + 1), hi1 = std::min(l1, r1 + d - 1);
-        const int lo2 = std::max(r2, l2 - d + 1), hi2 = std::min(l2, r2 + d - 1);
-        if (hi1 < lo1 || hi2 < lo2) continue;
-        if (fused_block(hi1 - lo1 + 1, hi2 - lo2 + 1)) continue;   // K5F mixes this block
-        const int L = pass == 0 ? hi1 - lo1 + 1 : hi2 - lo2 + 1;
-        const int64_t ngr = (nr + 7) / 8;
-        const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
-        const int fixed_lo = pass == 0 ? lo2 : lo1, fixed_hi = pass == 0 ? hi2 : hi1;
-        // several values of the other species per tile when one value's band is small (≈ 128 8-groups a tile)
-        const int64_t per_val = std::min<int64_t>(rows_per, nl) * ngr;
-        const int nfix = (int)std::max<int64_t>(1, std::min<int64_t>(fixed_hi - fixed_lo + 1,
-                                                                      MIX_GROUPS_PER_TILE / std::max<int64_t>(1, per_val)));
-        max_l = std::max(max_l, L);
-        p->nfix_max = std::max(p->nfix_max, nfix);
-        if (count) {
-          const int span = fixed_hi - fixed_lo + 1, ngrp = (span + nfix - 1) / nfix, nf_last = span - (ngrp - 1) * nfix;
-          const int64_t bands = (nl + rows_per - 1) / rows_per;
-          emit((nfix == 1 ? 0 : 4) + cls(L), (int64_t)(ngrp - 1) * bands, nullptr);
-          emit((nf_last == 1 ? 0 : 4) + cls(L), bands, nullptr);
-          continue;
-        }
-        for (int f = fixed_lo; f <= fixed_hi; f += nfix)
-          for (int64_t band = 0; band < nl; band += rows_per) {
-            const int nf = std::min(nfix, fixed_hi - f + 1);
-            const int bucket = (nf == 1 ? 0 : 4) + cls(L);
-            emit(bucket, 1, [&](MixTile2& t) {
-              const int64_t rows = std::min<int64_t>(rows_per, nl - band);
-              t = MixTile2{};
-              t.cl = pass == 0 ? l1 : l2;
-              t.n = pass == 0 ? l1 - r1 : l2 - r2;
-              t.lo = pass == 0 ? lo1 : lo2;
-              t.L = L;
-              t.e0 = 0;
-              t.ne = (int32_t)(rows * ngr);
-              t.nr = (int32_t)nr;
-              t.ngr = (int32_t)ngr;
-              t.pl0 = (int32_t)(lfirst + band);
-              t.pr0 = orr[Rk.k];
-              t.lkey = Lk.k;
-              t.rkey = Rk.k;
-              t.fixed = f;
-              t.nfix = nf;
-              t.band = (int32_t)band;
-              t.flags = pass;
-            });
-          }
-      }
-    }
-  };
   // Blocks whose both species' vectors are short (L1, L2 ≤ 8) are mixed by K5F in one pass (Θ read and written once);
   // longer ones keep the two passes, which run on the tensor pipe (measured: K5F with L up to 18 held one CTA per
   // SM at 130–200 registers and lost to the two passes: pair config 5 4.68 vs 3.18 ms; at L ≤ 8 it wins, pair
   // config 3 0.51 vs 0.80 ms). TN_PAIR_TWO_PASS=1 sends every block through the two passes.
-  p->nmix_fused = 0;
-  {
-    // K5F tiles: one per (left key, right key) block and band of ≈ 128 8-groups; both species mixed in one pass.
-    // MixTile2 fields: (cl, n, lo, L) of species 1; fixed = lo2, nfix = L2 of species 2; bucket = class of max(L1, L2)
-    auto walkf = [&](bool count, auto&& emit) {
-      for (const Key& Lk : lkeys) {
-        const auto sh = in_shard(Lk.k);
-        const int64_t nl = sh.second, lfirst = sh.first;
-        if (!nl) continue;
-        for (const Key& Rk : rkeys) {
-          const int lo1 = std::max(Rk.k1, Lk.k1 - d + 1), hi1 = std::min(Lk.k1, Rk.k1 + d - 1);
-          const int lo2 = std::max(Rk.k2, Lk.k2 - d + 1), hi2 = std::min(Lk.k2, Rk.k2 + d - 1);
-          if (hi1 < lo1 || hi2 < lo2) continue;
-          const int L1 = hi1 - lo1 + 1, L2 = hi2 - lo2 + 1, c = 0;
-          if (!fused_block(L1, L2)) continue;
-          max_l = std::max(max_l, std::max(L1, L2));
-          const int64_t ngr = (Rk.n + 7) / 8;
-          const int64_t rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / ngr);
-          if (count) {
-            emit(c, (nl + rows_per - 1) / rows_per, nullptr);
-            continue;
-          }
-          for (int64_t band = 0; band < nl; band += rows_per)
-            emit(c, 1, [&](MixTile2& t) {
-              const int64_t rows = std::min<int64_t>(rows_per, nl - band);
-              t = MixTile2{};
-              t.cl = Lk.k1;
-              t.n = Lk.k1 - Rk.k1;
-              t.lo = lo1;
-              t.L = L1;
-              t.e0 = 0;
-              t.ne = (int32_t)(rows * ngr);
-              t.nr = (int32_t)Rk.n;
-              t.ngr = (int32_t)ngr;
-              t.pl0 = (int32_t)(lfirst + band);
-              t.pr0 = orr[Rk.k];
-              t.lkey = Lk.k;
-              t.rkey = Rk.k;
-              t.fixed = lo2;
-              t.nfix = L2;
-              t.band = (int32_t)band;
-              t.flags = 2;
-            });
+  static const bool two_pass = getenv("TN_PAIR_TWO_PASS") != nullptr;
+  constexpr int FUSE_MAXL = 8;
+  // One enumeration of the (left key, right key) blocks of this shard computes every block's tile counts per launch
+  // bucket (a tile of a block has the block's L; only its last value group may cover fewer values of the other
+  // species); a prefix over the blocks gives each block's first slot per bucket, and one fill loop writes every
+  // tile straight into place — no sorting, copies or per-tile reallocation on the per-gate plan's path.
+  // Buckets: 0 = K5F; 1 + pass·8 + (multi ? 4 : 0) + class(L) for the two-pass tiles (single-value first).
+  constexpr int NB = 17;
+  struct BlkT {
+    int li, ri, lo1, hi1, lo2, hi2;
+    int64_t nl, lfirst, ngr, rows_per;
+    int nfix[2];      // 0, 0: a K5F block
+  };
+  std::vector<BlkT> blocks;
+  blocks.reserve(lkeys.size() * rkeys.size());
+  int64_t tot[NB] = {};
+  for (int li = 0; li < (int)lkeys.size(); ++li) {
+    const Key& Lk = lkeys[li];
+    const auto sh = in_shard(Lk.k);
+    if (!sh.second) continue;
+    for (int ri = 0; ri < (int)rkeys.size(); ++ri) {
+      const Key& Rk = rkeys[ri];
+      BlkT b;
+      b.lo1 = std::max(Rk.k1, Lk.k1 - d + 1);
+      b.hi1 = std::min(Lk.k1, Rk.k1 + d - 1);
+      b.lo2 = std::max(Rk.k2, Lk.k2 - d + 1);
+      b.hi2 = std::min(Lk.k2, Rk.k2 + d - 1);
+      if (b.hi1 < b.lo1 || b.hi2 < b.lo2) continue;
+      b.li = li;
+      b.ri = ri;
+      b.nl = sh.second;
+      b.lfirst = sh.first;
+      b.ngr = (Rk.n + 7) / 8;
+      b.rows_per = std::max<int64_t>(1, MIX_GROUPS_PER_TILE / b.ngr);
+      const int L1 = b.hi1 - b.lo1 + 1, L2 = b.hi2 - b.lo2 + 1;
+      const int64_t bands = (b.nl + b.rows_per - 1) / b.rows_per;
+      max_l = std::max(max_l, std::max(L1, L2));
+      if (!two_pass && L1 <= FUSE_MAXL && L2 <= FUSE_MAXL) {
+        tot[0] += bands;
+        b.nfix[0] = b.nfix[1] = 0;
+      } else {
+        for (int pass = 0; pass < 2; ++pass) {
+          const int L = pass == 0 ? L1 : L2, span = pass == 0 ? L2 : L1;
+          // several values of the other species per tile when one value's band is small (≈ 128 8-groups a tile)
+          const int64_t per_val = std::min<int64_t>(b.rows_per, b.nl) * b.ngr;
+          const int nfix = (int)std::max<int64_t>(1, std::min<int64_t>(span, MIX_GROUPS_PER_TILE / std::max<int64_t>(1, per_val)));
+          b.nfix[pass] = nfix;
+          p->nfix_max = std::max(p->nfix_max, nfix);
+          const int ngrp = (span + nfix - 1) / nfix, nf_last = span - (ngrp - 1) * nfix;
+          tot[1 + pass * 8 + (nfix == 1 ? 0 : 4) + cls(L)] += (ngrp - 1) * bands;
+          tot[1 + pass * 8 + (nf_last == 1 ? 0 : 4) + cls(L)] += bands;
         }
       }
-    };
-    int64_t tot = 0;
-    walkf(true, [&](int, int64_t n, auto&&) { tot += n; });
-    mix.resize((size_t)tot);
-    MixTile2* o = mix.data();
-    int64_t at = 0;
-    walkf(false, [&](int, int64_t, auto&& fill) {
-      if constexpr (!std::is_same_v<std::decay_t<decltype(fill)>, std::nullptr_t>) fill(o[at++]);
-    });
-    p->nmix_fused = tot;
-  }
-  for (int pass = 0; pass < 2; ++pass) {
-    int64_t cntb[8] = {};
-    walk(pass, true, [&](int bucket, int64_t n, auto&&) { cntb[bucket] += n; });
-    int64_t tot = 0, at[8];
-    for (int g = 0; g < 8; ++g) {
-      at[g] = tot;
-      tot += cntb[g];
+      blocks.push_back(b);
     }
-    const size_t b0 = mix.size();
-    mix.resize(b0 + (size_t)tot);
-    MixTile2* o = mix.data() + b0;
-    walk(pass, false, [&](int bucket, int64_t, auto&& fill) {
-      if constexpr (!std::is_same_v<std::decay_t<decltype(fill)>, std::nullptr_t>) fill(o[at[bucket]++]);
-    });
-    for (int g = 0; g < 8; ++g) p->nmix2_grp[pass][g >> 2][g & 3] = cntb[g];
-    p->nmix2_multi[pass] = cntb[4] + cntb[5] + cntb[6] + cntb[7];
-    p->nmix2[pass] = tot;
+  }
+  int64_t at[NB], all = 0;
+  for (int g = 0; g < NB; ++g) {
+    at[g] = all;
+    all += tot[g];
+  }
+  mix.resize((size_t)all);
+  MixTile2* o = mix.data();
+  for (const BlkT& b : blocks) {
+    const Key& Lk = lkeys[b.li];
+    const Key& Rk = rkeys[b.ri];
+    const int L1 = b.hi1 - b.lo1 + 1, L2 = b.hi2 - b.lo2 + 1;
+    auto base_tile = [&](int64_t band) {
+      MixTile2 t{};
+      t.e0 = 0;
+      t.ne = (int32_t)(std::min<int64_t>(b.rows_per, b.nl - band) * b.ngr);
+      t.nr = (int32_t)Rk.n;
+      t.ngr = (int32_t)b.ngr;
+      t.pl0 = (int32_t)(b.lfirst + band);
+      t.pr0 = orr[Rk.k];
+      t.lkey = Lk.k;
+      t.rkey = Rk.k;
+      t.band = (int32_t)band;
+      return t;
+    };
+    if (b.nfix[0] == 0) {   // K5F: species 1 in (cl, n, lo, L), species 2's lo / L in fixed / nfix
+      for (int64_t band = 0; band < b.nl; band += b.rows_per) {
+        MixTile2 t = base_tile(band);
+        t.cl = Lk.k1;
+        t.n = Lk.k1 - Rk.k1;
+        t.lo = b.lo1;
+        t.L = L1;
+        t.fixed = b.lo2;
+        t.nfix = L2;
+        t.flags = 2;
+        o[at[0]++] = t;
+      }
+      continue;
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      const int L = pass == 0 ? L1 : L2;
+      const int fixed_lo = pass == 0 ? b.lo2 : b.lo1, fixed_hi = pass == 0 ? b.hi2 : b.hi1, nfix = b.nfix[pass];
+      for (int f = fixed_lo; f <= fixed_hi; f += nfix) {
+        const int nf = std::min(nfix, fixed_hi - f + 1);
+        const int g = 1 + pass * 8 + (nf == 1 ? 0 : 4) + cls(L);
+        for (int64_t band = 0; band < b.nl; band += b.rows_per) {
+          MixTile2 t = base_tile(band);
+          t.cl = pass == 0 ? Lk.k1 : Lk.k2;
+          t.n = pass == 0 ? Lk.k1 - Rk.k1 : Lk.k2 - Rk.k2;
+          t.lo = pass == 0 ? b.lo1 : b.lo2;
+          t.L = L;
+          t.fixed = f;
+          t.nfix = nf;
+          t.flags = pass;
+          o[at[g]++] = t;
+        }
+      }
+    }
+  }
+  p->nmix_fused = tot[0];
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t n = 0;
+    for (int m = 0; m < 2; ++m)
+      for (int c = 0; c < 4; ++c) {
+        p->nmix2_grp[pass][m][c] = tot[1 + pass * 8 + m * 4 + c];
+        n += p->nmix2_grp[pass][m][c];
+      }
+    p->nmix2[pass] = n;
+    p->nmix2_multi[pass] = n - (p->nmix2_grp[pass][0][0] + p->nmix2_grp[pass][0][1] + p->nmix2_grp[pass][0][2] +
+                                p->nmix2_grp[pass][0][3]);
   }
   p->max_mix = max_l;
   p->nmix = 0;
