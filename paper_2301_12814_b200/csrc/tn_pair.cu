@@ -685,31 +685,53 @@ static cudaError_t launch_pair_mix_fused(const tn_plan* p, const SectorParams& s
 cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp1, const double* ll, const double* lr,
                             const double2* U, cudaStream_t s, const SectorParams* sp2_in) {
   const SectorParams& sp2 = sp2_in ? *sp2_in : sp1;   // pass 2 may read one set of buffers and write another
+  // The launches touch disjoint elements except pass 2 after pass 1: K5F (its own blocks) runs on an auxiliary
+  // stream beside both passes, and each pass's class launches are spread over the caller's stream and two more
+  // auxiliary ones (their tails and occupancy overlap, as K5's classes do), joined before pass 2 and at the end.
+  // TN_K5_SERIAL=1 keeps everything on the caller's stream.
+  static const bool serial = getenv("TN_K5_SERIAL") != nullptr;
+  AuxStreams* ap = nullptr;
+  if (!serial)
+    if (cudaError_t ea = aux_streams(s, &ap); ea != cudaSuccess) return ea;
+  cudaStream_t lanes[3] = {s, ap ? ap->st[0] : s, ap ? ap->st[1] : s};
+  cudaError_t e = cudaSuccess;
+  if (ap) e = cudaEventRecord(ap->fork, s);
   // K5F blocks (both species at once) read P from sp1's buffers and write Θ through sp2's (the same tables for a
   // plain exec; tn_theta_exec_remote: local workspace → the owners' buffers)
-  if (cudaError_t e = launch_pair_mix_fused(p, sp1, sp2, ll, lr, U, s); e != cudaSuccess) return e;
+  const bool fused_aux = ap && p->nmix_fused > 0;
+  if (e == cudaSuccess && fused_aux) e = cudaStreamWaitEvent(ap->st[2], ap->fork, 0);
+  if (e == cudaSuccess) e = launch_pair_mix_fused(p, sp1, sp2, ll, lr, U, fused_aux ? ap->st[2] : s);
+  if (e == cudaSuccess && fused_aux) e = cudaEventRecord(ap->join[2], ap->st[2]);
   const int Lmax = p->max_mix;
   const int Lc[4] = {std::min(Lmax, 8), std::min(Lmax, 16), std::min(Lmax, 32), Lmax};
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = 0; pass < 2 && e == cudaSuccess; ++pass) {
     if (p->nmix2[pass] == 0) continue;
     const MixTile2* tiles = p->d_mix2 + p->nmix_fused + (pass ? p->nmix2[0] : 0);
     const SectorParams& sp = pass ? sp2 : sp1;
-    for (int multi = 0; multi < 2; ++multi)
-      for (int c = 0; c < 4; ++c) {
+    if (ap && pass == 1) e = cudaEventRecord(ap->fork, s);   // pass 2 starts after pass 1 (joined into s)
+    bool used[3] = {true, false, false};
+    int lane = 0;
+    for (int multi = 0; multi < 2 && e == cudaSuccess; ++multi)
+      for (int c = 0; c < 4 && e == cudaSuccess; ++c) {
         const int64_t cnt = p->nmix2_grp[pass][multi][c];
-        if (cnt == 0) {
-          continue;
-        }
+        if (cnt == 0) continue;
         const int L = Lc[c], NT = (L + 7) >> 3, smax = mix_us_elems(L), nfix = multi ? p->nfix_max : 1;
+        cudaStream_t ls = lanes[lane];
+        if (ap && lane > 0 && !used[lane]) {
+          e = cudaStreamWaitEvent(ls, ap->fork, 0);
+          used[lane] = true;
+          if (e != cudaSuccess) break;
+        }
+        lane = (lane + 1) % 3;
 #define TN_P_LAUNCH(M, MULTI)                                                                                 \
   do {                                                                                                        \
     const size_t smem = (size_t)smax * (sizeof(double2) + sizeof(double)) + 2 * 8 * (M) * (size_t)nfix * sizeof(SecRef); \
     if (smem > 48 * 1024) {                                                                                   \
-      cudaError_t e = cudaFuncSetAttribute(k5p_mix<M, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      e = cudaFuncSetAttribute(k5p_mix<M, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
       if (e != cudaSuccess) return e;                                                                         \
     }                                                                                                         \
-    k5p_mix<M, MULTI><<<(unsigned)cnt, K5P_THREADS, smem, s>>>(sp, tiles, p->d_rowoff, p->d_coloff, p->nq,       \
-                                                               p->d_perm[0], p->d_perm[2], ll, lr, U, smax, nfix); \
+    k5p_mix<M, MULTI><<<(unsigned)cnt, K5P_THREADS, smem, ls>>>(sp, tiles, p->d_rowoff, p->d_coloff, p->nq,      \
+                                                                p->d_perm[0], p->d_perm[2], ll, lr, U, smax, nfix); \
   } while (0)
 #define TN_P_CLASS(M)                    \
   do {                                   \
@@ -729,11 +751,17 @@ cudaError_t launch_pair_mix(const tn_plan* p, const SectorParams& sp1, const dou
 #undef TN_P_CLASS
 #undef TN_P_LAUNCH
         tiles += cnt;
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+        e = cudaGetLastError();
+      }
+    // join this pass's auxiliary lanes back into s
+    for (int k = 1; k < 3 && e == cudaSuccess; ++k)
+      if (ap && used[k]) {
+        e = cudaEventRecord(ap->join[k - 1], lanes[k]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ap->join[k - 1], 0);
       }
   }
-  return cudaSuccess;
+  if (e == cudaSuccess && fused_aux) e = cudaStreamWaitEvent(s, ap->join[2], 0);
+  return e;
 }
 
 }  // namespace tn
