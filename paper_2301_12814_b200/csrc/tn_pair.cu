@@ -6,10 +6,12 @@
 // the single-charge path carries over pair by pair:
 //   P_m = A_m · B_m for every centre pair m = (m1, m2)   (K3 staging + K4 contraction, unchanged kernels)
 //   Θ(c1,c2)[α,β] = λlλr Σ_{m1,m2} U_{n1}[l1−c1][l1−m1] · conj(U_{n2}[l2−c2][l2−m2]) · P_m[α,β]
-// and the U⊗U* weight factorises, so the mix is applied one species at a time (K5P, two launches):
+// and the U⊗U* weight factorises, so the mix is applied one species at a time (K5P, two passes):
 //   pass 1:  Q(c1, m2) = Σ_{m1} U_{n1}[l1−c1][l1−m1] P(m1, m2)              (in place, per m2)
 //   pass 2:  Θ(c1, c2) = λlλr Σ_{m2} conj(U_{n2}[l2−c2][l2−m2]) Q(c1, m2)     (in place, per c1)
-// L1²L2 + L1L2² complex MACs per element instead of (L1L2)². Sector (c1, c2) is compact row-major; its rows
+// L1²L2 + L1L2² complex MACs per element instead of (L1L2)². Blocks whose two vectors are short (L1, L2 ≤ 8) take
+// both factors in ONE pass instead (K5F: Y = U1·X·U2ᴴ per element in shared memory / registers), reading and
+// writing Θ once. Sector (c1, c2) is compact row-major; its rows
 // are the sorted left positions with l − c ∈ [0, d−1]² — a union of whole pair segments, in sorted order —
 // and its columns likewise. P_m has exactly Θ(m)'s shape, so K4 writes it straight into Θ(m) as before;
 // the group's rows/columns are gathered through per-group position lists (d_rowperm / d_colperm).
@@ -64,19 +66,6 @@ tn_status build_pair_tables(tn_plan* p) {
     for (int b = 0; b < nk; ++b)
       P2[(size_t)(a + 1) * (nk + 1) + b + 1] = P2[(size_t)a * (nk + 1) + b + 1] + P2[(size_t)(a + 1) * (nk + 1) + b] -
                                                P2[(size_t)a * (nk + 1) + b] + cnt(oc, a * nk + b);
-  struct Blk {
-    int64_t L1, L2, mc;
-  };
-  auto blk = [&](int l, int r) {
-    const int l1 = l / nk, l2 = l % nk, r1 = r / nk, r2 = r % nk;
-    const int a0 = std::max(r1, l1 - d + 1), a1 = std::min(l1, r1 + d - 1);
-    const int b0 = std::max(r2, l2 - d + 1), b1 = std::min(l2, r2 + d - 1);
-    Blk x{std::max(0, a1 - a0 + 1), std::max(0, b1 - b0 + 1), 0};
-    if (x.L1 && x.L2)
-      x.mc = P2[(size_t)(a1 + 1) * (nk + 1) + b1 + 1] - P2[(size_t)a0 * (nk + 1) + b1 + 1] -
-             P2[(size_t)(a1 + 1) * (nk + 1) + b0] + P2[(size_t)a0 * (nk + 1) + b0];
-    return x;
-  };
   // the non-empty left / right pair keys with their charges: the O(keys²) loops below visit only these (no
   // divisions by N+1 in them)
   struct Key {
