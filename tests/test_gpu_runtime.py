@@ -162,3 +162,40 @@ def test_failed_call_does_not_poison_the_next(tn):
     out = gpu_theta(synth.make_config(1))[2]
     for g, r in zip(out, _alone(1)):
         assert np.array_equal(g, r)
+
+
+def test_plans_from_several_host_threads(tn):
+    # four host threads plan and execute gates concurrently, each on its own stream: the plan shells, the memory
+    # pool and the pinned upload ring are shared; every gate's Θ must equal the same gate run alone
+    import threading
+    cfgs = [1, 2, 1, 2]
+    results, errors = [None] * len(cfgs), []
+
+    def work(i, cfg):
+        try:
+            case = synth.make_config(cfg)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                t = to_dev(case)
+                outs = []
+                for _ in range(5):
+                    p = tn.Plan(case.d, case.N, *[np.ascontiguousarray(q) for q in (case.q_l, case.q_c, case.q_r)])
+                    U = tn.build_bs_unitary(p, case.theta, case.phi, stream=st)
+                    outs.append(tn.theta_exec(p, t["gk"], t["lk"], t["gk1"], t["ll"], t["lr"], U, stream=st))
+                    p.destroy()
+            st.synchronize()
+            results[i] = [[o.cpu().numpy() for o in out] for out in outs]
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i, c)) for i, c in enumerate(cfgs)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+    for cfg, res in zip(cfgs, results):
+        ref = _alone(cfg)
+        for out in res:
+            for g, r in zip(out, ref):
+                assert np.array_equal(g, r)
