@@ -255,7 +255,7 @@ tn_status build_pair_tables(tn_plan* p) {
   // longer ones keep the two passes, which run on the tensor pipe (measured: K5F with L up to 18 held one CTA per
   // SM at 130–200 registers and lost to the two passes: pair config 5 4.68 vs 3.18 ms; at L ≤ 8 it wins, pair
   // config 3 0.51 vs 0.80 ms). TN_PAIR_TWO_PASS=1 sends every block through the two passes.
-  static const bool two_pass = getenv("TN_PAIR_TWO_PASS") != nullptr;
+  const bool two_pass = getenv("TN_PAIR_TWO_PASS") != nullptr;   // read per plan (tests switch it)
   constexpr int FUSE_MAXL = 8;
   // One enumeration of the (left key, right key) blocks of this shard computes every block's tile counts per launch
   // bucket (a tile of a block has the block's L; only its last value group may cover fewer values of the other

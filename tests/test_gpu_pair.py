@@ -83,11 +83,18 @@ def test_pair_tables_bit_exact(tn, cfg):
     assert (f["f_contract"], f["f_mix"]) == (fc, fm)
 
 
+@pytest.mark.parametrize("mix", ["default", "two_pass"])
 @pytest.mark.parametrize("cfg", [0, 1, 2])
-def test_pair_parity(tn, cfg):
+def test_pair_parity(tn, cfg, mix, monkeypatch):
+    # default: these small-d configs are mixed by K5F (one pass, both species); two_pass: TN_PAIR_TWO_PASS=1 sends
+    # every block through the two K5P passes instead — both against the oracle
+    if mix == "two_pass":
+        monkeypatch.setenv("TN_PAIR_TWO_PASS", "1")
     ref, *_ = _oracle2(cfg)
-    _, got = gpu_theta2(tn, _pair(cfg))
-    _check(got, ref, TOL, f"pair config {cfg}")
+    plan, got = gpu_theta2(tn, _pair(cfg))
+    # set + K3 a/b + K4, then one K5F launch, or at least one launch per K5P pass
+    assert plan.exec_launches() == 5 if mix == "default" else plan.exec_launches() >= 6
+    _check(got, ref, TOL, f"pair config {cfg} ({mix})")
 
 
 @pytest.mark.parametrize("cfg", [1, 2])
