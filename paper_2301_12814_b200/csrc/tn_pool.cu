@@ -288,7 +288,8 @@ struct RingEvent {
 struct RingSeg {
   size_t start, end;
   const tn_plan* owner;
-  RingEvent* done;  // nullptr until the owner seals
+  RingEvent* done;        // nullptr until the owner seals
+  bool complete = false;  // sealed without an event (its uploads were waited for on the host)
 };
 struct PinnedRing {
   std::mutex mu;
@@ -311,6 +312,11 @@ void ring_pop_front(PinnedRing& r) {
 bool ring_reclaim(PinnedRing& r, bool wait) {
   bool any = false;
   while (!r.segs.empty()) {
+    if (r.segs.front().complete) {
+      ring_pop_front(r);
+      any = true;
+      continue;
+    }
     RingEvent* d = r.segs.front().done;
     if (!d) break;  // a plan still being built (possibly the caller): cannot wait for it
     cudaError_t e = wait ? cudaEventSynchronize(d->ev) : cudaEventQuery(d->ev);
@@ -351,7 +357,7 @@ char* ring_alloc(PinnedRing& r, size_t n, const tn_plan* owner) {
       }
     }
     if (at != SIZE_MAX) {
-      r.segs.push_back(RingSeg{at, at + n, owner, nullptr});
+      r.segs.push_back(RingSeg{at, at + n, owner, nullptr, false});
       r.head = at + n;
       return r.base + at;
     }
@@ -423,40 +429,20 @@ void plan_h2d_seal(tn_plan* p) {
     r.free_ev.push_back(d);
     d = nullptr;
   }
-  if (!d) {  // cannot fence the staged uploads: wait for them, then the ranges are free at once
+  if (!d) {  // cannot fence the staged uploads: wait for them on the host, then the ranges are free at once
     cudaStreamSynchronize(p->plan_stream);
     cudaGetLastError();
   }
   for (RingSeg& g : r.segs)
-    if (g.owner == p && !g.done) {
+    if (g.owner == p && !g.done && !g.complete) {
       if (d) {
         g.done = d;
         ++d->refs;
       } else {
-        g.owner = nullptr;  // marked complete below
+        g.complete = true;
       }
     }
-  if (!d) {
-    // ranges of p without an event: give them an already-complete event so FIFO reclaim can pass them
-    RingEvent* z = nullptr;
-    if (!r.free_ev.empty()) {
-      z = r.free_ev.back();
-      r.free_ev.pop_back();
-    } else {
-      z = new (std::nothrow) RingEvent();
-      if (z) cudaEventCreateWithFlags(&z->ev, cudaEventDisableTiming);
-    }
-    if (z) {
-      cudaEventRecord(z->ev, p->plan_stream);  // the stream is drained: complete immediately
-      cudaGetLastError();
-      for (RingSeg& g : r.segs)
-        if (!g.owner && !g.done) {
-          g.done = z;
-          ++z->refs;
-        }
-      if (z->refs == 0) r.free_ev.push_back(z);
-    }
-  }
+  if (d && d->refs == 0) r.free_ev.push_back(d);
   p->n_staged = 0;
 }
 
