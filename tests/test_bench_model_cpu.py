@@ -40,3 +40,37 @@ def test_comm_model_bytes(cfg, R):
     for name in ("slabs", "full_bcast", "slabs_and_owner_gather", "slabs_and_root_gather"):
         s, o = m[f"projected_speedup_{name}_serial"], m[f"projected_speedup_{name}_overlapped"]
         assert s <= o <= 4.0 / max(per) + 1e-9
+
+
+def _lines(name):
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", name)
+    import json
+    with open(path) as f:
+        return [json.loads(x) for x in f if x.strip()]
+
+
+def test_bench_line_carries_the_contract_keys():
+    # the committed closing bench line (profiles/r02_bench_final.jsonl) has every key the bench contract asks for
+    for d in _lines("r02_bench_final.jsonl"):
+        for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                  "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                  "gpu_launches", "clocks"):
+            assert k in d, k
+        assert d["warmup"] >= 3 and d["n_gpus"] == 1 and d["dtype"] == "f64" and "workload" in d["config"]
+        r = d["roofline"]
+        assert r["bound"] in ("hbm", "tensor", "alu") and r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-3)
+        assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"]) and d["cpu_baseline"]["kind"] == "oracle"
+        e = d["e2e"]
+        assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e) and e["h2d_bytes_per_step"] > 0
+        assert d["gpu_launches"] > 0 and not (set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
+                                                                               "sw_thermal_slowdown"})
+        # value = useful flops of the step / its time
+        f = d["config"]["f_contract"] + d["config"]["f_mix"]
+        assert d["value"] == pytest.approx(f / (d["ms_per_step"] * 1e-3) / 1e9, rel=2e-3)
+
+
+def test_reference_line_carries_the_contract_keys():
+    for d in _lines("r02_bench_ref.jsonl"):
+        assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
+        assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+        assert d["e2e"]["value"] == d["value"]
