@@ -31,12 +31,14 @@ __device__ __forceinline__ void load_group(double2 (&a)[KSM], const SecRef* __re
     a[ks] = make_double2(0.0, 0.0);
     if (valid && u < L) {
       const SecRef s = sec[u];
-      if (s.base) a[ks] = L2ONLY ? __ldcg(s.base + row * s.ld + col) : __ldcs(s.base + row * s.ld + col);
+      // ld.global.cg: P is read once, so it skips L1, but with the normal L2 policy — the streaming
+      // (evict-first) hint measured 2% slower on K5 (0.691 vs 0.675 ms at config 3)
+      if (s.base) a[ks] = __ldcg(s.base + row * s.ld + col);
     }
   }
 }
 
-// L2ONLY: P was written by other SMs during the same kernel → bypass L1 (ld.global.cg)
+// L2ONLY: P was written by other SMs during the same kernel → bypass L1 (ld.global.cg; every load is .cg now)
 // PF: groups further ahead (beyond the one held in registers) whose P lines are prefetched into L2
 // (PF = 2 measured slower at configs 3 and 4: 0.82 vs 0.78 ms, 6.57 vs 6.05 ms)
 // MULTI: the tile spans `nsub` sub-tiles of mt.ne 8-groups each, sub-tile i using sector tables sec + i·sstride
@@ -132,7 +134,7 @@ __device__ __forceinline__ void mix_tile_warp(const MixTile& mt, const SecRef* _
             const SecRef s = st_sec[t];  // output sector lo+t (every output sector is stored)
             const double re = acc[j][h] - acc[j][2 + h];
             const double im = acc[j][4 + h] - acc[j][h] - acc[j][2 + h];
-            __stcs(const_cast<double2*>(s.base) + row * s.ld + col, make_double2(re * scale, im * scale));
+            __stcg(const_cast<double2*>(s.base) + row * s.ld + col, make_double2(re * scale, im * scale));
           }
         }
     }

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(K5F_THREADS, 2)
           const int grp = t.e0 + k0 + (e >> 3);
           const int row = grp / t.ngr, col = (grp - row * t.ngr) * 8 + (e & 7);
           const double2* b = ldp[ij];
-          if (b && col < t.nr) v[q] = __ldcs(b + (int64_t)row * ldv[ij] + col);
+          if (b && col < t.nr) v[q] = __ldcg(b + (int64_t)row * ldv[ij] + col);
         }
       }
 #pragma unroll
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(K5F_THREADS, 2)
       for (int u = 0; u < LMAX; ++u)
         if (u < L2) {
           const int ij = a * L2 + u;
-          __stcs(stp[ij] + (int64_t)row * stv[ij] + col, make_double2(acc[u].x * scale, acc[u].y * scale));
+          __stcg(stp[ij] + (int64_t)row * stv[ij] + col, make_double2(acc[u].x * scale, acc[u].y * scale));
         }
     }
     __syncthreads();
