@@ -31,8 +31,10 @@ def _nccl_include() -> str:
 
 
 def cflags():
+    # TN_EXTRA_NVCC_FLAGS: extra -D switches for A/B builds of compile-time variants (measurement only)
+    extra = os.environ.get("TN_EXTRA_NVCC_FLAGS", "").split()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-                   "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(), "-Xptxas", "-warn-spills"]
+                   "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(), "-Xptxas", "-warn-spills"] + extra
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
